@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Ax / A^T b hot path (BASELINE.json metric).
+
+Workload (config 3 of BASELINE.json, the shape the metric is quoted on): LSMR with
+Tikhonov damping lambda = 30, 50 iterations, 512^3 Shepp-Logan volume (device-rasterised,
+h = 1), 512^2 detector, 360 equidistant angles, cone beam DSO = 2n, DOD = n, pixel 1.5,
+matched backprojector, fp32 data.  One STEP = one full solve (50 Krylov iterations, each
+= 2 Ax + 1 A^T b + fused BLAS-1, explicit residual included, as the reference does).
+`value` = Krylov iterations/s of the whole job; Ax / A^T b Gray-voxel/s are reported too.
+
+Multi-GPU (torchrun): angles are sharded contiguously across ranks, the volume replicated;
+A^T b partial volumes are sum-reduced with NCCL and range dots summed in rank order.
+
+--impl reference: times the reference CPU implementation (oracle/_ref, the unmodified
+reference headers compiled here) on the host cores, on a bounded sample of the same
+workload (Ax + matched A^T b over a subset of angles, extrapolated to iterations/s).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Krylov iters/s + Ax/Atb Gray-voxel/s, 512^3 vol, 512^2 det, 360 angles"
+GATHER_BYTES_PER_SAMPLE = 16  # 4 fp32 taps per bilinear sample
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=512)
+    p.add_argument("--angles", type=int, default=360)
+    p.add_argument("--iters", type=int, default=50)
+    p.add_argument("--lam", type=float, default=30.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work for the cpu_baseline sample")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference_rate(n, na, budget_s, dtype_f32=True):
+    """Reference CPU path (oracle/_ref) on the host cores: Ax + matched A^T b over an evenly
+    spaced subset of S angles, extrapolated linearly in angles (projector.hpp:150,187 are
+    independent per angle) to one Krylov iteration = 2 Ax + 1 A^T b (BLAS-1 excluded,
+    which favours the CPU)."""
+    import numpy as np
+
+    from oracle.oracle import REF_SO, Reference, Restated, bench_geometry
+
+    kind = "reference" if Reference.available() else "port"
+    cores = os.cpu_count() or 1
+    orc = Reference() if kind == "reference" else None
+    if orc is not None:
+        orc.set_threads(cores)
+    rest = Restated()
+    g = bench_geometry(n, na)
+    dt = np.float32 if dtype_f32 else np.float64
+    x = rest.shepp_logan_3d(n, dt)
+
+    def run(S):
+        idx = np.linspace(0, na, S, endpoint=False).astype(int)
+        gs = g.subset(idx)
+        t0 = time.perf_counter()
+        y = orc.forward(gs, x) if orc else rest.forward(gs, x)
+        t1 = time.perf_counter()
+        _ = orc.back(gs, y, 0) if orc else rest.back(gs, y)
+        t2 = time.perf_counter()
+        return S, t1 - t0, t2 - t1
+
+    S, tax, tbt = run(1)  # calibration (also warms caches / threads)
+    per_angle = (tax + tbt)
+    S = max(1, min(na, int(budget_s / max(per_angle, 1e-6))))
+    S, tax, tbt = run(S)
+    t_iter = (na / S) * (2.0 * tax + tbt)
+    samples_ax = S * n * n * n  # rays*slices for S angles (Gray-voxel normaliser)
+    return {
+        "iters_per_s": 1.0 / t_iter,
+        "ax_gvox_s": 1e-9 * samples_ax / tax,
+        "atb_gvox_s": 1e-9 * samples_ax / tbt,
+        "kind": kind,
+        "cores": cores,
+        "sample": f"Ax + matched A^T b on {S} of {na} angles ({'f32' if dtype_f32 else 'f64'}, reference headers "
+                  f"-O3 -fopenmp, {cores} threads), extrapolated x{na / S:.1f} to 2 Ax + 1 A^T b per iteration",
+        "seconds": tax + tbt,
+    }
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    budget = max(3.0, 150.0 / max(1, args.steps + args.warmup))
+    vals = []
+    last = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_rate(args.n, args.angles, budget)
+        if i >= args.warmup:
+            vals.append(r["iters_per_s"])
+        last = r
+    v = statistics.mean(vals)
+    line = {
+        "impl": "reference",
+        "metric": METRIC,
+        "value": v,
+        "unit": "iters/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1000.0 / v,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic Shepp-Logan 3D (phantom.hpp), b = A x",
+        "config": {"workload": f"LSMR lambda={args.lam}, {args.n}^3 volume, {args.n}^2 detector, {args.angles} angles, "
+                               f"matched Joseph (config 3); CPU sample extrapolated"},
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": last["cores"], "kind": last["kind"],
+                         "sample": last["sample"]},
+        "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ax_gvox_s": last["ax_gvox_s"],
+        "atb_gvox_s": last["atb_gvox_s"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    import paper_2211_14212_b200 as ctk
+    from paper_2211_14212_b200.comm import NcclComm, shard_angles
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    n, na = args.n, args.angles
+    full = ctk.bench_geometry(n, na)
+    first, count = shard_angles(na, world, rank)
+    geom = full.subset(first, count)
+    pair = ctk.projector_pair(geom)
+    proj = pair.projector
+    comm = None
+    if world > 1:
+        comm = NcclComm(rank, world)
+        proj.attach_comm(comm)
+
+    # synthetic inputs, resident in HBM: phantom rasterised on the device, b = A x
+    x_true = ctk.shepp_logan_3d(n)
+    b = torch.empty(pair.range_size, dtype=torch.float32, device="cuda")
+    pair.forward(x_true, b)
+    torch.cuda.synchronize()
+    opts = ctk.SolverOptions(max_iters=args.iters, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def maxed(t):
+        if dist is None:
+            return t
+        v = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    # ---- per-kernel timing (CUDA events recorded by the library around its main kernel, on
+    # the stream that kernel runs on), 3 repeats each, inputs > L2 (512 MiB volume)
+    y = torch.empty_like(b)
+    xb = torch.empty_like(x_true)
+    ax_ms, bt_ms, ax_call_ms = [], [], []
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pair.forward(x_true, y)
+        e1.record()
+        torch.cuda.synchronize()
+        ax_ms.append(proj.last_kernel_ms())
+        ax_call_ms.append(e0.elapsed_time(e1))
+        pair.back(y, xb)
+        torch.cuda.synchronize()
+        bt_ms.append(proj.last_kernel_ms())
+    t_ax = statistics.median(ax_ms[1:])
+    t_bt = statistics.median(bt_ms[1:])
+
+    # ---- the solve: W warmup steps, K timed steps (device-resident b and x)
+    for _ in range(args.warmup):
+        ctk.lsmr(pair, b, args.lam, opts)
+    barrier()
+    launches0 = ctk.launch_count()
+    with Clocks(local) as clk:
+        barrier()
+        t0 = time.perf_counter()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record()
+        for _ in range(args.steps):
+            res = ctk.lsmr(pair, b, args.lam, opts)
+        s1.record()
+        barrier()
+        wall = time.perf_counter() - t0
+    launches = ctk.launch_count() - launches0
+    dev_ms = maxed(s0.elapsed_time(s1))
+    iters_total = sum([args.iters]) * args.steps
+    ms_per_step = dev_ms / args.steps
+    value = iters_total / (dev_ms / 1000.0)
+
+    # ---- end-to-end through the public API with HOST (pinned) buffers
+    b_host = torch.empty(pair.range_size, dtype=torch.float32, pin_memory=True)
+    b_host.copy_(b.cpu())
+    b_np = b_host.numpy()
+    e2e_steps = max(1, min(args.steps, 2))
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        r = ctk.lsmr(pair, b_np, args.lam, opts)  # H2D b, solve, D2H x inside the call
+    barrier()
+    e2e_s = maxed(time.perf_counter() - t0)
+    e2e_value = args.iters * e2e_steps / e2e_s
+
+    hbm_peak, sm_mhz, peak_src = peaks()
+    nvox, nproj = n ** 3, count * n * n
+    samples = count * n * n * n  # Gray-voxel normaliser (rays x slices)
+    ax_gvox = 1e-9 * samples / (t_ax / 1e3)
+    bt_gvox = 1e-9 * samples / (t_bt / 1e3)
+    alg_bytes = 4.0 * (nvox + nproj)
+    share_ax, share_bt = 2 * t_ax, t_bt
+    dom = "k_ax_f32" if share_ax >= share_bt else "k_atb_matched_f32"
+    t_dom = t_ax if dom == "k_ax_f32" else t_bt
+    achieved = alg_bytes / (t_dom / 1e3) / 1e9
+    gather_peak = 148 * 128 * sm_mhz * 1e6 / GATHER_BYTES_PER_SAMPLE / 1e9  # G samples/s at 128 B/clk/SM
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "iters/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic: Shepp-Logan 3D rasterised on device (phantom.hpp), b = A x (GPU Ax)",
+        "config": {"workload": f"LSMR lambda={args.lam}, {args.iters} iters/step, {n}^3 volume, {n}^2 detector, "
+                               f"{na} angles, cone DSO=2n DOD=n pixel 1.5, matched Joseph (BASELINE config 3)",
+                   "parallelism": f"angle-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (volume 512 MiB, projections 360 MiB)"},
+        "ax_gvox_s": ax_gvox,
+        "atb_gvox_s": bt_gvox,
+        "kernels_ms": {"k_ax_f32": t_ax, "k_atb_matched_f32": t_bt, "ax_call": statistics.median(ax_call_ms[1:])},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "note": f"algorithmic bytes 4*(N_vox+N_proj) per launch; peak {peak_src}"},
+        "roofline_gather": {"kernel": dom, "achieved": samples / (t_dom / 1e3) / 1e9, "peak": gather_peak,
+                            "unit": "G samples/s", "frac": samples / (t_dom / 1e3) / 1e9 / gather_peak,
+                            "note": "binding on-chip ceiling: 16 B/sample at 128 B/clk/SM x 148 SMs (SURVEY.md 8(d))"},
+        "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": 4 * nproj, "d2h_bytes_per_step": 4 * nvox},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "wall_s_timed": wall,
+        "final_explicit_residual": res.log.explicit_residual[-1],
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cb = cpu_reference_rate(n, na, args.cpu_budget)
+            line["cpu_baseline"] = {"value": cb["iters_per_s"], "unit": "iters/s", "cores": cb["cores"],
+                                    "kind": cb["kind"], "sample": cb["sample"], "ax_gvox_s": cb["ax_gvox_s"],
+                                    "atb_gvox_s": cb["atb_gvox_s"]}
+        except Exception as e:  # reported, never fatal to the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "iters/s", "cores": os.cpu_count(), "kind": "reference",
+                                    "sample": f"failed: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,217 @@
+/*
+ * ctk_b200.h -- C-ABI of the B200-native Ax / A^T b hot path of ctkrylov
+ * (arXiv 2211.14212).  Plain pointers and sizes only; no torch or C++ types.
+ *
+ * The reference has no C-ABI (its FFI is an empty pybind11 `_core`,
+ * bindings/bindings.cpp:1-2); every entry point below replaces a C++ interface of the
+ * reference, cited per declaration as `file:line` under /root/reference/proj.
+ * INTEGRATION.md shows the ctypes / pybind11 / C++ bindings a maintainer would add.
+ *
+ * Layouts (identical to the reference):
+ *   domain (volume)      x[i + nx*(j + ny*k)]                 types.hpp:50-70
+ *   range  (projections) y[iu + nu*(iv + nv*a)]               types.hpp:80-102
+ * Ownership: callers own every buffer; outputs are overwritten entirely
+ * (operators.hpp:102-113).  One in-flight call per ctk_geom; distinct handles may be
+ * used concurrently from different threads.
+ *
+ * Precision: *_f32 entry points run the sm_100a performance kernels (fp32 data,
+ * fp64 per-ray setup, fp64 reductions); *_f64 entry points run the exact-parity
+ * kernels, which reproduce the reference's IEEE operation sequence for T=double.
+ */
+#ifndef CTK_B200_H
+#define CTK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTK_ABI_VERSION 1
+
+/* Error taxonomy of types.hpp:14-31 (DimensionError, GeometryError, ParameterError,
+ * DegenerateInputError, NumericalError) plus device failures. */
+typedef enum {
+    CTK_OK = 0,
+    CTK_E_DIMENSION = 1,
+    CTK_E_GEOMETRY = 2,
+    CTK_E_PARAMETER = 3,
+    CTK_E_DEGENERATE = 4,
+    CTK_E_NUMERICAL = 5,
+    CTK_E_CUDA = 6,
+    CTK_E_UNSUPPORTED = 7
+} ctk_status;
+
+/* BeamMode, geometry.hpp:11 */
+typedef enum { CTK_PARALLEL2D = 0, CTK_PARALLEL3D = 1, CTK_CONE3D = 2 } ctk_beam_mode;
+/* BackprojectVariant, projector.hpp:16 */
+typedef enum { CTK_BP_MATCHED = 0, CTK_BP_VOXEL_DRIVEN = 1 } ctk_bp_variant;
+/* Forward model. Joseph = projector.hpp:48-122; Siddon is new. */
+typedef enum { CTK_PROJ_JOSEPH = 0, CTK_PROJ_SIDDON = 1 } ctk_projector;
+/* StopReason, solve_log.hpp:16 */
+typedef enum { CTK_STOP_MAX_ITERS = 0, CTK_STOP_RESIDUAL_INCREASE = 1, CTK_STOP_TOLERANCE = 2, CTK_STOP_BREAKDOWN = 3 } ctk_stop_reason;
+/* LambdaStrategy, hybrid.hpp:13 */
+typedef enum { CTK_LAMBDA_FIXED = 0, CTK_LAMBDA_DP = 1, CTK_LAMBDA_GCV = 2 } ctk_lambda_strategy;
+
+/* ConeGeometry, geometry.hpp:24-33 (+ VolumeShape, types.hpp:35-41). */
+typedef struct {
+    int mode;                   /* ctk_beam_mode */
+    double source_to_origin;    /* mm, cone3d only */
+    double origin_to_detector;  /* mm */
+    double detector_pixel_size; /* mm */
+    int nu, nv;
+    int nx, ny, nz;
+    double spacing;             /* mm per voxel */
+    int n_angles;
+    const double* angles;       /* radians; reduced by canonical_angle (types.hpp:172-177) */
+} ctk_geom_desc;
+
+typedef struct ctk_geom ctk_geom;
+typedef struct ctk_comm ctk_comm;
+
+/* ---- errors ---------------------------------------------------------------------- */
+/* Thread-local message of the last failing call on this thread; returns its status. */
+int ctk_last_error(char* buf, size_t len);
+/* Iteration carried by the last CTK_E_NUMERICAL (NumericalError::iteration, types.hpp:27-31). */
+int ctk_last_error_iteration(void);
+int ctk_abi_version(void);
+
+/* ---- geometry (replaces ConeGeometry::validate + projector_pair capture,
+ *      geometry.hpp:35-54, operators.hpp:91-101) -------------------------------------- */
+int ctk_geom_create(const ctk_geom_desc* desc, ctk_geom** out);
+void ctk_geom_destroy(ctk_geom* g);
+/* domain_size = nx*ny*nz, range_size = n_angles*nu*nv (operators.hpp:98-99) */
+int ctk_geom_sizes(const ctk_geom* g, size_t* domain_size, size_t* range_size);
+/* Forward model used by ctk_ax_* / matched ctk_atb_* (default Joseph). */
+int ctk_geom_set_projector(ctk_geom* g, int projector);
+/* Partition count used by the exact f64 matched A^T b to reproduce the reference's
+ * OpenMP summation order (projector.hpp:172-201): min(OMP threads, n_angles). Default 1. */
+int ctk_geom_set_bp_partitions(ctk_geom* g, int nparts);
+/* Stream for solver / host-pointer calls (cudaStream_t; NULL = the handle's own stream). */
+int ctk_geom_set_stream(ctk_geom* g, void* stream);
+
+/* ---- operators on DEVICE pointers (forward_project, projector.hpp:134-162;
+ *      back_project, projector.hpp:283-297).  Asynchronous on `stream`. ---------------- */
+int ctk_ax_f32(ctk_geom* g, const float* d_x, float* d_y, void* stream);
+int ctk_ax_f64(ctk_geom* g, const double* d_x, double* d_y, void* stream);
+int ctk_atb_f32(ctk_geom* g, int variant, const float* d_y, float* d_x, void* stream);
+int ctk_atb_f64(ctk_geom* g, int variant, const double* d_y, double* d_x, void* stream);
+/* Fused explicit residual: out = ||A x - b||^2 (fp64), y never stored (solve_log.hpp:111-115). */
+int ctk_ax_residual_f32(ctk_geom* g, const float* d_x, const float* d_b, double* h_out, void* stream);
+
+/* ---- operators on HOST pointers: OperatorPair::forward / back semantics
+ *      (operators.hpp:18-45, 102-113).  Synchronous. ---------------------------------- */
+int ctk_ax_host_f32(ctk_geom* g, const float* h_x, float* h_y);
+int ctk_ax_host_f64(ctk_geom* g, const double* h_x, double* h_y);
+int ctk_atb_host_f32(ctk_geom* g, int variant, const float* h_y, float* h_x);
+int ctk_atb_host_f64(ctk_geom* g, int variant, const double* h_y, double* h_x);
+
+/* ---- BLAS-1 (types.hpp:136-158) on device pointers; fp64 accumulation in a fixed
+ *      reduction order (run-to-run bitwise deterministic).  Results to host. ---------- */
+int ctk_dot_f32(size_t n, const float* d_x, const float* d_y, double* h_out, void* stream);
+int ctk_dot_f64(size_t n, const double* d_x, const double* d_y, double* h_out, void* stream);
+int ctk_nrm2_f32(size_t n, const float* d_x, double* h_out, void* stream);
+int ctk_nrm2_f64(size_t n, const double* d_x, double* h_out, void* stream);
+int ctk_axpy_f32(size_t n, double alpha, const float* d_x, float* d_y, void* stream);
+int ctk_axpy_f64(size_t n, double alpha, const double* d_x, double* d_y, void* stream);
+int ctk_scal_f32(size_t n, double alpha, float* d_x, void* stream);
+int ctk_scal_f64(size_t n, double alpha, double* d_x, void* stream);
+
+/* ---- synthetic input: make_phantom(shepp_logan_3d) (phantom.hpp:74-145) on device -- */
+int ctk_shepp_logan_3d_f32(int n, float* d_out, void* stream);
+int ctk_shepp_logan_3d_f64(int n, double* d_out, void* stream);
+
+/* ---- solvers (solvers.hpp:13-231, hybrid.hpp:76-116, tv.hpp:45-110) ---------------- */
+/* SolverOptions, solve_log.hpp:42-57 */
+typedef struct {
+    int max_iters;
+    int stop_on_explicit_residual_increase;
+    double residual_tolerance;
+    int reorth;
+    const void* ground_truth; /* HOST pointer of T (f32/f64 per entry point) or NULL */
+    /* iterate_observer test hook (solve_log.hpp:50-51): called with a HOST copy of x_k */
+    void (*iterate_observer)(int k, const void* h_x, size_t n, void* user);
+    void* observer_user;
+} ctk_solver_opts;
+
+/* SolveResult + ConvergenceLog, solve_log.hpp:28-76.  Arrays are caller-allocated with
+ * `capacity` entries (max_iters, or outer*inner for cgls_tv). */
+typedef struct {
+    int capacity;
+    double* implicit_residual;
+    double* explicit_residual;
+    double* relative_error;
+    double* lambda;
+    int* outer_starts;  /* cgls_tv; capacity >= outer iterations */
+    int iterations;     /* entries written to implicit/explicit */
+    int n_relative_error;
+    int n_lambda;
+    int n_outer_starts;
+    int iterations_run;
+    int stop_reason;    /* ctk_stop_reason */
+    int stored_domain_basis;
+    int stored_range_basis;
+} ctk_solve_log;
+
+/* HybridStrategy, hybrid.hpp:15-33 */
+typedef struct {
+    int kind;            /* ctk_lambda_strategy */
+    double lambda;       /* fixed */
+    double noise_level;  /* dp */
+} ctk_hybrid_strategy;
+
+/* Host-pointer solvers (the reference's signatures: pair = (geom, variant)). */
+int ctk_cgls_f32(ctk_geom* g, int variant, const float* h_b, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_cgls_f64(ctk_geom* g, int variant, const double* h_b, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
+int ctk_lsqr_f32(ctk_geom* g, int variant, const float* h_b, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_lsqr_f64(ctk_geom* g, int variant, const double* h_b, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
+int ctk_lsmr_f32(ctk_geom* g, int variant, const float* h_b, double lambda, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_lsmr_f64(ctk_geom* g, int variant, const double* h_b, double lambda, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
+int ctk_hybrid_lsqr_f32(ctk_geom* g, int variant, const float* h_b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_hybrid_lsqr_f64(ctk_geom* g, int variant, const double* h_b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
+int ctk_cgls_tv_f32(ctk_geom* g, int variant, const float* h_b, double lambda, int outer_iters, int inner_iters, const ctk_solver_opts* o, int warm_start, float* h_x, ctk_solve_log* log);
+int ctk_cgls_tv_f64(ctk_geom* g, int variant, const double* h_b, double lambda, int outer_iters, int inner_iters, const ctk_solver_opts* o, int warm_start, double* h_x, ctk_solve_log* log);
+
+/* Device-resident variants: b and x are DEVICE pointers; identical semantics.
+ * solver: 0 cgls, 1 lsqr, 2 lsmr, 3 hybrid_lsqr, 4 cgls_tv.  `lambda` is the LSMR
+ * damping / TV weight; hybrid reads `s`; cgls_tv reads outer/inner/warm_start. */
+int ctk_solve_dev_f32(ctk_geom* g, int solver, int variant, const float* d_b, double lambda,
+                      const ctk_hybrid_strategy* s, int outer_iters, int inner_iters, int warm_start,
+                      const ctk_solver_opts* o, float* d_x, ctk_solve_log* log);
+int ctk_solve_dev_f64(ctk_geom* g, int solver, int variant, const double* d_b, double lambda,
+                      const ctk_hybrid_strategy* s, int outer_iters, int inner_iters, int warm_start,
+                      const ctk_solver_opts* o, double* d_x, ctk_solve_log* log);
+
+/* ---- multi-GPU angle sharding ------------------------------------- */
+/* Contiguous angle block of rank r among G ranks: [first, first+count). */
+int ctk_shard_angles(int n_angles, int nranks, int rank, int* first, int* count);
+/* Collectives as callbacks (NCCL below, or any transport e.g. torch.distributed).
+ * allreduce_sum: in-place sum of `count` elements (dtype 0=f32, 1=f64) of a DEVICE buffer
+ * on `stream`; allgather_f64: gathers one host double per rank into out[nranks]. */
+typedef struct {
+    int rank, nranks;
+    int (*allreduce_sum)(void* d_buf, size_t count, int dtype, void* stream, void* user);
+    int (*allgather_f64)(double value, double* h_out, void* user);
+    void* user;
+} ctk_comm_callbacks;
+int ctk_comm_create(const ctk_comm_callbacks* cb, ctk_comm** out);
+/* NCCL (dlopen'd libnccl.so.2): unique id is 128 bytes, exchanged by the caller. */
+int ctk_nccl_get_unique_id(void* out128);
+int ctk_comm_create_nccl(const void* id128, int nranks, int rank, ctk_comm** out);
+void ctk_comm_destroy(ctk_comm* c);
+/* Attach a communicator: the handle's angles are this rank's shard; A^T b partial
+ * volumes are sum-reduced and range-space dots are summed over ranks in rank order. */
+int ctk_geom_attach_comm(ctk_geom* g, ctk_comm* c);
+
+/* ---- instrumentation ----------------------------------------------------------------- */
+/* Number of this library's kernel launches since load (for bench gpu_launches). */
+uint64_t ctk_launch_count(void);
+/* Device time of the last ctk_ax_* / ctk_atb_* main kernel on this handle (CUDA events
+ * recorded on its stream around that kernel), ms.  Synchronises the handle's last event. */
+double ctk_geom_last_kernel_ms(ctk_geom* g);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTK_B200_H */

@@ -1,0 +1,566 @@
+"""Python mirror of the reference's public API for the Ax / A^T b hot path.
+
+Names, argument meaning and error behaviour follow ctkrylov (/root/reference/proj):
+
+=====================================  ==================================================
+this module                            reference
+=====================================  ==================================================
+``BeamMode``, ``ConeGeometry``         geometry.hpp:11, 24-55
+``equidistant_angles``                 geometry.hpp:57-64
+``default_geometry``                   geometry.hpp:66-87
+``canonical_angle``                    types.hpp:172-177
+``VolumeShape``                        types.hpp:35-41
+error classes                          types.hpp:14-31
+``BackprojectVariant``                 projector.hpp:16
+``forward_project`` / ``back_project`` projector.hpp:134-162, 283-297
+``OperatorPair`` / ``projector_pair``  operators.hpp:18-45, 91-115
+``SolverOptions`` / ``SolveResult``    solve_log.hpp:28-76
+``cgls`` ``lsqr`` ``lsmr``             solvers.hpp:13-231
+``HybridStrategy`` / ``hybrid_lsqr``   hybrid.hpp:15-33, 76-116
+``cgls_tv``                            tv.hpp:45-110
+=====================================  ==================================================
+
+Every computation runs in libctk_b200.so (sm_100a kernels + C++ solvers) through the
+C-ABI; there is no CPU path.  Host (numpy) inputs use the OperatorPair host-span
+semantics (copies in and out per call); CUDA torch tensors use the device-resident entry
+points.  dtype float32 selects the performance kernels, float64 the exact-parity kernels.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ---- errors (types.hpp:14-31) --------------------------------------------------------------
+class CtkError(RuntimeError):
+    pass
+
+
+class DimensionError(CtkError):
+    pass
+
+
+class GeometryError(CtkError):
+    pass
+
+
+class ParameterError(CtkError):
+    pass
+
+
+class DegenerateInputError(CtkError):
+    pass
+
+
+class NumericalError(CtkError):
+    def __init__(self, msg, iteration):
+        super().__init__(msg)
+        self.iteration = iteration
+
+
+class CudaError(CtkError):
+    pass
+
+
+class UnsupportedError(CtkError):
+    pass
+
+
+_ERR = {
+    L.CTK_E_DIMENSION: DimensionError,
+    L.CTK_E_GEOMETRY: GeometryError,
+    L.CTK_E_PARAMETER: ParameterError,
+    L.CTK_E_DEGENERATE: DegenerateInputError,
+    L.CTK_E_CUDA: CudaError,
+    L.CTK_E_UNSUPPORTED: UnsupportedError,
+}
+
+
+def _check(rc):
+    if rc == L.CTK_OK:
+        return
+    code, msg, it = L.last_error()
+    if rc == L.CTK_E_NUMERICAL:
+        raise NumericalError(msg, it)
+    raise _ERR.get(rc, CtkError)(msg)
+
+
+# ---- geometry -------------------------------------------------------------------------------
+class BeamMode(IntEnum):
+    parallel2d = 0
+    parallel3d = 1
+    cone3d = 2
+
+
+class BackprojectVariant(IntEnum):
+    matched = 0
+    voxel_driven = 1
+
+
+class ProjectorKind(IntEnum):
+    joseph = 0
+    siddon = 1
+
+
+class StopReason(IntEnum):
+    max_iters = 0
+    residual_increase = 1
+    tolerance = 2
+    breakdown = 3
+
+
+class LambdaStrategy(IntEnum):
+    fixed = 0
+    dp = 1
+    gcv = 2
+
+
+TWO_PI = 2.0 * math.pi
+
+
+def canonical_angle(a: float) -> float:
+    r = math.fmod(a, TWO_PI)
+    if r < 0.0:
+        r += TWO_PI
+    return r
+
+
+@dataclass
+class VolumeShape:
+    nx: int = 0
+    ny: int = 0
+    nz: int = 0
+    spacing: float = 1.0
+
+    def size(self) -> int:
+        return self.nx * self.ny * self.nz
+
+
+@dataclass
+class ConeGeometry:
+    mode: BeamMode = BeamMode.parallel2d
+    source_to_origin: float = 0.0
+    origin_to_detector: float = 0.0
+    detector_pixel_size: float = 1.0
+    nu: int = 0
+    nv: int = 0
+    vol: VolumeShape = field(default_factory=VolumeShape)
+    angles: Sequence[float] = field(default_factory=list)
+
+    def proj_shape(self):
+        return (len(self.angles), self.nu, self.nv)
+
+    def validate(self):
+        """ConeGeometry::validate (geometry.hpp:35-54)."""
+        v = self.vol
+        if len(self.angles) == 0:
+            raise GeometryError("geometry needs at least one angle")
+        if self.nu <= 0 or self.nv <= 0:
+            raise GeometryError("detector pixel counts must be positive")
+        if not self.detector_pixel_size > 0.0:
+            raise GeometryError("detector pixel size must be positive")
+        if not self.origin_to_detector > 0.0:
+            raise GeometryError("origin-to-detector distance must be positive")
+        if v.nx <= 0 or v.ny <= 0 or v.nz <= 0 or not v.spacing > 0.0:
+            raise GeometryError("geometry volume descriptor invalid")
+        if self.mode == BeamMode.parallel2d and (v.nz != 1 or self.nv != 1):
+            raise GeometryError("parallel2d requires nz = 1 and nv = 1")
+        if self.mode == BeamMode.cone3d:
+            if not self.source_to_origin > 0.0:
+                raise GeometryError("cone3d requires a positive source-to-origin distance")
+            hx, hy, hz = 0.5 * v.nx * v.spacing, 0.5 * v.ny * v.spacing, 0.5 * v.nz * v.spacing
+            if self.source_to_origin <= math.sqrt(hx * hx + hy * hy + hz * hz):
+                raise GeometryError("cone3d source lies inside the volume diagonal")
+
+    def desc(self):
+        ang = np.ascontiguousarray(np.asarray(self.angles, dtype=np.float64))
+        d = L.GeomDesc(int(self.mode), float(self.source_to_origin), float(self.origin_to_detector),
+                       float(self.detector_pixel_size), int(self.nu), int(self.nv), int(self.vol.nx),
+                       int(self.vol.ny), int(self.vol.nz), float(self.vol.spacing), len(ang),
+                       ang.ctypes.data_as(C.POINTER(C.c_double)))
+        d._keep = ang
+        return d
+
+    def subset(self, first: int, count: int) -> "ConeGeometry":
+        return ConeGeometry(self.mode, self.source_to_origin, self.origin_to_detector, self.detector_pixel_size,
+                            self.nu, self.nv, VolumeShape(self.vol.nx, self.vol.ny, self.vol.nz, self.vol.spacing),
+                            list(np.asarray(self.angles, dtype=np.float64)[first:first + count]))
+
+
+def equidistant_angles(n: int, start_rad: float = 0.0, range_rad: float = TWO_PI):
+    """geometry.hpp:57-64."""
+    if n <= 0:
+        raise GeometryError("angle count must be positive")
+    return [canonical_angle(start_rad + range_rad * i / n) for i in range(n)]
+
+
+def default_geometry(mode: BeamMode, vol: VolumeShape, n_angles: int, range_rad: float = TWO_PI) -> ConeGeometry:
+    """geometry.hpp:66-87."""
+    g = ConeGeometry(mode=BeamMode(mode), vol=vol, angles=equidistant_angles(n_angles, 0.0, range_rad))
+    n = max(vol.nx, vol.ny, vol.nz)
+    if g.mode == BeamMode.cone3d:
+        g.source_to_origin = 2.0 * n * vol.spacing
+        g.origin_to_detector = 1.0 * n * vol.spacing
+        g.detector_pixel_size = 1.5 * vol.spacing
+        g.nu = g.nv = (3 * n) // 2
+    else:
+        g.origin_to_detector = 1.0 * n * vol.spacing
+        g.detector_pixel_size = vol.spacing
+        g.nu = (3 * n) // 2
+        g.nv = 1 if g.mode == BeamMode.parallel2d else (3 * vol.nz) // 2
+    g.validate()
+    return g
+
+
+# ---- native projector handle ----------------------------------------------------------------
+def _is_torch_cuda(a) -> bool:
+    return type(a).__module__.startswith("torch") and getattr(a, "is_cuda", False)
+
+
+def _numel(a) -> int:
+    return int(a.size) if isinstance(a, np.ndarray) else int(a.numel())
+
+
+def _torch_stream():
+    import torch
+
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class Projector:
+    """Owns one native ctk_geom handle (validated geometry + device tables + workspace)."""
+
+    def __init__(self, geom: ConeGeometry, projector: ProjectorKind = ProjectorKind.joseph, bp_partitions: int = 1):
+        geom.validate()
+        self.geom = geom
+        self.lib = L.load()
+        h = C.c_void_p()
+        _check(self.lib.ctk_geom_create(C.byref(geom.desc()), C.byref(h)))
+        self.handle = h
+        if projector != ProjectorKind.joseph:
+            _check(self.lib.ctk_geom_set_projector(h, int(projector)))
+        if bp_partitions != 1:
+            _check(self.lib.ctk_geom_set_bp_partitions(h, int(bp_partitions)))
+        ds, rs = C.c_size_t(), C.c_size_t()
+        _check(self.lib.ctk_geom_sizes(h, C.byref(ds), C.byref(rs)))
+        self.domain_size, self.range_size = ds.value, rs.value
+        self._comm = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self.lib.ctk_geom_destroy(h)
+            self.handle = None
+
+    def attach_comm(self, comm):
+        _check(self.lib.ctk_geom_attach_comm(self.handle, comm.handle))
+        self._comm = comm
+
+    def last_kernel_ms(self) -> float:
+        return float(self.lib.ctk_geom_last_kernel_ms(self.handle))
+
+    @staticmethod
+    def _suffix(dtype):
+        dt = np.dtype(str(dtype).replace("torch.", ""))
+        if dt == np.float32:
+            return "f32"
+        if dt == np.float64:
+            return "f64"
+        raise ParameterError(f"unsupported dtype {dtype}; use float32 or float64")
+
+    def forward(self, x, y, stream=None):
+        """y <- A x (overwrites y).  numpy -> host entry point; CUDA tensors -> device."""
+        if _numel(x) != self.domain_size or _numel(y) != self.range_size:
+            raise DimensionError("operator domain size mismatch")
+        t = self._suffix(x.dtype)
+        if _is_torch_cuda(x):
+            _check(getattr(self.lib, f"ctk_ax_{t}")(self.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                                     stream if stream is not None else _torch_stream()))
+        else:
+            _check(getattr(self.lib, f"ctk_ax_host_{t}")(self.handle, x.ctypes.data_as(C.c_void_p), y.ctypes.data_as(C.c_void_p)))
+
+    def back(self, y, x, variant=BackprojectVariant.matched, stream=None):
+        if _numel(y) != self.range_size or _numel(x) != self.domain_size:
+            raise DimensionError("operator range size mismatch")
+        t = self._suffix(y.dtype)
+        if _is_torch_cuda(y):
+            _check(getattr(self.lib, f"ctk_atb_{t}")(self.handle, int(variant), C.c_void_p(y.data_ptr()),
+                                                      C.c_void_p(x.data_ptr()), stream if stream is not None else _torch_stream()))
+        else:
+            _check(getattr(self.lib, f"ctk_atb_host_{t}")(self.handle, int(variant), y.ctypes.data_as(C.c_void_p),
+                                                           x.ctypes.data_as(C.c_void_p)))
+
+    def residual2(self, x, b) -> float:
+        """||A x - b||^2 without storing A x (float32 CUDA tensors)."""
+        out = C.c_double()
+        _check(self.lib.ctk_ax_residual_f32(self.handle, C.c_void_p(x.data_ptr()), C.c_void_p(b.data_ptr()),
+                                            C.byref(out), _torch_stream()))
+        return out.value
+
+
+def _empty_like(a, n):
+    if _is_torch_cuda(a):
+        import torch
+
+        return torch.empty(n, dtype=a.dtype, device=a.device)
+    return np.empty(n, dtype=a.dtype)
+
+
+def _host(a, dtype=None):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a
+
+
+# ---- OperatorPair (operators.hpp:18-45) -----------------------------------------------------
+@dataclass
+class OperatorPair:
+    domain_size: int
+    range_size: int
+    matched: bool
+    domain_shape: VolumeShape
+    forward: Callable  # forward(x, y): y <- A x, overwrites y
+    back: Callable     # back(y, x):   x <- B y, overwrites x
+    dtype: np.dtype = np.dtype(np.float32)
+    projector: Optional[Projector] = None
+    variant: BackprojectVariant = BackprojectVariant.matched
+
+    def check_domain(self, n):
+        if n != self.domain_size:
+            raise DimensionError("operator domain size mismatch")
+
+    def check_range(self, n):
+        if n != self.range_size:
+            raise DimensionError("operator range size mismatch")
+
+    def apply_forward(self, x):
+        self.check_domain(x.size if isinstance(x, np.ndarray) else x.numel())
+        y = _empty_like(x, self.range_size)
+        self.forward(x, y)
+        return y
+
+    def apply_back(self, y):
+        self.check_range(y.size if isinstance(y, np.ndarray) else y.numel())
+        x = _empty_like(y, self.domain_size)
+        self.back(y, x)
+        return x
+
+
+def projector_pair(geom: ConeGeometry, variant: BackprojectVariant = BackprojectVariant.matched,
+                   dtype=np.float32, projector: ProjectorKind = ProjectorKind.joseph,
+                   bp_partitions: int = 1) -> OperatorPair:
+    """operators.hpp:91-115 -- the projector pair of a geometry, backed by the sm_100a kernels."""
+    geom.validate()
+    canon = ConeGeometry(geom.mode, geom.source_to_origin, geom.origin_to_detector, geom.detector_pixel_size,
+                         geom.nu, geom.nv, geom.vol, [canonical_angle(a) for a in geom.angles])
+    proj = Projector(canon, projector, bp_partitions)
+    v = BackprojectVariant(variant)
+    return OperatorPair(proj.domain_size, proj.range_size, v == BackprojectVariant.matched, canon.vol,
+                        lambda x, y: proj.forward(x, y), lambda y, x: proj.back(y, x, v), np.dtype(dtype), proj, v)
+
+
+def forward_project(vol, geom: ConeGeometry):
+    """projector.hpp:134-162.  Returns the projections as [n_angles, nv, nu]."""
+    p = Projector(geom)
+    x = vol if _is_torch_cuda(vol) else _host(vol).reshape(-1)
+    if _is_torch_cuda(x):
+        x = x.reshape(-1)
+    y = _empty_like(x, p.range_size)
+    p.forward(x, y)
+    return y.reshape(len(geom.angles), geom.nv, geom.nu)
+
+
+def back_project(proj, geom: ConeGeometry, variant: BackprojectVariant = BackprojectVariant.matched):
+    """projector.hpp:283-297.  Returns the volume as [nz, ny, nx]."""
+    n = (proj.size if isinstance(proj, np.ndarray) else proj.numel())
+    if n != len(geom.angles) * geom.nu * geom.nv:
+        raise DimensionError("projection shape does not match geometry descriptor")
+    p = Projector(geom)
+    y = proj.reshape(-1) if _is_torch_cuda(proj) else _host(proj).reshape(-1)
+    x = _empty_like(y, p.domain_size)
+    p.back(y, x, variant)
+    return x.reshape(geom.vol.nz, geom.vol.ny, geom.vol.nx)
+
+
+# ---- solvers --------------------------------------------------------------------------------
+@dataclass
+class SolverOptions:
+    max_iters: int = 100
+    stop_on_explicit_residual_increase: bool = True
+    residual_tolerance: float = 1e-6
+    reorth: bool = True
+    ground_truth: Optional[np.ndarray] = None
+    rng_seed: int = 0
+    iterate_observer: Optional[Callable[[int, np.ndarray], None]] = None
+
+    def validate(self):
+        if self.max_iters < 1:
+            raise ParameterError("max_iters must be >= 1")
+        if self.residual_tolerance < 0.0:
+            raise ParameterError("residual tolerance must be >= 0")
+
+
+@dataclass
+class ConvergenceLog:
+    implicit_residual: list
+    explicit_residual: list
+    relative_error: list
+    lambda_: list
+    solver: str
+    precision: str
+    matched: bool
+
+    def iterations(self):
+        return len(self.explicit_residual)
+
+
+@dataclass
+class SolveResult:
+    x: object
+    shape: VolumeShape
+    iterations_run: int
+    stop_reason: StopReason
+    log: ConvergenceLog
+    outer_starts: list = field(default_factory=list)
+    stored_domain_basis: int = 0
+    stored_range_basis: int = 0
+    warnings: list = field(default_factory=list)
+
+
+@dataclass
+class HybridStrategy:
+    kind: LambdaStrategy = LambdaStrategy.fixed
+    lambda_: float = 0.0
+    noise_level: float = 0.0
+
+    @staticmethod
+    def fixed(lam: float) -> "HybridStrategy":
+        if lam < 0.0:
+            raise ParameterError("fixed lambda must be nonnegative")
+        return HybridStrategy(LambdaStrategy.fixed, lam, 0.0)
+
+    @staticmethod
+    def dp(noise_level: float) -> "HybridStrategy":
+        if not (0.0 < noise_level < 1.0):
+            raise ParameterError("dp strategy needs a noise level in (0,1)")
+        return HybridStrategy(LambdaStrategy.dp, 0.0, noise_level)
+
+    @staticmethod
+    def gcv() -> "HybridStrategy":
+        return HybridStrategy(LambdaStrategy.gcv, 0.0, 0.0)
+
+
+_SOLVER_ID = {"cgls": 0, "lsqr": 1, "lsmr": 2, "hybrid_lsqr": 3, "cgls_tv": 4}
+
+
+def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=None, outer=1, inner=1, warm=False):
+    opts.validate()
+    if pair.projector is None:
+        raise ParameterError(f"{name}: the device solvers need a projector_pair (sm_100a operators)")
+    n_b = b.size if isinstance(b, np.ndarray) else b.numel()
+    pair.check_range(n_b)
+    proj = pair.projector
+    lib = proj.lib
+    dev = _is_torch_cuda(b)
+    t = Projector._suffix(b.dtype)
+    ndt = np.float32 if t == "f32" else np.float64
+    cap = outer * inner if name == "cgls_tv" else opts.max_iters
+    bufs = [np.zeros(cap + 1) for _ in range(4)]
+    starts = np.zeros(outer + 1, dtype=np.int32)
+    log = L.SolveLog(cap, *[a.ctypes.data_as(C.POINTER(C.c_double)) for a in bufs],
+                     starts.ctypes.data_as(C.POINTER(C.c_int)), 0, 0, 0, 0, 0, 0, 0, 0)
+    gt = None
+    if opts.ground_truth is not None:
+        gt = np.ascontiguousarray(np.asarray(opts.ground_truth), dtype=ndt).reshape(-1)
+        pair.check_domain(gt.size)
+    cb = L.OBSERVER()
+    if opts.iterate_observer is not None:
+        user = opts.iterate_observer
+
+        def _obs(k, ptr, n, _u):
+            arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_float if t == "f32" else C.c_double)), shape=(n,))
+            user(k, arr.copy())
+
+        cb = L.OBSERVER(_obs)
+    o = L.SolverOpts(opts.max_iters, int(opts.stop_on_explicit_residual_increase), opts.residual_tolerance,
+                     int(opts.reorth), gt.ctypes.data_as(C.c_void_p) if gt is not None else None, cb, None)
+    st = L.HybridStrategyC(int(strategy.kind), strategy.lambda_, strategy.noise_level) if strategy is not None else None
+    sid = _SOLVER_ID[name]
+    if dev:
+        import torch
+
+        x = torch.empty(pair.domain_size, dtype=b.dtype, device=b.device)
+        torch.cuda.current_stream().synchronize()
+        rc = getattr(lib, f"ctk_solve_dev_{t}")(proj.handle, sid, int(pair.variant), C.c_void_p(b.data_ptr()), lam,
+                                                 C.byref(st) if st is not None else None, outer, inner, int(warm),
+                                                 C.byref(o), C.c_void_p(x.data_ptr()), C.byref(log))
+    else:
+        bh = np.ascontiguousarray(np.asarray(b), dtype=ndt).reshape(-1)
+        x = np.empty(pair.domain_size, dtype=ndt)
+        bp, xp = bh.ctypes.data_as(C.c_void_p), x.ctypes.data_as(C.c_void_p)
+        v = int(pair.variant)
+        if name in ("cgls", "lsqr"):
+            rc = getattr(lib, f"ctk_{name}_{t}")(proj.handle, v, bp, C.byref(o), xp, C.byref(log))
+        elif name == "lsmr":
+            rc = getattr(lib, f"ctk_lsmr_{t}")(proj.handle, v, bp, lam, C.byref(o), xp, C.byref(log))
+        elif name == "hybrid_lsqr":
+            rc = getattr(lib, f"ctk_hybrid_lsqr_{t}")(proj.handle, v, bp, C.byref(st), C.byref(o), xp, C.byref(log))
+        else:
+            rc = getattr(lib, f"ctk_cgls_tv_{t}")(proj.handle, v, bp, lam, outer, inner, C.byref(o), int(warm), xp,
+                                                   C.byref(log))
+    _check(rc)
+    it = log.iterations
+    clog = ConvergenceLog(list(bufs[0][:it]), list(bufs[1][:it]), list(bufs[2][:log.n_relative_error]),
+                          list(bufs[3][:log.n_lambda]), name, "single" if t == "f32" else "double", pair.matched)
+    return SolveResult(x, pair.domain_shape, log.iterations_run, StopReason(log.stop_reason), clog,
+                       list(starts[:log.n_outer_starts]), log.stored_domain_basis, log.stored_range_basis)
+
+
+def cgls(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
+    """solvers.hpp:13-60."""
+    return _solve("cgls", pair, b, opts)
+
+
+def lsqr(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
+    """solvers.hpp:62-126."""
+    return _solve("lsqr", pair, b, opts)
+
+
+def lsmr(pair: OperatorPair, b, lambda_: float, opts: SolverOptions) -> SolveResult:
+    """solvers.hpp:128-231."""
+    opts.validate()
+    if lambda_ < 0.0:
+        raise ParameterError("lsmr: lambda must be nonnegative")
+    return _solve("lsmr", pair, b, opts, lam=lambda_)
+
+
+def hybrid_lsqr(pair: OperatorPair, b, strategy: HybridStrategy, opts: SolverOptions) -> SolveResult:
+    """hybrid.hpp:76-116."""
+    return _solve("hybrid_lsqr", pair, b, opts, strategy=strategy)
+
+
+def cgls_tv(pair: OperatorPair, b, lambda_: float, outer_iters: int, inner_iters: int, opts: SolverOptions,
+            warm_start: bool = False) -> SolveResult:
+    """tv.hpp:45-110."""
+    return _solve("cgls_tv", pair, b, opts, lam=lambda_, outer=outer_iters, inner=inner_iters, warm=warm_start)
+
+
+# ---- synthetic input (phantom.hpp:74-145), generated on the device ---------------------------
+def shepp_logan_3d(n: int, dtype="float32", device="cuda"):
+    import torch
+
+    t = torch.empty(n * n * n, dtype=getattr(torch, dtype), device=device)
+    lib = L.load()
+    suf = "f32" if dtype == "float32" else "f64"
+    _check(getattr(lib, f"ctk_shepp_logan_3d_{suf}")(n, C.c_void_p(t.data_ptr()), _torch_stream()))
+    return t
+
+
+def launch_count() -> int:
+    return int(L.load().ctk_launch_count())

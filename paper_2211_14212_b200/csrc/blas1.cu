@@ -1,0 +1,286 @@
+// Fused single-pass BLAS-1 for the solvers (types.hpp:136-158 and the inline vector
+// loops of solvers.hpp / krylov.hpp / gmres.hpp).  HBM-bound; every reduction accumulates
+// in fp64 over a FIXED partition (kRedBlocks contiguous chunks, fixed shuffle tree,
+// fixed-order finish) so results are bitwise run-to-run deterministic
+// (test_solvers.cpp:436-451 asks for identical logs).  Vectorised 16-byte loads when the
+// pointers allow it.
+#include "ctk_internal.h"
+#include "reduce.cuh"
+
+namespace ctkb {
+namespace {
+
+__global__ void k_finish_sum(const double* __restrict__ p, int n, double* __restrict__ out) {
+    double v = 0.0;
+    // each thread sums a contiguous run, then the fixed block tree
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = threadIdx.x * per, e = min(n, b + per);
+    for (int i = b; i < e; ++i) v += p[i];
+    v = block_sum(v);
+    if (threadIdx.x == 0) *out = v;
+}
+
+__global__ void k_finish_max(const double* __restrict__ p, int n, double* __restrict__ out) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) v = fmax(v, p[i]);
+    v = block_max(v);
+    if (threadIdx.x == 0) *out = v;
+}
+
+struct Chunk {
+    size_t b, e;
+};
+__device__ __forceinline__ Chunk my_chunk(size_t n) {
+    const size_t per = (n + gridDim.x - 1) / gridDim.x;
+    const size_t b = min(n, size_t(blockIdx.x) * per);
+    return {b, min(n, b + per)};
+}
+
+template <class T, class F>
+__device__ __forceinline__ double chunk_reduce(size_t n, F f) {
+    const Chunk c = my_chunk(n);
+    double acc = 0.0;
+    for (size_t i = c.b + threadIdx.x; i < c.e; i += blockDim.x) acc += f(i);
+    return block_sum(acc);
+}
+
+template <class T>
+__global__ void k_dot(size_t n, const T* __restrict__ a, const T* __restrict__ b, double* __restrict__ part) {
+    const double r = chunk_reduce<T>(n, [&](size_t i) { return double(a[i]) * double(b[i]); });
+    if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+template <class T>
+__global__ void k_diff_nrm2sq(size_t n, const T* __restrict__ a, const T* __restrict__ b, double* __restrict__ part) {
+    const double r = chunk_reduce<T>(n, [&](size_t i) {
+        const double d = double(a[i]) - double(b[i]);
+        return d * d;
+    });
+    if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+template <class T>
+__global__ void k_axpy_nrm2sq(size_t n, T alpha, const T* __restrict__ x, T* __restrict__ y, double* __restrict__ part) {
+    const double r = chunk_reduce<T>(n, [&](size_t i) {
+        const T v = y[i] + alpha * x[i];
+        y[i] = v;
+        return double(v) * double(v);
+    });
+    if (threadIdx.x == 0) part[blockIdx.x] = r;
+}
+
+template <class T>
+__global__ void k_absmax(size_t n, const T* __restrict__ x, double* __restrict__ part) {
+    const Chunk c = my_chunk(n);
+    double m = 0.0;
+    for (size_t i = c.b + threadIdx.x; i < c.e; i += blockDim.x) m = fmax(m, fabs(double(x[i])));
+    m = block_max(m);
+    if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+template <class T, class F>
+__global__ void k_map(size_t n, F f) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) f(i);
+}
+
+template <class T>
+struct AxpyF {
+    T a;
+    const T* x;
+    T* y;
+    __device__ void operator()(size_t i) const { y[i] += a * x[i]; }
+};
+template <class T>
+struct XpbyF {
+    const T* x;
+    T b;
+    T* y;
+    __device__ void operator()(size_t i) const { y[i] = x[i] + b * y[i]; }
+};
+template <class T>
+struct ScalF {
+    T a;
+    T* x;
+    __device__ void operator()(size_t i) const { x[i] *= a; }
+};
+template <class T>
+struct ScaleCopyF {
+    T a;
+    const T* x;
+    T* y;
+    __device__ void operator()(size_t i) const { y[i] = a * x[i]; }
+};
+template <class T>
+struct LsqrF {
+    T c1, c2;
+    T* x;
+    T* w;
+    const T* v;
+    __device__ void operator()(size_t i) const {
+        const T wi = w[i];
+        x[i] += c1 * wi;
+        w[i] = v[i] - c2 * wi;
+    }
+};
+template <class T>
+struct LsmrF {
+    T c1, c2, c3;
+    T* x;
+    T* h;
+    T* hbar;
+    const T* v;
+    __device__ void operator()(size_t i) const {
+        const T hi = h[i];
+        const T hb = hi - c1 * hbar[i];
+        hbar[i] = hb;
+        x[i] += c2 * hb;
+        h[i] = v[i] - c3 * hi;
+    }
+};
+template <class T>
+struct FillF {
+    T v;
+    T* x;
+    __device__ void operator()(size_t i) const { x[i] = v; }
+};
+
+template <class T, class F>
+void run_map(size_t n, F f, cudaStream_t s, const char* what) {
+    if (n == 0) return;
+    const size_t blocks = std::min<size_t>((n + 255) / 256, size_t(148) * 16);
+    k_map<T, F><<<unsigned(blocks), 256, 0, s>>>(n, f);
+    after_launch(what);
+}
+
+// block_dot: coef[i] = <basis_i, w>, partials[i][blk] then a fixed-order finish per i
+template <class T>
+__global__ void k_block_dot(size_t n, int m, const T* __restrict__ basis, size_t ld, const T* __restrict__ w,
+                            double* __restrict__ part) {
+    const Chunk c = my_chunk(n);
+    for (int q = 0; q < m; ++q) {
+        const T* bq = basis + size_t(q) * ld;
+        double acc = 0.0;
+        for (size_t i = c.b + threadIdx.x; i < c.e; i += blockDim.x) acc += double(bq[i]) * double(w[i]);
+        acc = block_sum(acc);
+        if (threadIdx.x == 0) part[size_t(q) * gridDim.x + blockIdx.x] = acc;
+    }
+}
+
+__global__ void k_finish_many(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+    const double* p = part + size_t(blockIdx.x) * nblk;
+    double v = 0.0;
+    const int per = (nblk + blockDim.x - 1) / blockDim.x;
+    const int b = threadIdx.x * per, e = min(nblk, b + per);
+    for (int i = b; i < e; ++i) v += p[i];
+    v = block_sum(v);
+    if (threadIdx.x == 0) out[blockIdx.x] = v;
+}
+
+template <class T>
+__global__ void k_block_axpy(size_t n, int m, double alpha, const double* __restrict__ coef, const T* __restrict__ basis,
+                             size_t ld, T* __restrict__ w) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        T acc = w[i];
+        for (int q = 0; q < m; ++q) acc += T(alpha * coef[q]) * basis[size_t(q) * ld + i];
+        w[i] = acc;
+    }
+}
+
+}  // namespace
+
+void finish_sum(const double* partials, int n, double* d_out, cudaStream_t s) {
+    k_finish_sum<<<1, 256, 0, s>>>(partials, n, d_out);
+    after_launch("k_finish_sum");
+}
+void finish_max(const double* partials, int n, double* d_out, cudaStream_t s) {
+    k_finish_max<<<1, 256, 0, s>>>(partials, n, d_out);
+    after_launch("k_finish_max");
+}
+
+template <class T>
+void reduce_dot(size_t n, const T* a, const T* b, double* d_res, RedWork w, cudaStream_t s) {
+    k_dot<T><<<kRedBlocks, kRedThreads, 0, s>>>(n, a, b, w.partials);
+    after_launch("k_dot");
+    finish_sum(w.partials, kRedBlocks, d_res, s);
+}
+template <class T>
+void reduce_diff_nrm2sq(size_t n, const T* a, const T* b, double* d_res, RedWork w, cudaStream_t s) {
+    k_diff_nrm2sq<T><<<kRedBlocks, kRedThreads, 0, s>>>(n, a, b, w.partials);
+    after_launch("k_diff_nrm2sq");
+    finish_sum(w.partials, kRedBlocks, d_res, s);
+}
+template <class T>
+void axpy_nrm2sq(size_t n, double alpha, const T* x, T* y, double* d_res, RedWork w, cudaStream_t s) {
+    k_axpy_nrm2sq<T><<<kRedBlocks, kRedThreads, 0, s>>>(n, T(alpha), x, y, w.partials);
+    after_launch("k_axpy_nrm2sq");
+    finish_sum(w.partials, kRedBlocks, d_res, s);
+}
+template <class T>
+void reduce_absmax(size_t n, const T* x, double* d_res, RedWork w, cudaStream_t s) {
+    k_absmax<T><<<kRedBlocks, kRedThreads, 0, s>>>(n, x, w.partials);
+    after_launch("k_absmax");
+    finish_max(w.partials, kRedBlocks, d_res, s);
+}
+template <class T>
+void axpy(size_t n, double alpha, const T* x, T* y, cudaStream_t s) {
+    run_map<T>(n, AxpyF<T>{T(alpha), x, y}, s, "k_axpy");
+}
+template <class T>
+void xpby(size_t n, const T* x, double beta, T* y, cudaStream_t s) {
+    run_map<T>(n, XpbyF<T>{x, T(beta), y}, s, "k_xpby");
+}
+template <class T>
+void scal(size_t n, double alpha, T* x, cudaStream_t s) {
+    run_map<T>(n, ScalF<T>{T(alpha), x}, s, "k_scal");
+}
+template <class T>
+void scale_copy(size_t n, double alpha, const T* x, T* y, cudaStream_t s) {
+    run_map<T>(n, ScaleCopyF<T>{T(alpha), x, y}, s, "k_scale_copy");
+}
+template <class T>
+void lsqr_update(size_t n, double c1, double c2, T* x, T* w, const T* v, cudaStream_t s) {
+    run_map<T>(n, LsqrF<T>{T(c1), T(c2), x, w, v}, s, "k_lsqr_update");
+}
+template <class T>
+void lsmr_update(size_t n, double c1, double c2, double c3, T* x, T* h, T* hbar, const T* v, cudaStream_t s) {
+    run_map<T>(n, LsmrF<T>{T(c1), T(c2), T(c3), x, h, hbar, v}, s, "k_lsmr_update");
+}
+template <class T>
+void fill(size_t n, T v, T* x, cudaStream_t s) {
+    run_map<T>(n, FillF<T>{v, x}, s, "k_fill");
+}
+template <class T>
+void block_dot(size_t n, int m, const T* basis, size_t ld, const T* w, double* d_coef, double* scratch, cudaStream_t s) {
+    if (m <= 0) return;
+    k_block_dot<T><<<kRedBlocks, kRedThreads, 0, s>>>(n, m, basis, ld, w, scratch);
+    after_launch("k_block_dot");
+    k_finish_many<<<m, 256, 0, s>>>(scratch, kRedBlocks, d_coef);
+    after_launch("k_finish_many");
+}
+template <class T>
+void block_axpy(size_t n, int m, double alpha, const double* d_coef, const T* basis, size_t ld, T* w, cudaStream_t s) {
+    if (m <= 0) return;
+    const size_t blocks = std::min<size_t>((n + 255) / 256, size_t(148) * 16);
+    k_block_axpy<T><<<unsigned(blocks), 256, 0, s>>>(n, m, alpha, d_coef, basis, ld, w);
+    after_launch("k_block_axpy");
+}
+
+#define CTK_INST(T)                                                                                        \
+    template void reduce_dot<T>(size_t, const T*, const T*, double*, RedWork, cudaStream_t);              \
+    template void reduce_diff_nrm2sq<T>(size_t, const T*, const T*, double*, RedWork, cudaStream_t);      \
+    template void axpy_nrm2sq<T>(size_t, double, const T*, T*, double*, RedWork, cudaStream_t);           \
+    template void reduce_absmax<T>(size_t, const T*, double*, RedWork, cudaStream_t);                     \
+    template void axpy<T>(size_t, double, const T*, T*, cudaStream_t);                                    \
+    template void xpby<T>(size_t, const T*, double, T*, cudaStream_t);                                    \
+    template void scal<T>(size_t, double, T*, cudaStream_t);                                              \
+    template void scale_copy<T>(size_t, double, const T*, T*, cudaStream_t);                              \
+    template void lsqr_update<T>(size_t, double, double, T*, T*, const T*, cudaStream_t);                 \
+    template void lsmr_update<T>(size_t, double, double, double, T*, T*, T*, const T*, cudaStream_t);     \
+    template void fill<T>(size_t, T, T*, cudaStream_t);                                                   \
+    template void block_dot<T>(size_t, int, const T*, size_t, const T*, double*, double*, cudaStream_t);  \
+    template void block_axpy<T>(size_t, int, double, const double*, const T*, size_t, T*, cudaStream_t);
+CTK_INST(float)
+CTK_INST(double)
+#undef CTK_INST
+
+}  // namespace ctkb

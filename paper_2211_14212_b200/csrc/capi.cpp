@@ -1,0 +1,358 @@
+// extern "C" surface of libctk_b200.so (include/ctk_b200.h).  Every entry point catches
+// the internal exceptions and returns the status of the reference's error taxonomy
+// (types.hpp:14-31); the message is kept thread-locally for ctk_last_error.
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "ctk_internal.h"
+
+namespace ctkb {
+Geometry* geometry_create(const ctk_geom_desc* d);
+void nccl_unique_id(void* out128);
+Comm* comm_create_nccl(const void* id128, int nranks, int rank);
+void comm_destroy(Comm* c);
+template <class T>
+void solve_device(Geometry& g, int solver, int variant, const T* d_b, double lambda, const ctk_hybrid_strategy* st,
+                  int outer, int inner, int warm, const ctk_solver_opts* o, T* d_x, ctk_solve_log* log);
+}  // namespace ctkb
+
+// ctk_geom / ctk_comm stay incomplete: the handles are ctkb::Geometry* / ctkb::Comm*.
+namespace {
+
+thread_local std::string t_msg;
+thread_local int t_code = 0;
+thread_local int t_iter = 0;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return CTK_OK;
+    } catch (const ctkb::Error& e) {
+        t_msg = e.what();
+        t_code = e.code;
+        t_iter = e.iteration;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        t_msg = "host allocation failed";
+        t_code = CTK_E_PARAMETER;
+        return t_code;
+    } catch (const std::exception& e) {
+        t_msg = e.what();
+        t_code = CTK_E_PARAMETER;
+        return t_code;
+    }
+}
+
+ctkb::Geometry& G(const ctk_geom* g) {
+    if (!g) ctkb::fail(CTK_E_PARAMETER, "null geometry handle");
+    return *reinterpret_cast<ctkb::Geometry*>(const_cast<ctk_geom*>(g));
+}
+
+cudaStream_t S(ctkb::Geometry& g, void* stream) { return stream ? static_cast<cudaStream_t>(stream) : g.stream; }
+
+void check_variant(int v) {
+    if (v != CTK_BP_MATCHED && v != CTK_BP_VOXEL_DRIVEN) ctkb::fail(CTK_E_PARAMETER, "unknown backprojector variant");
+}
+
+template <class T>
+void ax_dev(ctkb::Geometry& g, const T* x, T* y, cudaStream_t s) {
+    g.require_angles();
+    if (g.projector != CTK_PROJ_JOSEPH) ctkb::fail(CTK_E_UNSUPPORTED, "Siddon projector is not built in this round");
+    if constexpr (sizeof(T) == 4) ctkb::ax_f32(g, x, y, s);
+    else {
+        CTK_CUDA(cudaEventRecord(g.ev0, s));
+        ctkb::launch_ax_exact_f64(g, x, y, s);
+        CTK_CUDA(cudaEventRecord(g.ev1, s));
+    }
+}
+
+template <class T>
+void atb_dev(ctkb::Geometry& g, int variant, const T* y, T* x, cudaStream_t s) {
+    g.require_angles();
+    check_variant(variant);
+    if (g.projector != CTK_PROJ_JOSEPH) ctkb::fail(CTK_E_UNSUPPORTED, "Siddon projector is not built in this round");
+    if constexpr (sizeof(T) == 4) {
+        if (variant == CTK_BP_MATCHED) ctkb::atb_matched_f32(g, y, x, s);
+        else ctkb::atb_voxel_f32(g, y, x, s);
+    } else {
+        CTK_CUDA(cudaEventRecord(g.ev0, s));
+        if (variant == CTK_BP_MATCHED) ctkb::launch_atb_matched_exact_f64(g, y, x, s);
+        else ctkb::launch_atb_voxel_f64(g, y, x, s);
+        CTK_CUDA(cudaEventRecord(g.ev1, s));
+    }
+    if (g.comm) ctkb::comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
+}
+
+template <class T>
+void ax_host(ctkb::Geometry& g, const T* hx, T* hy) {
+    const size_t nd = g.domain(), nr = g.range();
+    g.host_x.ensure(sizeof(T) * nd);
+    g.host_y.ensure(sizeof(T) * nr);
+    CTK_CUDA(cudaMemcpyAsync(g.host_x.p, hx, sizeof(T) * nd, cudaMemcpyHostToDevice, g.stream));
+    ax_dev<T>(g, g.host_x.as<T>(), g.host_y.as<T>(), g.stream);
+    CTK_CUDA(cudaMemcpyAsync(hy, g.host_y.p, sizeof(T) * nr, cudaMemcpyDeviceToHost, g.stream));
+    CTK_CUDA(cudaStreamSynchronize(g.stream));
+}
+
+template <class T>
+void atb_host(ctkb::Geometry& g, int variant, const T* hy, T* hx) {
+    const size_t nd = g.domain(), nr = g.range();
+    g.host_x.ensure(sizeof(T) * nd);
+    g.host_y.ensure(sizeof(T) * nr);
+    CTK_CUDA(cudaMemcpyAsync(g.host_y.p, hy, sizeof(T) * nr, cudaMemcpyHostToDevice, g.stream));
+    atb_dev<T>(g, variant, g.host_y.as<T>(), g.host_x.as<T>(), g.stream);
+    CTK_CUDA(cudaMemcpyAsync(hx, g.host_x.p, sizeof(T) * nd, cudaMemcpyDeviceToHost, g.stream));
+    CTK_CUDA(cudaStreamSynchronize(g.stream));
+}
+
+template <class T>
+void solve_host(ctkb::Geometry& g, int solver, int variant, const T* hb, double lambda, const ctk_hybrid_strategy* st,
+                int outer, int inner, int warm, const ctk_solver_opts* o, T* hx, ctk_solve_log* log) {
+    if (!hb || !hx) ctkb::fail(CTK_E_PARAMETER, "null host buffer");
+    const size_t nd = g.domain(), nr = g.range();
+    ctkb::DevBuf db, dx;
+    db.ensure(sizeof(T) * nr);
+    dx.ensure(sizeof(T) * nd);
+    CTK_CUDA(cudaMemcpyAsync(db.p, hb, sizeof(T) * nr, cudaMemcpyHostToDevice, g.stream));
+    ctkb::solve_device<T>(g, solver, variant, db.as<T>(), lambda, st, outer, inner, warm, o, dx.as<T>(), log);
+    CTK_CUDA(cudaMemcpyAsync(hx, dx.p, sizeof(T) * nd, cudaMemcpyDeviceToHost, g.stream));
+    CTK_CUDA(cudaStreamSynchronize(g.stream));
+}
+
+ctkb::RedWork global_work() {
+    static thread_local ctkb::DevBuf buf;
+    buf.ensure(sizeof(double) * (size_t(ctkb::kRedBlocks) * ctkb::kRedSlots + ctkb::kRedSlots));
+    ctkb::RedWork w;
+    w.partials = buf.as<double>();
+    w.results = w.partials + size_t(ctkb::kRedBlocks) * ctkb::kRedSlots;
+    return w;
+}
+
+template <class T>
+void dot_dev(size_t n, const T* x, const T* y, double* out, void* stream) {
+    auto s = static_cast<cudaStream_t>(stream);
+    auto w = global_work();
+    ctkb::reduce_dot<T>(n, x, y, w.results, w, s);
+    CTK_CUDA(cudaMemcpyAsync(out, w.results, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CTK_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int ctk_last_error(char* buf, size_t len) {
+    if (buf && len) {
+        std::strncpy(buf, t_msg.c_str(), len - 1);
+        buf[len - 1] = 0;
+    }
+    return t_code;
+}
+int ctk_last_error_iteration(void) { return t_iter; }
+int ctk_abi_version(void) { return CTK_ABI_VERSION; }
+
+int ctk_geom_create(const ctk_geom_desc* desc, ctk_geom** out) {
+    return guard([&] {
+        if (!out) ctkb::fail(CTK_E_PARAMETER, "null output handle");
+        *out = nullptr;
+        *out = reinterpret_cast<ctk_geom*>(ctkb::geometry_create(desc));
+    });
+}
+void ctk_geom_destroy(ctk_geom* g) { delete reinterpret_cast<ctkb::Geometry*>(g); }
+
+int ctk_geom_sizes(const ctk_geom* g, size_t* d, size_t* r) {
+    return guard([&] {
+        if (d) *d = G(g).domain();
+        if (r) *r = G(g).range();
+    });
+}
+int ctk_geom_set_projector(ctk_geom* g, int p) {
+    return guard([&] {
+        if (p != CTK_PROJ_JOSEPH && p != CTK_PROJ_SIDDON) ctkb::fail(CTK_E_PARAMETER, "unknown projector");
+        G(g).projector = p;
+    });
+}
+int ctk_geom_set_bp_partitions(ctk_geom* g, int n) {
+    return guard([&] {
+        if (n < 1) ctkb::fail(CTK_E_PARAMETER, "partitions must be >= 1");
+        G(g).bp_parts = n;
+    });
+}
+int ctk_geom_set_stream(ctk_geom* g, void* stream) {
+    return guard([&] {
+        auto& gg = G(g);
+        if (gg.own_stream && gg.stream) cudaStreamDestroy(gg.stream);
+        gg.own_stream = false;
+        gg.stream = static_cast<cudaStream_t>(stream);
+        if (!stream) {
+            CTK_CUDA(cudaStreamCreateWithFlags(&gg.stream, cudaStreamNonBlocking));
+            gg.own_stream = true;
+        }
+    });
+}
+
+int ctk_ax_f32(ctk_geom* g, const float* x, float* y, void* s) {
+    return guard([&] { ax_dev<float>(G(g), x, y, S(G(g), s)); });
+}
+int ctk_ax_f64(ctk_geom* g, const double* x, double* y, void* s) {
+    return guard([&] { ax_dev<double>(G(g), x, y, S(G(g), s)); });
+}
+int ctk_atb_f32(ctk_geom* g, int v, const float* y, float* x, void* s) {
+    return guard([&] { atb_dev<float>(G(g), v, y, x, S(G(g), s)); });
+}
+int ctk_atb_f64(ctk_geom* g, int v, const double* y, double* x, void* s) {
+    return guard([&] { atb_dev<double>(G(g), v, y, x, S(G(g), s)); });
+}
+int ctk_ax_residual_f32(ctk_geom* g, const float* x, const float* b, double* out, void* s) {
+    return guard([&] {
+        auto& gg = G(g);
+        gg.require_angles();
+        auto st = S(gg, s);
+        auto w = ctkb::red_work(&gg);
+        ctkb::ax_residual_f32(gg, x, b, w.results, st);
+        CTK_CUDA(cudaMemcpyAsync(gg.pinned, w.results, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CTK_CUDA(cudaStreamSynchronize(st));
+        double v = gg.pinned[0];
+        if (gg.comm) v = ctkb::comm_sum_scalar(gg.comm, v);
+        *out = v;
+    });
+}
+
+int ctk_ax_host_f32(ctk_geom* g, const float* x, float* y) { return guard([&] { ax_host<float>(G(g), x, y); }); }
+int ctk_ax_host_f64(ctk_geom* g, const double* x, double* y) { return guard([&] { ax_host<double>(G(g), x, y); }); }
+int ctk_atb_host_f32(ctk_geom* g, int v, const float* y, float* x) {
+    return guard([&] { atb_host<float>(G(g), v, y, x); });
+}
+int ctk_atb_host_f64(ctk_geom* g, int v, const double* y, double* x) {
+    return guard([&] { atb_host<double>(G(g), v, y, x); });
+}
+
+int ctk_dot_f32(size_t n, const float* x, const float* y, double* out, void* s) {
+    return guard([&] { dot_dev<float>(n, x, y, out, s); });
+}
+int ctk_dot_f64(size_t n, const double* x, const double* y, double* out, void* s) {
+    return guard([&] { dot_dev<double>(n, x, y, out, s); });
+}
+int ctk_nrm2_f32(size_t n, const float* x, double* out, void* s) {
+    return guard([&] {
+        dot_dev<float>(n, x, x, out, s);
+        *out = std::sqrt(*out);
+    });
+}
+int ctk_nrm2_f64(size_t n, const double* x, double* out, void* s) {
+    return guard([&] {
+        dot_dev<double>(n, x, x, out, s);
+        *out = std::sqrt(*out);
+    });
+}
+int ctk_axpy_f32(size_t n, double a, const float* x, float* y, void* s) {
+    return guard([&] { ctkb::axpy<float>(n, a, x, y, static_cast<cudaStream_t>(s)); });
+}
+int ctk_axpy_f64(size_t n, double a, const double* x, double* y, void* s) {
+    return guard([&] { ctkb::axpy<double>(n, a, x, y, static_cast<cudaStream_t>(s)); });
+}
+int ctk_scal_f32(size_t n, double a, float* x, void* s) {
+    return guard([&] { ctkb::scal<float>(n, a, x, static_cast<cudaStream_t>(s)); });
+}
+int ctk_scal_f64(size_t n, double a, double* x, void* s) {
+    return guard([&] { ctkb::scal<double>(n, a, x, static_cast<cudaStream_t>(s)); });
+}
+
+int ctk_shepp_logan_3d_f32(int n, float* out, void* s) {
+    return guard([&] {
+        if (n < 8) ctkb::fail(CTK_E_PARAMETER, "phantom size must be at least 8");
+        ctkb::launch_shepp_logan_f32(n, out, static_cast<cudaStream_t>(s));
+    });
+}
+int ctk_shepp_logan_3d_f64(int n, double* out, void* s) {
+    return guard([&] {
+        if (n < 8) ctkb::fail(CTK_E_PARAMETER, "phantom size must be at least 8");
+        ctkb::launch_shepp_logan_f64(n, out, static_cast<cudaStream_t>(s));
+    });
+}
+
+#define CTK_SOLVE_HOST(NAME, T, SOLVER)                                                                       \
+    int NAME(ctk_geom* g, int variant, const T* b, const ctk_solver_opts* o, T* x, ctk_solve_log* log) {      \
+        return guard([&] { solve_host<T>(G(g), SOLVER, variant, b, 0.0, nullptr, 1, 1, 0, o, x, log); });   \
+    }
+CTK_SOLVE_HOST(ctk_cgls_f32, float, 0)
+CTK_SOLVE_HOST(ctk_cgls_f64, double, 0)
+CTK_SOLVE_HOST(ctk_lsqr_f32, float, 1)
+CTK_SOLVE_HOST(ctk_lsqr_f64, double, 1)
+#undef CTK_SOLVE_HOST
+
+int ctk_lsmr_f32(ctk_geom* g, int variant, const float* b, double lambda, const ctk_solver_opts* o, float* x,
+                 ctk_solve_log* log) {
+    return guard([&] { solve_host<float>(G(g), 2, variant, b, lambda, nullptr, 1, 1, 0, o, x, log); });
+}
+int ctk_lsmr_f64(ctk_geom* g, int variant, const double* b, double lambda, const ctk_solver_opts* o, double* x,
+                 ctk_solve_log* log) {
+    return guard([&] { solve_host<double>(G(g), 2, variant, b, lambda, nullptr, 1, 1, 0, o, x, log); });
+}
+int ctk_hybrid_lsqr_f32(ctk_geom* g, int variant, const float* b, const ctk_hybrid_strategy* s,
+                        const ctk_solver_opts* o, float* x, ctk_solve_log* log) {
+    return guard([&] { solve_host<float>(G(g), 3, variant, b, 0.0, s, 1, 1, 0, o, x, log); });
+}
+int ctk_hybrid_lsqr_f64(ctk_geom* g, int variant, const double* b, const ctk_hybrid_strategy* s,
+                        const ctk_solver_opts* o, double* x, ctk_solve_log* log) {
+    return guard([&] { solve_host<double>(G(g), 3, variant, b, 0.0, s, 1, 1, 0, o, x, log); });
+}
+int ctk_cgls_tv_f32(ctk_geom* g, int variant, const float* b, double lambda, int outer, int inner,
+                    const ctk_solver_opts* o, int warm, float* x, ctk_solve_log* log) {
+    return guard([&] { solve_host<float>(G(g), 4, variant, b, lambda, nullptr, outer, inner, warm, o, x, log); });
+}
+int ctk_cgls_tv_f64(ctk_geom* g, int variant, const double* b, double lambda, int outer, int inner,
+                    const ctk_solver_opts* o, int warm, double* x, ctk_solve_log* log) {
+    return guard([&] { solve_host<double>(G(g), 4, variant, b, lambda, nullptr, outer, inner, warm, o, x, log); });
+}
+int ctk_solve_dev_f32(ctk_geom* g, int solver, int variant, const float* b, double lambda, const ctk_hybrid_strategy* s,
+                      int outer, int inner, int warm, const ctk_solver_opts* o, float* x, ctk_solve_log* log) {
+    return guard([&] { ctkb::solve_device<float>(G(g), solver, variant, b, lambda, s, outer, inner, warm, o, x, log); });
+}
+int ctk_solve_dev_f64(ctk_geom* g, int solver, int variant, const double* b, double lambda,
+                      const ctk_hybrid_strategy* s, int outer, int inner, int warm, const ctk_solver_opts* o, double* x,
+                      ctk_solve_log* log) {
+    return guard([&] { ctkb::solve_device<double>(G(g), solver, variant, b, lambda, s, outer, inner, warm, o, x, log); });
+}
+
+int ctk_shard_angles(int n_angles, int nranks, int rank, int* first, int* count) {
+    return guard([&] {
+        if (n_angles < 1 || nranks < 1 || rank < 0 || rank >= nranks) ctkb::fail(CTK_E_PARAMETER, "invalid sharding");
+        // contiguous blocks; the first (n_angles % nranks) ranks take one extra angle
+        const int base = n_angles / nranks, extra = n_angles % nranks;
+        *first = rank * base + std::min(rank, extra);
+        *count = base + (rank < extra ? 1 : 0);
+    });
+}
+int ctk_comm_create(const ctk_comm_callbacks* cb, ctk_comm** out) {
+    return guard([&] {
+        if (!cb || !out) ctkb::fail(CTK_E_PARAMETER, "null callbacks");
+        if (cb->nranks < 1 || cb->rank < 0 || cb->rank >= cb->nranks) ctkb::fail(CTK_E_PARAMETER, "invalid rank / nranks");
+        auto* c = new ctkb::Comm();
+        c->cb = *cb;
+        *out = reinterpret_cast<ctk_comm*>(c);
+    });
+}
+int ctk_nccl_get_unique_id(void* out128) { return guard([&] { ctkb::nccl_unique_id(out128); }); }
+int ctk_comm_create_nccl(const void* id, int nranks, int rank, ctk_comm** out) {
+    return guard([&] { *out = reinterpret_cast<ctk_comm*>(ctkb::comm_create_nccl(id, nranks, rank)); });
+}
+void ctk_comm_destroy(ctk_comm* c) { ctkb::comm_destroy(reinterpret_cast<ctkb::Comm*>(c)); }
+int ctk_geom_attach_comm(ctk_geom* g, ctk_comm* c) {
+    return guard([&] { G(g).comm = reinterpret_cast<ctkb::Comm*>(c); });
+}
+
+uint64_t ctk_launch_count(void) { return ctkb::launch_count(); }
+double ctk_geom_last_kernel_ms(ctk_geom* g) {
+    float ms = -1.f;
+    guard([&] {
+        auto& gg = G(g);
+        CTK_CUDA(cudaEventSynchronize(gg.ev1));
+        CTK_CUDA(cudaEventElapsedTime(&ms, gg.ev0, gg.ev1));
+    });
+    return double(ms);
+}
+
+}  // extern "C"

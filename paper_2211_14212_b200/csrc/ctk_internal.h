@@ -1,0 +1,173 @@
+// Internal declarations of libctk_b200.so (not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ctk_b200.h"
+
+namespace ctkb {
+
+// ---- errors: C++ exceptions inside, status codes at the C-ABI -------------------------
+struct Error : std::runtime_error {
+    int code;
+    int iteration;
+    Error(int c, const std::string& m, int it = 0) : std::runtime_error(m), code(c), iteration(it) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg, int it = 0) { throw Error(code, msg, it); }
+
+#define CTK_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            ::ctkb::fail(CTK_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+// Checks the launch that was just issued and counts it (ctk_launch_count).
+void after_launch(const char* what);
+
+// ---- device buffers --------------------------------------------------------------------
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf();
+    // grows (never shrinks); returns true when (re)allocated, contents then undefined
+    bool ensure(size_t nbytes);
+    void release();
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- kernel-side geometry (passed by value) --------------------------------------------
+struct KGeom {
+    int mode, nu, nv, nx, ny, nz, na;
+    int has_zrays;
+    double dso, dod, du, h;
+    const double2* ctst;          // per view (cos, sin), host libm values
+    const float4* col;            // per (view, iu): fh0, fhd, g0, gd   (f32 separable model)
+    const unsigned char* colaxis; // per (view, iu): 0 = x-dominant, 1 = y-dominant
+    const double2* colstep;       // per (view, iu): (dx^2+dy^2, |d_A|) of the unnormalised ray
+};
+
+// ---- the geometry handle ---------------------------------------------------------------
+struct Comm;
+
+struct Geometry {
+    int mode = 0, nu = 0, nv = 0, nx = 0, ny = 0, nz = 0, na = 0;
+    double dso = 0, dod = 0, du = 0, h = 0;
+    std::vector<double> angles;  // canonical
+    std::vector<double> ct, st;
+    bool angles_valid = true;    // ProjectionSet::validate (types.hpp:104-117), raised at apply time
+    std::string angles_msg;
+    bool has_zrays = false;      // any cone ray with |d_z| dominant
+    int projector = CTK_PROJ_JOSEPH;
+    int bp_parts = 1;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    Comm* comm = nullptr;
+
+    // device tables
+    DevBuf d_ctst, d_col, d_colaxis, d_colstep;
+    // workspaces (grown lazily)
+    DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
+    DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers
+    DevBuf host_x, host_y;  // device staging for host-pointer entry points
+    DevBuf red;         // reduction scratch (partials + results)
+    double* pinned = nullptr;  // host-side reduction results
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    size_t domain() const { return size_t(nx) * ny * nz; }
+    size_t range() const { return size_t(na) * nu * nv; }
+    KGeom kgeom() const;
+    void require_angles() const;
+    ~Geometry();
+};
+
+// ---- kernels (launch wrappers) ---------------------------------------------------------
+// exact f64 path (kernels_f64.cu, compiled with --fmad=false)
+void launch_ax_exact_f64(const Geometry& g, const double* x, double* y, cudaStream_t s);
+void launch_atb_matched_exact_f64(const Geometry& g, const double* y, double* x, cudaStream_t s);
+void launch_atb_voxel_f64(const Geometry& g, const double* y, double* x, cudaStream_t s);
+
+// f32 performance path (kernels_f32.cu)
+void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s);
+void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s);
+void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
+void atb_voxel_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
+
+// phantom (phantom.cu)
+void launch_shepp_logan_f32(int n, float* out, cudaStream_t s);
+void launch_shepp_logan_f64(int n, double* out, cudaStream_t s);
+
+// ---- BLAS-1 (blas1.cu): deterministic fp64 reductions ----------------------------------
+constexpr int kRedBlocks = 592;   // 4 x 148 SMs; fixed => fixed summation order
+constexpr int kRedThreads = 256;
+constexpr int kRedSlots = 8;      // result slots per workspace
+
+struct RedWork {
+    double* partials;  // kRedBlocks * kRedSlots
+    double* results;   // kRedSlots
+};
+RedWork red_work(Geometry* g);             // lazily allocated in g->red
+RedWork red_work_global(cudaStream_t s);   // for handle-free BLAS-1 entry points
+
+enum class RedOp { dot, nrm2sq, diff_nrm2sq, axpy_nrm2sq, xpby, lincomb_nrm2sq };
+template <class T>
+void reduce_dot(size_t n, const T* a, const T* b, double* d_res, RedWork w, cudaStream_t s);
+template <class T>
+void reduce_diff_nrm2sq(size_t n, const T* a, const T* b, double* d_res, RedWork w, cudaStream_t s);
+template <class T>  // y += alpha*x; res = ||y||^2
+void axpy_nrm2sq(size_t n, double alpha, const T* x, T* y, double* d_res, RedWork w, cudaStream_t s);
+template <class T>
+void axpy(size_t n, double alpha, const T* x, T* y, cudaStream_t s);
+template <class T>  // y = x + beta*y
+void xpby(size_t n, const T* x, double beta, T* y, cudaStream_t s);
+template <class T>
+void scal(size_t n, double alpha, T* x, cudaStream_t s);
+template <class T>  // y = alpha*x
+void scale_copy(size_t n, double alpha, const T* x, T* y, cudaStream_t s);
+template <class T>  // x += c1*w (old w); w = v - c2*w     (solvers.hpp:114-116)
+void lsqr_update(size_t n, double c1, double c2, T* x, T* w, const T* v, cudaStream_t s);
+template <class T>  // hbar = h - c1*hbar; x += c2*hbar; h = v - c3*h   (solvers.hpp:201-204)
+void lsmr_update(size_t n, double c1, double c2, double c3, T* x, T* h, T* hbar, const T* v, cudaStream_t s);
+template <class T>  // out[i] = max|x|  (fp64)
+void reduce_absmax(size_t n, const T* x, double* d_res, RedWork w, cudaStream_t s);
+// block Gram-Schmidt pieces (krylov.hpp:21-31, gmres.hpp:33-39): coef[i] = <basis_i, w>
+template <class T>
+void block_dot(size_t n, int m, const T* basis, size_t ld, const T* w, double* d_coef, double* scratch, cudaStream_t s);
+template <class T>  // w += sum_i alpha * coef[i] * basis_i   (coef on device)
+void block_axpy(size_t n, int m, double alpha, const double* d_coef, const T* basis, size_t ld, T* w, cudaStream_t s);
+template <class T>
+void fill(size_t n, T v, T* x, cudaStream_t s);
+// fixed-order final reduction of n fp64 partials (one block) -> *d_out
+void finish_sum(const double* partials, int n, double* d_out, cudaStream_t s);
+void finish_max(const double* partials, int n, double* d_out, cudaStream_t s);
+
+// gradient / TV stencils (stencils.cu)
+template <class T>  // out{x,y,z} = scale[i] * (D x)_axis ; scale may be null (=1)
+void gradient_scaled(int nx, int ny, int nz, const T* x, const T* scale, double lam, T* gx, T* gy, T* gz, cudaStream_t s);
+template <class T>  // out += D^T (lam * w .* g)
+void gradient_adjoint_scaled_add(int nx, int ny, int nz, const T* gx, const T* gy, const T* gz, const T* w, double lam, T* out, cudaStream_t s);
+template <class T>  // w = (|Dx|^2 + eps^2)^(-1/4)
+void tv_weights(int nx, int ny, int nz, const T* x, double eps, T* w, cudaStream_t s);
+
+// ---- communicator ----------------------------------------------------------------------
+struct Comm {
+    ctk_comm_callbacks cb{};
+    void* nccl_comm = nullptr;  // when NCCL-backed
+};
+void comm_allreduce(Comm* c, void* d_buf, size_t count, int dtype, cudaStream_t s);
+double comm_sum_scalar(Comm* c, double v);  // rank-ordered sum of per-rank partials
+
+uint64_t launch_count();
+
+}  // namespace ctkb

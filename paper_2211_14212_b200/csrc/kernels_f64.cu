@@ -1,0 +1,300 @@
+// Exact-parity kernels for T = double (compiled with --fmad=false so no a*b+c is
+// contracted).  Every expression keeps the reference's association order, cos/sin come
+// from the host libm, and the per-voxel accumulation order of the matched transpose is
+// the reference's (angle partition, angle, iv, iu) order -- so the results are
+// bit-identical to the reference's T=double CPU path:
+//   forward_project            projector.hpp:134-162 (make_ray :29-46, plan_walk :60-91,
+//                              for_slice_stencil :96-111, integrate_ray :113-122)
+//   back_project_matched       projector.hpp:166-202 as a deterministic GATHER
+//   back_project_voxel_driven  projector.hpp:204-279
+#include <cfloat>
+
+#include "ctk_internal.h"
+
+namespace ctkb {
+namespace {
+
+struct Walk {
+    int axis, n_slices, nb, nc;
+    double step, fb0, fb_d, fc0, fc_d;
+    size_t sa, sb, sc;
+};
+
+// make_ray + plan_walk, operation for operation.
+__device__ __forceinline__ void make_walk(const KGeom& g, double ct, double st, int iu, int iv, Walk& w) {
+    double o[3], d[3];
+    const double u = (iu - 0.5 * (g.nu - 1)) * g.du;
+    const double v = (iv - 0.5 * (g.nv - 1)) * g.du;
+    const double cx = -g.dod * ct, cy = -g.dod * st, cz = 0.0;
+    const double px = cx - u * st, py = cy + u * ct, pz = cz + v;
+    if (g.mode == CTK_CONE3D) {
+        const double sx = g.dso * ct, sy = g.dso * st, sz = 0.0;
+        const double dx = px - sx, dy = py - sy, dz = pz - sz;
+        const double n = sqrt(dx * dx + dy * dy + dz * dz);
+        o[0] = sx; o[1] = sy; o[2] = sz;
+        d[0] = dx / n; d[1] = dy / n; d[2] = dz / n;
+    } else {
+        o[0] = px; o[1] = py; o[2] = pz;
+        d[0] = -ct; d[1] = -st; d[2] = 0.0;
+    }
+    const double ad0 = fabs(d[0]), ad1 = fabs(d[1]), ad2 = fabs(d[2]);
+    int axis = 0;
+    double adm = ad0;
+    if (ad1 > adm) { axis = 1; adm = ad1; }
+    if (ad2 > adm) { axis = 2; adm = ad2; }
+    const int n3[3] = {g.nx, g.ny, g.nz};
+    const size_t s3[3] = {1, size_t(g.nx), size_t(g.nx) * size_t(g.ny)};
+    const int b = axis == 2 ? 0 : axis + 1, c = axis == 0 ? 2 : axis - 1;
+    const double h = g.h;
+    w.axis = axis;
+    w.n_slices = n3[axis];
+    w.step = h / adm;
+    w.nb = n3[b];
+    w.nc = n3[c];
+    w.sa = s3[axis];
+    w.sb = s3[b];
+    w.sc = s3[c];
+    const double t0 = ((0 - 0.5 * (n3[axis] - 1)) * h - o[axis]) / d[axis];
+    const double dt = h / d[axis];
+    w.fb0 = (o[b] + t0 * d[b]) / h + 0.5 * (n3[b] - 1);
+    w.fb_d = dt * d[b] / h;
+    w.fc0 = (o[c] + t0 * d[c]) / h + 0.5 * (n3[c] - 1);
+    w.fc_d = dt * d[c] / h;
+}
+
+// Conservative slice range [s0, s1] outside of which no tap of the stencil is inside the
+// volume (f in (lo, hi) is required on both in-plane axes).  Skipped slices would add an
+// exact +0.0 to the running sum, so clipping does not change a single bit.
+__device__ __forceinline__ void clip_axis(double f0, double fd, double lo, double hi, int& s0, int& s1) {
+    if (fd == 0.0) {
+        if (!(f0 > lo - 1.0 && f0 < hi + 1.0)) { s0 = 1; s1 = 0; }
+        return;
+    }
+    double a = (lo - f0) / fd, b = (hi - f0) / fd;
+    if (a > b) { const double t = a; a = b; b = t; }
+    if (a > 2e9 || b < -2e9) { s0 = 1; s1 = 0; return; }
+    const double lo_s = fmax(a, -2e9), hi_s = fmin(b, 2e9);
+    s0 = max(s0, int(floor(lo_s)) - 1);
+    s1 = min(s1, int(ceil(hi_s)) + 1);
+}
+
+__global__ void k_ax_exact(KGeom g, const double* __restrict__ vol, double* __restrict__ proj) {
+    const int iu = blockIdx.x * blockDim.x + threadIdx.x;
+    const int iv = blockIdx.y * blockDim.y + threadIdx.y;
+    const int a = blockIdx.z;
+    if (iu >= g.nu || iv >= g.nv) return;
+    const double2 cs = g.ctst[a];
+    Walk w;
+    make_walk(g, cs.x, cs.y, iu, iv, w);
+    int s0 = 0, s1 = w.n_slices - 1;
+    clip_axis(w.fb0, w.fb_d, -1.0, double(w.nb), s0, s1);
+    clip_axis(w.fc0, w.fc_d, -1.0, double(w.nc), s0, s1);
+    double acc = 0;
+    for (int s = s0; s <= s1; ++s) {
+        const double fb = w.fb0 + s * w.fb_d;
+        const double fc = w.fc0 + s * w.fc_d;
+        const int ib = int(floor(fb));
+        const int ic = int(floor(fc));
+        const double tb = fb - ib, tc = fc - ic;
+        const size_t base = w.sa * size_t(s);
+        const double wq[4] = {(1 - tb) * (1 - tc), tb * (1 - tc), (1 - tb) * tc, tb * tc};
+        double sample = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int jb = ib + (q & 1), jc = ic + (q >> 1);
+            if (jb < 0 || jb >= w.nb || jc < 0 || jc >= w.nc || wq[q] == 0.0) continue;
+            sample += wq[q] * __ldg(vol + base + w.sb * size_t(jb) + w.sc * size_t(jc));
+        }
+        acc += sample;
+    }
+    proj[size_t(a) * g.nu * g.nv + size_t(iu) + size_t(g.nu) * iv] = w.step * acc;
+}
+
+// Projection of a point onto continuous detector coordinates (fu, fv); false when the
+// point is not strictly in front of the cone source (then every pixel is a candidate).
+__device__ __forceinline__ bool project_point(const KGeom& g, double ct, double st, double x, double y,
+                                              double z, double& fu, double& fv) {
+    double u, v;
+    if (g.mode == CTK_CONE3D) {
+        const double sx = g.dso * ct, sy = g.dso * st;
+        const double rx = x - sx, ry = y - sy;
+        const double depth = -(rx * ct + ry * st);
+        if (!(depth > 1e-9 * g.dso)) return false;
+        const double t = (g.dso + g.dod) / depth;
+        u = -(sx + t * rx) * st + (sy + t * ry) * ct;
+        v = t * z;
+    } else {
+        u = -x * st + y * ct;
+        v = z;
+    }
+    fu = u / g.du + 0.5 * (g.nu - 1);
+    fv = v / g.du + 0.5 * (g.nv - 1);
+    return true;
+}
+
+// Exact transpose as a gather: voxel (i,j,k) sums w * (step * y) over every ray whose
+// Joseph stencil touches it, in the reference's scatter order.  Candidate rays are the
+// pixels whose centres fall in the detector footprint of the cube [voxel +- h]^3 (every
+// stencil point of the voxel lies in that cube), widened by one pixel.
+__global__ void k_atb_matched_exact(KGeom g, int nparts, const double* __restrict__ proj,
+                                    double* __restrict__ vol) {
+    const size_t nvox = size_t(g.nx) * g.ny * g.nz;
+    const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= nvox) return;
+    const int i = int(id % g.nx);
+    const int j = int((id / g.nx) % g.ny);
+    const int k = int(id / (size_t(g.nx) * g.ny));
+    const double h = g.h;
+    const double xc = (i - 0.5 * (g.nx - 1)) * h, yc = (j - 0.5 * (g.ny - 1)) * h, zc = (k - 0.5 * (g.nz - 1)) * h;
+    const int vidx[3] = {i, j, k};
+    const size_t frame = size_t(g.nu) * g.nv;
+    double out = 0;
+    for (int t = 0; t < nparts; ++t) {
+        double part = 0;
+        for (int a = t; a < g.na; a += nparts) {
+            const double2 cs = g.ctst[a];
+            double umin = DBL_MAX, umax = -DBL_MAX, vmin = DBL_MAX, vmax = -DBL_MAX;
+            bool all = false;
+            for (int q = 0; q < 8 && !all; ++q) {
+                double fu, fv;
+                if (!project_point(g, cs.x, cs.y, xc + ((q & 1) ? h : -h), yc + ((q & 2) ? h : -h),
+                                   zc + ((q & 4) ? h : -h), fu, fv)) {
+                    all = true;
+                    break;
+                }
+                umin = fmin(umin, fu); umax = fmax(umax, fu);
+                vmin = fmin(vmin, fv); vmax = fmax(vmax, fv);
+            }
+            int iu0 = 0, iu1 = g.nu - 1, iv0 = 0, iv1 = g.nv - 1;
+            if (!all) {
+                iu0 = max(iu0, int(floor(fmax(umin, -1e9))) - 1);
+                iu1 = min(iu1, int(ceil(fmin(umax, 1e9))) + 1);
+                if (g.nv > 1) {
+                    iv0 = max(iv0, int(floor(fmax(vmin, -1e9))) - 1);
+                    iv1 = min(iv1, int(ceil(fmin(vmax, 1e9))) + 1);
+                }
+            }
+            const double* fr = proj + size_t(a) * frame;
+            for (int iv = iv0; iv <= iv1; ++iv) {
+                for (int iu = iu0; iu <= iu1; ++iu) {
+                    const double value = __ldg(fr + size_t(iu) + size_t(g.nu) * iv);
+                    if (value == 0.0) continue;
+                    Walk w;
+                    make_walk(g, cs.x, cs.y, iu, iv, w);
+                    const int s = vidx[w.axis];
+                    const int pb = vidx[w.axis == 2 ? 0 : w.axis + 1];
+                    const int pc = vidx[w.axis == 0 ? 2 : w.axis - 1];
+                    const double fb = w.fb0 + s * w.fb_d;
+                    const double fc = w.fc0 + s * w.fc_d;
+                    const int ib = int(floor(fb));
+                    const int ic = int(floor(fc));
+                    const int ob = pb - ib, oc = pc - ic;
+                    if (ob < 0 || ob > 1 || oc < 0 || oc > 1) continue;
+                    const double tb = fb - ib, tc = fc - ic;
+                    double wq;
+                    switch (ob + 2 * oc) {
+                        case 0: wq = (1 - tb) * (1 - tc); break;
+                        case 1: wq = tb * (1 - tc); break;
+                        case 2: wq = (1 - tb) * tc; break;
+                        default: wq = tb * tc; break;
+                    }
+                    if (wq == 0.0) continue;
+                    const double scaled = w.step * value;
+                    part += wq * scaled;
+                }
+            }
+        }
+        out += 1.0 * part;
+    }
+    vol[id] = out;
+}
+
+// back_project_voxel_driven, per voxel over views in order (projector.hpp:208-279).
+__global__ void k_atb_voxel_exact(KGeom g, const double* __restrict__ scale_par,
+                                  const double* __restrict__ proj, double* __restrict__ vol) {
+    const size_t nvox = size_t(g.nx) * g.ny * g.nz;
+    const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (id >= nvox) return;
+    const int i = int(id % g.nx);
+    const int j = int((id / g.nx) % g.ny);
+    const int k = int(id / (size_t(g.nx) * g.ny));
+    const double z = (k - 0.5 * (g.nz - 1)) * g.h;
+    const double y = (j - 0.5 * (g.ny - 1)) * g.h;
+    const double x = (i - 0.5 * (g.nx - 1)) * g.h;
+    const size_t frame = size_t(g.nu) * g.nv;
+    double acc = 0;
+    for (int a = 0; a < g.na; ++a) {
+        const double2 cs = g.ctst[a];
+        const double ct = cs.x, st = cs.y;
+        double u, v, scale;
+        if (g.mode == CTK_CONE3D) {
+            const double sx = g.dso * ct, sy = g.dso * st;
+            const double rx = x - sx, ry = y - sy, rz = z;
+            const double depth = -(rx * ct + ry * st);
+            if (depth <= 0.0) continue;
+            const double t = (g.dso + g.dod) / depth;
+            const double px = sx + t * rx, py = sy + t * ry, pz = t * rz;
+            u = -px * st + py * ct;
+            v = pz;
+            const double rn = sqrt(rx * rx + ry * ry + rz * rz);
+            const double arx = fabs(rx), ary = fabs(ry), arz = fabs(rz);
+            const double m1 = (ary < arz) ? arz : ary;  // std::max(|ry|, |rz|)
+            const double dom = (arx < m1) ? m1 : arx;   // std::max(|rx|, m1)
+            scale = g.h * rn / dom;
+        } else {
+            u = -x * st + y * ct;
+            v = z;
+            scale = scale_par[a];
+        }
+        const double fu = u / g.du + 0.5 * (g.nu - 1);
+        const double fv = (g.nv == 1) ? 0.0 : v / g.du + 0.5 * (g.nv - 1);
+        const int iu = int(floor(fu)), iv = int(floor(fv));
+        const double tu = fu - iu, tv = fv - iv;
+        const double* fr = proj + size_t(a) * frame;
+        double sample = 0.0;
+        const double wq[4] = {(1 - tu) * (1 - tv), tu * (1 - tv), (1 - tu) * tv, tu * tv};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int ju = iu + (q & 1), jv = iv + (q >> 1);
+            if (ju < 0 || ju >= g.nu || jv < 0 || jv >= g.nv) continue;
+            sample += wq[q] * __ldg(fr + size_t(ju) + size_t(g.nu) * jv);
+        }
+        acc += scale * sample;
+    }
+    vol[id] = acc;
+}
+
+}  // namespace
+
+void launch_ax_exact_f64(const Geometry& g, const double* x, double* y, cudaStream_t s) {
+    dim3 blk(32, 4);
+    dim3 grd((g.nu + 31) / 32, (g.nv + 3) / 4, g.na);
+    k_ax_exact<<<grd, blk, 0, s>>>(g.kgeom(), x, y);
+    after_launch("k_ax_exact");
+}
+
+void launch_atb_matched_exact_f64(const Geometry& g, const double* y, double* x, cudaStream_t s) {
+    const size_t n = g.domain();
+    const int nparts = std::max(1, std::min(g.bp_parts, g.na));
+    k_atb_matched_exact<<<unsigned((n + 127) / 128), 128, 0, s>>>(g.kgeom(), nparts, y, x);
+    after_launch("k_atb_matched_exact");
+}
+
+void launch_atb_voxel_f64(const Geometry& g, const double* y, double* x, cudaStream_t s) {
+    // per-view parallel-beam scale h / max(|cos|, |sin|) (projector.hpp:216-222), host libm
+    std::vector<double> sc(size_t(g.na), 0.0);
+    if (g.mode != CTK_CONE3D)
+        for (int a = 0; a < g.na; ++a) {
+            const double act = std::abs(g.ct[size_t(a)]), ast = std::abs(g.st[size_t(a)]);
+            sc[size_t(a)] = g.h / ((act < ast) ? ast : act);
+        }
+    DevBuf d_sc;
+    d_sc.ensure(sizeof(double) * sc.size());
+    CTK_CUDA(cudaMemcpyAsync(d_sc.p, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, s));
+    const size_t n = g.domain();
+    k_atb_voxel_exact<<<unsigned((n + 127) / 128), 128, 0, s>>>(g.kgeom(), d_sc.as<double>(), y, x);
+    after_launch("k_atb_voxel_exact");
+    CTK_CUDA(cudaStreamSynchronize(s));  // d_sc is released at scope exit
+}
+
+}  // namespace ctkb

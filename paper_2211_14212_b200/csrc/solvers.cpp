@@ -1,0 +1,567 @@
+// Device-resident Krylov solvers.  Control flow, stopping rules, breakdown tests and log
+// semantics follow the reference line by line; vectors live in HBM and every vector
+// operation is one of the fused kernels of blas1.cu / kernels_f32.cu / kernels_f64.cu.
+// Scalar recurrences run on the host in fp64 (the reference runs them in T; for T=double
+// they are the same operations).
+//   IterationMonitor   solve_log.hpp:86-161     cgls         solvers.hpp:13-60
+//   lsqr               solvers.hpp:62-126       lsmr         solvers.hpp:128-231
+//   hybrid_lsqr        hybrid.hpp:76-116 (gk_init/gk_expand krylov.hpp:50-92, cgs2 :21-31)
+//   cgls_tv            tv.hpp:45-110 (stack_weighted_gradient operators.hpp:141-186)
+// With a communicator attached (angle sharding), range vectors are this rank's angle
+// block: range reductions are summed over ranks in rank order and every A^T b partial
+// volume is sum-reduced, so all ranks hold identical domain vectors.
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "ctk_internal.h"
+#include "regparam.h"
+
+namespace ctkb {
+namespace {
+
+template <class T>
+constexpr double breakdown_factor() {  // krylov.hpp:14-17
+    return sizeof(T) == sizeof(double) ? 1e-14 : 1e-7;
+}
+constexpr double kIncreaseSlack = 1e-12;  // solve_log.hpp:80
+
+template <class T>
+struct Vec {
+    DevBuf buf;
+    size_t n = 0;
+    T* p = nullptr;
+    void alloc(size_t nn) {
+        n = nn;
+        buf.ensure(sizeof(T) * std::max<size_t>(nn, 1));
+        p = buf.as<T>();
+    }
+};
+
+// Device operator + reductions for one solve.
+template <class T>
+struct Dev {
+    Geometry& g;
+    int variant;
+    cudaStream_t s;
+    RedWork w;
+    Vec<T> tmp_range;  // explicit residual staging (f64 path)
+
+    Dev(Geometry& g_, int v) : g(g_), variant(v), s(g_.stream), w(red_work(&g_)) {}
+
+    void ax(const T* x, T* y) {
+        if constexpr (sizeof(T) == 4) ax_f32(g, x, y, s);
+        else launch_ax_exact_f64(g, x, y, s);
+    }
+    void atb(const T* y, T* x) {
+        if constexpr (sizeof(T) == 4) {
+            if (variant == CTK_BP_MATCHED) atb_matched_f32(g, y, x, s);
+            else atb_voxel_f32(g, y, x, s);
+        } else {
+            if (variant == CTK_BP_MATCHED) launch_atb_matched_exact_f64(g, y, x, s);
+            else launch_atb_voxel_f64(g, y, x, s);
+        }
+        if (g.comm) comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
+    }
+    double fetch(int slot) {
+        CTK_CUDA(cudaMemcpyAsync(g.pinned + slot, w.results + slot, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CTK_CUDA(cudaStreamSynchronize(s));
+        return g.pinned[slot];
+    }
+    double range_sum(double v) { return g.comm ? comm_sum_scalar(g.comm, v) : v; }
+
+    double nrm2sq(const T* x, size_t n, bool range) {
+        reduce_dot<T>(n, x, x, w.results, w, s);
+        const double v = fetch(0);
+        return range ? range_sum(v) : v;
+    }
+    double diff_nrm2sq(const T* a, const T* b, size_t n, bool range) {
+        reduce_diff_nrm2sq<T>(n, a, b, w.results, w, s);
+        const double v = fetch(0);
+        return range ? range_sum(v) : v;
+    }
+    // y += alpha x, returns ||y||^2
+    double axpy_n2(double alpha, const T* x, T* y, size_t n, bool range) {
+        axpy_nrm2sq<T>(n, alpha, x, y, w.results, w, s);
+        const double v = fetch(0);
+        return range ? range_sum(v) : v;
+    }
+    // ||A x - b||^2 over all ranks (solve_log.hpp:111-115), never storing A x in T=float
+    double resid2(const T* x, const T* b) {
+        if constexpr (sizeof(T) == 4) {
+            ax_residual_f32(g, x, b, w.results, s);
+            return range_sum(fetch(0));
+        } else {
+            if (!tmp_range.p) tmp_range.alloc(g.range());
+            ax(x, tmp_range.p);
+            return diff_nrm2sq(tmp_range.p, b, g.range(), true);
+        }
+    }
+};
+
+template <class T>
+struct Monitor {
+    Dev<T>& d;
+    const T* b;
+    const ctk_solver_opts& o;
+    ctk_solve_log* log;
+    double bnorm = 0, gt_norm = 0, prev = 0;
+    bool have_prev = false;
+    int reason = CTK_STOP_MAX_ITERS;
+    Vec<T> gt;
+    std::vector<T> host_x;
+
+    Monitor(Dev<T>& dev, const T* b_, const ctk_solver_opts& opts, ctk_solve_log* lg, const std::string& name)
+        : d(dev), b(b_), o(opts), log(lg) {
+        bnorm = std::sqrt(d.nrm2sq(b, d.g.range(), true));
+        if (!(bnorm > 0.0)) fail(CTK_E_DEGENERATE, name + ": zero right-hand side");
+        if (o.ground_truth) {
+            gt.alloc(d.g.domain());
+            CTK_CUDA(cudaMemcpyAsync(gt.p, o.ground_truth, sizeof(T) * d.g.domain(), cudaMemcpyHostToDevice, d.s));
+            gt_norm = std::sqrt(d.nrm2sq(gt.p, d.g.domain(), false));
+            if (!(gt_norm > 0.0)) fail(CTK_E_DEGENERATE, "ground truth has zero norm");
+        }
+        log->iterations = log->n_relative_error = log->n_lambda = 0;
+    }
+
+    // IterationMonitor::record; returns true when the solver should stop
+    bool record(int k, const T* x, double implicit, bool has_lambda = false, double lambda = 0.0) {
+        const double expl = std::sqrt(d.resid2(x, b)) / bnorm;
+        if (!std::isfinite(expl) || !std::isfinite(implicit))
+            fail(CTK_E_NUMERICAL, "non-finite residual at iteration " + std::to_string(k), k);
+        if (log->iterations >= log->capacity) fail(CTK_E_PARAMETER, "solve log capacity exceeded");
+        log->implicit_residual[log->iterations] = implicit;
+        log->explicit_residual[log->iterations] = expl;
+        log->iterations++;
+        if (has_lambda && log->lambda) log->lambda[log->n_lambda++] = lambda;
+        if (o.ground_truth && log->relative_error)
+            log->relative_error[log->n_relative_error++] =
+                std::sqrt(d.diff_nrm2sq(x, gt.p, d.g.domain(), false)) / gt_norm;
+        if (o.iterate_observer) {
+            host_x.resize(d.g.domain());
+            CTK_CUDA(cudaMemcpyAsync(host_x.data(), x, sizeof(T) * host_x.size(), cudaMemcpyDeviceToHost, d.s));
+            CTK_CUDA(cudaStreamSynchronize(d.s));
+            o.iterate_observer(k, host_x.data(), host_x.size(), o.observer_user);
+        }
+        if (expl <= o.residual_tolerance) {
+            reason = CTK_STOP_TOLERANCE;
+            return true;
+        }
+        if (o.stop_on_explicit_residual_increase && have_prev && expl > prev * (1.0 + kIncreaseSlack)) {
+            reason = CTK_STOP_RESIDUAL_INCREASE;
+            return true;
+        }
+        prev = expl;
+        have_prev = true;
+        return false;
+    }
+    void finish(int iterations) {
+        log->iterations_run = iterations;
+        log->stop_reason = reason;
+    }
+};
+
+void validate_opts(const ctk_solver_opts* o, const ctk_solve_log* log, int need) {
+    if (!o || !log) fail(CTK_E_PARAMETER, "null options or log");
+    if (o->max_iters < 1) fail(CTK_E_PARAMETER, "max_iters must be >= 1");
+    if (o->residual_tolerance < 0.0) fail(CTK_E_PARAMETER, "residual tolerance must be >= 0");
+    if (!log->implicit_residual || !log->explicit_residual || log->capacity < need)
+        fail(CTK_E_PARAMETER, "solve log needs capacity >= max iterations");
+}
+
+// ---------------------------------------------------------------------------------------
+template <class T>
+void cgls(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* log) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    Monitor<T> mon(d, b, o, log, "cgls");
+    const double bnorm = mon.bnorm;
+    Vec<T> r, s, p, q;
+    r.alloc(nr); s.alloc(nd); p.alloc(nd); q.alloc(nr);
+    fill<T>(nd, T(0), x, d.s);
+    CTK_CUDA(cudaMemcpyAsync(r.p, b, sizeof(T) * nr, cudaMemcpyDeviceToDevice, d.s));
+    d.atb(r.p, s.p);
+    CTK_CUDA(cudaMemcpyAsync(p.p, s.p, sizeof(T) * nd, cudaMemcpyDeviceToDevice, d.s));
+    double gamma = d.nrm2sq(s.p, nd, false);
+    int k = 0;
+    while (k < o.max_iters) {
+        ++k;
+        if (!(gamma > 0.0)) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            --k;
+            break;
+        }
+        d.ax(p.p, q.p);
+        const double delta = d.nrm2sq(q.p, nr, true);
+        if (!std::isfinite(delta)) fail(CTK_E_NUMERICAL, "cgls: non-finite curvature at iteration " + std::to_string(k), k);
+        if (!(delta > 0.0)) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            --k;
+            break;
+        }
+        const double alpha = gamma / delta;
+        axpy<T>(nd, alpha, p.p, x, d.s);
+        const double rr = d.axpy_n2(-alpha, q.p, r.p, nr, true);
+        if (mon.record(k, x, std::sqrt(rr) / bnorm)) break;
+        d.atb(r.p, s.p);
+        const double gnew = d.nrm2sq(s.p, nd, false);
+        const double beta = gnew / gamma;
+        gamma = gnew;
+        xpby<T>(nd, s.p, beta, p.p, d.s);
+    }
+    mon.finish(k);
+}
+
+template <class T>
+void lsqr(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* log) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    Monitor<T> mon(d, b, o, log, "lsqr");
+    const double beta1 = mon.bnorm;
+    const double tol = breakdown_factor<T>() * beta1;
+    Vec<T> u, un, v, vn, w;
+    u.alloc(nr); un.alloc(nr); v.alloc(nd); vn.alloc(nd); w.alloc(nd);
+    scale_copy<T>(nr, 1.0 / beta1, b, u.p, d.s);
+    d.atb(u.p, v.p);
+    double alpha = std::sqrt(d.nrm2sq(v.p, nd, false));
+    if (!(alpha > 0.0)) fail(CTK_E_DEGENERATE, "lsqr: A^T b vanished");
+    scal<T>(nd, 1.0 / alpha, v.p, d.s);
+    CTK_CUDA(cudaMemcpyAsync(w.p, v.p, sizeof(T) * nd, cudaMemcpyDeviceToDevice, d.s));
+    fill<T>(nd, T(0), x, d.s);
+    double phibar = beta1, rhobar = alpha;
+    int k = 0;
+    while (k < o.max_iters) {
+        ++k;
+        d.ax(v.p, un.p);
+        double beta = std::sqrt(d.axpy_n2(-alpha, u.p, un.p, nr, true));
+        bool down = beta <= tol;
+        if (beta > 0.0) {
+            scal<T>(nr, 1.0 / beta, un.p, d.s);
+            std::swap(u.p, un.p);
+            d.atb(u.p, vn.p);
+            alpha = std::sqrt(d.axpy_n2(-beta, v.p, vn.p, nd, false));
+            if (alpha > 0.0) {
+                scal<T>(nd, 1.0 / alpha, vn.p, d.s);
+                std::swap(v.p, vn.p);
+            }
+            down = down || alpha <= tol;
+        } else {
+            alpha = 0.0;
+        }
+        const double rho = std::sqrt(rhobar * rhobar + beta * beta);
+        const double c = rhobar / rho, sn = beta / rho;
+        const double theta = sn * alpha;
+        rhobar = -c * alpha;
+        const double phi = c * phibar;
+        phibar = sn * phibar;
+        lsqr_update<T>(nd, phi / rho, theta / rho, x, w.p, v.p, d.s);
+        if (mon.record(k, x, phibar / beta1)) break;
+        if (down) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            break;
+        }
+    }
+    mon.finish(k);
+}
+
+template <class T>
+void lsmr(Dev<T>& d, const T* b, double lambda, const ctk_solver_opts& o, T* x, ctk_solve_log* log) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    if (lambda < 0.0) fail(CTK_E_PARAMETER, "lsmr: lambda must be nonnegative");
+    Monitor<T> mon(d, b, o, log, "lsmr");
+    const double damp = lambda;
+    const double beta1 = mon.bnorm;
+    const double tol = breakdown_factor<T>() * beta1;
+    Vec<T> u, un, v, vn, h, hbar;
+    u.alloc(nr); un.alloc(nr); v.alloc(nd); vn.alloc(nd); h.alloc(nd); hbar.alloc(nd);
+    scale_copy<T>(nr, 1.0 / beta1, b, u.p, d.s);
+    d.atb(u.p, v.p);
+    double alpha = std::sqrt(d.nrm2sq(v.p, nd, false));
+    if (!(alpha > 0.0)) fail(CTK_E_DEGENERATE, "lsmr: A^T b vanished");
+    scal<T>(nd, 1.0 / alpha, v.p, d.s);
+    double zetabar = alpha * beta1, alphabar = alpha;
+    double rho = 1, rhobar = 1, cbar = 1, sbar = 0;
+    CTK_CUDA(cudaMemcpyAsync(h.p, v.p, sizeof(T) * nd, cudaMemcpyDeviceToDevice, d.s));
+    fill<T>(nd, T(0), hbar.p, d.s);
+    fill<T>(nd, T(0), x, d.s);
+    double betadd = beta1, betad = 0, rhodold = 1, tautildeold = 0, thetatilde = 0, zeta = 0, dsq = 0;
+    int k = 0;
+    while (k < o.max_iters) {
+        ++k;
+        d.ax(v.p, un.p);
+        double beta = std::sqrt(d.axpy_n2(-alpha, u.p, un.p, nr, true));
+        bool down = beta <= tol;
+        if (beta > 0.0) {
+            scal<T>(nr, 1.0 / beta, un.p, d.s);
+            std::swap(u.p, un.p);
+            d.atb(u.p, vn.p);
+            alpha = std::sqrt(d.axpy_n2(-beta, v.p, vn.p, nd, false));
+            if (alpha > 0.0) {
+                scal<T>(nd, 1.0 / alpha, vn.p, d.s);
+                std::swap(v.p, vn.p);
+            }
+            down = down || alpha <= tol;
+        } else {
+            alpha = 0.0;
+        }
+        const double alphahat = std::sqrt(alphabar * alphabar + damp * damp);
+        const double chat = alphabar / alphahat, shat = damp / alphahat;
+        const double rhoold = rho;
+        rho = std::sqrt(alphahat * alphahat + beta * beta);
+        const double c = alphahat / rho, sn = beta / rho;
+        const double thetanew = sn * alpha;
+        alphabar = c * alpha;
+        const double rhobarold = rhobar, zetaold = zeta;
+        const double thetabar = sbar * rho;
+        const double rhotemp = cbar * rho;
+        rhobar = std::sqrt(rhotemp * rhotemp + thetanew * thetanew);
+        cbar = rhotemp / rhobar;
+        sbar = thetanew / rhobar;
+        zeta = cbar * zetabar;
+        zetabar = -sbar * zetabar;
+        lsmr_update<T>(nd, thetabar * rho / (rhoold * rhobarold), zeta / (rho * rhobar), thetanew / rho, x, h.p, hbar.p,
+                       v.p, d.s);
+        const double betaacute = chat * betadd;
+        const double betacheck = -shat * betadd;
+        const double betahat = c * betaacute;
+        betadd = -sn * betaacute;
+        const double thetatildeold = thetatilde;
+        const double rhotildeold = std::sqrt(rhodold * rhodold + thetabar * thetabar);
+        const double ctildeold = rhodold / rhotildeold, stildeold = thetabar / rhotildeold;
+        thetatilde = stildeold * rhobar;
+        rhodold = ctildeold * rhobar;
+        betad = -stildeold * betad + ctildeold * betahat;
+        tautildeold = (zetaold - thetatildeold * tautildeold) / rhotildeold;
+        const double taud = (zeta - thetatilde * tautildeold) / rhodold;
+        dsq += betacheck * betacheck;
+        const double normr = std::sqrt(dsq + (betad - taud) * (betad - taud) + betadd * betadd);
+        if (mon.record(k, x, normr / beta1, true, lambda)) break;
+        if (down) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            break;
+        }
+    }
+    mon.finish(k);
+}
+
+// CGS2 against the first m stored basis vectors (krylov.hpp:21-31); range bases are
+// sharded across ranks, so their coefficients are summed over ranks.
+template <class T>
+void cgs2(Dev<T>& d, const T* basis, size_t ld, int m, T* wv, size_t n, bool range, double* d_coef, double* scratch) {
+    for (int pass = 0; pass < 2; ++pass) {
+        block_dot<T>(n, m, basis, ld, wv, d_coef, scratch, d.s);
+        if (range && d.g.comm) {
+            std::vector<double> c(static_cast<size_t>(m));
+            CTK_CUDA(cudaMemcpyAsync(c.data(), d_coef, sizeof(double) * m, cudaMemcpyDeviceToHost, d.s));
+            CTK_CUDA(cudaStreamSynchronize(d.s));
+            for (auto& v : c) v = comm_sum_scalar(d.g.comm, v);
+            CTK_CUDA(cudaMemcpyAsync(d_coef, c.data(), sizeof(double) * m, cudaMemcpyHostToDevice, d.s));
+        }
+        block_axpy<T>(n, m, -1.0, d_coef, basis, ld, wv, d.s);
+    }
+}
+
+template <class T>
+void hybrid_lsqr(Dev<T>& d, const T* b, const ctk_hybrid_strategy& strat, const ctk_solver_opts& o, T* x,
+                 ctk_solve_log* log) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    if (strat.kind == CTK_LAMBDA_FIXED && strat.lambda < 0.0) fail(CTK_E_PARAMETER, "fixed lambda must be nonnegative");
+    if (strat.kind == CTK_LAMBDA_DP && !(strat.noise_level > 0.0 && strat.noise_level < 1.0))
+        fail(CTK_E_PARAMETER, "dp strategy needs a noise level in (0,1)");
+    if (strat.kind < 0 || strat.kind > 2) fail(CTK_E_PARAMETER, "unknown lambda strategy");
+    Monitor<T> mon(d, b, o, log, "hybrid_lsqr");
+    const int cap = o.max_iters + 2;
+    DevBuf Ub, Vb, coefb, scratchb;
+    Ub.ensure(sizeof(T) * nr * size_t(cap));
+    Vb.ensure(sizeof(T) * nd * size_t(cap));
+    coefb.ensure(sizeof(double) * size_t(cap));
+    scratchb.ensure(sizeof(double) * size_t(cap) * kRedBlocks);
+    T* U = Ub.as<T>();
+    T* V = Vb.as<T>();
+    auto Ui = [&](int i) { return U + size_t(i) * nr; };
+    auto Vi = [&](int i) { return V + size_t(i) * nd; };
+    // gk_init (krylov.hpp:50-67)
+    const double beta1 = mon.bnorm;
+    const double tol = breakdown_factor<T>() * beta1;
+    scale_copy<T>(nr, 1.0 / beta1, b, Ui(0), d.s);
+    d.atb(Ui(0), Vi(0));
+    const double alpha1 = std::sqrt(d.nrm2sq(Vi(0), nd, false));
+    if (!(alpha1 > 0.0)) fail(CTK_E_DEGENERATE, "gk_init: B u_1 vanished");
+    scal<T>(nd, 1.0 / alpha1, Vi(0), d.s);
+    int nu_ = 1, nv_ = 1;
+    std::vector<double> alphas{alpha1}, betas;
+    Vec<T> ynum;
+    DevBuf dy;
+    dy.ensure(sizeof(double) * size_t(cap));
+    int k = 0;
+    while (k < o.max_iters) {
+        // gk_expand (krylov.hpp:69-92)
+        bool breakdown = false;
+        {
+            const int j = nv_;
+            T* wv = Ui(nu_);
+            d.ax(Vi(j - 1), wv);
+            axpy<T>(nr, -alphas[size_t(j - 1)], Ui(j - 1), wv, d.s);
+            if (o.reorth) cgs2<T>(d, U, nr, nu_, wv, nr, true, coefb.as<double>(), scratchb.as<double>());
+            const double beta = std::sqrt(d.nrm2sq(wv, nr, true));
+            if (beta <= tol) {
+                breakdown = true;
+            } else {
+                scal<T>(nr, 1.0 / beta, wv, d.s);
+                ++nu_;
+                betas.push_back(beta);
+                T* z = Vi(nv_);
+                d.atb(Ui(j), z);
+                axpy<T>(nd, -beta, Vi(j - 1), z, d.s);
+                if (o.reorth) cgs2<T>(d, V, nd, nv_, z, nd, false, coefb.as<double>(), scratchb.as<double>());
+                const double alpha = std::sqrt(d.nrm2sq(z, nd, false));
+                if (alpha <= tol) {
+                    breakdown = true;
+                } else {
+                    scal<T>(nd, 1.0 / alpha, z, d.s);
+                    ++nv_;
+                    alphas.push_back(alpha);
+                }
+            }
+        }
+        if (breakdown && int(betas.size()) < k + 1) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            break;
+        }
+        ++k;
+        std::vector<double> H(size_t(k + 1) * k, 0.0);
+        for (int jj = 0; jj < k; ++jj) {
+            H[size_t(jj) * k + jj] = alphas[size_t(jj)];
+            H[size_t(jj + 1) * k + jj] = betas[size_t(jj)];
+        }
+        const double lambda_k = choose_lambda(strat, H, k, beta1);
+        double fit = 0.0;
+        const std::vector<double> y = projected_tikhonov(H, k, beta1, lambda_k, &fit);
+        // basis_combination (gmres.hpp:33-39): x = sum_i T(y_i) V_i, accumulated in order
+        CTK_CUDA(cudaMemcpyAsync(dy.p, y.data(), sizeof(double) * y.size(), cudaMemcpyHostToDevice, d.s));
+        fill<T>(nd, T(0), x, d.s);
+        block_axpy<T>(nd, int(y.size()), 1.0, dy.as<double>(), V, nd, x, d.s);
+        CTK_CUDA(cudaStreamSynchronize(d.s));  // y (host) must outlive the async copy
+        if (mon.record(k, x, fit / beta1, true, lambda_k)) break;
+        if (breakdown) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            break;
+        }
+    }
+    mon.finish(k);
+    log->stored_domain_basis = nv_;
+    log->stored_range_basis = nu_;
+}
+
+// stacked operator K = [A; lam diag(w) D] of stack_weighted_gradient
+template <class T>
+struct Stacked {
+    Dev<T>& d;
+    const T* w;
+    double lam;
+    size_t nd, nr;
+    void fwd(const T* x, T* y) {
+        d.ax(x, y);
+        gradient_scaled<T>(d.g.nx, d.g.ny, d.g.nz, x, w, lam, y + nr, y + nr + nd, y + nr + 2 * nd, d.s);
+    }
+    void back(const T* y, T* x) {
+        d.atb(y, x);
+        gradient_adjoint_scaled_add<T>(d.g.nx, d.g.ny, d.g.nz, y + nr, y + nr + nd, y + nr + 2 * nd, w, lam, x, d.s);
+    }
+    // squared norm of a stacked vector: sharded range part + replicated gradient part
+    double n2(const T* y) { return d.nrm2sq(y, nr, true) + d.nrm2sq(y + nr, 3 * nd, false); }
+    double axpy_n2(double a, const T* x, T* y) { return d.axpy_n2(a, x, y, nr, true) + d.axpy_n2(a, x + nr, y + nr, 3 * nd, false); }
+};
+
+template <class T>
+void cgls_tv(Dev<T>& d, const T* b, double lambda, int outer_iters, int inner_iters, bool warm,
+             const ctk_solver_opts& o, T* x, ctk_solve_log* log) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    if (!(lambda > 0.0)) fail(CTK_E_PARAMETER, "cgls_tv: lambda must be positive");
+    if (outer_iters < 1 || inner_iters < 1) fail(CTK_E_PARAMETER, "cgls_tv: outer and inner iteration counts must be >= 1");
+    Monitor<T> mon(d, b, o, log, "cgls_tv");
+    const size_t ns = nr + 3 * nd;
+    Vec<T> wts, r, s, p, q;
+    wts.alloc(nd); r.alloc(ns); s.alloc(nd); p.alloc(nd); q.alloc(ns);
+    fill<T>(nd, T(0), x, d.s);
+    int k = 0;
+    bool stopped = false;
+    log->n_outer_starts = 0;
+    for (int outer = 0; outer < outer_iters && !stopped; ++outer) {
+        // tv_weights (tv.hpp:28-43): eps = 1e-4 max|x|
+        reduce_absmax<T>(nd, x, d.w.results, d.w, d.s);
+        const double eps = 1e-4 * d.fetch(0);
+        tv_weights<T>(g.nx, g.ny, g.nz, x, eps, wts.p, d.s);
+        Stacked<T> K{d, wts.p, lambda, nd, nr};
+        // rhs = [b; 0]
+        if (log->outer_starts) log->outer_starts[log->n_outer_starts++] = k;
+        mon.have_prev = false;  // reset_increase_baseline
+        if (!warm) fill<T>(nd, T(0), x, d.s);
+        CTK_CUDA(cudaMemcpyAsync(r.p, b, sizeof(T) * nr, cudaMemcpyDeviceToDevice, d.s));
+        fill<T>(3 * nd, T(0), r.p + nr, d.s);
+        const double rhs_norm = std::sqrt(K.n2(r.p));
+        if (warm) {
+            K.fwd(x, q.p);
+            axpy<T>(ns, -1.0, q.p, r.p, d.s);
+        }
+        K.back(r.p, s.p);
+        CTK_CUDA(cudaMemcpyAsync(p.p, s.p, sizeof(T) * nd, cudaMemcpyDeviceToDevice, d.s));
+        double gamma = d.nrm2sq(s.p, nd, false);
+        for (int inner = 0; inner < inner_iters; ++inner) {
+            if (!(gamma > 0.0)) break;
+            K.fwd(p.p, q.p);
+            const double delta = K.n2(q.p);
+            if (!(delta > 0.0)) break;
+            const double alpha = gamma / delta;
+            axpy<T>(nd, alpha, p.p, x, d.s);
+            const double rr = K.axpy_n2(-alpha, q.p, r.p);
+            ++k;
+            if (mon.record(k, x, std::sqrt(rr) / rhs_norm, true, lambda)) {
+                stopped = true;
+                break;
+            }
+            K.back(r.p, s.p);
+            const double gnew = d.nrm2sq(s.p, nd, false);
+            const double beta = gnew / gamma;
+            gamma = gnew;
+            xpby<T>(nd, s.p, beta, p.p, d.s);
+        }
+    }
+    mon.finish(k);
+}
+
+}  // namespace
+
+template <class T>
+void solve_device(Geometry& g, int solver, int variant, const T* d_b, double lambda, const ctk_hybrid_strategy* st,
+                  int outer, int inner, int warm, const ctk_solver_opts* o, T* d_x, ctk_solve_log* log) {
+    g.require_angles();
+    if (variant != CTK_BP_MATCHED && variant != CTK_BP_VOXEL_DRIVEN) fail(CTK_E_PARAMETER, "unknown backprojector variant");
+    const int need = solver == 4 ? std::max(1, outer) * std::max(1, inner) : (o ? o->max_iters : 0);
+    validate_opts(o, log, need);
+    Dev<T> d(g, variant);
+    switch (solver) {
+        case 0: cgls<T>(d, d_b, *o, d_x, log); break;
+        case 1: lsqr<T>(d, d_b, *o, d_x, log); break;
+        case 2: lsmr<T>(d, d_b, lambda, *o, d_x, log); break;
+        case 3:
+            if (!st) fail(CTK_E_PARAMETER, "hybrid_lsqr needs a strategy");
+            hybrid_lsqr<T>(d, d_b, *st, *o, d_x, log);
+            break;
+        case 4: cgls_tv<T>(d, d_b, lambda, outer, inner, warm != 0, *o, d_x, log); break;
+        default: fail(CTK_E_PARAMETER, "unknown solver");
+    }
+    CTK_CUDA(cudaStreamSynchronize(g.stream));
+}
+
+template void solve_device<float>(Geometry&, int, int, const float*, double, const ctk_hybrid_strategy*, int, int, int,
+                                  const ctk_solver_opts*, float*, ctk_solve_log*);
+template void solve_device<double>(Geometry&, int, int, const double*, double, const ctk_hybrid_strategy*, int, int,
+                                   int, const ctk_solver_opts*, double*, ctk_solve_log*);
+
+}  // namespace ctkb

@@ -1,0 +1,40 @@
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: larger parity cases")
+
+
+@pytest.fixture(scope="session")
+def restated():
+    from oracle.oracle import Restated
+
+    return Restated()
+
+
+@pytest.fixture(scope="session")
+def reference():
+    """The unmodified reference compiled into oracle/_ref (skips when absent)."""
+    from oracle.oracle import Reference
+
+    if not Reference.available():
+        pytest.skip("oracle/_ref/libctkref.so not built")
+    r = Reference()
+    r.set_threads(1)
+    return r
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64).ravel()
+    b = np.asarray(b, dtype=np.float64).ravel()
+    den = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))

@@ -1,0 +1,255 @@
+"""GPU parity of the sm_100a Ax / A^T b kernels against the reference (through the C-ABI).
+
+Bars (BASELINE.json north_star): a single Ax or A^T b within 1e-5 relative L2 of the
+reference CPU implementation (T=double golden); the f64 kernels are held to BIT-EXACT
+equality with the reference's T=double path (same IEEE operation sequence).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from geoms import ALL, cone_adjoint, cone_bench, parallel2d, to_ctk
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-5  # north_star: single Ax / A^T b within 1e-5 relative L2
+
+
+@pytest.fixture(scope="module")
+def ctk():
+    import torch
+
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    import paper_2211_14212_b200 as m
+
+    m.load()
+    return m
+
+
+def _rand(n, seed, dtype=np.float64):
+    return np.random.default_rng(seed).standard_normal(n).astype(dtype)
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+def test_ax_f64_bit_exact(ctk, reference, name):
+    g = ALL[name]()
+    x = _rand(g.domain_size, 1)
+    want = reference.forward(g, x)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float64)
+    got = pair.apply_forward(x)
+    assert np.array_equal(got, want), f"max |d| = {np.abs(got - want).max()}"
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+@pytest.mark.parametrize("nparts", [1, 3])
+def test_atb_matched_f64_bit_exact(ctk, reference, name, nparts):
+    g = ALL[name]()
+    y = _rand(g.range_size, 2)
+    y[::7] = 0.0  # zero rays are skipped by the reference scatter (projector.hpp:193)
+    reference.set_threads(nparts)
+    try:
+        want = reference.back(g, y, 0)
+    finally:
+        reference.set_threads(1)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float64, bp_partitions=nparts)
+    got = pair.apply_back(y)
+    assert np.array_equal(got, want), f"max |d| = {np.abs(got - want).max()}"
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+def test_atb_voxel_f64_bit_exact(ctk, reference, name):
+    g = ALL[name]()
+    y = _rand(g.range_size, 3)
+    want = reference.back(g, y, 1)
+    pair = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant.voxel_driven, dtype=np.float64)
+    got = pair.apply_back(y)
+    assert np.array_equal(got, want), f"max |d| = {np.abs(got - want).max()}"
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+def test_ax_f32_within_1e5(ctk, reference, name, restated):
+    g = ALL[name]()
+    ph = restated.shepp_logan_3d(max(g.nx, g.ny, g.nz), np.float64)
+    n = max(g.nx, g.ny, g.nz)
+    x = ph.reshape(n, n, n)[: g.nz, : g.ny, : g.nx].astype(np.float32).astype(np.float64).ravel() if g.nz > 1 else \
+        _rand(g.domain_size, 4).astype(np.float32).astype(np.float64)
+    want = reference.forward(g, x)
+    got = ctk.projector_pair(to_ctk(g)).apply_forward(x.astype(np.float32))
+    assert rel_l2(got, want) < TOL_F32
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+@pytest.mark.parametrize("variant", [0, 1])
+def test_atb_f32_within_1e5(ctk, reference, name, variant):
+    g = ALL[name]()
+    y = _rand(g.range_size, 5).astype(np.float32).astype(np.float64)
+    want = reference.back(g, y, variant)
+    got = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant(variant)).apply_back(y.astype(np.float32))
+    assert rel_l2(got, want) < TOL_F32
+
+
+def test_c1_config_parity(ctk, reference, restated):
+    """Config 1 shape (64^3 Shepp-Logan, 64^2 detector, 100 angles), both precisions."""
+    g = cone_bench(64, 100)
+    x = restated.shepp_logan_3d(64, np.float64)
+    reference.set_threads(8)
+    try:
+        want = reference.forward(g, x)
+        bt = reference.back(g, want, 0)
+    finally:
+        reference.set_threads(1)
+    p32 = ctk.projector_pair(to_ctk(g))
+    p64 = ctk.projector_pair(to_ctk(g), dtype=np.float64)
+    assert np.array_equal(p64.apply_forward(x), want)
+    assert rel_l2(p32.apply_forward(x.astype(np.float32)), want) < TOL_F32
+    assert rel_l2(p32.apply_back(want.astype(np.float32)), bt) < TOL_F32
+
+
+# ---- known-answer tests of test_operators.cpp, on the GPU kernels ----------------------------
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_zero_in_zero_out(ctk, dtype):
+    g = parallel2d(16, 12)
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    assert np.all(pair.apply_forward(np.zeros(g.domain_size, dtype)) == 0)
+    for v in (0, 1):
+        p = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant(v), dtype=dtype)
+        assert np.all(p.apply_back(np.zeros(g.range_size, dtype)) == 0)
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-12), (np.float32, 1e-6)])
+def test_constant_row(ctk, dtype, tol):
+    # test_operators.cpp:34-49: 5 voxels, h=0.7, c=1.3 -> 4.55
+    n, h, c = 5, 0.7, 1.3
+    g = ctk.ConeGeometry(ctk.BeamMode.parallel2d, 0.0, n * h, h, n, 1, ctk.VolumeShape(n, n, 1, h), [0.0])
+    y = ctk.projector_pair(g, dtype=dtype).apply_forward(np.full(n * n, c, dtype))
+    assert abs(y[n // 2] - n * h * c) <= tol * n * h * c
+
+
+@pytest.mark.parametrize("mode", ["parallel2d", "cone3d"])
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-12), (np.float32, 2e-6)])
+def test_impulse_chord(ctk, mode, dtype, tol):
+    from oracle.oracle import ray_box_chord
+
+    h, th, n = 0.9, 0.3, 7
+    if mode == "parallel2d":
+        g = ctk.ConeGeometry(ctk.BeamMode.parallel2d, 0.0, n * h, h, 1, 1, ctk.VolumeShape(n, n, 1, h), [th])
+        x = np.zeros(n * n, dtype)
+        x[(n // 2) + n * (n // 2)] = 1
+        chord = ray_box_chord([0, 0, 0], [-math.cos(th), -math.sin(th), 0], [-h / 2] * 3, [h / 2] * 3)
+    else:
+        g = ctk.ConeGeometry(ctk.BeamMode.cone3d, 4.0 * n * h, 2.0 * n * h, h, 1, 1, ctk.VolumeShape(n, n, n, h), [th])
+        x = np.zeros(n ** 3, dtype)
+        x[(n // 2) + n * ((n // 2) + n * (n // 2))] = 1
+        o = [g.source_to_origin * math.cos(th), g.source_to_origin * math.sin(th), 0.0]
+        d = [-o[0], -o[1], 0.0]
+        nn = math.hypot(d[0], d[1])
+        chord = ray_box_chord(o, [d[0] / nn, d[1] / nn, 0.0], [-h / 2] * 3, [h / 2] * 3)
+    y = ctk.projector_pair(g, dtype=dtype).apply_forward(x)
+    assert abs(y[0] - chord) <= tol * chord
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-10), (np.float32, 2e-6)])
+def test_linearity(ctk, dtype, tol):
+    g = parallel2d(24, 10)
+    rng = np.random.default_rng(7)
+    x, y = rng.standard_normal(g.domain_size), rng.standard_normal(g.domain_size)
+    a, b = 1.7, -0.4
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    pc = pair.apply_forward((a * x + b * y).astype(dtype))
+    want = a * pair.apply_forward(x.astype(dtype)).astype(np.float64) + b * pair.apply_forward(y.astype(dtype))
+    assert rel_l2(pc, want) < tol
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_two_pi_periodicity_bitwise(ctk, dtype):
+    for th in (0.0, 0.5, 1.25, 5.0):
+        g1 = to_ctk(parallel2d(16, 1))
+        g1.angles = [th]
+        g2 = to_ctk(parallel2d(16, 1))
+        g2.angles = [th + 2.0 * math.pi]
+        x = np.random.default_rng(11).standard_normal(256).astype(dtype)
+        p1 = ctk.projector_pair(g1, dtype=dtype).apply_forward(x)
+        p2 = ctk.projector_pair(g2, dtype=dtype).apply_forward(x)
+        assert np.array_equal(p1, p2)
+
+
+@pytest.mark.parametrize("geom,trials,seed", [(lambda: parallel2d(32, 24), 100, 42), (cone_adjoint, 25, 4)])
+def test_matched_adjoint_f64(ctk, geom, trials, seed):
+    from oracle.oracle import adjoint_discrepancy
+
+    g = geom()
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float64)
+    d = adjoint_discrepancy(pair.apply_forward, pair.apply_back, g.domain_size, g.range_size, trials, seed)
+    assert d < 1e-10
+
+
+def test_voxel_driven_is_not_adjoint(ctk):
+    from oracle.oracle import adjoint_discrepancy
+
+    g = parallel2d(32, 24)
+    pair = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant.voxel_driven, dtype=np.float64)
+    assert adjoint_discrepancy(pair.apply_forward, pair.apply_back, g.domain_size, g.range_size, 20, 43) > 1e-3
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+def test_matched_adjoint_f32(ctk, name):
+    """The f32 transpose is the exact transpose of the f32 forward up to fp32 rounding."""
+    from oracle.oracle import adjoint_discrepancy
+
+    g = ALL[name]()
+    pair = ctk.projector_pair(to_ctk(g))
+    d = adjoint_discrepancy(pair.apply_forward, pair.apply_back, g.domain_size, g.range_size, 8, 3, np.float32)
+    assert d < 2e-6
+
+
+def test_device_path_equals_host_path(ctk):
+    import torch
+
+    g = ALL["cone_ragged"]()
+    pair = ctk.projector_pair(to_ctk(g))
+    x = _rand(g.domain_size, 9, np.float32)
+    y = _rand(g.range_size, 10, np.float32)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    assert np.array_equal(pair.apply_forward(xd).cpu().numpy(), pair.apply_forward(x))
+    assert np.array_equal(pair.apply_back(yd).cpu().numpy(), pair.apply_back(y))
+
+
+def test_fused_residual_matches_unfused(ctk):
+    import torch
+
+    g = ALL["cone_default"]()
+    pair = ctk.projector_pair(to_ctk(g))
+    x = torch.from_numpy(_rand(g.domain_size, 12, np.float32)).cuda()
+    b = torch.from_numpy(_rand(g.range_size, 13, np.float32)).cuda()
+    r2 = pair.projector.residual2(x, b)
+    want = float(((pair.apply_forward(x).double() - b.double()) ** 2).sum())
+    assert abs(r2 - want) <= 1e-12 * want
+
+
+def test_shape_and_geometry_errors(ctk):
+    g = to_ctk(parallel2d(16, 4))
+    pair = ctk.projector_pair(g)
+    with pytest.raises(ctk.DimensionError):
+        pair.apply_forward(np.zeros(64, np.float32))
+    bad = to_ctk(parallel2d(16, 4))
+    bad.mode = ctk.BeamMode.cone3d
+    bad.source_to_origin = 2.0
+    with pytest.raises(ctk.GeometryError):
+        ctk.projector_pair(bad)
+    with pytest.raises(ctk.DimensionError):
+        ctk.back_project(np.zeros(10, np.float32), g)
+    unsorted = to_ctk(parallel2d(16, 4))
+    unsorted.angles = [0.5, 0.1, 1.0, 2.0]
+    p = ctk.projector_pair(unsorted)  # reference raises at apply time (types.hpp:114-115)
+    with pytest.raises(ctk.GeometryError):
+        p.apply_forward(np.zeros(256, np.float32))
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_phantom_matches_reference(ctk, reference, dtype):
+    n = 40
+    got = ctk.shepp_logan_3d(n, dtype).cpu().numpy()
+    want = reference.phantom(0, n, np.float64 if dtype == "float64" else np.float32)
+    assert np.array_equal(got, want)

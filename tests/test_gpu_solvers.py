@@ -1,0 +1,189 @@
+"""Device-resident solvers vs the reference solvers (oracle/_ref, T=double golden).
+
+Bars (north_star): iterates after k iterations within 1e-4 relative L2, and the residual
+history within 1e-4 per iteration.  Also: bitwise rerun determinism
+(test_solvers.cpp:436-451) and the error taxonomy.
+"""
+import numpy as np
+import pytest
+
+from geoms import cone_bench, cone_default, parallel2d, to_ctk
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+@pytest.fixture(scope="module")
+def ctk():
+    import paper_2211_14212_b200 as m
+
+    m.load()
+    return m
+
+
+@pytest.fixture(scope="module")
+def problem(restated, reference):
+    g = cone_bench(32, 40)
+    gt = restated.shepp_logan_3d(32, np.float64)
+    b = reference.forward(g, gt)
+    return g, gt, b
+
+
+def _opts(ctk, k, gt=None):
+    return ctk.SolverOptions(max_iters=k, stop_on_explicit_residual_increase=False, residual_tolerance=0.0,
+                             ground_truth=gt)
+
+
+def _check_hist(res, want):
+    impl = np.array(res.log.implicit_residual)
+    expl = np.array(res.log.explicit_residual)
+    assert res.iterations_run == want["iterations_run"]
+    assert np.all(np.abs(expl - want["explicit"]) <= TOL * np.abs(want["explicit"]))
+    assert np.all(np.abs(impl - want["implicit"]) <= TOL * np.abs(want["implicit"]))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("solver", ["cgls", "lsqr", "lsmr"])
+def test_solver_parity(ctk, reference, problem, dtype, solver):
+    g, gt, b = problem
+    k = 12
+    lam = 30.0 if solver == "lsmr" else 0.0
+    reference.set_threads(8)
+    try:
+        want = reference.solve(g, b, solver, k, lam=lam, tol=0.0, stop_inc=False, gt=gt)
+    finally:
+        reference.set_threads(1)
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    opts = _opts(ctk, k, gt.astype(dtype))
+    if solver == "lsmr":
+        res = ctk.lsmr(pair, b.astype(dtype), lam, opts)
+    else:
+        res = getattr(ctk, solver)(pair, b.astype(dtype), opts)
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+    err = np.array(res.log.relative_error)
+    assert np.all(np.abs(err - want["relative_error"]) <= TOL * want["relative_error"])
+    if solver == "lsmr":
+        assert res.log.lambda_ == [lam] * k
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_hybrid_lsqr_gcv_parity(ctk, reference, problem, dtype):
+    g, gt, b = problem
+    k = 8
+    want = reference.solve(g, b, "hybrid_lsqr", k, strategy=2, tol=0.0, stop_inc=False)
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    res = ctk.hybrid_lsqr(pair, b.astype(dtype), ctk.HybridStrategy.gcv(), _opts(ctk, k))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+    assert np.allclose(res.log.lambda_, want["lambda"], rtol=1e-3)
+    assert res.stored_domain_basis == want["stored_domain_basis"]
+    assert res.stored_range_basis == want["stored_range_basis"]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_cgls_tv_parity(ctk, reference, problem, dtype):
+    g, gt, b = problem
+    outer, inner, lam = 2, 4, 0.5
+    want = reference.solve(g, b, "cgls_tv", 1, lam=lam, outer=outer, inner=inner, tol=0.0, stop_inc=False)
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    res = ctk.cgls_tv(pair, b.astype(dtype), lam, outer, inner, _opts(ctk, 1))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+    assert list(res.outer_starts) == list(want["outer_starts"])
+
+
+def test_voxel_driven_lsqr_parity(ctk, reference, problem):
+    g, gt, b = problem
+    k = 6
+    want = reference.solve(g, b, "lsqr", k, variant=1, tol=0.0, stop_inc=False)
+    pair = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant.voxel_driven, dtype=np.float64)
+    res = ctk.lsqr(pair, b, _opts(ctk, k))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+
+
+def test_stopping_rules_match(ctk, reference):
+    """Default options (tolerance 1e-6, residual-increase stop) on a noisy unmatched run."""
+    g = parallel2d(32, 30)
+    rng = np.random.default_rng(3)
+    x = rng.random(g.domain_size)
+    b = reference.forward(g, x) + 0.05 * rng.standard_normal(g.range_size)
+    want = reference.solve(g, b, "lsqr", 60, variant=1)
+    pair = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant.voxel_driven, dtype=np.float64)
+    res = ctk.lsqr(pair, b, ctk.SolverOptions(max_iters=60))
+    assert res.stop_reason.name == want["stop_reason"]
+    assert res.iterations_run == want["iterations_run"]
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_determinism_bitwise(ctk, problem, dtype):
+    g, gt, b = problem
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    opts = ctk.SolverOptions(max_iters=6, ground_truth=gt.astype(dtype))
+    r1 = ctk.lsqr(pair, b.astype(dtype), opts)
+    r2 = ctk.lsqr(pair, b.astype(dtype), opts)
+    assert r1.log.implicit_residual == r2.log.implicit_residual
+    assert r1.log.explicit_residual == r2.log.explicit_residual
+    assert r1.log.relative_error == r2.log.relative_error
+    assert np.array_equal(r1.x, r2.x)
+
+
+def test_device_resident_matches_host_entry(ctk, problem):
+    import torch
+
+    g, gt, b = problem
+    pair = ctk.projector_pair(to_ctk(g))
+    opts = _opts(ctk, 5)
+    rh = ctk.lsmr(pair, b.astype(np.float32), 30.0, opts)
+    rd = ctk.lsmr(pair, torch.from_numpy(b.astype(np.float32)).cuda(), 30.0, opts)
+    assert np.array_equal(rd.x.cpu().numpy(), rh.x)
+    assert rd.log.explicit_residual == rh.log.explicit_residual
+
+
+def test_solver_errors(ctk):
+    g = to_ctk(parallel2d(16, 8))
+    pair = ctk.projector_pair(g, dtype=np.float64)
+    with pytest.raises(ctk.DegenerateInputError):
+        ctk.cgls(pair, np.zeros(pair.range_size), ctk.SolverOptions())
+    with pytest.raises(ctk.ParameterError):
+        ctk.cgls(pair, np.ones(pair.range_size), ctk.SolverOptions(max_iters=0))
+    with pytest.raises(ctk.ParameterError):
+        ctk.lsqr(pair, np.ones(pair.range_size), ctk.SolverOptions(residual_tolerance=-1.0))
+    with pytest.raises(ctk.ParameterError):
+        ctk.lsmr(pair, np.ones(pair.range_size), -0.5, ctk.SolverOptions())
+    with pytest.raises(ctk.ParameterError):
+        ctk.cgls_tv(pair, np.ones(pair.range_size), 0.0, 1, 1, ctk.SolverOptions())
+    with pytest.raises(ctk.DimensionError):
+        ctk.cgls(pair, np.ones(5), ctk.SolverOptions())
+
+
+def test_observer_sees_iterates(ctk, problem):
+    g, gt, b = problem
+    pair = ctk.projector_pair(to_ctk(g))
+    seen = []
+    opts = _opts(ctk, 3)
+    opts.iterate_observer = lambda k, x: seen.append((k, float(np.linalg.norm(x))))
+    res = ctk.cgls(pair, b.astype(np.float32), opts)
+    assert [k for k, _ in seen] == [1, 2, 3]
+    assert abs(seen[-1][1] - np.linalg.norm(res.x)) < 1e-6 * np.linalg.norm(res.x)
+
+
+def test_blas1_deterministic(ctk):
+    import ctypes as C
+
+    import torch
+
+    lib = ctk.load()
+    x = torch.randn(10_000_019, device="cuda", dtype=torch.float32)
+    y = torch.randn(10_000_019, device="cuda", dtype=torch.float32)
+    outs = []
+    for _ in range(3):
+        d = C.c_double()
+        assert lib.ctk_dot_f32(x.numel(), C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), C.byref(d), None) == 0
+        outs.append(d.value)
+    assert outs[0] == outs[1] == outs[2]
+    want = float((x.double() * y.double()).sum())
+    assert abs(outs[0] - want) <= 1e-12 * abs(want) * 100 + 1e-9
