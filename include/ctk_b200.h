@@ -92,7 +92,8 @@ int ctk_geom_set_bp_partitions(ctk_geom* g, int nparts);
 int ctk_geom_set_stream(ctk_geom* g, void* stream);
 
 /* ---- operators on DEVICE pointers (forward_project, projector.hpp:134-162;
- *      back_project, projector.hpp:283-297).  Asynchronous on `stream`. ---------------- */
+ *      back_project, projector.hpp:283-297).  Asynchronous on `stream` (a cudaStream_t;
+ *      NULL = the legacy default stream, as everywhere in CUDA). ----------------------- */
 int ctk_ax_f32(ctk_geom* g, const float* d_x, float* d_y, void* stream);
 int ctk_ax_f64(ctk_geom* g, const double* d_x, double* d_y, void* stream);
 int ctk_atb_f32(ctk_geom* g, int variant, const float* d_y, float* d_x, void* stream);
@@ -182,6 +183,15 @@ int ctk_solve_dev_f32(ctk_geom* g, int solver, int variant, const float* d_b, do
 int ctk_solve_dev_f64(ctk_geom* g, int solver, int variant, const double* d_b, double lambda,
                       const ctk_hybrid_strategy* s, int outer_iters, int inner_iters, int warm_start,
                       const ctk_solver_opts* o, double* d_x, ctk_solve_log* log);
+
+/* ---- host fp64 projected-problem helpers of hybrid LSQR (no GPU needed).  H is the
+ *      (k+1) x k projected matrix, row-major. ------------------------------------------- */
+/* gcv_lambda, regparam.hpp:114-159 (returns the linear-convention parameter) */
+int ctk_projected_gcv_lambda(const double* H, int k, double beta1, double* out);
+/* dp_lambda, regparam.hpp:79-113 */
+int ctk_projected_dp_lambda(const double* H, int k, double beta1, double noise_level, double* out);
+/* projected_tikhonov, hybrid.hpp:37-55: y (k entries) and the data-fit residual */
+int ctk_projected_tikhonov(const double* H, int k, double beta1, double lambda, double* y, double* fit_resid);
 
 /* ---- multi-GPU angle sharding ------------------------------------- */
 /* Contiguous angle block of rank r among G ranks: [first, first+count). */

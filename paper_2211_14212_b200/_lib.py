@@ -136,6 +136,9 @@ def load():
         "ctk_comm_create_nccl": (i, [vp, i, i, C.POINTER(vp)]),
         "ctk_comm_destroy": (None, [vp]),
         "ctk_launch_count": (C.c_uint64, []),
+        "ctk_projected_gcv_lambda": (i, [pd, i, d, pd]),
+        "ctk_projected_dp_lambda": (i, [pd, i, d, d, pd]),
+        "ctk_projected_tikhonov": (i, [pd, i, d, d, pd, pd]),
     }
     for t in ("f32", "f64"):
         sig[f"ctk_cgls_{t}"] = (i, [vp, i, vp, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])

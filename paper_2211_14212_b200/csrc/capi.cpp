@@ -1,11 +1,13 @@
 // extern "C" surface of libctk_b200.so (include/ctk_b200.h).  Every entry point catches
 // the internal exceptions and returns the status of the reference's error taxonomy
 // (types.hpp:14-31); the message is kept thread-locally for ctk_last_error.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
 
 #include "ctk_internal.h"
+#include "regparam.h"
 
 namespace ctkb {
 Geometry* geometry_create(const ctk_geom_desc* d);
@@ -50,7 +52,9 @@ ctkb::Geometry& G(const ctk_geom* g) {
     return *reinterpret_cast<ctkb::Geometry*>(const_cast<ctk_geom*>(g));
 }
 
-cudaStream_t S(ctkb::Geometry& g, void* stream) { return stream ? static_cast<cudaStream_t>(stream) : g.stream; }
+// Device-pointer entry points follow the CUDA convention: the caller's stream, NULL = the
+// legacy default stream (so work is ordered with the caller's default-stream producers).
+cudaStream_t S(ctkb::Geometry&, void* stream) { return static_cast<cudaStream_t>(stream); }
 
 void check_variant(int v) {
     if (v != CTK_BP_MATCHED && v != CTK_BP_VOXEL_DRIVEN) ctkb::fail(CTK_E_PARAMETER, "unknown backprojector variant");
@@ -315,6 +319,26 @@ int ctk_solve_dev_f64(ctk_geom* g, int solver, int variant, const double* b, dou
                       const ctk_hybrid_strategy* s, int outer, int inner, int warm, const ctk_solver_opts* o, double* x,
                       ctk_solve_log* log) {
     return guard([&] { ctkb::solve_device<double>(G(g), solver, variant, b, lambda, s, outer, inner, warm, o, x, log); });
+}
+
+int ctk_projected_gcv_lambda(const double* H, int k, double beta1, double* out) {
+    return guard([&] {
+        if (!H || !out || k < 1) ctkb::fail(CTK_E_PARAMETER, "projected problem must have a (k+1) x k matrix, k >= 1");
+        *out = ctkb::gcv_lambda(std::vector<double>(H, H + size_t(k + 1) * k), k, beta1);
+    });
+}
+int ctk_projected_dp_lambda(const double* H, int k, double beta1, double nl, double* out) {
+    return guard([&] {
+        if (!H || !out || k < 1) ctkb::fail(CTK_E_PARAMETER, "projected problem must have a (k+1) x k matrix, k >= 1");
+        *out = ctkb::dp_lambda(std::vector<double>(H, H + size_t(k + 1) * k), k, beta1, nl);
+    });
+}
+int ctk_projected_tikhonov(const double* H, int k, double beta1, double lambda, double* y, double* fit) {
+    return guard([&] {
+        if (!H || !y || k < 1) ctkb::fail(CTK_E_PARAMETER, "projected problem must have a (k+1) x k matrix, k >= 1");
+        auto v = ctkb::projected_tikhonov(std::vector<double>(H, H + size_t(k + 1) * k), k, beta1, lambda, fit);
+        std::copy(v.begin(), v.end(), y);
+    });
 }
 
 int ctk_shard_angles(int n_angles, int nranks, int rank, int* first, int* count) {

@@ -20,6 +20,7 @@
 // tap, and the four bilinear taps of a sample need no bounds checks.
 //   proj_t[a][iu][iv] detector columns contiguous (gathers read consecutive rows).
 #include <cfloat>
+#include <cstdlib>
 
 #include "ctk_internal.h"
 #include "reduce.cuh"
@@ -382,6 +383,187 @@ k_atb_matched_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, 
     }
 }
 
+// ---- matched A^T b, plane-driven (v2) ---------------------------------------------------
+// Pass CLASS (0: x-dominant columns, planes x = s, rows p = y; 1: y-dominant columns,
+// planes y = s, rows p = x).  A CTA owns one plane s, PB rows [p0, p0+PB) and a band of
+// KB slices [k0, k0+KB) along z, and loops over all views.  Per view:
+//  phase 1  one thread per candidate detector column iu marches its detector rows iv
+//           (exactly the forward's f32 fz = fmaf(vd, fmaf(s, gd, g0), cz)) and builds the
+//           transposed z-interpolation Z[e][k] = sum_iv wz * (step*y) in shared memory;
+//           it registers itself in the (at most two) rows its in-plane stencil touches;
+//  phase 2  thread p owns row p (KB accumulators in registers) and adds wh * Z[e][:] of
+//           the columns registered in its row, sorted by column -> deterministic order.
+// Work per (voxel, view) is ~ the forward's per-sample work; no candidate search.
+constexpr int BP_PB = 256, BP_KB = 32, BP_ZS = 36, BP_SL = 8;
+
+template <int CLASS>
+__global__ void __launch_bounds__(BP_PB)
+k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, int ptiles) {
+    extern __shared__ __align__(16) float sm[];
+    float* Z = sm;                                        // [BP_PB][BP_ZS]
+    int* lists = reinterpret_cast<int*>(Z + BP_PB * BP_ZS);  // [BP_PB][BP_SL]
+    int* cnt = lists + BP_PB * BP_SL;                     // [BP_PB]
+    float* eth = reinterpret_cast<float*>(cnt + BP_PB);   // [BP_PB]
+    float* vdtab = eth + BP_PB;                           // [nv]
+    __shared__ int s_iu0, s_iu1;
+
+    const int t = threadIdx.x;
+    const int s = blockIdx.y;
+    const int ptile = blockIdx.x % ptiles, kband = blockIdx.x / ptiles;
+    const int p0 = ptile * BP_PB, k0 = kband * BP_KB;
+    const int nh = CLASS ? g.nx : g.ny;
+    const int p = p0 + t;
+    for (int q = t; q < g.nv; q += BP_PB) vdtab[q] = float(row_coord(g, q));
+    const float czf = 0.5f * float(g.nz - 1);
+    const float cvf = 0.5f * float(g.nv - 1);
+    const float invdu = float(1.0 / g.du);
+    const float fs = float(s);
+    const double h = g.h;
+    // world coordinates of the plane and of the tile's row segment ends
+    const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
+    const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
+
+    float acc[BP_KB];
+#pragma unroll
+    for (int m = 0; m < BP_KB; ++m) acc[m] = 0.f;
+
+    for (int a = 0; a < g.na; ++a) {
+        if (t == 0) {
+            const double2 tr = g.ctst[a];
+            bool ok1, ok2;
+            const double u1 = CLASS ? proj_u(g, tr.x, tr.y, r_lo, plane_c, ok1) : proj_u(g, tr.x, tr.y, plane_c, r_lo, ok1);
+            const double u2 = CLASS ? proj_u(g, tr.x, tr.y, r_hi, plane_c, ok2) : proj_u(g, tr.x, tr.y, plane_c, r_hi, ok2);
+            int i0 = 0, i1 = g.nu - 1;
+            if (ok1 && ok2) {
+                i0 = max(i0, int(floor(fmax(fmin(u1, u2), -1e9))) - 1);
+                i1 = min(i1, int(ceil(fmin(fmax(u1, u2), 1e9))) + 1);
+            }
+            s_iu0 = i0;
+            s_iu1 = i1;
+        }
+        __syncthreads();
+        const int iu0 = s_iu0, iu1 = s_iu1;
+        __syncthreads();  // s_iu* is rewritten for the next view
+        for (int cbase = iu0; cbase <= iu1; cbase += BP_PB) {
+            // ---- phase 1 ----
+            cnt[t] = 0;
+            __syncthreads();
+            const int iu = cbase + t;
+            if (iu <= iu1) {
+                const int c = a * g.nu + iu;
+                if (g.colaxis[c] == CLASS) {
+                    const float4 cd = g.col[c];
+                    const float fh = fmaf(fs, cd.y, cd.x);
+                    const float fih = floorf(fh);
+                    const int ih = int(fih);
+                    const float th = fh - fih;
+                    if (ih + 1 >= p0 && ih <= p0 + BP_PB - 1 && ih + 1 >= 0 && ih < nh) {
+                        float* zr = Z + t * BP_ZS;
+#pragma unroll
+                        for (int m = 0; m < BP_KB; ++m) zr[m] = 0.f;
+                        const float gs = fmaf(fs, cd.w, cd.z);
+                        int v0 = 0, v1 = g.nv - 1;
+                        if (gs > 0.f) {
+                            const float rg = invdu / gs;
+                            v0 = max(v0, int(floorf(fmaf(float(k0) - 1.f - czf, rg, cvf))) - 1);
+                            v1 = min(v1, int(ceilf(fmaf(float(k0 + BP_KB) - czf, rg, cvf))) + 1);
+                        }
+                        const double dA = g.colstep[c].y;
+                        const float* pc = pt + size_t(c) * g.nv;
+                        for (int iv = v0; iv <= v1; ++iv) {
+                            if (g.has_zrays && fabs(row_coord(g, iv)) > dA) continue;
+                            const float fz = fmaf(vdtab[iv], gs, czf);
+                            const float fiz = floorf(fz);
+                            const int kk = int(fiz) - k0;
+                            const float tz = fz - fiz;
+                            if (kk < -1 || kk >= BP_KB) continue;
+                            const float yv = __ldg(pc + iv);
+                            if (kk >= 0) zr[kk] = fmaf(1.f - tz, yv, zr[kk]);
+                            if (kk + 1 < BP_KB) zr[kk + 1] = fmaf(tz, yv, zr[kk + 1]);
+                        }
+                        eth[t] = th;
+                        if (ih >= p0) {
+                            const int sl = atomicAdd(&cnt[ih - p0], 1);
+                            if (sl < BP_SL) lists[(ih - p0) * BP_SL + sl] = (t << 1);
+                        }
+                        if (ih + 1 <= p0 + BP_PB - 1 && th != 0.f) {
+                            const int sl = atomicAdd(&cnt[ih + 1 - p0], 1);
+                            if (sl < BP_SL) lists[(ih + 1 - p0) * BP_SL + sl] = (t << 1) | 1;
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            // ---- phase 2: row p gathers its registered columns in column order ----
+            const int n = cnt[t];
+            if (n > 0 && p < nh) {
+                if (n <= BP_SL) {
+                    int lst[BP_SL];
+#pragma unroll
+                    for (int q = 0; q < BP_SL; ++q) lst[q] = q < n ? lists[t * BP_SL + q] : 0x7fffffff;
+#pragma unroll
+                    for (int i = 1; i < BP_SL; ++i)
+#pragma unroll
+                        for (int j = BP_SL - 1; j >= i; --j)
+                            if (lst[j - 1] > lst[j]) { const int tmp = lst[j]; lst[j] = lst[j - 1]; lst[j - 1] = tmp; }
+#pragma unroll
+                    for (int q = 0; q < BP_SL; ++q) {
+                        if (q >= n) break;
+                        const int e = lst[q] >> 1;
+                        const float th = eth[e];
+                        const float wh = (lst[q] & 1) ? th : 1.f - th;
+                        const float4* zr = reinterpret_cast<const float4*>(Z + e * BP_ZS);
+#pragma unroll
+                        for (int m4 = 0; m4 < BP_KB / 4; ++m4) {
+                            const float4 z4 = zr[m4];
+                            acc[4 * m4 + 0] = fmaf(wh, z4.x, acc[4 * m4 + 0]);
+                            acc[4 * m4 + 1] = fmaf(wh, z4.y, acc[4 * m4 + 1]);
+                            acc[4 * m4 + 2] = fmaf(wh, z4.z, acc[4 * m4 + 2]);
+                            acc[4 * m4 + 3] = fmaf(wh, z4.w, acc[4 * m4 + 3]);
+                        }
+                    }
+                } else {
+                    // overflow (very fine detector sampling): scan every column of the chunk in order
+                    for (int e = 0; e < BP_PB && cbase + e <= iu1; ++e) {
+                        const int c = a * g.nu + cbase + e;
+                        if (g.colaxis[c] != CLASS) continue;
+                        const float4 cd = g.col[c];
+                        const float fh = fmaf(fs, cd.y, cd.x);
+                        const float fih = floorf(fh);
+                        const int ih = int(fih);
+                        const float th = fh - fih;
+                        float wh;
+                        if (ih == p) wh = 1.f - th;
+                        else if (ih + 1 == p && th != 0.f) wh = th;
+                        else continue;
+                        const float4* zr = reinterpret_cast<const float4*>(Z + e * BP_ZS);
+#pragma unroll
+                        for (int m4 = 0; m4 < BP_KB / 4; ++m4) {
+                            const float4 z4 = zr[m4];
+                            acc[4 * m4 + 0] = fmaf(wh, z4.x, acc[4 * m4 + 0]);
+                            acc[4 * m4 + 1] = fmaf(wh, z4.y, acc[4 * m4 + 1]);
+                            acc[4 * m4 + 2] = fmaf(wh, z4.z, acc[4 * m4 + 2]);
+                            acc[4 * m4 + 3] = fmaf(wh, z4.w, acc[4 * m4 + 3]);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (p < nh) {
+#pragma unroll
+        for (int m = 0; m < BP_KB; ++m) {
+            const int k = k0 + m;
+            if (k >= g.nz) break;
+            const size_t o = CLASS ? size_t(p) + size_t(g.nx) * (size_t(s) + size_t(g.ny) * k)
+                                   : size_t(s) + size_t(g.nx) * (size_t(p) + size_t(g.ny) * k);
+            if (CLASS == 0) x[o] = acc[m];
+            else x[o] += acc[m];
+        }
+    }
+}
+
 // z-dominant rays of the matched transpose (only launched when the geometry has them):
 // thread per voxel, candidates from the footprint of the cube [voxel +- h]^3.
 __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x) {
@@ -564,6 +746,23 @@ void launch_matched(Geometry& g, float* x, cudaStream_t s) {
     after_launch("k_atb_matched_f32");
 }
 
+template <int CLASS>
+void launch_plane(Geometry& g, float* x, cudaStream_t s) {
+    const int nh = CLASS ? g.nx : g.ny;
+    const int planes = CLASS ? g.ny : g.nx;
+    const int ptiles = (nh + BP_PB - 1) / BP_PB;
+    const int kbands = (g.nz + BP_KB - 1) / BP_KB;
+    const size_t smem = sizeof(float) * (size_t(BP_PB) * BP_ZS + size_t(BP_PB) * BP_SL + 2 * BP_PB + g.nv);
+    static size_t configured = 0;
+    if (smem > configured) {
+        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        configured = smem;
+    }
+    dim3 grd(unsigned(ptiles * kbands), unsigned(planes));
+    k_atb_plane_f32<CLASS><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
+    after_launch("k_atb_plane_f32");
+}
+
 template <int KZ>
 void launch_voxel(Geometry& g, float* x, cudaStream_t s) {
     const int kblocks = (g.nz + 32 * KZ - 1) / (32 * KZ);
@@ -604,12 +803,21 @@ void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out,
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
     transpose_proj<true>(g, y, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    switch (pick_kz(g.nz)) {
-        case 1: launch_matched<1>(g, x, s); break;
-        case 2: launch_matched<2>(g, x, s); break;
-        case 4: launch_matched<4>(g, x, s); break;
-        case 8: launch_matched<8>(g, x, s); break;
-        default: launch_matched<16>(g, x, s); break;
+    static const bool column_gather = [] {
+        const char* e = std::getenv("CTK_BP_ALGO");
+        return e && e[0] == '1';
+    }();
+    if (column_gather) {
+        switch (pick_kz(g.nz)) {
+            case 1: launch_matched<1>(g, x, s); break;
+            case 2: launch_matched<2>(g, x, s); break;
+            case 4: launch_matched<4>(g, x, s); break;
+            case 8: launch_matched<8>(g, x, s); break;
+            default: launch_matched<16>(g, x, s); break;
+        }
+    } else {
+        launch_plane<0>(g, x, s);
+        launch_plane<1>(g, x, s);
     }
     CTK_CUDA(cudaEventRecord(g.ev1, s));
     if (g.has_zrays) {

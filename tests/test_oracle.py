@@ -1,0 +1,204 @@
+"""CPU tests pinning the oracle (test infrastructure) before it is trusted as a checker:
+the C restatement is bit-identical to the compiled reference, reproduces the reference's
+own known-answer tests (test_operators.cpp), and matches the committed golden fixtures;
+the numpy solver restatement matches the reference solvers."""
+import glob
+import math
+import os
+
+import numpy as np
+import pytest
+
+from geoms import ALL, cone_adjoint, parallel2d
+from conftest import rel_l2
+
+from oracle.oracle import (Geom, adjoint_discrepancy, cgls, cgls_tv, dp_lambda, gcv_lambda, hybrid_lsqr, lsmr, lsqr,
+                           ray_box_chord)
+
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
+
+
+def _geom_from(d):
+    return Geom(int(d["mode"]), float(d["dso"]), float(d["dod"]), float(d["du"]), int(d["nu"]), int(d["nv"]),
+                int(d["nx"]), int(d["ny"]), int(d["nz"]), float(d["h"]), np.asarray(d["angles"]))
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_restated_matches_golden(restated, path):
+    d = np.load(path)
+    g = _geom_from(d)
+    assert np.array_equal(restated.forward(g, d["x"]), d["ax"])
+    assert np.array_equal(restated.forward(g, d["x"].astype(np.float32)), d["ax_f32"])
+    assert np.array_equal(restated.back(g, d["y"], 0, 1), d["atb_matched"])
+    assert np.array_equal(restated.back(g, d["y"], 1), d["atb_voxel"])
+
+
+@pytest.mark.parametrize("path", GOLDEN, ids=[os.path.basename(p) for p in GOLDEN])
+def test_numpy_solvers_match_golden(restated, path):
+    d = np.load(path)
+    g = _geom_from(d)
+    fwd = lambda v: restated.forward(g, v)  # noqa: E731
+    back = lambda v: restated.back(g, v)  # noqa: E731
+    for name, fn in (("cgls", cgls), ("lsqr", lsqr)):
+        r = fn(fwd, back, d["b"], 5, tol=0.0, stop_inc=False)
+        assert rel_l2(r["x"], d[f"{name}_x"]) < 1e-10
+        assert np.allclose(r["explicit"], d[f"{name}_explicit"], rtol=1e-10)
+    r = lsmr(fwd, back, d["b"], 3.0, 5, tol=0.0, stop_inc=False)
+    assert rel_l2(r["x"], d["lsmr_x"]) < 1e-10
+    assert np.allclose(r["implicit"], d["lsmr_implicit"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_restated_bit_exact_vs_reference(restated, reference, name, dtype):
+    g = ALL[name]()
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(g.domain_size).astype(dtype)
+    y = rng.standard_normal(g.range_size).astype(dtype)
+    assert np.array_equal(restated.forward(g, x), reference.forward(g, x))
+    assert np.array_equal(restated.back(g, y, 1), reference.back(g, y, 1))
+    for p in (1, 4):
+        reference.set_threads(p)
+        try:
+            assert np.array_equal(restated.back(g, y, 0, p), reference.back(g, y, 0))
+        finally:
+            reference.set_threads(1)
+
+
+def test_walk_parameters(restated):
+    g = ALL["cone_ragged"]()
+    ax, w = restated.walk(g, 2, 3, 4)
+    assert ax in (0, 1, 2) and w[0] >= g.h
+
+
+# ---- known-answer tests of test_operators.cpp on the oracle ---------------------------------
+def test_kat_zero(restated):
+    g = parallel2d(16, 12)
+    assert np.all(restated.forward(g, np.zeros(g.domain_size)) == 0)
+    assert np.all(restated.back(g, np.zeros(g.range_size)) == 0)
+
+
+def test_kat_constant_row(restated):
+    n, h, c = 5, 0.7, 1.3
+    g = Geom(0, 0.0, n * h, h, n, 1, n, n, 1, h, np.array([0.0]))
+    y = restated.forward(g, np.full(n * n, c))
+    assert y[n // 2] == pytest.approx(n * h * c, rel=1e-12)
+
+
+def test_kat_impulse_chord(restated):
+    h, th, n = 0.9, 0.3, 7
+    g = Geom(0, 0.0, n * h, h, 1, 1, n, n, 1, h, np.array([th]))
+    x = np.zeros(n * n)
+    x[n // 2 + n * (n // 2)] = 1
+    chord = ray_box_chord([0, 0, 0], [-math.cos(th), -math.sin(th), 0], [-h / 2] * 3, [h / 2] * 3)
+    assert restated.forward(g, x)[0] == pytest.approx(chord, rel=1e-12)
+    g = Geom(2, 4.0 * n * h, 2.0 * n * h, h, 1, 1, n, n, n, h, np.array([th]))
+    x = np.zeros(n ** 3)
+    x[n // 2 + n * (n // 2 + n * (n // 2))] = 1
+    o = [g.dso * math.cos(th), g.dso * math.sin(th), 0.0]
+    nn = math.hypot(o[0], o[1])
+    chord = ray_box_chord(o, [-o[0] / nn, -o[1] / nn, 0.0], [-h / 2] * 3, [h / 2] * 3)
+    assert restated.forward(g, x)[0] == pytest.approx(chord, rel=1e-12)
+
+
+def test_kat_linearity_periodicity(restated):
+    g = parallel2d(24, 10)
+    rng = np.random.default_rng(7)
+    x, y = rng.standard_normal(g.domain_size), rng.standard_normal(g.domain_size)
+    pc = restated.forward(g, 1.7 * x - 0.4 * y)
+    assert rel_l2(pc, 1.7 * restated.forward(g, x) - 0.4 * restated.forward(g, y)) < 1e-10
+    for th in (0.0, 0.5, 1.25, 5.0):
+        g1, g2 = parallel2d(16, 1), parallel2d(16, 1)
+        g1.angles, g2.angles = np.array([th]), np.array([th + 2 * math.pi])
+        v = rng.standard_normal(256)
+        assert np.array_equal(restated.forward(g1, v), restated.forward(g2, v))
+
+
+def test_kat_adjoint(restated):
+    for g, trials, seed in ((parallel2d(32, 24), 30, 42), (cone_adjoint(), 10, 4)):
+        f = lambda v, g=g: restated.forward(g, v)  # noqa: E731
+        b = lambda v, g=g: restated.back(g, v)  # noqa: E731
+        assert adjoint_discrepancy(f, b, g.domain_size, g.range_size, trials, seed) < 1e-10
+    g = parallel2d(32, 24)
+    bv = lambda v: restated.back(g, v, 1)  # noqa: E731
+    assert adjoint_discrepancy(lambda v: restated.forward(g, v), bv, g.domain_size, g.range_size, 20, 43) > 1e-3
+
+
+def test_gradient_and_weights_vs_reference(restated, reference):
+    rng = np.random.default_rng(5)
+    shape = (9, 7, 5)
+    v = rng.standard_normal(int(np.prod(shape)))
+    d = restated.gradient(shape, v)
+    import ctypes as C
+
+    want = [np.zeros_like(v) for _ in range(3)]
+    reference.lib.ref_gradient_f64(*shape, v.ctypes.data_as(C.POINTER(C.c_double)),
+                                   *[w.ctypes.data_as(C.POINTER(C.c_double)) for w in want])
+    for a, b in zip(d, want):
+        assert np.array_equal(a, b)
+    adj = restated.gradient_adjoint(shape, *d)
+    want_adj = np.zeros_like(v)
+    reference.lib.ref_gradient_adjoint_f64(*shape, *[w.ctypes.data_as(C.POINTER(C.c_double)) for w in want],
+                                           want_adj.ctypes.data_as(C.POINTER(C.c_double)))
+    assert np.array_equal(adj, want_adj)
+    assert np.array_equal(restated.tv_weights(shape, v), reference.tv_weights(shape, v))
+
+
+# ---- numpy solver restatement vs the reference solvers -------------------------------------
+@pytest.fixture(scope="module")
+def small_problem(restated):
+    from geoms import cone_bench
+
+    g = cone_bench(16, 12)
+    gt = restated.shepp_logan_3d(16, np.float64)
+    return g, gt, restated.forward(g, gt)
+
+
+@pytest.mark.parametrize("solver", ["cgls", "lsqr", "lsmr"])
+def test_numpy_solvers_vs_reference(restated, reference, small_problem, solver):
+    g, gt, b = small_problem
+    f = lambda v: restated.forward(g, v)  # noqa: E731
+    bk = lambda v: restated.back(g, v)  # noqa: E731
+    lam = 30.0 if solver == "lsmr" else 0.0
+    want = reference.solve(g, b, solver, 10, lam=lam, tol=0.0, stop_inc=False, gt=gt)
+    got = (lsmr(f, bk, b, lam, 10, tol=0.0, stop_inc=False, gt=gt) if solver == "lsmr"
+           else {"cgls": cgls, "lsqr": lsqr}[solver](f, bk, b, 10, tol=0.0, stop_inc=False, gt=gt))
+    assert rel_l2(got["x"], want["x"]) < 1e-9
+    assert np.allclose(got["explicit"], want["explicit"], rtol=1e-9)
+    assert np.allclose(got["implicit"], want["implicit"], rtol=1e-9)
+    assert np.allclose(got["relative_error"], want["relative_error"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("strategy", ["gcv", "dp", "fixed"])
+def test_numpy_hybrid_vs_reference(restated, reference, small_problem, strategy):
+    g, gt, b = small_problem
+    f = lambda v: restated.forward(g, v)  # noqa: E731
+    bk = lambda v: restated.back(g, v)  # noqa: E731
+    sid = {"fixed": 0, "dp": 1, "gcv": 2}[strategy]
+    want = reference.solve(g, b, "hybrid_lsqr", 8, strategy=sid, lam=0.5, noise_level=0.01, tol=0.0, stop_inc=False)
+    got = hybrid_lsqr(f, bk, b, 8, strategy=strategy, lam=0.5, nl=0.01, tol=0.0, stop_inc=False)
+    assert rel_l2(got["x"], want["x"]) < 1e-7
+    assert np.allclose(got["explicit"], want["explicit"], rtol=1e-7)
+    assert np.allclose(got["lambda"], want["lambda"], rtol=1e-5, atol=1e-12)
+
+
+def test_numpy_cgls_tv_vs_reference(restated, reference, small_problem):
+    g, gt, b = small_problem
+    f = lambda v: restated.forward(g, v)  # noqa: E731
+    bk = lambda v: restated.back(g, v)  # noqa: E731
+    want = reference.solve(g, b, "cgls_tv", 1, lam=0.5, outer=2, inner=4, tol=0.0, stop_inc=False)
+    got = cgls_tv(f, bk, b, (16, 16, 16), 0.5, 2, 4, restated, tol=0.0, stop_inc=False)
+    assert rel_l2(got["x"], want["x"]) < 1e-9
+    assert np.allclose(got["explicit"], want["explicit"], rtol=1e-9)
+    assert list(got["outer_starts"]) == list(want["outer_starts"])
+
+
+def test_regparam_numpy_vs_reference(reference):
+    rng = np.random.default_rng(1)
+    for k in (1, 3, 7, 15):
+        H = np.zeros((k + 1, k))
+        for j in range(k):
+            H[j, j] = 1.0 + rng.random()
+            H[j + 1, j] = 0.5 * rng.random()
+        assert gcv_lambda(H, 2.0) == pytest.approx(reference.gcv_lambda(H, 2.0), rel=1e-6)
+        assert dp_lambda(H, 2.0, 0.05) == pytest.approx(reference.dp_lambda(H, 2.0, 0.05), rel=1e-6, abs=1e-14)
