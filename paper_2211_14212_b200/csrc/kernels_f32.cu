@@ -14,10 +14,10 @@
 // a dominant z component (steep cone rows) take a generic per-ray path.
 //
 // Layouts in HBM (f32):
-//   vx[i][k+1][j+1]  (ny+2)x(nz+2) zero-padded plane per x-slice  (x-dominant rays)
-//   vy[j][k+1][i+1]  (nx+2)x(nz+2) zero-padded plane per y-slice  (y-dominant rays)
-// so that a warp of 32 consecutive detector columns reads 32 consecutive addresses per
-// tap, and the four bilinear taps of a sample need no bounds checks.
+//   qx[i][k+1][j+1]  bilinear quads (16 B) of each x-slice plane      (x-dominant rays)
+//   qy[j][k+1][i+1]  bilinear quads (16 B) of each y-slice plane      (y-dominant rays)
+// so that a warp of 32 consecutive detector columns reads 32 consecutive quads per
+// sample: one 16-byte load, no bounds checks (zero padding is in the quads).
 //   proj_t[a][iu][iv] detector columns contiguous (gathers read consecutive rows).
 #include <cfloat>
 #include <cstdlib>
@@ -128,39 +128,68 @@ __device__ float march_generic(const KGeom& g, const WalkF& w, const float* __re
     }
     return w.step * acc;
 }
-
-// ---- relayout: x[i + nx(j + ny k)] -> vx / vy padded planes ----------------------------
-// vy[j][k+1][i+1]: x stays fastest (coalesced both ways)
-__global__ void k_relayout_y(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ vy) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int k = blockIdx.y;
-    const int j = blockIdx.z;
-    if (i >= nx) return;
-    const size_t pitch = size_t(nx) + 2, plane = pitch * (size_t(nz) + 2);
-    vy[size_t(j) * plane + size_t(k + 1) * pitch + i + 1] = __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k));
+// ---- quad relayout: x[i + nx(j + ny k)] -> bilinear quads per slice plane -------------
+// qx[i][k+1][j+1] = (v(i,j,k), v(i,j+1,k), v(i,j,k+1), v(i,j+1,k+1))   x-dominant rays
+// qy[j][k+1][i+1] = (v(i,j,k), v(i+1,j,k), v(i,j,k+1), v(i+1,j,k+1))   y-dominant rays
+// for in-plane indices h in [-1, nh-1] and k in [-1, nz-1]; taps outside the volume are 0
+// (Joseph's zero padding, projector.hpp:108).  One 16-byte load per bilinear sample.
+__device__ __forceinline__ float vox(const float* __restrict__ x, int nx, int ny, int nz, int i, int j, int k) {
+    return (i >= 0 && i < nx && j >= 0 && j < ny && k >= 0 && k < nz)
+               ? __ldg(x + size_t(i) + size_t(nx) * (size_t(j) + size_t(ny) * k))
+               : 0.f;
 }
 
-// vx[i][k+1][j+1]: 32x32 tile transpose of (i, j) per z-plane
-__global__ void k_relayout_x(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ vx) {
-    __shared__ float tile[32][33];
-    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32, k = blockIdx.z;
-    const size_t pitch = size_t(ny) + 2, plane = pitch * (size_t(nz) + 2);
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int i = i0 + threadIdx.x, j = j0 + r;
-        tile[r][threadIdx.x] = (i < nx && j < ny) ? __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k)) : 0.f;
+__global__ void k_quads_y(int nx, int ny, int nz, const float* __restrict__ x, float4* __restrict__ qy) {
+    const int io = blockIdx.x * blockDim.x + threadIdx.x;  // i + 1
+    const int ko = blockIdx.y;                             // k + 1
+    const int j = blockIdx.z;
+    if (io > nx) return;
+    const int i = io - 1, k = ko - 1;
+    const size_t pitch = size_t(nx) + 1, plane = pitch * (size_t(nz) + 1);
+    qy[size_t(j) * plane + size_t(ko) * pitch + io] =
+        make_float4(vox(x, nx, ny, nz, i, j, k), vox(x, nx, ny, nz, i + 1, j, k), vox(x, nx, ny, nz, i, j, k + 1),
+                    vox(x, nx, ny, nz, i + 1, j, k + 1));
+}
+
+// 32(i) x 33(j) x 2(k) tile through shared memory so both the reads (along i) and the
+// quad writes (along j) are coalesced
+__global__ void k_quads_x(int nx, int ny, int nz, const float* __restrict__ x, float4* __restrict__ qx) {
+    __shared__ float tile[2][33][33];
+    const int i0 = blockIdx.x * 32, jo0 = blockIdx.y * 32, ko = blockIdx.z;
+    const int k = ko - 1;
+    for (int r = threadIdx.y; r < 2 * 33; r += blockDim.y) {
+        const int kz = r / 33, jj = r % 33;
+        tile[kz][jj][threadIdx.x] = vox(x, nx, ny, nz, i0 + threadIdx.x, jo0 - 1 + jj, k + kz);
     }
     __syncthreads();
+    const size_t pitch = size_t(ny) + 1, plane = pitch * (size_t(nz) + 1);
+    const int jo = jo0 + threadIdx.x;  // j + 1
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int i = i0 + r, j = j0 + threadIdx.x;
-        if (i < nx && j < ny) vx[size_t(i) * plane + size_t(k + 1) * pitch + j + 1] = tile[threadIdx.x][r];
+        const int i = i0 + r;
+        if (i < nx && jo <= ny) {
+            const int jj = threadIdx.x;  // tile row of j = jo - 1
+            qx[size_t(i) * plane + size_t(ko) * pitch + jo] =
+                make_float4(tile[0][jj][r], tile[0][jj + 1][r], tile[1][jj][r], tile[1][jj + 1][r]);
+        }
     }
+}
+
+// floor without the conversion pipe: t = (f - 0.5) + 1.5*2^23 rounds to an integer n with
+// n = floor(f) except at exact integers, where n may be f - 1 with frac 1.0 -- the same
+// bilinear weights (1 on tap f).  Valid for |f| < 2^22.
+__device__ __forceinline__ void split(float f, int& i, float& frac) {
+    const float M = 12582912.0f;
+    const float t = __fadd_rn(__fadd_rn(f, -0.5f), M);
+    const float fi = __fadd_rn(t, -M);
+    i = __float_as_int(t) - __float_as_int(M);
+    frac = __fadd_rn(f, -fi);
 }
 
 // ---- forward projection ----------------------------------------------------------------
 // RESID=false: y[a][iv][iu] = A x.   RESID=true: per-block partial of sum (Ax - b)^2.
 template <bool RESID>
 __global__ void __launch_bounds__(FWD_BX * FWD_BY)
-k_ax_f32(KGeom g, const float* __restrict__ vx, const float* __restrict__ vy, const float* __restrict__ xs,
+k_ax_f32(KGeom g, const float4* __restrict__ qx, const float4* __restrict__ qy, const float* __restrict__ xs,
          float* __restrict__ y, const float* __restrict__ b, double* __restrict__ partials) {
     const int iu = blockIdx.x * FWD_BX + threadIdx.x;
     const int iv = blockIdx.y * FWD_BY + threadIdx.y;
@@ -171,7 +200,7 @@ k_ax_f32(KGeom g, const float* __restrict__ vx, const float* __restrict__ vy, co
         const int c = a * g.nu + iu;
         const double2 cs = g.colstep[c];
         const double v = row_coord(g, iv);
-        if (is_zray(g, cs, v)) {
+        if (g.has_zrays && is_zray(g, cs, v)) {
             const double2 tr = g.ctst[a];
             WalkF w;
             walk_generic(g, tr.x, tr.y, iu, iv, w);
@@ -181,30 +210,34 @@ k_ax_f32(KGeom g, const float* __restrict__ vx, const float* __restrict__ vy, co
             const int A = g.colaxis[c];
             const int nh = A ? g.nx : g.ny;
             const int ns = A ? g.ny : g.nx;
-            const int pitch = nh + 2;
-            const size_t plane = size_t(pitch) * (g.nz + 2);
-            const float* base = (A ? vy : vx) + pitch + 1;
+            const int pitch = nh + 1;
+            const int plane = pitch * (g.nz + 1);
+            const float4* base = (A ? qy : qx) + pitch + 1;  // quad of (h, z) at base[z*pitch + h]
             const float vd = float(v);
             const float czf = 0.5f * float(g.nz - 1);
             int s0 = 0, s1 = ns - 1;
             clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
             clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
             float acc = 0.f;
+            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+#pragma unroll 4
             for (int s = s0; s <= s1; ++s) {
                 const float fs = float(s);
                 const float fh = fmaf(fs, cd.y, cd.x);
                 const float gs = fmaf(fs, cd.w, cd.z);
                 const float fz = fmaf(vd, gs, czf);
-                const float fih = floorf(fh), fiz = floorf(fz);
-                const int ih = int(fih), iz = int(fiz);
-                if (ih < -1 || ih >= nh || iz < -1 || iz >= g.nz) continue;
-                const float th = fh - fih, tz = fz - fiz;
-                const float* p = base + size_t(s) * plane + iz * pitch + ih;
-                const float v00 = __ldg(p), v10 = __ldg(p + 1);
-                const float v01 = __ldg(p + pitch), v11 = __ldg(p + pitch + 1);
-                const float a0 = fmaf(th, v10 - v00, v00);
-                const float a1 = fmaf(th, v11 - v01, v01);
-                acc += fmaf(tz, a1 - a0, a0);
+                int ih, iz;
+                float th, tz;
+                split(fh, ih, th);
+                split(fz, iz, tz);
+                // sample inside the padded plane <=> some tap inside the volume
+                const bool in = unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
+                const int off = in ? s * plane + iz * pitch + ih : -pitch - 1;  // -pitch-1: quad (-1,-1), in bounds
+                const float4 q = __ldg(base + off);
+                const float a0 = fmaf(th, q.y - q.x, q.x);
+                const float a1 = fmaf(th, q.w - q.z, q.z);
+                const float smp = fmaf(tz, a1 - a0, a0);
+                acc += in ? smp : 0.f;
             }
             out = ray_step(g, cs, v) * acc;
         }
@@ -261,150 +294,30 @@ __device__ __forceinline__ double proj_u(const KGeom& g, double ct, double st, d
     return (-x * st + y * ct) / g.du + 0.5 * (g.nu - 1);
 }
 
-// ---- matched A^T b: exact transpose of k_ax_f32 as a deterministic gather ---------------
-// One warp per voxel column (i, j) and block of 32*KZ slices along z; lane l owns
-// k = kb + l + 32 m.  The per-(column, view) horizontal work (candidate detector
-// columns, in-plane weight) is warp-uniform; the per-voxel part gathers along the
-// contiguous detector column proj_t[a][iu][:], so lanes read consecutive rows.
-template <int KZ>
-__global__ void __launch_bounds__(128)
-k_atb_matched_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, int kblocks) {
-    extern __shared__ float vdtab[];  // detector row coordinates as f32 (same values as k_ax_f32)
-    for (int t = threadIdx.x + blockDim.x * threadIdx.y; t < g.nv; t += blockDim.x * blockDim.y)
-        vdtab[t] = float(row_coord(g, t));
-    __syncthreads();
-    const int lane = threadIdx.x;
-    const long wid = long(blockIdx.x) * blockDim.y + threadIdx.y;
-    const long ncol = long(g.nx) * g.ny;
-    if (wid >= ncol * kblocks) return;
-    const int kb = int(wid / ncol) * 32 * KZ;
-    const long col = wid % ncol;
-    const int i = int(col % g.nx), j = int(col / g.nx);
-    const double h = g.h;
-    const double xc = (i - 0.5 * (g.nx - 1)) * h, yc = (j - 0.5 * (g.ny - 1)) * h;
-    const float czf = 0.5f * float(g.nz - 1);
-    const float cvf = 0.5f * float(g.nv - 1);
-    const float invdu = float(1.0 / g.du);
-    float acc[KZ];
-#pragma unroll
-    for (int m = 0; m < KZ; ++m) acc[m] = 0.f;
-
-    for (int a = 0; a < g.na; ++a) {
-        const double2 tr = g.ctst[a];
-        // candidate columns: footprint of the in-plane stencil segments
-        // {(x_i, y_j +- h)} (x-dominant rays) and {(x_i +- h, y_j)} (y-dominant rays)
-        double umin = DBL_MAX, umax = -DBL_MAX;
-        bool ok = true;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            bool okq;
-            const double px = xc + (q == 0 ? -h : (q == 1 ? h : 0.0));
-            const double py = yc + (q == 2 ? -h : (q == 3 ? h : 0.0));
-            const double fu = proj_u(g, tr.x, tr.y, px, py, okq);
-            ok = ok && okq;
-            umin = fmin(umin, fu);
-            umax = fmax(umax, fu);
-        }
-        int iu0 = 0, iu1 = g.nu - 1;
-        if (ok) {
-            iu0 = max(iu0, int(floor(fmax(umin, -1e9))) - 1);
-            iu1 = min(iu1, int(ceil(fmin(umax, 1e9))) + 1);
-        }
-        for (int iu = iu0; iu <= iu1; ++iu) {
-            const int c = a * g.nu + iu;
-            const int A = g.colaxis[c];
-            const float4 cd = g.col[c];
-            const int s = A ? j : i;
-            const int pos = A ? i : j;
-            const float fs = float(s);
-            const float fh = fmaf(fs, cd.y, cd.x);
-            const float fih = floorf(fh);
-            const int ih = int(fih);
-            const float th = fh - fih;
-            float wh;
-            if (pos == ih) wh = 1.f - th;
-            else if (pos == ih + 1) wh = th;
-            else continue;
-            if (wh == 0.f) continue;
-            const float gs = fmaf(fs, cd.w, cd.z);
-            const double dA = g.colstep[c].y;
-            const float* pc = pt + size_t(c) * g.nv;
-            if (gs > 0.f) {
-                // rows with floor(fz) in {k-1, k}: vd in ((k-1-cz)/gs, (k+1-cz)/gs)
-                const float rg = invdu / gs;
-#pragma unroll
-                for (int m = 0; m < KZ; ++m) {
-                    const int k = kb + lane + 32 * m;
-                    if (k >= g.nz) break;
-                    const float kc = float(k) - czf;
-                    const int r0 = max(0, int(floorf(fmaf(kc - 1.f, rg, cvf) - 1e-3f)));
-                    const int r1 = min(g.nv - 1, int(ceilf(fmaf(kc + 1.f, rg, cvf) + 1e-3f)));
-                    for (int iv = r0; iv <= r1; ++iv) {
-                        const float vd = vdtab[iv];
-                        if (g.has_zrays && fabs(row_coord(g, iv)) > dA) continue;  // z-ray: other pass
-                        const float fz = fmaf(vd, gs, czf);
-                        const float fiz = floorf(fz);
-                        const int iz = int(fiz);
-                        const float tz = fz - fiz;
-                        float wz;
-                        if (k == iz) wz = 1.f - tz;
-                        else if (k == iz + 1) wz = tz;
-                        else continue;
-                        acc[m] = fmaf(wh * wz, __ldg(pc + iv), acc[m]);
-                    }
-                }
-            } else {
-                // degenerate geometry (stencil point not in front of the source): scan all rows
-#pragma unroll
-                for (int m = 0; m < KZ; ++m) {
-                    const int k = kb + lane + 32 * m;
-                    if (k >= g.nz) break;
-                    for (int iv = 0; iv < g.nv; ++iv) {
-                        const float vd = vdtab[iv];
-                        if (g.has_zrays && fabs(row_coord(g, iv)) > dA) continue;
-                        const float fz = fmaf(vd, gs, czf);
-                        const float fiz = floorf(fz);
-                        const int iz = int(fiz);
-                        const float tz = fz - fiz;
-                        float wz;
-                        if (k == iz) wz = 1.f - tz;
-                        else if (k == iz + 1) wz = tz;
-                        else continue;
-                        acc[m] = fmaf(wh * wz, __ldg(pc + iv), acc[m]);
-                    }
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int m = 0; m < KZ; ++m) {
-        const int k = kb + lane + 32 * m;
-        if (k < g.nz) x[size_t(i) + size_t(g.nx) * (size_t(j) + size_t(g.ny) * k)] = acc[m];
-    }
-}
-
-// ---- matched A^T b, plane-driven (v2) ---------------------------------------------------
+// ---- matched A^T b, plane-driven ------------------------------------------------------
 // Pass CLASS (0: x-dominant columns, planes x = s, rows p = y; 1: y-dominant columns,
-// planes y = s, rows p = x).  A CTA owns one plane s, PB rows [p0, p0+PB) and a band of
-// KB slices [k0, k0+KB) along z, and loops over all views.  Per view:
+// planes y = s, rows p = x).  A CTA owns one plane s, BP_PB rows [p0, p0+BP_PB) and a band
+// of BP_KB slices [k0, k0+BP_KB) along z, and loops over all views.  Per view:
 //  phase 1  one thread per candidate detector column iu marches its detector rows iv
-//           (exactly the forward's f32 fz = fmaf(vd, fmaf(s, gd, g0), cz)) and builds the
-//           transposed z-interpolation Z[e][k] = sum_iv wz * (step*y) in shared memory;
-//           it registers itself in the (at most two) rows its in-plane stencil touches;
-//  phase 2  thread p owns row p (KB accumulators in registers) and adds wh * Z[e][:] of
+//           (exactly the forward's f32 fz = fmaf(vd, fmaf(s, gd, g0), cz); 16-byte column
+//           loads) and accumulates the transposed z-interpolation Z[k][e] = sum wz*(step*y)
+//           in shared memory; it registers itself in the (at most two) rows its in-plane
+//           stencil touches;
+//  phase 2  thread p owns row p (BP_KB accumulators in registers) and adds wh * Z[:][e] of
 //           the columns registered in its row, sorted by column -> deterministic order.
-// Work per (voxel, view) is ~ the forward's per-sample work; no candidate search.
-constexpr int BP_PB = 256, BP_KB = 32, BP_ZS = 36, BP_SL = 8;
+// Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
+// their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
+constexpr int BP_PB = 256, BP_KB = 32, BP_SL = 8;
 
 template <int CLASS>
 __global__ void __launch_bounds__(BP_PB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, int ptiles) {
     extern __shared__ __align__(16) float sm[];
-    float* Z = sm;                                        // [BP_PB][BP_ZS]
-    int* lists = reinterpret_cast<int*>(Z + BP_PB * BP_ZS);  // [BP_PB][BP_SL]
-    int* cnt = lists + BP_PB * BP_SL;                     // [BP_PB]
-    float* eth = reinterpret_cast<float*>(cnt + BP_PB);   // [BP_PB]
-    float* vdtab = eth + BP_PB;                           // [nv]
+    float* Z = sm;                                              // [BP_KB][BP_PB]
+    int* lists = reinterpret_cast<int*>(Z + BP_KB * BP_PB);     // [BP_PB][BP_SL]
+    int* cnt = lists + BP_PB * BP_SL;                           // [BP_PB]
+    float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_PB]
+    float* vdtab = eth + BP_PB;                                 // [nv]
     __shared__ int s_iu0, s_iu1;
 
     const int t = threadIdx.x;
@@ -419,6 +332,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     const float invdu = float(1.0 / g.du);
     const float fs = float(s);
     const double h = g.h;
+    const bool vec4 = (g.nv & 3) == 0;
     // world coordinates of the plane and of the tile's row segment ends
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
@@ -458,9 +372,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                     const int ih = int(fih);
                     const float th = fh - fih;
                     if (ih + 1 >= p0 && ih <= p0 + BP_PB - 1 && ih + 1 >= 0 && ih < nh) {
-                        float* zr = Z + t * BP_ZS;
 #pragma unroll
-                        for (int m = 0; m < BP_KB; ++m) zr[m] = 0.f;
+                        for (int m = 0; m < BP_KB; ++m) Z[m * BP_PB + t] = 0.f;
                         const float gs = fmaf(fs, cd.w, cd.z);
                         int v0 = 0, v1 = g.nv - 1;
                         if (gs > 0.f) {
@@ -470,16 +383,25 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                         }
                         const double dA = g.colstep[c].y;
                         const float* pc = pt + size_t(c) * g.nv;
-                        for (int iv = v0; iv <= v1; ++iv) {
-                            if (g.has_zrays && fabs(row_coord(g, iv)) > dA) continue;
+                        auto add = [&](int iv, float yv) {
+                            if (g.has_zrays && fabs(row_coord(g, iv)) > dA) return;
                             const float fz = fmaf(vdtab[iv], gs, czf);
                             const float fiz = floorf(fz);
                             const int kk = int(fiz) - k0;
                             const float tz = fz - fiz;
-                            if (kk < -1 || kk >= BP_KB) continue;
-                            const float yv = __ldg(pc + iv);
-                            if (kk >= 0) zr[kk] = fmaf(1.f - tz, yv, zr[kk]);
-                            if (kk + 1 < BP_KB) zr[kk + 1] = fmaf(tz, yv, zr[kk + 1]);
+                            if (kk >= 0 && kk < BP_KB) Z[kk * BP_PB + t] = fmaf(1.f - tz, yv, Z[kk * BP_PB + t]);
+                            if (kk + 1 >= 0 && kk + 1 < BP_KB) Z[(kk + 1) * BP_PB + t] = fmaf(tz, yv, Z[(kk + 1) * BP_PB + t]);
+                        };
+                        if (vec4) {
+                            for (int b4 = v0 & ~3; b4 <= v1; b4 += 4) {
+                                const float4 y4 = __ldg(reinterpret_cast<const float4*>(pc + b4));
+                                if (b4 >= v0) add(b4, y4.x);
+                                if (b4 + 1 >= v0 && b4 + 1 <= v1) add(b4 + 1, y4.y);
+                                if (b4 + 2 >= v0 && b4 + 2 <= v1) add(b4 + 2, y4.z);
+                                if (b4 + 3 <= v1) add(b4 + 3, y4.w);
+                            }
+                        } else {
+                            for (int iv = v0; iv <= v1; ++iv) add(iv, __ldg(pc + iv));
                         }
                         eth[t] = th;
                         if (ih >= p0) {
@@ -512,15 +434,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                         const int e = lst[q] >> 1;
                         const float th = eth[e];
                         const float wh = (lst[q] & 1) ? th : 1.f - th;
-                        const float4* zr = reinterpret_cast<const float4*>(Z + e * BP_ZS);
 #pragma unroll
-                        for (int m4 = 0; m4 < BP_KB / 4; ++m4) {
-                            const float4 z4 = zr[m4];
-                            acc[4 * m4 + 0] = fmaf(wh, z4.x, acc[4 * m4 + 0]);
-                            acc[4 * m4 + 1] = fmaf(wh, z4.y, acc[4 * m4 + 1]);
-                            acc[4 * m4 + 2] = fmaf(wh, z4.z, acc[4 * m4 + 2]);
-                            acc[4 * m4 + 3] = fmaf(wh, z4.w, acc[4 * m4 + 3]);
-                        }
+                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_PB + e], acc[m]);
                     }
                 } else {
                     // overflow (very fine detector sampling): scan every column of the chunk in order
@@ -536,15 +451,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                         if (ih == p) wh = 1.f - th;
                         else if (ih + 1 == p && th != 0.f) wh = th;
                         else continue;
-                        const float4* zr = reinterpret_cast<const float4*>(Z + e * BP_ZS);
 #pragma unroll
-                        for (int m4 = 0; m4 < BP_KB / 4; ++m4) {
-                            const float4 z4 = zr[m4];
-                            acc[4 * m4 + 0] = fmaf(wh, z4.x, acc[4 * m4 + 0]);
-                            acc[4 * m4 + 1] = fmaf(wh, z4.y, acc[4 * m4 + 1]);
-                            acc[4 * m4 + 2] = fmaf(wh, z4.z, acc[4 * m4 + 2]);
-                            acc[4 * m4 + 3] = fmaf(wh, z4.w, acc[4 * m4 + 3]);
-                        }
+                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_PB + e], acc[m]);
                     }
                 }
             }
@@ -564,8 +472,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     }
 }
 
-// z-dominant rays of the matched transpose (only launched when the geometry has them):
-// thread per voxel, candidates from the footprint of the cube [voxel +- h]^3.
 __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x) {
     const size_t nvox = size_t(g.nx) * g.ny * g.nz;
     const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -711,20 +617,20 @@ int pick_kz(int nz) {
     return 16;
 }
 
-void relayout(Geometry& g, const float* x, cudaStream_t s) {
-    const size_t nvx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
-    const size_t nvy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
-    if (g.vx.ensure(nvx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vx.p, 0, nvx * sizeof(float), s));
-    if (g.vy.ensure(nvy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vy.p, 0, nvy * sizeof(float), s));
+void build_quads(Geometry& g, const float* x, cudaStream_t s) {
+    const size_t nqx = size_t(g.nx) * (size_t(g.ny) + 1) * (size_t(g.nz) + 1);
+    const size_t nqy = size_t(g.ny) * (size_t(g.nx) + 1) * (size_t(g.nz) + 1);
+    g.vx.ensure(nqx * sizeof(float4));
+    g.vy.ensure(nqy * sizeof(float4));
     {
-        dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.ny + 31) / 32, g.nz);
-        k_relayout_x<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vx.as<float>());
-        after_launch("k_relayout_x");
+        dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.ny + 1 + 31) / 32, g.nz + 1);
+        k_quads_x<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vx.as<float4>());
+        after_launch("k_quads_x");
     }
     {
-        dim3 blk(128), grd((g.nx + 127) / 128, g.nz, g.ny);
-        k_relayout_y<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vy.as<float>());
-        after_launch("k_relayout_y");
+        dim3 blk(128), grd((g.nx + 1 + 127) / 128, g.nz + 1, g.ny);
+        k_quads_y<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vy.as<float4>());
+        after_launch("k_quads_y");
     }
 }
 
@@ -736,23 +642,13 @@ void transpose_proj(Geometry& g, const float* y, cudaStream_t s) {
     after_launch("k_proj_transpose");
 }
 
-template <int KZ>
-void launch_matched(Geometry& g, float* x, cudaStream_t s) {
-    const int kblocks = (g.nz + 32 * KZ - 1) / (32 * KZ);
-    const long warps = long(g.nx) * g.ny * kblocks;
-    dim3 blk(32, 4);
-    const unsigned grd = unsigned((warps + 3) / 4);
-    k_atb_matched_f32<KZ><<<grd, blk, sizeof(float) * g.nv, s>>>(g.kgeom(), g.proj_t.as<float>(), x, kblocks);
-    after_launch("k_atb_matched_f32");
-}
-
 template <int CLASS>
 void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int nh = CLASS ? g.nx : g.ny;
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz + BP_KB - 1) / BP_KB;
-    const size_t smem = sizeof(float) * (size_t(BP_PB) * BP_ZS + size_t(BP_PB) * BP_SL + 2 * BP_PB + g.nv);
+    const size_t smem = sizeof(float) * (size_t(BP_PB) * BP_KB + size_t(BP_PB) * BP_SL + 2 * BP_PB + g.nv);
     static size_t configured = 0;
     if (smem > configured) {
         CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -778,22 +674,22 @@ dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + FWD_BX - 1) / FWD_BX, (g.
 }  // namespace
 
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
-    relayout(g, x, s);
+    build_quads(g, x, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    k_ax_f32<false><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(g.kgeom(), g.vx.as<float>(), g.vy.as<float>(), x, y,
+    k_ax_f32<false><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(g.kgeom(), g.vx.as<float4>(), g.vy.as<float4>(), x, y,
                                                                  nullptr, nullptr);
     after_launch("k_ax_f32");
     CTK_CUDA(cudaEventRecord(g.ev1, s));
 }
 
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
-    relayout(g, x, s);
+    build_quads(g, x, s);
     const dim3 grd = fwd_grid(g);
     const size_t nblk = size_t(grd.x) * grd.y * grd.z;
     g.proj_t.ensure(std::max(g.range() * sizeof(float), nblk * sizeof(double)));
     double* partials = g.proj_t.as<double>();
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    k_ax_f32<true><<<grd, dim3(FWD_BX, FWD_BY), 0, s>>>(g.kgeom(), g.vx.as<float>(), g.vy.as<float>(), x, nullptr, b,
+    k_ax_f32<true><<<grd, dim3(FWD_BX, FWD_BY), 0, s>>>(g.kgeom(), g.vx.as<float4>(), g.vy.as<float4>(), x, nullptr, b,
                                                         partials);
     after_launch("k_ax_f32_residual");
     CTK_CUDA(cudaEventRecord(g.ev1, s));
@@ -803,22 +699,8 @@ void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out,
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
     transpose_proj<true>(g, y, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    static const bool column_gather = [] {
-        const char* e = std::getenv("CTK_BP_ALGO");
-        return e && e[0] == '1';
-    }();
-    if (column_gather) {
-        switch (pick_kz(g.nz)) {
-            case 1: launch_matched<1>(g, x, s); break;
-            case 2: launch_matched<2>(g, x, s); break;
-            case 4: launch_matched<4>(g, x, s); break;
-            case 8: launch_matched<8>(g, x, s); break;
-            default: launch_matched<16>(g, x, s); break;
-        }
-    } else {
-        launch_plane<0>(g, x, s);
-        launch_plane<1>(g, x, s);
-    }
+    launch_plane<0>(g, x, s);
+    launch_plane<1>(g, x, s);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
     if (g.has_zrays) {
         const size_t n = g.domain();
