@@ -1,261 +1,11 @@
-// sm_100a performance kernels for T = float: Joseph forward projection (Ax) and its
-// exact transpose / the voxel-driven backprojection (A^T b).
-//
-// Ray model (separable restatement of make_ray + plan_walk, projector.hpp:29-91).  For a
-// view a and detector column iu, the unnormalised ray d = P - S has horizontal part
-// (dx, dy) independent of the detector row.  Rays whose dominant axis A is x or y
-// (|d_A| >= |dz|) walk the slices s of A; in slice s the ray sits at
-//     fh(s) = fh0 + s*fhd                   (in-plane horizontal index: y if A=x, x if A=y)
-//     fz(s) = vd(iv) * (g0 + s*gd) + cz     (z index; vd = detector row coordinate)
-// with {fh0, fhd, g0, gd} a per-(view, column) f32 table computed in fp64 on the host,
-// and path length per slice step = h*|d|/|d_A| (= h/|dir_A|, projector.hpp:77).  Both
-// the forward and the transpose evaluate exactly these f32 expressions, so the matched
-// A^T b is the exact transpose of this Ax up to fp32 rounding of the products.  Rays with
-// a dominant z component (steep cone rows) take a generic per-ray path.
-//
-// Layouts in HBM (f32):
-//   qx[i][k+1][j+1]  bilinear quads (16 B) of each x-slice plane      (x-dominant rays)
-//   qy[j][k+1][i+1]  bilinear quads (16 B) of each y-slice plane      (y-dominant rays)
-// so that a warp of 32 consecutive detector columns reads 32 consecutive quads per
-// sample: one 16-byte load, no bounds checks (zero padding is in the quads).
-//   proj_t[a][iu][iv] detector columns contiguous (gathers read consecutive rows).
-#include <cfloat>
-#include <cstdlib>
-
-#include "ctk_internal.h"
-#include "reduce.cuh"
+// A^T b for T = float on sm_100a: the exact transpose of fwd_f32.cu (matched) and the
+// voxel-driven backprojection (projector.hpp:204-279).  Both gather from the projections
+// transposed to pt[a][iu][iv] (detector columns contiguous; step-scaled for matched), so
+// no float atomics are used and every voxel sums its contributions in a fixed order.
+#include "f32_common.cuh"
 
 namespace ctkb {
 namespace {
-
-constexpr int FWD_BX = 32, FWD_BY = 8;  // rays per forward block: 32 columns x 8 rows
-
-__device__ __forceinline__ double row_coord(const KGeom& g, int iv) { return (iv - 0.5 * (g.nv - 1)) * g.du; }
-
-// path length per slice step of ray (column c, row coordinate v)
-__device__ __forceinline__ float ray_step(const KGeom& g, double2 cs, double v) {
-    if (g.mode == CTK_CONE3D) {
-        const double av = fabs(v);
-        const double dom = av > cs.y ? av : cs.y;
-        return float(g.h * sqrt(cs.x + v * v) / dom);
-    }
-    return float(g.h / cs.y);
-}
-
-__device__ __forceinline__ bool is_zray(const KGeom& g, double2 cs, double v) {
-    return g.mode == CTK_CONE3D && fabs(v) > cs.y;
-}
-
-__device__ __forceinline__ void clip_affine(double f0, double fd, double lo, double hi, int& s0, int& s1) {
-    if (fd == 0.0) {
-        if (!(f0 > lo - 1.0 && f0 < hi + 1.0)) { s0 = 1; s1 = 0; }
-        return;
-    }
-    double a = (lo - f0) / fd, b = (hi - f0) / fd;
-    if (a > b) { const double t = a; a = b; b = t; }
-    if (a > 2e9 || b < -2e9) { s0 = 1; s1 = 0; return; }
-    s0 = max(s0, int(floor(fmax(a, -2e9))) - 1);
-    s1 = min(s1, int(ceil(fmin(b, 2e9))) + 1);
-}
-
-// ---- generic walk (z-dominant rays): plan_walk in fp64, positions in f32 ----------------
-struct WalkF {
-    int axis, ns, nb, nc;
-    float fb0, fbd, fc0, fcd, step;
-    int sa, sb, sc;
-};
-
-__device__ void walk_generic(const KGeom& g, double ct, double st, int iu, int iv, WalkF& w) {
-    const double u = (iu - 0.5 * (g.nu - 1)) * g.du;
-    const double v = (iv - 0.5 * (g.nv - 1)) * g.du;
-    double o[3], d[3];
-    const double px = -g.dod * ct - u * st, py = -g.dod * st + u * ct, pz = v;
-    if (g.mode == CTK_CONE3D) {
-        o[0] = g.dso * ct; o[1] = g.dso * st; o[2] = 0.0;
-        d[0] = px - o[0]; d[1] = py - o[1]; d[2] = pz;
-        const double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-        d[0] /= n; d[1] /= n; d[2] /= n;
-    } else {
-        o[0] = px; o[1] = py; o[2] = pz;
-        d[0] = -ct; d[1] = -st; d[2] = 0.0;
-    }
-    const double ad0 = fabs(d[0]), ad1 = fabs(d[1]), ad2 = fabs(d[2]);
-    int axis = 0;
-    double adm = ad0;
-    if (ad1 > adm) { axis = 1; adm = ad1; }
-    if (ad2 > adm) { axis = 2; adm = ad2; }
-    const int n3[3] = {g.nx, g.ny, g.nz};
-    const int s3[3] = {1, g.nx, g.nx * g.ny};
-    const int b = axis == 2 ? 0 : axis + 1, c = axis == 0 ? 2 : axis - 1;
-    const double h = g.h;
-    const double t0 = ((0 - 0.5 * (n3[axis] - 1)) * h - o[axis]) / d[axis];
-    const double dt = h / d[axis];
-    w.axis = axis;
-    w.ns = n3[axis];
-    w.nb = n3[b];
-    w.nc = n3[c];
-    w.sa = s3[axis];
-    w.sb = s3[b];
-    w.sc = s3[c];
-    w.step = float(h / adm);
-    w.fb0 = float((o[b] + t0 * d[b]) / h + 0.5 * (n3[b] - 1));
-    w.fbd = float(dt * d[b] / h);
-    w.fc0 = float((o[c] + t0 * d[c]) / h + 0.5 * (n3[c] - 1));
-    w.fcd = float(dt * d[c] / h);
-}
-
-__device__ float march_generic(const KGeom& g, const WalkF& w, const float* __restrict__ vol) {
-    int s0 = 0, s1 = w.ns - 1;
-    clip_affine(w.fb0, w.fbd, -1.0, w.nb, s0, s1);
-    clip_affine(w.fc0, w.fcd, -1.0, w.nc, s0, s1);
-    float acc = 0.f;
-    for (int s = s0; s <= s1; ++s) {
-        const float fb = fmaf(float(s), w.fbd, w.fb0);
-        const float fc = fmaf(float(s), w.fcd, w.fc0);
-        const float fib = floorf(fb), fic = floorf(fc);
-        const int ib = int(fib), ic = int(fic);
-        const float tb = fb - fib, tc = fc - fic;
-        const float* p = vol + size_t(s) * w.sa;
-        const bool b0 = ib >= 0 && ib < w.nb, b1 = ib + 1 >= 0 && ib + 1 < w.nb;
-        const bool c0 = ic >= 0 && ic < w.nc, c1 = ic + 1 >= 0 && ic + 1 < w.nc;
-        const float v00 = (b0 && c0) ? __ldg(p + ib * w.sb + ic * w.sc) : 0.f;
-        const float v10 = (b1 && c0) ? __ldg(p + (ib + 1) * w.sb + ic * w.sc) : 0.f;
-        const float v01 = (b0 && c1) ? __ldg(p + ib * w.sb + (ic + 1) * w.sc) : 0.f;
-        const float v11 = (b1 && c1) ? __ldg(p + (ib + 1) * w.sb + (ic + 1) * w.sc) : 0.f;
-        const float a0 = fmaf(tb, v10 - v00, v00);
-        const float a1 = fmaf(tb, v11 - v01, v01);
-        acc += fmaf(tc, a1 - a0, a0);
-    }
-    return w.step * acc;
-}
-// ---- quad relayout: x[i + nx(j + ny k)] -> bilinear quads per slice plane -------------
-// qx[i][k+1][j+1] = (v(i,j,k), v(i,j+1,k), v(i,j,k+1), v(i,j+1,k+1))   x-dominant rays
-// qy[j][k+1][i+1] = (v(i,j,k), v(i+1,j,k), v(i,j,k+1), v(i+1,j,k+1))   y-dominant rays
-// for in-plane indices h in [-1, nh-1] and k in [-1, nz-1]; taps outside the volume are 0
-// (Joseph's zero padding, projector.hpp:108).  One 16-byte load per bilinear sample.
-__device__ __forceinline__ float vox(const float* __restrict__ x, int nx, int ny, int nz, int i, int j, int k) {
-    return (i >= 0 && i < nx && j >= 0 && j < ny && k >= 0 && k < nz)
-               ? __ldg(x + size_t(i) + size_t(nx) * (size_t(j) + size_t(ny) * k))
-               : 0.f;
-}
-
-__global__ void k_quads_y(int nx, int ny, int nz, const float* __restrict__ x, float4* __restrict__ qy) {
-    const int io = blockIdx.x * blockDim.x + threadIdx.x;  // i + 1
-    const int ko = blockIdx.y;                             // k + 1
-    const int j = blockIdx.z;
-    if (io > nx) return;
-    const int i = io - 1, k = ko - 1;
-    const size_t pitch = size_t(nx) + 1, plane = pitch * (size_t(nz) + 1);
-    qy[size_t(j) * plane + size_t(ko) * pitch + io] =
-        make_float4(vox(x, nx, ny, nz, i, j, k), vox(x, nx, ny, nz, i + 1, j, k), vox(x, nx, ny, nz, i, j, k + 1),
-                    vox(x, nx, ny, nz, i + 1, j, k + 1));
-}
-
-// 32(i) x 33(j) x 2(k) tile through shared memory so both the reads (along i) and the
-// quad writes (along j) are coalesced
-__global__ void k_quads_x(int nx, int ny, int nz, const float* __restrict__ x, float4* __restrict__ qx) {
-    __shared__ float tile[2][33][33];
-    const int i0 = blockIdx.x * 32, jo0 = blockIdx.y * 32, ko = blockIdx.z;
-    const int k = ko - 1;
-    for (int r = threadIdx.y; r < 2 * 33; r += blockDim.y) {
-        const int kz = r / 33, jj = r % 33;
-        tile[kz][jj][threadIdx.x] = vox(x, nx, ny, nz, i0 + threadIdx.x, jo0 - 1 + jj, k + kz);
-    }
-    __syncthreads();
-    const size_t pitch = size_t(ny) + 1, plane = pitch * (size_t(nz) + 1);
-    const int jo = jo0 + threadIdx.x;  // j + 1
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int i = i0 + r;
-        if (i < nx && jo <= ny) {
-            const int jj = threadIdx.x;  // tile row of j = jo - 1
-            qx[size_t(i) * plane + size_t(ko) * pitch + jo] =
-                make_float4(tile[0][jj][r], tile[0][jj + 1][r], tile[1][jj][r], tile[1][jj + 1][r]);
-        }
-    }
-}
-
-// floor without the conversion pipe: t = (f - 0.5) + 1.5*2^23 rounds to an integer n with
-// n = floor(f) except at exact integers, where n may be f - 1 with frac 1.0 -- the same
-// bilinear weights (1 on tap f).  Valid for |f| < 2^22.
-__device__ __forceinline__ void split(float f, int& i, float& frac) {
-    const float M = 12582912.0f;
-    const float t = __fadd_rn(__fadd_rn(f, -0.5f), M);
-    const float fi = __fadd_rn(t, -M);
-    i = __float_as_int(t) - __float_as_int(M);
-    frac = __fadd_rn(f, -fi);
-}
-
-// ---- forward projection ----------------------------------------------------------------
-// RESID=false: y[a][iv][iu] = A x.   RESID=true: per-block partial of sum (Ax - b)^2.
-template <bool RESID>
-__global__ void __launch_bounds__(FWD_BX * FWD_BY)
-k_ax_f32(KGeom g, const float4* __restrict__ qx, const float4* __restrict__ qy, const float* __restrict__ xs,
-         float* __restrict__ y, const float* __restrict__ b, double* __restrict__ partials) {
-    const int iu = blockIdx.x * FWD_BX + threadIdx.x;
-    const int iv = blockIdx.y * FWD_BY + threadIdx.y;
-    const int a = blockIdx.z;
-    float out = 0.f;
-    const bool live = iu < g.nu && iv < g.nv;
-    if (live) {
-        const int c = a * g.nu + iu;
-        const double2 cs = g.colstep[c];
-        const double v = row_coord(g, iv);
-        if (g.has_zrays && is_zray(g, cs, v)) {
-            const double2 tr = g.ctst[a];
-            WalkF w;
-            walk_generic(g, tr.x, tr.y, iu, iv, w);
-            out = march_generic(g, w, xs);
-        } else {
-            const float4 cd = g.col[c];
-            const int A = g.colaxis[c];
-            const int nh = A ? g.nx : g.ny;
-            const int ns = A ? g.ny : g.nx;
-            const int pitch = nh + 1;
-            const int plane = pitch * (g.nz + 1);
-            const float4* base = (A ? qy : qx) + pitch + 1;  // quad of (h, z) at base[z*pitch + h]
-            const float vd = float(v);
-            const float czf = 0.5f * float(g.nz - 1);
-            int s0 = 0, s1 = ns - 1;
-            clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
-            clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
-            float acc = 0.f;
-            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
-#pragma unroll 4
-            for (int s = s0; s <= s1; ++s) {
-                const float fs = float(s);
-                const float fh = fmaf(fs, cd.y, cd.x);
-                const float gs = fmaf(fs, cd.w, cd.z);
-                const float fz = fmaf(vd, gs, czf);
-                int ih, iz;
-                float th, tz;
-                split(fh, ih, th);
-                split(fz, iz, tz);
-                // sample inside the padded plane <=> some tap inside the volume
-                const bool in = unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
-                const int off = in ? s * plane + iz * pitch + ih : -pitch - 1;  // -pitch-1: quad (-1,-1), in bounds
-                const float4 q = __ldg(base + off);
-                const float a0 = fmaf(th, q.y - q.x, q.x);
-                const float a1 = fmaf(th, q.w - q.z, q.z);
-                const float smp = fmaf(tz, a1 - a0, a0);
-                acc += in ? smp : 0.f;
-            }
-            out = ray_step(g, cs, v) * acc;
-        }
-    }
-    const size_t o = size_t(a) * g.nu * g.nv + size_t(iv) * g.nu + iu;
-    if (!RESID) {
-        if (live) y[o] = out;
-    } else {
-        double r = 0.0;
-        if (live) {
-            const double d = double(out) - double(__ldg(b + o));
-            r = d * d;
-        }
-        r = block_sum(r);
-        if (threadIdx.x == 0 && threadIdx.y == 0)
-            partials[(size_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = r;
-    }
-}
 
 // ---- projection transpose for the gathers: pt[a][iu][iv] = (step?) * y[a][iv][iu] ------
 template <bool SCALE>
@@ -280,19 +30,6 @@ __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __
     }
 }
 
-// horizontal detector coordinate (continuous pixel index) of the point (x, y)
-__device__ __forceinline__ double proj_u(const KGeom& g, double ct, double st, double x, double y, bool& ok) {
-    ok = true;
-    if (g.mode == CTK_CONE3D) {
-        const double sx = g.dso * ct, sy = g.dso * st;
-        const double rx = x - sx, ry = y - sy;
-        const double depth = -(rx * ct + ry * st);
-        if (!(depth > 1e-9 * g.dso)) { ok = false; return 0.0; }
-        const double t = (g.dso + g.dod) / depth;
-        return (-(sx + t * rx) * st + (sy + t * ry) * ct) / g.du + 0.5 * (g.nu - 1);
-    }
-    return (-x * st + y * ct) / g.du + 0.5 * (g.nu - 1);
-}
 
 // ---- matched A^T b, plane-driven ------------------------------------------------------
 // Pass CLASS (0: x-dominant columns, planes x = s, rows p = y; 1: y-dominant columns,
@@ -617,23 +354,6 @@ int pick_kz(int nz) {
     return 16;
 }
 
-void build_quads(Geometry& g, const float* x, cudaStream_t s) {
-    const size_t nqx = size_t(g.nx) * (size_t(g.ny) + 1) * (size_t(g.nz) + 1);
-    const size_t nqy = size_t(g.ny) * (size_t(g.nx) + 1) * (size_t(g.nz) + 1);
-    g.vx.ensure(nqx * sizeof(float4));
-    g.vy.ensure(nqy * sizeof(float4));
-    {
-        dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.ny + 1 + 31) / 32, g.nz + 1);
-        k_quads_x<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vx.as<float4>());
-        after_launch("k_quads_x");
-    }
-    {
-        dim3 blk(128), grd((g.nx + 1 + 127) / 128, g.nz + 1, g.ny);
-        k_quads_y<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vy.as<float4>());
-        after_launch("k_quads_y");
-    }
-}
-
 template <bool SCALE>
 void transpose_proj(Geometry& g, const float* y, cudaStream_t s) {
     g.proj_t.ensure(g.range() * sizeof(float));
@@ -669,32 +389,7 @@ void launch_voxel(Geometry& g, float* x, cudaStream_t s) {
     after_launch("k_atb_voxel_f32");
 }
 
-dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + FWD_BX - 1) / FWD_BX, (g.nv + FWD_BY - 1) / FWD_BY, g.na); }
-
 }  // namespace
-
-void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
-    build_quads(g, x, s);
-    CTK_CUDA(cudaEventRecord(g.ev0, s));
-    k_ax_f32<false><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(g.kgeom(), g.vx.as<float4>(), g.vy.as<float4>(), x, y,
-                                                                 nullptr, nullptr);
-    after_launch("k_ax_f32");
-    CTK_CUDA(cudaEventRecord(g.ev1, s));
-}
-
-void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
-    build_quads(g, x, s);
-    const dim3 grd = fwd_grid(g);
-    const size_t nblk = size_t(grd.x) * grd.y * grd.z;
-    g.proj_t.ensure(std::max(g.range() * sizeof(float), nblk * sizeof(double)));
-    double* partials = g.proj_t.as<double>();
-    CTK_CUDA(cudaEventRecord(g.ev0, s));
-    k_ax_f32<true><<<grd, dim3(FWD_BX, FWD_BY), 0, s>>>(g.kgeom(), g.vx.as<float4>(), g.vy.as<float4>(), x, nullptr, b,
-                                                        partials);
-    after_launch("k_ax_f32_residual");
-    CTK_CUDA(cudaEventRecord(g.ev1, s));
-    finish_sum(partials, int(nblk), d_out, s);
-}
 
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
     transpose_proj<true>(g, y, s);

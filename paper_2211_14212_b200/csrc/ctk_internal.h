@@ -77,6 +77,7 @@ struct Geometry {
 
     // device tables
     DevBuf d_ctst, d_col, d_colaxis, d_colstep;
+    DevBuf d_vorder;  // views grouped by ray class (x-dominant first) for L2 reuse in Ax
     // workspaces (grown lazily)
     DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
     DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers

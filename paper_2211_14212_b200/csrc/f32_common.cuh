@@ -1,0 +1,147 @@
+// Shared device helpers of the f32 performance kernels (fwd_f32.cu, bp_f32.cu).
+//
+// Ray model (separable restatement of make_ray + plan_walk, projector.hpp:29-91).  For a
+// view a and detector column iu, the unnormalised ray d = P - S has horizontal part
+// (dx, dy) independent of the detector row.  Rays whose dominant axis A is x or y
+// (|d_A| >= |dz|) walk the slices s of A; in slice s the ray sits at
+//     fh(s) = fh0 + s*fhd                   (in-plane horizontal index: y if A=x, x if A=y)
+//     fz(s) = vd(iv) * (g0 + s*gd) + cz     (z index; vd = detector row coordinate)
+// with {fh0, fhd, g0, gd} a per-(view, column) f32 table computed in fp64 on the host,
+// and path length per slice step = h*|d|/|d_A| (= h/|dir_A|, projector.hpp:77).  Both
+// the forward and the transpose evaluate exactly these f32 expressions, so the matched
+// A^T b is the exact transpose of this Ax up to fp32 rounding of the products.  Rays with
+// a dominant z component (steep cone rows) take a generic per-ray path.
+#pragma once
+#include <cfloat>
+
+#include "ctk_internal.h"
+#include "reduce.cuh"
+
+namespace ctkb {
+namespace {
+
+__device__ __forceinline__ double row_coord(const KGeom& g, int iv) { return (iv - 0.5 * (g.nv - 1)) * g.du; }
+
+// path length per slice step of ray (column c, row coordinate v)
+__device__ __forceinline__ float ray_step(const KGeom& g, double2 cs, double v) {
+    if (g.mode == CTK_CONE3D) {
+        const double av = fabs(v);
+        const double dom = av > cs.y ? av : cs.y;
+        return float(g.h * sqrt(cs.x + v * v) / dom);
+    }
+    return float(g.h / cs.y);
+}
+
+__device__ __forceinline__ bool is_zray(const KGeom& g, double2 cs, double v) {
+    return g.mode == CTK_CONE3D && fabs(v) > cs.y;
+}
+
+__device__ __forceinline__ void clip_affine(double f0, double fd, double lo, double hi, int& s0, int& s1) {
+    if (fd == 0.0) {
+        if (!(f0 > lo - 1.0 && f0 < hi + 1.0)) { s0 = 1; s1 = 0; }
+        return;
+    }
+    double a = (lo - f0) / fd, b = (hi - f0) / fd;
+    if (a > b) { const double t = a; a = b; b = t; }
+    if (a > 2e9 || b < -2e9) { s0 = 1; s1 = 0; return; }
+    s0 = max(s0, int(floor(fmax(a, -2e9))) - 1);
+    s1 = min(s1, int(ceil(fmin(b, 2e9))) + 1);
+}
+
+// ---- generic walk (z-dominant rays): plan_walk in fp64, positions in f32 ----------------
+struct WalkF {
+    int axis, ns, nb, nc;
+    float fb0, fbd, fc0, fcd, step;
+    int sa, sb, sc;
+};
+
+__device__ void walk_generic(const KGeom& g, double ct, double st, int iu, int iv, WalkF& w) {
+    const double u = (iu - 0.5 * (g.nu - 1)) * g.du;
+    const double v = (iv - 0.5 * (g.nv - 1)) * g.du;
+    double o[3], d[3];
+    const double px = -g.dod * ct - u * st, py = -g.dod * st + u * ct, pz = v;
+    if (g.mode == CTK_CONE3D) {
+        o[0] = g.dso * ct; o[1] = g.dso * st; o[2] = 0.0;
+        d[0] = px - o[0]; d[1] = py - o[1]; d[2] = pz;
+        const double n = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+        d[0] /= n; d[1] /= n; d[2] /= n;
+    } else {
+        o[0] = px; o[1] = py; o[2] = pz;
+        d[0] = -ct; d[1] = -st; d[2] = 0.0;
+    }
+    const double ad0 = fabs(d[0]), ad1 = fabs(d[1]), ad2 = fabs(d[2]);
+    int axis = 0;
+    double adm = ad0;
+    if (ad1 > adm) { axis = 1; adm = ad1; }
+    if (ad2 > adm) { axis = 2; adm = ad2; }
+    const int n3[3] = {g.nx, g.ny, g.nz};
+    const int s3[3] = {1, g.nx, g.nx * g.ny};
+    const int b = axis == 2 ? 0 : axis + 1, c = axis == 0 ? 2 : axis - 1;
+    const double h = g.h;
+    const double t0 = ((0 - 0.5 * (n3[axis] - 1)) * h - o[axis]) / d[axis];
+    const double dt = h / d[axis];
+    w.axis = axis;
+    w.ns = n3[axis];
+    w.nb = n3[b];
+    w.nc = n3[c];
+    w.sa = s3[axis];
+    w.sb = s3[b];
+    w.sc = s3[c];
+    w.step = float(h / adm);
+    w.fb0 = float((o[b] + t0 * d[b]) / h + 0.5 * (n3[b] - 1));
+    w.fbd = float(dt * d[b] / h);
+    w.fc0 = float((o[c] + t0 * d[c]) / h + 0.5 * (n3[c] - 1));
+    w.fcd = float(dt * d[c] / h);
+}
+
+__device__ float march_generic(const KGeom& g, const WalkF& w, const float* __restrict__ vol) {
+    int s0 = 0, s1 = w.ns - 1;
+    clip_affine(w.fb0, w.fbd, -1.0, w.nb, s0, s1);
+    clip_affine(w.fc0, w.fcd, -1.0, w.nc, s0, s1);
+    float acc = 0.f;
+    for (int s = s0; s <= s1; ++s) {
+        const float fb = fmaf(float(s), w.fbd, w.fb0);
+        const float fc = fmaf(float(s), w.fcd, w.fc0);
+        const float fib = floorf(fb), fic = floorf(fc);
+        const int ib = int(fib), ic = int(fic);
+        const float tb = fb - fib, tc = fc - fic;
+        const float* p = vol + size_t(s) * w.sa;
+        const bool b0 = ib >= 0 && ib < w.nb, b1 = ib + 1 >= 0 && ib + 1 < w.nb;
+        const bool c0 = ic >= 0 && ic < w.nc, c1 = ic + 1 >= 0 && ic + 1 < w.nc;
+        const float v00 = (b0 && c0) ? __ldg(p + ib * w.sb + ic * w.sc) : 0.f;
+        const float v10 = (b1 && c0) ? __ldg(p + (ib + 1) * w.sb + ic * w.sc) : 0.f;
+        const float v01 = (b0 && c1) ? __ldg(p + ib * w.sb + (ic + 1) * w.sc) : 0.f;
+        const float v11 = (b1 && c1) ? __ldg(p + (ib + 1) * w.sb + (ic + 1) * w.sc) : 0.f;
+        const float a0 = fmaf(tb, v10 - v00, v00);
+        const float a1 = fmaf(tb, v11 - v01, v01);
+        acc += fmaf(tc, a1 - a0, a0);
+    }
+    return w.step * acc;
+}
+// horizontal detector coordinate (continuous pixel index) of the point (x, y)
+__device__ __forceinline__ double proj_u(const KGeom& g, double ct, double st, double x, double y, bool& ok) {
+    ok = true;
+    if (g.mode == CTK_CONE3D) {
+        const double sx = g.dso * ct, sy = g.dso * st;
+        const double rx = x - sx, ry = y - sy;
+        const double depth = -(rx * ct + ry * st);
+        if (!(depth > 1e-9 * g.dso)) { ok = false; return 0.0; }
+        const double t = (g.dso + g.dod) / depth;
+        return (-(sx + t * rx) * st + (sy + t * ry) * ct) / g.du + 0.5 * (g.nu - 1);
+    }
+    return (-x * st + y * ct) / g.du + 0.5 * (g.nu - 1);
+}
+
+// floor without the conversion pipe: t = (f - 0.5) + 1.5*2^23 rounds to an integer n with
+// n = floor(f) except at exact integers, where n may be f - 1 with frac 1.0 -- the same
+// bilinear weights (weight 1 on tap f).  Valid for |f| < 2^22.
+__device__ __forceinline__ void split(float f, int& i, float& frac) {
+    const float M = 12582912.0f;
+    const float t = __fadd_rn(__fadd_rn(f, -0.5f), M);
+    const float fi = __fadd_rn(t, -M);
+    i = __float_as_int(t) - __float_as_int(M);
+    frac = __fadd_rn(f, -fi);
+}
+
+}  // namespace
+}  // namespace ctkb

@@ -1,0 +1,180 @@
+// Joseph forward projection Ax for T = float (projector.hpp:113-162) on sm_100a.
+//
+// Layouts in HBM (f32, zero-padded so the four bilinear taps need no bounds checks):
+//   vx[i][k+1][j+1]  pitch ny+2, one plane per x-slice   (x-dominant rays walk x)
+//   vy[j][k+1][i+1]  pitch nx+2, one plane per y-slice   (y-dominant rays walk y)
+// A warp is 32 consecutive detector columns of one row; their taps in a slice are
+// consecutive addresses of one or two plane rows.
+//
+// Grid order = L2 reuse.  The volume (512 MiB at 512^3) does not fit the 126 MB L2, and
+// every view crosses all of it.  Blocks are dispatched with the detector-row band
+// SLOWEST: at any time the resident blocks cover every view of one band of rows, whose
+// rays stay in one z-slab of the volume, so each slab comes from HBM about once per Ax
+// instead of once per view.  Views are visited class by class (x-dominant first) so only
+// one of the two layout copies is hot at a time.
+#include "f32_common.cuh"
+
+namespace ctkb {
+namespace {
+
+constexpr int FWD_BX = 32, FWD_BY = 8;  // rays per block: 32 columns x 8 rows
+
+// vy[j][k+1][i+1]: x stays fastest (coalesced both ways)
+__global__ void k_relayout_y(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ vy) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    const int j = blockIdx.z;
+    if (i >= nx) return;
+    const size_t pitch = size_t(nx) + 2, plane = pitch * (size_t(nz) + 2);
+    vy[size_t(j) * plane + size_t(k + 1) * pitch + i + 1] = __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k));
+}
+
+// vx[i][k+1][j+1]: 32x32 tile transpose of (i, j) per z-plane
+__global__ void k_relayout_x(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ vx) {
+    __shared__ float tile[32][33];
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32, k = blockIdx.z;
+    const size_t pitch = size_t(ny) + 2, plane = pitch * (size_t(nz) + 2);
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + threadIdx.x, j = j0 + r;
+        tile[r][threadIdx.x] = (i < nx && j < ny) ? __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k)) : 0.f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, j = j0 + threadIdx.x;
+        if (i < nx && j < ny) vx[size_t(i) * plane + size_t(k + 1) * pitch + j + 1] = tile[threadIdx.x][r];
+    }
+}
+
+// RESID=false: y[a][iv][iu] = A x.   RESID=true: per-block partial of sum (Ax - b)^2.
+// Off = int (volumes with ns*(nh+2)*(nz+2) < 2^31) or long long.
+template <bool RESID, class Off>
+__global__ void __launch_bounds__(FWD_BX * FWD_BY)
+k_ax_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ vx, const float* __restrict__ vy,
+         const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b, double* __restrict__ partials) {
+    const int iu = blockIdx.x * FWD_BX + threadIdx.x;
+    const int a = vorder[blockIdx.y];
+    const int iv = blockIdx.z * FWD_BY + threadIdx.y;
+    float out = 0.f;
+    const bool live = iu < g.nu && iv < g.nv;
+    if (live) {
+        const int c = a * g.nu + iu;
+        const double2 cs = g.colstep[c];
+        const double v = row_coord(g, iv);
+        if (g.has_zrays && is_zray(g, cs, v)) {
+            const double2 tr = g.ctst[a];
+            WalkF w;
+            walk_generic(g, tr.x, tr.y, iu, iv, w);
+            out = march_generic(g, w, xs);
+        } else {
+            const float4 cd = g.col[c];
+            const int A = g.colaxis[c];
+            const int nh = A ? g.nx : g.ny;
+            const int ns = A ? g.ny : g.nx;
+            const Off pitch = nh + 2;
+            const Off plane = pitch * Off(g.nz + 2);
+            const float* base = (A ? vy : vx) + pitch + 1;  // tap (h, z) of slice s at base[s*plane + z*pitch + h]
+            const float vd = float(v);
+            const float czf = 0.5f * float(g.nz - 1);
+            int s0 = 0, s1 = ns - 1;
+            clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
+            clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
+            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            float acc = 0.f;
+#pragma unroll 4
+            for (int s = s0; s <= s1; ++s) {
+                const float fs = float(s);
+                const float fh = fmaf(fs, cd.y, cd.x);
+                const float gs = fmaf(fs, cd.w, cd.z);
+                const float fz = fmaf(vd, gs, czf);
+                int ih, iz;
+                float th, tz;
+                split(fh, ih, th);
+                split(fz, iz, tz);
+                // some tap inside the volume <=> ih in [-1, nh-1] and iz in [-1, nz-1]
+                const bool in = unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
+                const Off off = in ? Off(s) * plane + Off(iz) * pitch + ih : -(pitch + 1);  // else: padding corner
+                const float* p = base + off;
+                const float v00 = __ldg(p), v10 = __ldg(p + 1);
+                const float v01 = __ldg(p + pitch), v11 = __ldg(p + pitch + 1);
+                const float a0 = fmaf(th, v10 - v00, v00);
+                const float a1 = fmaf(th, v11 - v01, v01);
+                const float smp = fmaf(tz, a1 - a0, a0);
+                acc += in ? smp : 0.f;
+            }
+            out = ray_step(g, cs, v) * acc;
+        }
+    }
+    const size_t o = size_t(a) * g.nu * g.nv + size_t(iv) * g.nu + iu;
+    if (!RESID) {
+        if (live) y[o] = out;
+    } else {
+        double r = 0.0;
+        if (live) {
+            const double d = double(out) - double(__ldg(b + o));
+            r = d * d;
+        }
+        r = block_sum(r);
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            partials[(size_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = r;
+    }
+}
+
+void relayout(Geometry& g, const float* x, cudaStream_t s) {
+    const size_t nvx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
+    const size_t nvy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
+    if (g.vx.ensure(nvx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vx.p, 0, nvx * sizeof(float), s));
+    if (g.vy.ensure(nvy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vy.p, 0, nvy * sizeof(float), s));
+    {
+        dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.ny + 31) / 32, g.nz);
+        k_relayout_x<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vx.as<float>());
+        after_launch("k_relayout_x");
+    }
+    {
+        dim3 blk(128), grd((g.nx + 127) / 128, g.nz, g.ny);
+        k_relayout_y<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vy.as<float>());
+        after_launch("k_relayout_y");
+    }
+}
+
+dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + FWD_BX - 1) / FWD_BX, g.na, (g.nv + FWD_BY - 1) / FWD_BY); }
+
+bool wide_offsets(const Geometry& g) {
+    const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz + 2);
+    return mx >= 2147483000.0;
+}
+
+template <bool RESID>
+void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s) {
+    const KGeom k = g.kgeom();
+    const int* vo = g.d_vorder.as<int>();
+    if (wide_offsets(g))
+        k_ax_f32<RESID, long long><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(k, vo, g.vx.as<float>(), g.vy.as<float>(),
+                                                                                x, y, b, partials);
+    else
+        k_ax_f32<RESID, int><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(k, vo, g.vx.as<float>(), g.vy.as<float>(), x,
+                                                                          y, b, partials);
+    after_launch(RESID ? "k_ax_f32_residual" : "k_ax_f32");
+}
+
+}  // namespace
+
+void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
+    relayout(g, x, s);
+    CTK_CUDA(cudaEventRecord(g.ev0, s));
+    launch_ax<false>(g, x, y, nullptr, nullptr, s);
+    CTK_CUDA(cudaEventRecord(g.ev1, s));
+}
+
+void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
+    relayout(g, x, s);
+    const dim3 grd = fwd_grid(g);
+    const size_t nblk = size_t(grd.x) * grd.y * grd.z;
+    g.proj_t.ensure(std::max(g.range() * sizeof(float), nblk * sizeof(double)));
+    double* partials = g.proj_t.as<double>();
+    CTK_CUDA(cudaEventRecord(g.ev0, s));
+    launch_ax<true>(g, x, nullptr, b, partials, s);
+    CTK_CUDA(cudaEventRecord(g.ev1, s));
+    finish_sum(partials, int(nblk), d_out, s);
+}
+
+}  // namespace ctkb

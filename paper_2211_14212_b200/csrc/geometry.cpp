@@ -192,6 +192,17 @@ Geometry* geometry_create(const ctk_geom_desc* d) {
                 if (g->mode == CTK_CONE3D && vmax > dA) g->has_zrays = true;
             }
         }
+        // view visiting order of the forward kernel: x-dominant views (majority of their
+        // columns) first, each group in angle order
+        std::vector<int> vorder;
+        for (int pass = 0; pass < 2; ++pass)
+            for (int a = 0; a < g->na; ++a) {
+                int nxd = 0;
+                for (int iu = 0; iu < g->nu; ++iu) nxd += cax[size_t(a) * g->nu + iu] == 0;
+                if ((2 * nxd >= g->nu) == (pass == 0)) vorder.push_back(a);
+            }
+        g->d_vorder.ensure(sizeof(int) * vorder.size());
+        CTK_CUDA(cudaMemcpy(g->d_vorder.p, vorder.data(), sizeof(int) * vorder.size(), cudaMemcpyHostToDevice));
         g->d_ctst.ensure(sizeof(double2) * ctst.size());
         g->d_col.ensure(sizeof(float4) * col.size());
         g->d_colaxis.ensure(cax.size());
