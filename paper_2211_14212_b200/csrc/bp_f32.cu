@@ -54,12 +54,14 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     int* lists = reinterpret_cast<int*>(Z + BP_KB * BP_PB);     // [BP_PB][BP_SL]
     int* cnt = lists + BP_PB * BP_SL;                           // [BP_PB]
     float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_PB]
-    float* vdtab = eth + BP_PB;                                 // [nv]
-    __shared__ int s_iu0, s_iu1;
+    int2* urange = reinterpret_cast<int2*>(eth + BP_PB);        // [na]
+    float* vdtab = reinterpret_cast<float*>(urange + g.na);     // [nv]
 
     const int t = threadIdx.x;
-    const int s = blockIdx.y;
-    const int ptile = blockIdx.x % ptiles, kband = blockIdx.x / ptiles;
+    // plane index fastest: a wave of resident CTAs shares one (row tile, z band), so per
+    // view it reads only that band's detector rows -> the projections stay L2-resident
+    const int s = blockIdx.x;
+    const int ptile = blockIdx.y % ptiles, kband = blockIdx.y / ptiles;
     const int p0 = ptile * BP_PB, k0 = kband * BP_KB;
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
@@ -78,23 +80,24 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
 #pragma unroll
     for (int m = 0; m < BP_KB; ++m) acc[m] = 0.f;
 
-    for (int a = 0; a < g.na; ++a) {
-        if (t == 0) {
-            const double2 tr = g.ctst[a];
-            bool ok1, ok2;
-            const double u1 = CLASS ? proj_u(g, tr.x, tr.y, r_lo, plane_c, ok1) : proj_u(g, tr.x, tr.y, plane_c, r_lo, ok1);
-            const double u2 = CLASS ? proj_u(g, tr.x, tr.y, r_hi, plane_c, ok2) : proj_u(g, tr.x, tr.y, plane_c, r_hi, ok2);
-            int i0 = 0, i1 = g.nu - 1;
-            if (ok1 && ok2) {
-                i0 = max(i0, int(floor(fmax(fmin(u1, u2), -1e9))) - 1);
-                i1 = min(i1, int(ceil(fmin(fmax(u1, u2), 1e9))) + 1);
-            }
-            s_iu0 = i0;
-            s_iu1 = i1;
+    // candidate detector-column range of every view for this tile (projection of the
+    // tile's row segment in the plane), computed once, in parallel
+    for (int a = t; a < g.na; a += BP_PB) {
+        const double2 tr = g.ctst[a];
+        bool ok1, ok2;
+        const double u1 = CLASS ? proj_u(g, tr.x, tr.y, r_lo, plane_c, ok1) : proj_u(g, tr.x, tr.y, plane_c, r_lo, ok1);
+        const double u2 = CLASS ? proj_u(g, tr.x, tr.y, r_hi, plane_c, ok2) : proj_u(g, tr.x, tr.y, plane_c, r_hi, ok2);
+        int i0 = 0, i1 = g.nu - 1;
+        if (ok1 && ok2) {
+            i0 = max(i0, int(floor(fmax(fmin(u1, u2), -1e9))) - 1);
+            i1 = min(i1, int(ceil(fmin(fmax(u1, u2), 1e9))) + 1);
         }
-        __syncthreads();
-        const int iu0 = s_iu0, iu1 = s_iu1;
-        __syncthreads();  // s_iu* is rewritten for the next view
+        urange[a] = make_int2(i0, i1);
+    }
+    __syncthreads();
+
+    for (int a = 0; a < g.na; ++a) {
+        const int iu0 = urange[a].x, iu1 = urange[a].y;
         for (int cbase = iu0; cbase <= iu1; cbase += BP_PB) {
             // ---- phase 1 ----
             cnt[t] = 0;
@@ -368,13 +371,15 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz + BP_KB - 1) / BP_KB;
-    const size_t smem = sizeof(float) * (size_t(BP_PB) * BP_KB + size_t(BP_PB) * BP_SL + 2 * BP_PB + g.nv);
+    const size_t smem =
+        sizeof(float) * (size_t(BP_PB) * BP_KB + size_t(BP_PB) * BP_SL + 2 * BP_PB + g.nv) + sizeof(int2) * g.na;
+    if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     static size_t configured = 0;
     if (smem > configured) {
         CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         configured = smem;
     }
-    dim3 grd(unsigned(ptiles * kbands), unsigned(planes));
+    dim3 grd(unsigned(planes), unsigned(ptiles * kbands));
     k_atb_plane_f32<CLASS><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
     after_launch("k_atb_plane_f32");
 }
