@@ -121,27 +121,62 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                             v0 = max(v0, int(floorf(fmaf(float(k0) - 1.f - czf, rg, cvf))) - 1);
                             v1 = min(v1, int(ceilf(fmaf(float(k0 + BP_KB) - czf, rg, cvf))) + 1);
                         }
-                        const double dA = g.colstep[c].y;
+                        if (g.has_zrays) {
+                            // rows whose ray is z-dominant (|v| > |d_A|) belong to the generic
+                            // pass; they form the two ends of the column: clip exactly
+                            const double dA = g.colstep[c].y;
+                            const double cv = 0.5 * (g.nv - 1), r = dA / g.du;
+                            int lo = max(v0, int(ceil(cv - r)) - 1), hi = min(v1, int(floor(cv + r)) + 1);
+                            while (lo <= hi && fabs(row_coord(g, lo)) > dA) ++lo;
+                            while (hi >= lo && fabs(row_coord(g, hi)) > dA) --hi;
+                            v0 = lo;
+                            v1 = hi;
+                        }
                         const float* pc = pt + size_t(c) * g.nv;
-                        auto add = [&](int iv, float yv) {
-                            if (g.has_zrays && fabs(row_coord(g, iv)) > dA) return;
-                            const float fz = fmaf(vdtab[iv], gs, czf);
-                            const float fiz = floorf(fz);
-                            const int kk = int(fiz) - k0;
-                            const float tz = fz - fiz;
-                            if (kk >= 0 && kk < BP_KB) Z[kk * BP_PB + t] = fmaf(1.f - tz, yv, Z[kk * BP_PB + t]);
-                            if (kk + 1 >= 0 && kk + 1 < BP_KB) Z[(kk + 1) * BP_PB + t] = fmaf(tz, yv, Z[(kk + 1) * BP_PB + t]);
-                        };
-                        if (vec4) {
-                            for (int b4 = v0 & ~3; b4 <= v1; b4 += 4) {
-                                const float4 y4 = __ldg(reinterpret_cast<const float4*>(pc + b4));
-                                if (b4 >= v0) add(b4, y4.x);
-                                if (b4 + 1 >= v0 && b4 + 1 <= v1) add(b4 + 1, y4.y);
-                                if (b4 + 2 >= v0 && b4 + 2 <= v1) add(b4 + 2, y4.z);
-                                if (b4 + 3 <= v1) add(b4 + 3, y4.w);
+                        float* zc = Z + t;
+                        if (gs > 0.f) {
+                            // fz increases with iv, so each Z[k] is final once the march passes
+                            // it: accumulate in registers (A -> Z[cur], B -> Z[cur+1]) and
+                            // store each entry once, branch-free
+                            int cur = -(1 << 20);
+                            float A = 0.f, B = 0.f;
+                            auto add = [&](int iv, float yv) {
+                                int iz;
+                                float tz;
+                                split(fmaf(vdtab[iv], gs, czf), iz, tz);
+                                const int kk = iz - k0;
+                                const int adv = kk - cur;
+                                if (adv >= 1 && unsigned(cur) < unsigned(BP_KB)) zc[cur * BP_PB] = A;
+                                if (adv >= 2 && unsigned(cur + 1) < unsigned(BP_KB)) zc[(cur + 1) * BP_PB] = B;
+                                const float w0 = (1.f - tz) * yv, w1 = tz * yv;
+                                A = (adv == 0) ? A + w0 : ((adv == 1) ? B + w0 : w0);
+                                B = (adv == 0) ? B + w1 : w1;
+                                cur = kk;
+                            };
+                            if (vec4) {
+                                for (int b4 = v0 & ~3; b4 <= v1; b4 += 4) {
+                                    const float4 y4 = __ldg(reinterpret_cast<const float4*>(pc + b4));
+                                    if (b4 >= v0) add(b4, y4.x);
+                                    if (b4 + 1 >= v0 && b4 + 1 <= v1) add(b4 + 1, y4.y);
+                                    if (b4 + 2 >= v0 && b4 + 2 <= v1) add(b4 + 2, y4.z);
+                                    if (b4 + 3 <= v1) add(b4 + 3, y4.w);
+                                }
+                            } else {
+                                for (int iv = v0; iv <= v1; ++iv) add(iv, __ldg(pc + iv));
                             }
+                            if (unsigned(cur) < unsigned(BP_KB)) zc[cur * BP_PB] = A;
+                            if (unsigned(cur + 1) < unsigned(BP_KB)) zc[(cur + 1) * BP_PB] = B;
                         } else {
-                            for (int iv = v0; iv <= v1; ++iv) add(iv, __ldg(pc + iv));
+                            // degenerate geometry (stencil point not in front of the source)
+                            for (int iv = v0; iv <= v1; ++iv) {
+                                const float yv = __ldg(pc + iv);
+                                int iz;
+                                float tz;
+                                split(fmaf(vdtab[iv], gs, czf), iz, tz);
+                                const int kk = iz - k0;
+                                if (unsigned(kk) < unsigned(BP_KB)) zc[kk * BP_PB] = fmaf(1.f - tz, yv, zc[kk * BP_PB]);
+                                if (unsigned(kk + 1) < unsigned(BP_KB)) zc[(kk + 1) * BP_PB] = fmaf(tz, yv, zc[(kk + 1) * BP_PB]);
+                            }
                         }
                         eth[t] = th;
                         if (ih >= p0) {

@@ -122,201 +122,6 @@ k_ax_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ vx, 
     }
 }
 
-// ---- shared-memory staged variant ------------------------------------------------------
-// The 256 rays of a block (32 columns x 8 rows of one view) cross each slice inside a small
-// box of the slice plane.  Per chunk of ST slices the block stages those boxes (exact
-// extents from the four corner rays: fh is monotone in the column, fz in the row and the
-// column, so the extremes are at corners; +-1 margin for rounding) from the padded layout
-// into shared memory with coalesced row loads, then every ray reads its 4 taps with LDS
-// (lanes = consecutive columns -> consecutive banks).  Blocks whose columns mix ray
-// classes or contain z-dominant rays, and chunks whose box exceeds the buffer, use the
-// direct path above.
-constexpr int ST = 8, SWM = 64, SHM = 16, SWS = SWM + 1;  // slices/chunk, box W/H max, row stride
-
-struct BoxInfo {
-    int hlo, zlo, w, h;
-};
-
-template <bool RESID, class Off>
-__global__ void __launch_bounds__(FWD_BX * FWD_BY)
-k_ax_staged_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ vx, const float* __restrict__ vy,
-                const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
-                double* __restrict__ partials) {
-    __shared__ float buf[ST * SHM * SWS];
-    __shared__ BoxInfo box[ST];
-    __shared__ int s_lo, s_hi, s_bad;
-    const int tid = threadIdx.x + FWD_BX * threadIdx.y;
-    const int iu = blockIdx.x * FWD_BX + threadIdx.x;
-    const int a = vorder[blockIdx.y];
-    const int iv = blockIdx.z * FWD_BY + threadIdx.y;
-    const int u_first = blockIdx.x * FWD_BX, u_last = min(u_first + FWD_BX, g.nu) - 1;
-    const int v_first = blockIdx.z * FWD_BY, v_last = min(v_first + FWD_BY, g.nv) - 1;
-    const bool live = iu < g.nu && iv < g.nv;
-    const int cl = a * g.nu + (live ? iu : u_first);
-    const int A0 = g.colaxis[a * g.nu + u_first];
-    const double v = row_coord(g, live ? iv : v_first);
-    const double2 cs = g.colstep[cl];
-    const bool uniform_ok = g.colaxis[cl] == A0 && !(g.has_zrays && is_zray(g, cs, v));
-    if (tid == 0) {
-        s_lo = INT_MAX;
-        s_hi = INT_MIN;
-    }
-    const int staged = __syncthreads_and(uniform_ok);
-    float out = 0.f;
-    if (!staged) {
-        // mixed tile: per-ray direct path (identical arithmetic)
-        if (live) {
-            if (g.has_zrays && is_zray(g, cs, v)) {
-                const double2 tr = g.ctst[a];
-                WalkF w;
-                walk_generic(g, tr.x, tr.y, iu, iv, w);
-                out = march_generic(g, w, xs);
-            } else {
-                const float4 cd = g.col[cl];
-                const int A = g.colaxis[cl];
-                const int nh = A ? g.nx : g.ny;
-                const int ns = A ? g.ny : g.nx;
-                const Off pitch = nh + 2;
-                const Off plane = pitch * Off(g.nz + 2);
-                const float* base = (A ? vy : vx) + pitch + 1;
-                const float vd = float(v);
-                const float czf = 0.5f * float(g.nz - 1);
-                int s0 = 0, s1 = ns - 1;
-                clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
-                clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
-                float acc = 0.f;
-                for (int s = s0; s <= s1; ++s) {
-                    const float fs = float(s);
-                    const float fh = fmaf(fs, cd.y, cd.x);
-                    const float fz = fmaf(vd, fmaf(fs, cd.w, cd.z), czf);
-                    int ih, iz;
-                    float th, tz;
-                    split(fh, ih, th);
-                    split(fz, iz, tz);
-                    const bool in = unsigned(ih + 1) <= unsigned(nh) && unsigned(iz + 1) <= unsigned(g.nz);
-                    const Off off = in ? Off(s) * plane + Off(iz) * pitch + ih : -(pitch + 1);
-                    const float* p = base + off;
-                    const float a0 = fmaf(th, __ldg(p + 1) - __ldg(p), __ldg(p));
-                    const float a1 = fmaf(th, __ldg(p + pitch + 1) - __ldg(p + pitch), __ldg(p + pitch));
-                    acc += in ? fmaf(tz, a1 - a0, a0) : 0.f;
-                }
-                out = ray_step(g, cs, v) * acc;
-            }
-        }
-    } else {
-        const int A = A0;
-        const int nh = A ? g.nx : g.ny;
-        const int ns = A ? g.ny : g.nx;
-        const Off pitch = nh + 2;
-        const Off plane = pitch * Off(g.nz + 2);
-        const float* gbase = (A ? vy : vx) + pitch + 1;
-        const float4 cd = g.col[cl];
-        const float vd = float(v);
-        const float czf = 0.5f * float(g.nz - 1);
-        int s0 = 0, s1 = ns - 1;
-        clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
-        clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
-        if (!live) { s0 = 1; s1 = 0; }
-        if (s0 <= s1) {
-            atomicMin(&s_lo, s0);
-            atomicMax(&s_hi, s1);
-        }
-        __syncthreads();
-        const int S0 = s_lo, S1 = s_hi;
-        float acc = 0.f;
-        for (int sc = S0; sc <= S1; sc += ST) {
-            // ---- boxes of the chunk's slices from the 4 corner rays (warp 0) ----
-            if (tid < 32) {
-                const int j = tid >> 2, corner = tid & 3;
-                const int cu = (corner & 1) ? u_last : u_first, cv = (corner & 2) ? v_last : v_first;
-                const float4 cc = g.col[a * g.nu + cu];
-                const float fs = float(sc + j);
-                const float fh = fmaf(fs, cc.y, cc.x);
-                const float fz = fmaf(float(row_coord(g, cv)), fmaf(fs, cc.w, cc.z), czf);
-                int ih, iz;
-                float th, tz;
-                split(fh, ih, th);
-                split(fz, iz, tz);
-                int hmin = ih, hmax = ih, zmin = iz, zmax = iz;
-#pragma unroll
-                for (int o = 1; o <= 2; o <<= 1) {
-                    hmin = min(hmin, __shfl_xor_sync(0xffffffffu, hmin, o));
-                    hmax = max(hmax, __shfl_xor_sync(0xffffffffu, hmax, o));
-                    zmin = min(zmin, __shfl_xor_sync(0xffffffffu, zmin, o));
-                    zmax = max(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
-                }
-                if (corner == 0) {
-                    const int hlo = max(hmin - 1, -1), hhi = min(hmax + 2, nh);
-                    const int zlo = max(zmin - 1, -1), zhi = min(zmax + 2, g.nz);
-                    box[j] = BoxInfo{hlo, zlo, max(0, hhi - hlo + 1), max(0, zhi - zlo + 1)};
-                }
-                const int big = __any_sync(0xffffffffu, corner == 0 && (min(hmax + 2, nh) - max(hmin - 1, -1) + 1 > SWM ||
-                                                                       min(zmax + 2, g.nz) - max(zmin - 1, -1) + 1 > SHM));
-                if (tid == 0) s_bad = big;
-            }
-            __syncthreads();
-            const bool bad = s_bad;
-            if (!bad) {
-                // ---- stage: one box row per warp iteration, lanes along h ----
-                for (int row = threadIdx.y; row < ST * SHM; row += FWD_BY) {
-                    const int j = row / SHM, r = row % SHM;
-                    const BoxInfo bx = box[j];
-                    if (r >= bx.h || sc + j > S1) continue;
-                    const float* src = gbase + Off(sc + j) * plane + Off(bx.zlo + r) * pitch + bx.hlo;
-                    float* dst = buf + (j * SHM + r) * SWS;
-                    for (int c = threadIdx.x; c < bx.w; c += FWD_BX) dst[c] = __ldg(src + c);
-                }
-                __syncthreads();
-            }
-            // ---- march the chunk ----
-            const int e = min(sc + ST - 1, min(s1, S1));
-            for (int s = max(sc, s0); s <= e; ++s) {
-                const float fs = float(s);
-                const float fh = fmaf(fs, cd.y, cd.x);
-                const float fz = fmaf(vd, fmaf(fs, cd.w, cd.z), czf);
-                int ih, iz;
-                float th, tz;
-                split(fh, ih, th);
-                split(fz, iz, tz);
-                const bool in = unsigned(ih + 1) <= unsigned(nh) && unsigned(iz + 1) <= unsigned(g.nz);
-                float v00, v10, v01, v11;
-                const BoxInfo bx = box[s - sc];
-                const int bh = ih - bx.hlo, bz = iz - bx.zlo;
-                if (!bad && bh >= 0 && bh + 1 < bx.w && bz >= 0 && bz + 1 < bx.h) {
-                    const float* p = buf + ((s - sc) * SHM + bz) * SWS + bh;
-                    v00 = p[0];
-                    v10 = p[1];
-                    v01 = p[SWS];
-                    v11 = p[SWS + 1];
-                } else {
-                    const float* p = gbase + (in ? Off(s) * plane + Off(iz) * pitch + ih : -(pitch + 1));
-                    v00 = __ldg(p);
-                    v10 = __ldg(p + 1);
-                    v01 = __ldg(p + pitch);
-                    v11 = __ldg(p + pitch + 1);
-                }
-                const float a0 = fmaf(th, v10 - v00, v00);
-                const float a1 = fmaf(th, v11 - v01, v01);
-                acc += in ? fmaf(tz, a1 - a0, a0) : 0.f;
-            }
-            __syncthreads();  // buffer and boxes are rewritten by the next chunk
-        }
-        out = live ? ray_step(g, cs, v) * acc : 0.f;
-    }
-    const size_t o = size_t(a) * g.nu * g.nv + size_t(iv) * g.nu + iu;
-    if (!RESID) {
-        if (live) y[o] = out;
-    } else {
-        double r = 0.0;
-        if (live) {
-            const double d = double(out) - double(__ldg(b + o));
-            r = d * d;
-        }
-        r = block_sum(r);
-        if (tid == 0) partials[(size_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = r;
-    }
-}
-
 void relayout(Geometry& g, const float* x, cudaStream_t s) {
     const size_t nvx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
     const size_t nvy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
@@ -345,20 +150,6 @@ template <bool RESID>
 void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s) {
     const KGeom k = g.kgeom();
     const int* vo = g.d_vorder.as<int>();
-    static const bool direct = [] {
-        const char* e = std::getenv("CTK_AX_DIRECT");
-        return e && e[0] == '1';
-    }();
-    if (!direct) {
-        if (wide_offsets(g))
-            k_ax_staged_f32<RESID, long long><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(
-                k, vo, g.vx.as<float>(), g.vy.as<float>(), x, y, b, partials);
-        else
-            k_ax_staged_f32<RESID, int><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(
-                k, vo, g.vx.as<float>(), g.vy.as<float>(), x, y, b, partials);
-        after_launch(RESID ? "k_ax_staged_f32_residual" : "k_ax_staged_f32");
-        return;
-    }
     if (wide_offsets(g))
         k_ax_f32<RESID, long long><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(k, vo, g.vx.as<float>(), g.vy.as<float>(),
                                                                                 x, y, b, partials);
