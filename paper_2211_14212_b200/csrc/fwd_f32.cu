@@ -122,6 +122,114 @@ k_ax_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ vx, 
     }
 }
 
+// ---- z-fastest variant ------------------------------------------------------------------
+// All rays of one detector column share fh(s) exactly (it depends on the column only), so a
+// warp of 32 consecutive detector ROWS of one column has a single in-plane index ih per
+// slice and consecutive z indices.  With the layouts stored z-fastest,
+//   wx[i][j+1][k+1]  (x-dominant rays: slice i, h = j)     wy[j][i+1][k+1]  (h = i)
+// each of the 4 tap loads of a warp covers one contiguous z run (1-2 cache lines) instead
+// of two partial rows of a y/x-fastest plane.
+constexpr int ZW_BR = 32, ZW_BC = 8;  // block: 32 detector rows (lanes) x 8 columns
+
+// x[i + nx(j + ny k)] -> wx[i][j+1][k+1] and wy[j][i+1][k+1]: 32x32 (i, k) tile transposes
+__global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ wx,
+                                 float* __restrict__ wy) {
+    __shared__ float tile[32][33];
+    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + threadIdx.x, k = k0 + r;
+        tile[r][threadIdx.x] = (i < nx && k < nz) ? __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k)) : 0.f;
+    }
+    __syncthreads();
+    const size_t pz = size_t(nz) + 2;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, k = k0 + threadIdx.x;
+        if (i < nx && k < nz) {
+            const float v = tile[threadIdx.x][r];
+            wx[(size_t(i) * (ny + 2) + (j + 1)) * pz + k + 1] = v;
+            wy[(size_t(j) * (nx + 2) + (i + 1)) * pz + k + 1] = v;
+        }
+    }
+}
+
+template <bool RESID, class Off>
+__global__ void __launch_bounds__(ZW_BR * ZW_BC)
+k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
+               const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
+               double* __restrict__ partials) {
+    __shared__ float outs[ZW_BR][ZW_BC + 1];
+    const int iv = blockIdx.z * ZW_BR + threadIdx.x;
+    const int a = vorder[blockIdx.y];
+    const int iu = blockIdx.x * ZW_BC + threadIdx.y;
+    float out = 0.f;
+    const bool live = iu < g.nu && iv < g.nv;
+    if (live) {
+        const int c = a * g.nu + iu;
+        const double2 cs = g.colstep[c];
+        const double v = row_coord(g, iv);
+        if (g.has_zrays && is_zray(g, cs, v)) {
+            const double2 tr = g.ctst[a];
+            WalkF w;
+            walk_generic(g, tr.x, tr.y, iu, iv, w);
+            out = march_generic(g, w, xs);
+        } else {
+            const float4 cd = g.col[c];
+            const int A = g.colaxis[c];
+            const int nh = A ? g.nx : g.ny;
+            const int ns = A ? g.ny : g.nx;
+            const Off pz = g.nz + 2;
+            const Off plane = pz * Off(nh + 2);
+            const float* base = (A ? wy : wx) + pz + 1;  // tap (h, z) of slice s at base[s*plane + h*pz + z]
+            const float vd = float(v);
+            const float czf = 0.5f * float(g.nz - 1);
+            int s0 = 0, s1 = ns - 1;
+            clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
+            clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
+            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            float acc = 0.f;
+#pragma unroll 4
+            for (int s = s0; s <= s1; ++s) {
+                const float fs = float(s);
+                const float fh = fmaf(fs, cd.y, cd.x);
+                const float gs = fmaf(fs, cd.w, cd.z);
+                const float fz = fmaf(vd, gs, czf);
+                int ih, iz;
+                float th, tz;
+                split(fh, ih, th);
+                split(fz, iz, tz);
+                const bool in = unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
+                const Off off = in ? Off(s) * plane + Off(ih) * pz + iz : -(pz + 1);
+                const float* p = base + off;
+                const float v00 = __ldg(p), v01 = __ldg(p + 1);          // (ih, iz), (ih, iz+1)
+                const float v10 = __ldg(p + pz), v11 = __ldg(p + pz + 1);  // (ih+1, iz), (ih+1, iz+1)
+                const float a0 = fmaf(th, v10 - v00, v00);
+                const float a1 = fmaf(th, v11 - v01, v01);
+                const float smp = fmaf(tz, a1 - a0, a0);
+                acc += in ? smp : 0.f;
+            }
+            out = ray_step(g, cs, v) * acc;
+        }
+    }
+    if (!RESID) {
+        // transpose through shared memory so the stores run along detector columns
+        outs[threadIdx.x][threadIdx.y] = out;
+        __syncthreads();
+        const int t = threadIdx.x + ZW_BR * threadIdx.y;
+        const int r = t / ZW_BC, cc = t % ZW_BC;
+        const int ivw = blockIdx.z * ZW_BR + r, iuw = blockIdx.x * ZW_BC + cc;
+        if (ivw < g.nv && iuw < g.nu) y[size_t(a) * g.nu * g.nv + size_t(ivw) * g.nu + iuw] = outs[r][cc];
+    } else {
+        double rr = 0.0;
+        if (live) {
+            const double d = double(out) - double(__ldg(b + size_t(a) * g.nu * g.nv + size_t(iv) * g.nu + iu));
+            rr = d * d;
+        }
+        rr = block_sum(rr);
+        if (threadIdx.x == 0 && threadIdx.y == 0)
+            partials[(size_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = rr;
+    }
+}
+
 void relayout(Geometry& g, const float* x, cudaStream_t s) {
     const size_t nvx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
     const size_t nvy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
@@ -139,7 +247,30 @@ void relayout(Geometry& g, const float* x, cudaStream_t s) {
     }
 }
 
-dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + FWD_BX - 1) / FWD_BX, g.na, (g.nv + FWD_BY - 1) / FWD_BY); }
+// row-fast layout kernel (k_ax_f32) unless CTK_AX_KERNEL=rowfast is not set: the z-fast
+// kernel is the default
+bool use_zfast() {
+    static const bool v = [] {
+        const char* e = std::getenv("CTK_AX_KERNEL");
+        return !(e && e[0] == 'r');
+    }();
+    return v;
+}
+
+void relayout_zfast(Geometry& g, const float* x, cudaStream_t s) {
+    const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
+    const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
+    if (g.vx.ensure(nwx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vx.p, 0, nwx * sizeof(float), s));
+    if (g.vy.ensure(nwy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vy.p, 0, nwy * sizeof(float), s));
+    dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.nz + 31) / 32, g.ny);
+    k_relayout_zfast<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vx.as<float>(), g.vy.as<float>());
+    after_launch("k_relayout_zfast");
+}
+
+dim3 fwd_grid(const Geometry& g) {
+    if (use_zfast()) return dim3((g.nu + ZW_BC - 1) / ZW_BC, g.na, (g.nv + ZW_BR - 1) / ZW_BR);
+    return dim3((g.nu + FWD_BX - 1) / FWD_BX, g.na, (g.nv + FWD_BY - 1) / FWD_BY);
+}
 
 bool wide_offsets(const Geometry& g) {
     const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz + 2);
@@ -150,26 +281,37 @@ template <bool RESID>
 void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s) {
     const KGeom k = g.kgeom();
     const int* vo = g.d_vorder.as<int>();
-    if (wide_offsets(g))
-        k_ax_f32<RESID, long long><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(k, vo, g.vx.as<float>(), g.vy.as<float>(),
-                                                                                x, y, b, partials);
-    else
-        k_ax_f32<RESID, int><<<fwd_grid(g), dim3(FWD_BX, FWD_BY), 0, s>>>(k, vo, g.vx.as<float>(), g.vy.as<float>(), x,
-                                                                          y, b, partials);
+    const float* v0 = g.vx.as<float>();
+    const float* v1 = g.vy.as<float>();
+    if (use_zfast()) {
+        const dim3 blk(ZW_BR, ZW_BC);
+        if (wide_offsets(g)) k_ax_zfast_f32<RESID, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
+        else k_ax_zfast_f32<RESID, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
+        after_launch(RESID ? "k_ax_zfast_f32_residual" : "k_ax_zfast_f32");
+        return;
+    }
+    const dim3 blk(FWD_BX, FWD_BY);
+    if (wide_offsets(g)) k_ax_f32<RESID, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
+    else k_ax_f32<RESID, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
     after_launch(RESID ? "k_ax_f32_residual" : "k_ax_f32");
+}
+
+void prepare(Geometry& g, const float* x, cudaStream_t s) {
+    if (use_zfast()) relayout_zfast(g, x, s);
+    else relayout(g, x, s);
 }
 
 }  // namespace
 
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
-    relayout(g, x, s);
+    prepare(g, x, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
     launch_ax<false>(g, x, y, nullptr, nullptr, s);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
 }
 
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
-    relayout(g, x, s);
+    prepare(g, x, s);
     const dim3 grd = fwd_grid(g);
     const size_t nblk = size_t(grd.x) * grd.y * grd.z;
     g.proj_t.ensure(std::max(g.range() * sizeof(float), nblk * sizeof(double)));
