@@ -1,10 +1,11 @@
 // Joseph forward projection Ax for T = float (projector.hpp:113-162) on sm_100a.
 //
-// Layouts in HBM (f32, zero-padded so the four bilinear taps need no bounds checks):
-//   vx[i][k+1][j+1]  pitch ny+2, one plane per x-slice   (x-dominant rays walk x)
-//   vy[j][k+1][i+1]  pitch nx+2, one plane per y-slice   (y-dominant rays walk y)
-// A warp is 32 consecutive detector columns of one row; their taps in a slice are
-// consecutive addresses of one or two plane rows.
+// Layouts in HBM (f32, z fastest, zero-padded so the four bilinear taps need no checks):
+//   wx[i][j+1][k+1]  one plane per x-slice, h = y   (x-dominant rays walk x)
+//   wy[j][i+1][k+1]  one plane per y-slice, h = x   (y-dominant rays walk y)
+// All rays of one detector column share fh(s) exactly (it depends on the column only), so
+// a warp = 32 consecutive detector ROWS of one column has one in-plane index ih per slice
+// and consecutive z indices: each tap load of the warp is one contiguous z run (1-2 lines).
 //
 // Grid order = L2 reuse.  The volume (512 MiB at 512^3) does not fit the 126 MB L2, and
 // every view crosses all of it.  Blocks are dispatched with the detector-row band
@@ -19,108 +20,6 @@
 
 namespace ctkb {
 namespace {
-
-constexpr int FWD_BX = 32, FWD_BY = 8;  // rays per block: 32 columns x 8 rows
-
-// vy[j][k+1][i+1]: x stays fastest (coalesced both ways)
-__global__ void k_relayout_y(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ vy) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int k = blockIdx.y;
-    const int j = blockIdx.z;
-    if (i >= nx) return;
-    const size_t pitch = size_t(nx) + 2, plane = pitch * (size_t(nz) + 2);
-    vy[size_t(j) * plane + size_t(k + 1) * pitch + i + 1] = __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k));
-}
-
-// vx[i][k+1][j+1]: 32x32 tile transpose of (i, j) per z-plane
-__global__ void k_relayout_x(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ vx) {
-    __shared__ float tile[32][33];
-    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32, k = blockIdx.z;
-    const size_t pitch = size_t(ny) + 2, plane = pitch * (size_t(nz) + 2);
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int i = i0 + threadIdx.x, j = j0 + r;
-        tile[r][threadIdx.x] = (i < nx && j < ny) ? __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k)) : 0.f;
-    }
-    __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-        const int i = i0 + r, j = j0 + threadIdx.x;
-        if (i < nx && j < ny) vx[size_t(i) * plane + size_t(k + 1) * pitch + j + 1] = tile[threadIdx.x][r];
-    }
-}
-
-// RESID=false: y[a][iv][iu] = A x.   RESID=true: per-block partial of sum (Ax - b)^2.
-// Off = int (volumes with ns*(nh+2)*(nz+2) < 2^31) or long long.
-template <bool RESID, class Off>
-__global__ void __launch_bounds__(FWD_BX * FWD_BY)
-k_ax_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ vx, const float* __restrict__ vy,
-         const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b, double* __restrict__ partials) {
-    const int iu = blockIdx.x * FWD_BX + threadIdx.x;
-    const int a = vorder[blockIdx.y];
-    const int iv = blockIdx.z * FWD_BY + threadIdx.y;
-    float out = 0.f;
-    const bool live = iu < g.nu && iv < g.nv;
-    if (live) {
-        const int c = a * g.nu + iu;
-        const double2 cs = g.colstep[c];
-        const double v = row_coord(g, iv);
-        if (g.has_zrays && is_zray(g, cs, v)) {
-            const double2 tr = g.ctst[a];
-            WalkF w;
-            walk_generic(g, tr.x, tr.y, iu, iv, w);
-            out = march_generic(g, w, xs);
-        } else {
-            const float4 cd = g.col[c];
-            const int A = g.colaxis[c];
-            const int nh = A ? g.nx : g.ny;
-            const int ns = A ? g.ny : g.nx;
-            const Off pitch = nh + 2;
-            const Off plane = pitch * Off(g.nz + 2);
-            const float* base = (A ? vy : vx) + pitch + 1;  // tap (h, z) of slice s at base[s*plane + z*pitch + h]
-            const float vd = float(v);
-            const float czf = 0.5f * float(g.nz - 1);
-            int s0 = 0, s1 = ns - 1;
-            clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
-            clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
-            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
-            float acc = 0.f;
-#pragma unroll 4
-            for (int s = s0; s <= s1; ++s) {
-                const float fs = float(s);
-                const float fh = fmaf(fs, cd.y, cd.x);
-                const float gs = fmaf(fs, cd.w, cd.z);
-                const float fz = fmaf(vd, gs, czf);
-                int ih, iz;
-                float th, tz;
-                split(fh, ih, th);
-                split(fz, iz, tz);
-                // some tap inside the volume <=> ih in [-1, nh-1] and iz in [-1, nz-1]
-                const bool in = unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
-                const Off off = in ? Off(s) * plane + Off(iz) * pitch + ih : -(pitch + 1);  // else: padding corner
-                const float* p = base + off;
-                const float v00 = __ldg(p), v10 = __ldg(p + 1);
-                const float v01 = __ldg(p + pitch), v11 = __ldg(p + pitch + 1);
-                const float a0 = fmaf(th, v10 - v00, v00);
-                const float a1 = fmaf(th, v11 - v01, v01);
-                const float smp = fmaf(tz, a1 - a0, a0);
-                acc += in ? smp : 0.f;
-            }
-            out = ray_step(g, cs, v) * acc;
-        }
-    }
-    const size_t o = size_t(a) * g.nu * g.nv + size_t(iv) * g.nu + iu;
-    if (!RESID) {
-        if (live) y[o] = out;
-    } else {
-        double r = 0.0;
-        if (live) {
-            const double d = double(out) - double(__ldg(b + o));
-            r = d * d;
-        }
-        r = block_sum(r);
-        if (threadIdx.x == 0 && threadIdx.y == 0)
-            partials[(size_t(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = r;
-    }
-}
 
 // ---- z-fastest variant ------------------------------------------------------------------
 // All rays of one detector column share fh(s) exactly (it depends on the column only), so a
@@ -182,30 +81,43 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             const float* base = (A ? wy : wx) + pz + 1;  // tap (h, z) of slice s at base[s*plane + h*pz + z]
             const float vd = float(v);
             const float czf = 0.5f * float(g.nz - 1);
+            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            // a sample contributes iff some tap is inside the volume: ih in [-1, nh-1] and
+            // iz in [-1, nz-1].  ih(s) and iz(s) are monotone in s (monotone roundings of
+            // affine functions), so the contributing slices form one interval; find it
+            // exactly with the kernel's own f32 arithmetic, starting from the fp64 estimate.
+            auto inside = [&](int s) {
+                const float fs = float(s);
+                int ih, iz;
+                float th, tz;
+                split(fmaf(fs, cd.y, cd.x), ih, th);
+                split(fmaf(vd, fmaf(fs, cd.w, cd.z), czf), iz, tz);
+                return unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
+            };
             int s0 = 0, s1 = ns - 1;
             clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
             clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
-            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            while (s0 <= s1 && !inside(s0)) ++s0;
+            while (s1 >= s0 && !inside(s1)) --s1;
+            if (s0 <= s1) {
+                while (s0 > 0 && inside(s0 - 1)) --s0;
+                while (s1 < ns - 1 && inside(s1 + 1)) ++s1;
+            }
             float acc = 0.f;
+            const float* ps = base + Off(s0) * plane;
 #pragma unroll 4
-            for (int s = s0; s <= s1; ++s) {
+            for (int s = s0; s <= s1; ++s, ps += plane) {
                 const float fs = float(s);
-                const float fh = fmaf(fs, cd.y, cd.x);
-                const float gs = fmaf(fs, cd.w, cd.z);
-                const float fz = fmaf(vd, gs, czf);
                 int ih, iz;
                 float th, tz;
-                split(fh, ih, th);
-                split(fz, iz, tz);
-                const bool in = unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
-                const Off off = in ? Off(s) * plane + Off(ih) * pz + iz : -(pz + 1);
-                const float* p = base + off;
+                split(fmaf(fs, cd.y, cd.x), ih, th);
+                split(fmaf(vd, fmaf(fs, cd.w, cd.z), czf), iz, tz);
+                const float* p = ps + (ih * int(pz) + iz);
                 const float v00 = __ldg(p), v01 = __ldg(p + 1);          // (ih, iz), (ih, iz+1)
                 const float v10 = __ldg(p + pz), v11 = __ldg(p + pz + 1);  // (ih+1, iz), (ih+1, iz+1)
                 const float a0 = fmaf(th, v10 - v00, v00);
                 const float a1 = fmaf(th, v11 - v01, v01);
-                const float smp = fmaf(tz, a1 - a0, a0);
-                acc += in ? smp : 0.f;
+                acc += fmaf(tz, a1 - a0, a0);
             }
             out = ray_step(g, cs, v) * acc;
         }
@@ -230,33 +142,6 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
     }
 }
 
-void relayout(Geometry& g, const float* x, cudaStream_t s) {
-    const size_t nvx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
-    const size_t nvy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
-    if (g.vx.ensure(nvx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vx.p, 0, nvx * sizeof(float), s));
-    if (g.vy.ensure(nvy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vy.p, 0, nvy * sizeof(float), s));
-    {
-        dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.ny + 31) / 32, g.nz);
-        k_relayout_x<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vx.as<float>());
-        after_launch("k_relayout_x");
-    }
-    {
-        dim3 blk(128), grd((g.nx + 127) / 128, g.nz, g.ny);
-        k_relayout_y<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vy.as<float>());
-        after_launch("k_relayout_y");
-    }
-}
-
-// row-fast layout kernel (k_ax_f32) unless CTK_AX_KERNEL=rowfast is not set: the z-fast
-// kernel is the default
-bool use_zfast() {
-    static const bool v = [] {
-        const char* e = std::getenv("CTK_AX_KERNEL");
-        return !(e && e[0] == 'r');
-    }();
-    return v;
-}
-
 void relayout_zfast(Geometry& g, const float* x, cudaStream_t s) {
     const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
     const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
@@ -267,10 +152,7 @@ void relayout_zfast(Geometry& g, const float* x, cudaStream_t s) {
     after_launch("k_relayout_zfast");
 }
 
-dim3 fwd_grid(const Geometry& g) {
-    if (use_zfast()) return dim3((g.nu + ZW_BC - 1) / ZW_BC, g.na, (g.nv + ZW_BR - 1) / ZW_BR);
-    return dim3((g.nu + FWD_BX - 1) / FWD_BX, g.na, (g.nv + FWD_BY - 1) / FWD_BY);
-}
+dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + ZW_BC - 1) / ZW_BC, g.na, (g.nv + ZW_BR - 1) / ZW_BR); }
 
 bool wide_offsets(const Geometry& g) {
     const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz + 2);
@@ -283,23 +165,13 @@ void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* pa
     const int* vo = g.d_vorder.as<int>();
     const float* v0 = g.vx.as<float>();
     const float* v1 = g.vy.as<float>();
-    if (use_zfast()) {
-        const dim3 blk(ZW_BR, ZW_BC);
-        if (wide_offsets(g)) k_ax_zfast_f32<RESID, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
-        else k_ax_zfast_f32<RESID, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
-        after_launch(RESID ? "k_ax_zfast_f32_residual" : "k_ax_zfast_f32");
-        return;
-    }
-    const dim3 blk(FWD_BX, FWD_BY);
-    if (wide_offsets(g)) k_ax_f32<RESID, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
-    else k_ax_f32<RESID, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
-    after_launch(RESID ? "k_ax_f32_residual" : "k_ax_f32");
+    const dim3 blk(ZW_BR, ZW_BC);
+    if (wide_offsets(g)) k_ax_zfast_f32<RESID, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
+    else k_ax_zfast_f32<RESID, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
+    after_launch(RESID ? "k_ax_zfast_f32_residual" : "k_ax_zfast_f32");
 }
 
-void prepare(Geometry& g, const float* x, cudaStream_t s) {
-    if (use_zfast()) relayout_zfast(g, x, s);
-    else relayout(g, x, s);
-}
+void prepare(Geometry& g, const float* x, cudaStream_t s) { relayout_zfast(g, x, s); }
 
 }  // namespace
 
