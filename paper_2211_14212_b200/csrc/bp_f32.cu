@@ -35,41 +35,29 @@ __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __
 // Pass CLASS (0: x-dominant columns, planes x = s, rows p = y; 1: y-dominant columns,
 // planes y = s, rows p = x).  A CTA owns one plane s, BP_PB rows [p0, p0+BP_PB) and a band
 // of BP_KB slices [k0, k0+BP_KB) along z, and loops over all views.  Per view:
-//  collect  the detector columns of this class whose in-plane stencil touches the tile are
-//           compacted into an entry list in column order (block prefix sum of ballots) and
-//           registered in the (at most two) rows their stencil touches;
-//  phase 1  work items = (entry, half band), spread evenly over the 256 threads: each
-//           marches the entry's detector rows iv with exactly the forward's f32
-//           fz = fmaf(vd, fmaf(s, gd, g0), cz) (16-byte column loads) and writes the
-//           transposed z-interpolation Z[k][e] = sum wz*(step*y) (one store per entry,
-//           rolling register accumulation: fz increases with iv);
+//  phase 1  one thread per candidate detector column iu marches its detector rows iv
+//           (exactly the forward's f32 fz = fmaf(vd, fmaf(s, gd, g0), cz); 16-byte column
+//           loads) and accumulates the transposed z-interpolation Z[k][e] = sum wz*(step*y)
+//           in shared memory; it registers itself in the (at most two) rows its in-plane
+//           stencil touches;
 //  phase 2  thread p owns row p (BP_KB accumulators in registers) and adds wh * Z[:][e] of
-//           the entries registered in its row, sorted by entry -> deterministic order.
-// Z[k][e] has row stride BP_EMAX: phase-1 lanes (consecutive e) and phase-2 lanes
-// (consecutive rows -> consecutive e) hit distinct banks.
-constexpr int BP_PB = 256, BP_KB = 32, BP_SL = 8, BP_EMAX = 512, BP_HB = BP_KB / 2;
-
-size_t plane_smem_bytes(int nv, int na) {
-    return sizeof(float) * (size_t(BP_KB) * BP_EMAX + size_t(BP_PB) * BP_SL + BP_PB + 3 * size_t(BP_EMAX) + nv) +
-           sizeof(int2) * size_t(na);
-}
+//           the columns registered in its row, sorted by column -> deterministic order.
+// Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
+// their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
+constexpr int BP_PB = 256, BP_KB = 32, BP_SL = 8;
 
 template <int CLASS>
 __global__ void __launch_bounds__(BP_PB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, int ptiles) {
     extern __shared__ __align__(16) float sm[];
-    float* Z = sm;                                              // [BP_KB][BP_EMAX]
-    int* lists = reinterpret_cast<int*>(Z + BP_KB * BP_EMAX);   // [BP_PB][BP_SL]
+    float* Z = sm;                                              // [BP_KB][BP_PB]
+    int* lists = reinterpret_cast<int*>(Z + BP_KB * BP_PB);     // [BP_PB][BP_SL]
     int* cnt = lists + BP_PB * BP_SL;                           // [BP_PB]
-    float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_EMAX] in-plane fraction
-    float* egs = eth + BP_EMAX;                                 // [BP_EMAX] G(s) of the entry
-    int* ecol = reinterpret_cast<int*>(egs + BP_EMAX);          // [BP_EMAX] column index a*nu+iu
-    int2* urange = reinterpret_cast<int2*>(ecol + BP_EMAX);     // [na]
+    float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_PB]
+    int2* urange = reinterpret_cast<int2*>(eth + BP_PB);        // [na]
     float* vdtab = reinterpret_cast<float*>(urange + g.na);     // [nv]
-    __shared__ int wsum[BP_PB / 32];
-    __shared__ int s_count;
 
-    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int t = threadIdx.x;
     // plane index fastest: a wave of resident CTAs shares one (row tile, z band), so per
     // view it reads only that band's detector rows -> the projections stay L2-resident
     const int s = blockIdx.x;
@@ -88,6 +76,10 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
 
+    float acc[BP_KB];
+#pragma unroll
+    for (int m = 0; m < BP_KB; ++m) acc[m] = 0.f;
+
     // candidate detector-column range of every view for this tile (projection of the
     // tile's row segment in the plane), computed once, in parallel
     for (int a = t; a < g.na; a += BP_PB) {
@@ -104,136 +96,102 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     }
     __syncthreads();
 
-    float acc[BP_KB];
-#pragma unroll
-    for (int m = 0; m < BP_KB; ++m) acc[m] = 0.f;
-
     for (int a = 0; a < g.na; ++a) {
         const int iu0 = urange[a].x, iu1 = urange[a].y;
-        int cb = iu0;
-        while (cb <= iu1) {
-            // ---- collect up to BP_EMAX entries (column order) ----
+        for (int cbase = iu0; cbase <= iu1; cbase += BP_PB) {
+            // ---- phase 1 ----
             cnt[t] = 0;
-            if (t == 0) s_count = 0;
             __syncthreads();
-            while (cb <= iu1 && s_count <= BP_EMAX - BP_PB) {
-                const int base = s_count;
-                const int iu = cb + t;
-                bool valid = false;
-                int ih = 0, c = 0;
-                float th = 0.f, gs = 0.f;
-                if (iu <= iu1) {
-                    c = a * g.nu + iu;
-                    if (g.colaxis[c] == CLASS) {
-                        const float4 cd = g.col[c];
-                        const float fh = fmaf(fs, cd.y, cd.x);
-                        const float fih = floorf(fh);
-                        ih = int(fih);
-                        th = fh - fih;
-                        gs = fmaf(fs, cd.w, cd.z);
-                        valid = ih + 1 >= p0 && ih <= p0 + BP_PB - 1 && ih + 1 >= 0 && ih < nh;
-                    }
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, valid);
-                if (lane == 0) wsum[wid] = __popc(bal);
-                __syncthreads();
-                int e = base + __popc(bal & ((1u << lane) - 1u));
-                for (int w = 0; w < wid; ++w) e += wsum[w];
-                if (valid) {
-                    eth[e] = th;
-                    egs[e] = gs;
-                    ecol[e] = c;
-                    if (ih >= p0) {
-                        const int sl = atomicAdd(&cnt[ih - p0], 1);
-                        if (sl < BP_SL) lists[(ih - p0) * BP_SL + sl] = (e << 1);
-                    }
-                    if (ih + 1 <= p0 + BP_PB - 1 && th != 0.f) {
-                        const int sl = atomicAdd(&cnt[ih + 1 - p0], 1);
-                        if (sl < BP_SL) lists[(ih + 1 - p0) * BP_SL + sl] = (e << 1) | 1;
-                    }
-                }
-                __syncthreads();
-                if (t == 0) {
-                    int tot = base;
-                    for (int w = 0; w < BP_PB / 32; ++w) tot += wsum[w];
-                    s_count = tot;
-                }
-                __syncthreads();
-                cb += BP_PB;
-            }
-            const int E = s_count;
-            // ---- phase 1: (entry, half band) items ----
-            for (int item = t; item < 2 * E; item += BP_PB) {
-                const int e = item >> 1, hb = item & 1;
-                const int kb0 = k0 + hb * BP_HB;
-                float* zc = Z + hb * BP_HB * BP_EMAX + e;
+            const int iu = cbase + t;
+            if (iu <= iu1) {
+                const int c = a * g.nu + iu;
+                if (g.colaxis[c] == CLASS) {
+                    const float4 cd = g.col[c];
+                    const float fh = fmaf(fs, cd.y, cd.x);
+                    const float fih = floorf(fh);
+                    const int ih = int(fih);
+                    const float th = fh - fih;
+                    if (ih + 1 >= p0 && ih <= p0 + BP_PB - 1 && ih + 1 >= 0 && ih < nh) {
 #pragma unroll
-                for (int m = 0; m < BP_HB; ++m) zc[m * BP_EMAX] = 0.f;
-                const float gs = egs[e];
-                const int c = ecol[e];
-                int v0 = 0, v1 = g.nv - 1;
-                if (gs > 0.f) {
-                    const float rg = invdu / gs;
-                    v0 = max(v0, int(floorf(fmaf(float(kb0) - 1.f - czf, rg, cvf))) - 1);
-                    v1 = min(v1, int(ceilf(fmaf(float(kb0 + BP_HB) - czf, rg, cvf))) + 1);
-                }
-                if (g.has_zrays) {
-                    // rows whose ray is z-dominant (|v| > |d_A|) belong to the generic pass;
-                    // they form the two ends of the column: clip exactly
-                    const double dA = g.colstep[c].y;
-                    const double cv = 0.5 * (g.nv - 1), r = dA / g.du;
-                    int lo = max(v0, int(ceil(cv - r)) - 1), hi = min(v1, int(floor(cv + r)) + 1);
-                    while (lo <= hi && fabs(row_coord(g, lo)) > dA) ++lo;
-                    while (hi >= lo && fabs(row_coord(g, hi)) > dA) --hi;
-                    v0 = lo;
-                    v1 = hi;
-                }
-                const float* pc = pt + size_t(c) * g.nv;
-                if (gs > 0.f) {
-                    int cur = -(1 << 20);
-                    float A = 0.f, B = 0.f;
-                    auto add = [&](int iv, float yv) {
-                        int iz;
-                        float tz;
-                        split(fmaf(vdtab[iv], gs, czf), iz, tz);
-                        const int kk = iz - kb0;
-                        const int adv = kk - cur;
-                        if (adv >= 1 && unsigned(cur) < unsigned(BP_HB)) zc[cur * BP_EMAX] = A;
-                        if (adv >= 2 && unsigned(cur + 1) < unsigned(BP_HB)) zc[(cur + 1) * BP_EMAX] = B;
-                        const float w0 = (1.f - tz) * yv, w1 = tz * yv;
-                        A = (adv == 0) ? A + w0 : ((adv == 1) ? B + w0 : w0);
-                        B = (adv == 0) ? B + w1 : w1;
-                        cur = kk;
-                    };
-                    if (vec4) {
-                        for (int b4 = v0 & ~3; b4 <= v1; b4 += 4) {
-                            const float4 y4 = __ldg(reinterpret_cast<const float4*>(pc + b4));
-                            if (b4 >= v0) add(b4, y4.x);
-                            if (b4 + 1 >= v0 && b4 + 1 <= v1) add(b4 + 1, y4.y);
-                            if (b4 + 2 >= v0 && b4 + 2 <= v1) add(b4 + 2, y4.z);
-                            if (b4 + 3 <= v1) add(b4 + 3, y4.w);
+                        for (int m = 0; m < BP_KB; ++m) Z[m * BP_PB + t] = 0.f;
+                        const float gs = fmaf(fs, cd.w, cd.z);
+                        int v0 = 0, v1 = g.nv - 1;
+                        if (gs > 0.f) {
+                            const float rg = invdu / gs;
+                            v0 = max(v0, int(floorf(fmaf(float(k0) - 1.f - czf, rg, cvf))) - 1);
+                            v1 = min(v1, int(ceilf(fmaf(float(k0 + BP_KB) - czf, rg, cvf))) + 1);
                         }
-                    } else {
-                        for (int iv = v0; iv <= v1; ++iv) add(iv, __ldg(pc + iv));
-                    }
-                    if (unsigned(cur) < unsigned(BP_HB)) zc[cur * BP_EMAX] = A;
-                    if (unsigned(cur + 1) < unsigned(BP_HB)) zc[(cur + 1) * BP_EMAX] = B;
-                } else {
-                    // degenerate geometry (stencil point not in front of the source)
-                    for (int iv = v0; iv <= v1; ++iv) {
-                        const float yv = __ldg(pc + iv);
-                        int iz;
-                        float tz;
-                        split(fmaf(vdtab[iv], gs, czf), iz, tz);
-                        const int kk = iz - kb0;
-                        if (unsigned(kk) < unsigned(BP_HB)) zc[kk * BP_EMAX] = fmaf(1.f - tz, yv, zc[kk * BP_EMAX]);
-                        if (unsigned(kk + 1) < unsigned(BP_HB))
-                            zc[(kk + 1) * BP_EMAX] = fmaf(tz, yv, zc[(kk + 1) * BP_EMAX]);
+                        if (g.has_zrays) {
+                            // rows whose ray is z-dominant (|v| > |d_A|) belong to the generic
+                            // pass; they form the two ends of the column: clip exactly
+                            const double dA = g.colstep[c].y;
+                            const double cv = 0.5 * (g.nv - 1), r = dA / g.du;
+                            int lo = max(v0, int(ceil(cv - r)) - 1), hi = min(v1, int(floor(cv + r)) + 1);
+                            while (lo <= hi && fabs(row_coord(g, lo)) > dA) ++lo;
+                            while (hi >= lo && fabs(row_coord(g, hi)) > dA) --hi;
+                            v0 = lo;
+                            v1 = hi;
+                        }
+                        const float* pc = pt + size_t(c) * g.nv;
+                        float* zc = Z + t;
+                        if (gs > 0.f) {
+                            // fz increases with iv, so each Z[k] is final once the march passes
+                            // it: accumulate in registers (A -> Z[cur], B -> Z[cur+1]) and
+                            // store each entry once, branch-free
+                            int cur = -(1 << 20);
+                            float A = 0.f, B = 0.f;
+                            auto add = [&](int iv, float yv) {
+                                int iz;
+                                float tz;
+                                split(fmaf(vdtab[iv], gs, czf), iz, tz);
+                                const int kk = iz - k0;
+                                const int adv = kk - cur;
+                                if (adv >= 1 && unsigned(cur) < unsigned(BP_KB)) zc[cur * BP_PB] = A;
+                                if (adv >= 2 && unsigned(cur + 1) < unsigned(BP_KB)) zc[(cur + 1) * BP_PB] = B;
+                                const float w0 = (1.f - tz) * yv, w1 = tz * yv;
+                                A = (adv == 0) ? A + w0 : ((adv == 1) ? B + w0 : w0);
+                                B = (adv == 0) ? B + w1 : w1;
+                                cur = kk;
+                            };
+                            if (vec4) {
+                                for (int b4 = v0 & ~3; b4 <= v1; b4 += 4) {
+                                    const float4 y4 = __ldg(reinterpret_cast<const float4*>(pc + b4));
+                                    if (b4 >= v0) add(b4, y4.x);
+                                    if (b4 + 1 >= v0 && b4 + 1 <= v1) add(b4 + 1, y4.y);
+                                    if (b4 + 2 >= v0 && b4 + 2 <= v1) add(b4 + 2, y4.z);
+                                    if (b4 + 3 <= v1) add(b4 + 3, y4.w);
+                                }
+                            } else {
+                                for (int iv = v0; iv <= v1; ++iv) add(iv, __ldg(pc + iv));
+                            }
+                            if (unsigned(cur) < unsigned(BP_KB)) zc[cur * BP_PB] = A;
+                            if (unsigned(cur + 1) < unsigned(BP_KB)) zc[(cur + 1) * BP_PB] = B;
+                        } else {
+                            // degenerate geometry (stencil point not in front of the source)
+                            for (int iv = v0; iv <= v1; ++iv) {
+                                const float yv = __ldg(pc + iv);
+                                int iz;
+                                float tz;
+                                split(fmaf(vdtab[iv], gs, czf), iz, tz);
+                                const int kk = iz - k0;
+                                if (unsigned(kk) < unsigned(BP_KB)) zc[kk * BP_PB] = fmaf(1.f - tz, yv, zc[kk * BP_PB]);
+                                if (unsigned(kk + 1) < unsigned(BP_KB)) zc[(kk + 1) * BP_PB] = fmaf(tz, yv, zc[(kk + 1) * BP_PB]);
+                            }
+                        }
+                        eth[t] = th;
+                        if (ih >= p0) {
+                            const int sl = atomicAdd(&cnt[ih - p0], 1);
+                            if (sl < BP_SL) lists[(ih - p0) * BP_SL + sl] = (t << 1);
+                        }
+                        if (ih + 1 <= p0 + BP_PB - 1 && th != 0.f) {
+                            const int sl = atomicAdd(&cnt[ih + 1 - p0], 1);
+                            if (sl < BP_SL) lists[(ih + 1 - p0) * BP_SL + sl] = (t << 1) | 1;
+                        }
                     }
                 }
             }
             __syncthreads();
-            // ---- phase 2: row p gathers its registered entries in entry order ----
+            // ---- phase 2: row p gathers its registered columns in column order ----
             const int n = cnt[t];
             if (n > 0 && p < nh) {
                 if (n <= BP_SL) {
@@ -252,12 +210,14 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                         const float th = eth[e];
                         const float wh = (lst[q] & 1) ? th : 1.f - th;
 #pragma unroll
-                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_EMAX + e], acc[m]);
+                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_PB + e], acc[m]);
                     }
                 } else {
-                    // overflow (very fine detector sampling): scan every entry in order
-                    for (int e = 0; e < E; ++e) {
-                        const float4 cd = g.col[ecol[e]];
+                    // overflow (very fine detector sampling): scan every column of the chunk in order
+                    for (int e = 0; e < BP_PB && cbase + e <= iu1; ++e) {
+                        const int c = a * g.nu + cbase + e;
+                        if (g.colaxis[c] != CLASS) continue;
+                        const float4 cd = g.col[c];
                         const float fh = fmaf(fs, cd.y, cd.x);
                         const float fih = floorf(fh);
                         const int ih = int(fih);
@@ -267,7 +227,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                         else if (ih + 1 == p && th != 0.f) wh = th;
                         else continue;
 #pragma unroll
-                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_EMAX + e], acc[m]);
+                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_PB + e], acc[m]);
                     }
                 }
             }
@@ -287,8 +247,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     }
 }
 
-// z-dominant rays of the matched transpose (only launched when the geometry has them):
-// thread per voxel, candidates from the footprint of the cube [voxel +- h]^3.
 __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x) {
     const size_t nvox = size_t(g.nx) * g.ny * g.nz;
     const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -448,7 +406,8 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz + BP_KB - 1) / BP_KB;
-    const size_t smem = plane_smem_bytes(g.nv, g.na);
+    const size_t smem =
+        sizeof(float) * (size_t(BP_PB) * BP_KB + size_t(BP_PB) * BP_SL + 2 * BP_PB + g.nv) + sizeof(int2) * g.na;
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     static size_t configured = 0;
     if (smem > configured) {
