@@ -304,6 +304,165 @@ static int orc_stencil(const orc_walk* w, int s, size_t idx[4], double wgt[4]) {
 ORC_DEFINE(double, f64)
 ORC_DEFINE(float, f32)
 
+/* ---- Siddon exact-length projector (new: absent from the reference).
+ * Ray geometry = make_ray (projector.hpp:29-46).  Voxel (i,j,k) is the box
+ * [(i - n/2) h, (i + 1 - n/2) h] x ... (centres at (i - (n-1)/2) h, types.hpp:50).  The
+ * weight of (ray, voxel) is the length of the ray inside the voxel box, i.e. the slab
+ * chord of tests/oracles.hpp:89-107 applied to that voxel.  Every plane crossing is
+ * evaluated as alpha_a(q) = ((q - n_a/2) h - o_a) * inv_a with inv_a = 1/d_a, both by the
+ * forward DDA and by the transpose, so the two see bit-identical segment lengths.  A ray
+ * parallel to an axis belongs to the half-open slab [plane q, plane q+1) containing o_a. */
+typedef struct {
+    double o[3], d[3], inv[3];
+} orc_ray;
+
+static void orc_make_ray(const orc_geom* g, double ct, double st, int iu, int iv, orc_ray* r) {
+    const double u = (iu - 0.5 * (g->nu - 1)) * g->du;
+    const double v = (iv - 0.5 * (g->nv - 1)) * g->du;
+    const double cx = -g->dod * ct, cy = -g->dod * st, cz = 0.0;
+    const double px = cx - u * st, py = cy + u * ct, pz = cz + v;
+    if (g->mode == 2) {
+        const double sx = g->dso * ct, sy = g->dso * st, sz = 0.0;
+        const double dx = px - sx, dy = py - sy, dz = pz - sz;
+        const double n = sqrt(dx * dx + dy * dy + dz * dz);
+        r->o[0] = sx; r->o[1] = sy; r->o[2] = sz;
+        r->d[0] = dx / n; r->d[1] = dy / n; r->d[2] = dz / n;
+    } else {
+        r->o[0] = px; r->o[1] = py; r->o[2] = pz;
+        r->d[0] = -ct; r->d[1] = -st; r->d[2] = 0.0;
+    }
+    for (int a = 0; a < 3; ++a) r->inv[a] = r->d[a] != 0.0 ? 1.0 / r->d[a] : 0.0;
+}
+
+static double orc_plane_alpha(const orc_ray* r, int a, int q, int n, double h) {
+    return ((q - 0.5 * n) * h - r->o[a]) * r->inv[a];
+}
+
+/* slab index of a coordinate: floor((c - lo) / h) with lo = -n h / 2 */
+static int orc_slab(double c, int n, double h) { return (int)floor(c / h + 0.5 * n); }
+
+/* chord of ray r inside voxel idx3 (0 if it misses) */
+static double orc_voxel_chord(const orc_ray* r, const int n3[3], double h, const int idx3[3]) {
+    double lo = -INFINITY, hi = INFINITY;
+    for (int a = 0; a < 3; ++a) {
+        if (r->d[a] == 0.0) {
+            if (orc_slab(r->o[a], n3[a], h) != idx3[a]) return 0.0;
+            continue;
+        }
+        const double a0 = orc_plane_alpha(r, a, idx3[a], n3[a], h);
+        const double a1 = orc_plane_alpha(r, a, idx3[a] + 1, n3[a], h);
+        lo = fmax(lo, fmin(a0, a1));
+        hi = fmin(hi, fmax(a0, a1));
+    }
+    return hi > lo ? hi - lo : 0.0;
+}
+
+/* DDA over the voxels the ray crosses; calls fn(idx, length) in traversal order */
+#define ORC_SIDDON_WALK(g, r, BODY)                                                         \
+    do {                                                                                     \
+        const int n3_[3] = {(g)->nx, (g)->ny, (g)->nz};                                      \
+        const double h_ = (g)->h;                                                            \
+        double amin_ = -INFINITY, amax_ = INFINITY;                                          \
+        int ok_ = 1;                                                                         \
+        for (int a_ = 0; a_ < 3 && ok_; ++a_) {                                              \
+            if ((r).d[a_] == 0.0) {                                                          \
+                const int s_ = orc_slab((r).o[a_], n3_[a_], h_);                             \
+                if (s_ < 0 || s_ >= n3_[a_]) ok_ = 0;                                        \
+                continue;                                                                    \
+            }                                                                                \
+            const double e0_ = orc_plane_alpha(&(r), a_, 0, n3_[a_], h_);                    \
+            const double e1_ = orc_plane_alpha(&(r), a_, n3_[a_], n3_[a_], h_);              \
+            amin_ = fmax(amin_, fmin(e0_, e1_));                                             \
+            amax_ = fmin(amax_, fmax(e0_, e1_));                                             \
+        }                                                                                    \
+        if (ok_ && amin_ < amax_) {                                                          \
+            int ix_[3], st_[3];                                                              \
+            double an_[3];                                                                   \
+            for (int a_ = 0; a_ < 3; ++a_) {                                                 \
+                if ((r).d[a_] == 0.0) {                                                      \
+                    ix_[a_] = orc_slab((r).o[a_], n3_[a_], h_);                              \
+                    st_[a_] = 0;                                                             \
+                    an_[a_] = INFINITY;                                                      \
+                    continue;                                                                \
+                }                                                                            \
+                st_[a_] = (r).d[a_] > 0.0 ? 1 : -1;                                          \
+                /* voxel entered at amin: the slab whose entry plane crossing is <= amin */  \
+                int q_ = st_[a_] > 0 ? 0 : n3_[a_] - 1;                                       \
+                while (1) {                                                                  \
+                    const double ax_ = orc_plane_alpha(&(r), a_, st_[a_] > 0 ? q_ + 1 : q_, n3_[a_], h_); \
+                    if (ax_ > amin_ || (st_[a_] > 0 ? q_ == n3_[a_] - 1 : q_ == 0)) break;  \
+                    q_ += st_[a_];                                                           \
+                }                                                                            \
+                ix_[a_] = q_;                                                                \
+                an_[a_] = orc_plane_alpha(&(r), a_, st_[a_] > 0 ? q_ + 1 : q_, n3_[a_], h_); \
+            }                                                                                \
+            double acur_ = amin_;                                                            \
+            while (acur_ < amax_) {                                                          \
+                double anext_ = fmin(amax_, fmin(an_[0], fmin(an_[1], an_[2])));             \
+                const double len_ = anext_ - acur_;                                          \
+                const size_t idx_ = (size_t)ix_[0] + (size_t)n3_[0] * ((size_t)ix_[1] + (size_t)n3_[1] * ix_[2]); \
+                if (len_ > 0.0) { BODY }                                                     \
+                if (anext_ >= amax_) break;                                                  \
+                int out_ = 0;                                                                \
+                for (int a_ = 0; a_ < 3; ++a_)                                               \
+                    if (an_[a_] == anext_) {                                                 \
+                        ix_[a_] += st_[a_];                                                  \
+                        if (ix_[a_] < 0 || ix_[a_] >= n3_[a_]) out_ = 1;                     \
+                        an_[a_] = orc_plane_alpha(&(r), a_, st_[a_] > 0 ? ix_[a_] + 1 : ix_[a_], n3_[a_], h_); \
+                    }                                                                        \
+                if (out_) break;                                                             \
+                acur_ = anext_;                                                              \
+            }                                                                                \
+        }                                                                                    \
+    } while (0)
+
+#define ORC_SIDDON_DEFINE(T, SUF)                                                               \
+    void orc_siddon_forward_##SUF(const orc_geom* g, const T* vol, T* proj) {                  \
+        const size_t frame = (size_t)g->nu * g->nv;                                            \
+        for (int a = 0; a < g->na; ++a) {                                                      \
+            const double th = orc_canonical_angle(g->angles[a]);                               \
+            const double ct = cos(th), st = sin(th);                                           \
+            for (int iv = 0; iv < g->nv; ++iv)                                                 \
+                for (int iu = 0; iu < g->nu; ++iu) {                                           \
+                    orc_ray r;                                                                 \
+                    orc_make_ray(g, ct, st, iu, iv, &r);                                       \
+                    T acc = 0;                                                                 \
+                    ORC_SIDDON_WALK(g, r, { acc += (T)len_ * vol[idx_]; });                    \
+                    proj[(size_t)a * frame + (size_t)iu + (size_t)g->nu * iv] = acc;           \
+                }                                                                              \
+        }                                                                                      \
+    }                                                                                          \
+    /* exact transpose as a scatter in (angle, iv, iu, traversal) order */                     \
+    void orc_siddon_back_##SUF(const orc_geom* g, const T* proj, T* vol) {                     \
+        const size_t frame = (size_t)g->nu * g->nv;                                            \
+        const size_t nvox = (size_t)g->nx * g->ny * g->nz;                                     \
+        for (size_t i = 0; i < nvox; ++i) vol[i] = 0;                                          \
+        for (int a = 0; a < g->na; ++a) {                                                      \
+            const double th = orc_canonical_angle(g->angles[a]);                               \
+            const double ct = cos(th), st = sin(th);                                           \
+            for (int iv = 0; iv < g->nv; ++iv)                                                 \
+                for (int iu = 0; iu < g->nu; ++iu) {                                           \
+                    const T value = proj[(size_t)a * frame + (size_t)iu + (size_t)g->nu * iv]; \
+                    if (value == (T)0) continue;                                               \
+                    orc_ray r;                                                                 \
+                    orc_make_ray(g, ct, st, iu, iv, &r);                                       \
+                    ORC_SIDDON_WALK(g, r, { vol[idx_] += (T)len_ * value; });                  \
+                }                                                                              \
+        }                                                                                      \
+    }
+
+ORC_SIDDON_DEFINE(double, f64)
+ORC_SIDDON_DEFINE(float, f32)
+
+/* chord of one ray with one voxel (both in the conventions above), for the tests */
+double orc_siddon_chord(const orc_geom* g, int a, int iu, int iv, int i, int j, int k) {
+    const double th = orc_canonical_angle(g->angles[a]);
+    orc_ray r;
+    orc_make_ray(g, cos(th), sin(th), iu, iv, &r);
+    const int n3[3] = {g->nx, g->ny, g->nz}, idx3[3] = {i, j, k};
+    return orc_voxel_chord(&r, n3, g->h, idx3);
+}
+
 /* Walk description of one ray, exposed so tests can pin the kernels' per-ray setup
  * (axis, step, affine slice indices) against the restated plan_walk. */
 void orc_walk_params(const orc_geom* g, int a, int iu, int iv, int* axis, double out5[5]) {

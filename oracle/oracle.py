@@ -124,6 +124,7 @@ class Restated:
                 getattr(self.lib, f"orc_{nm}_{s}").restype = None
             self.lib[f"orc_back_matched_{s}"].restype = None
         self.lib.orc_canonical_angle.restype = C.c_double
+        self.lib.orc_siddon_chord.restype = C.c_double
         self.lib.orc_canonical_angle.argtypes = [C.c_double]
 
     def forward(self, g: Geom, x):
@@ -143,6 +144,26 @@ class Restated:
         else:
             getattr(self.lib, f"orc_back_voxel_{_suf(y.dtype)}")(C.byref(gs), _ptr(y, ct), _ptr(x, ct))
         return x
+
+    def siddon_forward(self, g: Geom, x):
+        """Siddon exact-length Ax (new; chord = tests/oracles.hpp:89-107 per voxel)."""
+        x = np.ascontiguousarray(x)
+        y = np.zeros(g.range_size, dtype=x.dtype)
+        gs = g.cstruct()
+        getattr(self.lib, f"orc_siddon_forward_{_suf(x.dtype)}")(C.byref(gs), _ptr(x, _ct(x.dtype)), _ptr(y, _ct(x.dtype)))
+        return y
+
+    def siddon_back(self, g: Geom, y):
+        """Exact transpose of siddon_forward (scatter in traversal order)."""
+        y = np.ascontiguousarray(y)
+        x = np.zeros(g.domain_size, dtype=y.dtype)
+        gs = g.cstruct()
+        getattr(self.lib, f"orc_siddon_back_{_suf(y.dtype)}")(C.byref(gs), _ptr(y, _ct(y.dtype)), _ptr(x, _ct(y.dtype)))
+        return x
+
+    def siddon_chord(self, g: Geom, a, iu, iv, i, j, k):
+        gs = g.cstruct()
+        return self.lib.orc_siddon_chord(C.byref(gs), a, iu, iv, i, j, k)
 
     def walk(self, g: Geom, a, iu, iv):
         ax = C.c_int()

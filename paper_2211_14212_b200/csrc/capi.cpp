@@ -63,29 +63,14 @@ void check_variant(int v) {
 template <class T>
 void ax_dev(ctkb::Geometry& g, const T* x, T* y, cudaStream_t s) {
     g.require_angles();
-    if (g.projector != CTK_PROJ_JOSEPH) ctkb::fail(CTK_E_UNSUPPORTED, "Siddon projector is not built in this round");
-    if constexpr (sizeof(T) == 4) ctkb::ax_f32(g, x, y, s);
-    else {
-        CTK_CUDA(cudaEventRecord(g.ev0, s));
-        ctkb::launch_ax_exact_f64(g, x, y, s);
-        CTK_CUDA(cudaEventRecord(g.ev1, s));
-    }
+    ctkb::op_ax<T>(g, x, y, s);
 }
 
 template <class T>
 void atb_dev(ctkb::Geometry& g, int variant, const T* y, T* x, cudaStream_t s) {
     g.require_angles();
     check_variant(variant);
-    if (g.projector != CTK_PROJ_JOSEPH) ctkb::fail(CTK_E_UNSUPPORTED, "Siddon projector is not built in this round");
-    if constexpr (sizeof(T) == 4) {
-        if (variant == CTK_BP_MATCHED) ctkb::atb_matched_f32(g, y, x, s);
-        else ctkb::atb_voxel_f32(g, y, x, s);
-    } else {
-        CTK_CUDA(cudaEventRecord(g.ev0, s));
-        if (variant == CTK_BP_MATCHED) ctkb::launch_atb_matched_exact_f64(g, y, x, s);
-        else ctkb::launch_atb_voxel_f64(g, y, x, s);
-        CTK_CUDA(cudaEventRecord(g.ev1, s));
-    }
+    ctkb::op_atb<T>(g, variant, y, x, s);
     if (g.comm) ctkb::comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
 }
 
@@ -213,6 +198,7 @@ int ctk_ax_residual_f32(ctk_geom* g, const float* x, const float* b, double* out
     return guard([&] {
         auto& gg = G(g);
         gg.require_angles();
+        if (gg.projector != CTK_PROJ_JOSEPH) ctkb::fail(CTK_E_UNSUPPORTED, "fused residual is Joseph-only");
         auto st = S(gg, s);
         auto w = ctkb::red_work(&gg);
         ctkb::ax_residual_f32(gg, x, b, w.results, st);

@@ -105,7 +105,19 @@ void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out,
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
 void atb_voxel_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
 
-// phantom (phantom.cu)
+// operator dispatch (ops.cpp): projector model x precision x variant
+template <class T>
+void op_ax(Geometry& g, const T* x, T* y, cudaStream_t s);
+template <class T>
+void op_atb(Geometry& g, int variant, const T* y, T* x, cudaStream_t s);
+
+// Siddon exact-length projector and its transpose (siddon.cu, --fmad=false)
+template <class T>
+void siddon_ax(const Geometry& g, const T* x, T* y, cudaStream_t s);
+template <class T>
+void siddon_atb(const Geometry& g, const T* y, T* x, cudaStream_t s);
+
+// phantom (stencils.cu)
 void launch_shepp_logan_f32(int n, float* out, cudaStream_t s);
 void launch_shepp_logan_f64(int n, double* out, cudaStream_t s);
 

@@ -51,18 +51,9 @@ struct Dev {
 
     Dev(Geometry& g_, int v) : g(g_), variant(v), s(g_.stream), w(red_work(&g_)) {}
 
-    void ax(const T* x, T* y) {
-        if constexpr (sizeof(T) == 4) ax_f32(g, x, y, s);
-        else launch_ax_exact_f64(g, x, y, s);
-    }
+    void ax(const T* x, T* y) { op_ax<T>(g, x, y, s); }
     void atb(const T* y, T* x) {
-        if constexpr (sizeof(T) == 4) {
-            if (variant == CTK_BP_MATCHED) atb_matched_f32(g, y, x, s);
-            else atb_voxel_f32(g, y, x, s);
-        } else {
-            if (variant == CTK_BP_MATCHED) launch_atb_matched_exact_f64(g, y, x, s);
-            else launch_atb_voxel_f64(g, y, x, s);
-        }
+        op_atb<T>(g, variant, y, x, s);
         if (g.comm) comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
     }
     double fetch(int slot) {
@@ -91,9 +82,12 @@ struct Dev {
     // ||A x - b||^2 over all ranks (solve_log.hpp:111-115), never storing A x in T=float
     double resid2(const T* x, const T* b) {
         if constexpr (sizeof(T) == 4) {
-            ax_residual_f32(g, x, b, w.results, s);
-            return range_sum(fetch(0));
-        } else {
+            if (g.projector == CTK_PROJ_JOSEPH) {
+                ax_residual_f32(g, x, b, w.results, s);
+                return range_sum(fetch(0));
+            }
+        }
+        {
             if (!tmp_range.p) tmp_range.alloc(g.range());
             ax(x, tmp_range.p);
             return diff_nrm2sq(tmp_range.p, b, g.range(), true);

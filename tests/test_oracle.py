@@ -202,3 +202,62 @@ def test_regparam_numpy_vs_reference(reference):
             H[j + 1, j] = 0.5 * rng.random()
         assert gcv_lambda(H, 2.0) == pytest.approx(reference.gcv_lambda(H, 2.0), rel=1e-6)
         assert dp_lambda(H, 2.0, 0.05) == pytest.approx(reference.dp_lambda(H, 2.0, 0.05), rel=1e-6, abs=1e-14)
+
+
+# ---- Siddon exact-length restatement (new code: pinned by the reference's chord KAT) -----
+def test_siddon_chord_kat(restated):
+    """test_operators.cpp:51-103's impulse geometry: Siddon gives the ray-box chord exactly."""
+    h, th, n = 0.9, 0.3, 7
+    g = Geom(0, 0.0, n * h, h, 1, 1, n, n, 1, h, np.array([th]))
+    x = np.zeros(n * n)
+    x[n // 2 + n * (n // 2)] = 1
+    chord = ray_box_chord([0, 0, 0], [-math.cos(th), -math.sin(th), 0], [-h / 2] * 3, [h / 2] * 3)
+    assert restated.siddon_forward(g, x)[0] == pytest.approx(chord, rel=1e-14)
+    g = Geom(2, 4.0 * n * h, 2.0 * n * h, h, 1, 1, n, n, n, h, np.array([th]))
+    x = np.zeros(n ** 3)
+    x[n // 2 + n * (n // 2 + n * (n // 2))] = 1
+    o = [g.dso * math.cos(th), g.dso * math.sin(th), 0.0]
+    nn = math.hypot(o[0], o[1])
+    chord = ray_box_chord(o, [-o[0] / nn, -o[1] / nn, 0.0], [-h / 2] * 3, [h / 2] * 3)
+    assert restated.siddon_forward(g, x)[0] == pytest.approx(chord, rel=1e-12)
+
+
+def test_siddon_whole_box_chord(restated):
+    """A constant volume integrates to c * (chord of the ray through the whole volume box)."""
+    from geoms import cone_ragged
+
+    g = cone_ragged()
+    c = 1.7
+    y = restated.siddon_forward(g, np.full(g.domain_size, c))
+    half = [0.5 * g.nx * g.h, 0.5 * g.ny * g.h, 0.5 * g.nz * g.h]
+    for (a, iu, iv) in [(0, 11, 8), (3, 0, 0), (5, 22, 16), (7, 5, 12)]:
+        th = g.angles[a]
+        ct, st = math.cos(th), math.sin(th)
+        u = (iu - 0.5 * (g.nu - 1)) * g.du
+        v = (iv - 0.5 * (g.nv - 1)) * g.du
+        px, py, pz = -g.dod * ct - u * st, -g.dod * st + u * ct, v
+        s = [g.dso * ct, g.dso * st, 0.0]
+        d = [px - s[0], py - s[1], pz - s[2]]
+        nd = math.sqrt(sum(t * t for t in d))
+        want = c * ray_box_chord(s, [t / nd for t in d], [-t for t in half], half)
+        assert y[a * g.nu * g.nv + iv * g.nu + iu] == pytest.approx(want, rel=1e-12, abs=1e-12)
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+def test_siddon_adjoint_and_linearity(restated, name):
+    g = ALL[name]()
+    f = lambda v: restated.siddon_forward(g, v)  # noqa: E731
+    b = lambda v: restated.siddon_back(g, v)  # noqa: E731
+    assert adjoint_discrepancy(f, b, g.domain_size, g.range_size, 5, 11) < 1e-12
+    rng = np.random.default_rng(2)
+    x, y = rng.standard_normal(g.domain_size), rng.standard_normal(g.domain_size)
+    assert rel_l2(f(1.7 * x - 0.4 * y), 1.7 * f(x) - 0.4 * f(y)) < 1e-12
+
+
+def test_siddon_close_to_joseph(restated):
+    """Two discretisations of the same line integral agree to discretisation error."""
+    from geoms import cone_bench
+
+    g = cone_bench(32, 12)
+    x = restated.shepp_logan_3d(32, np.float64)
+    assert rel_l2(restated.siddon_forward(g, x), restated.forward(g, x)) < 0.05
