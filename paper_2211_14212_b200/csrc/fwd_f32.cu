@@ -51,16 +51,22 @@ __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict
     }
 }
 
-template <bool RESID, class Off>
+// MODE 0: y = A x1.   MODE 1: per-block partial of sum (A x1 - b)^2 (y never stored).
+// MODE 2 (dual): partials of (A x1 - b)^2 AND y = A x2 in one walk -- the solvers' explicit
+// residual of x_k (solve_log.hpp:111-115) fused with the next iteration's A v_{k+1}: the
+// ray setup, slice walk, floors and offsets are shared, only the taps are read twice.
+template <int MODE, class Off>
 __global__ void __launch_bounds__(ZW_BR * ZW_BC)
 k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
-               const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
+               const float* __restrict__ w2x, const float* __restrict__ w2y, const float* __restrict__ xs,
+               const float* __restrict__ xs2, float* __restrict__ y, const float* __restrict__ b,
                double* __restrict__ partials) {
+    constexpr bool DUAL = MODE == 2;
     __shared__ float outs[ZW_BR][ZW_BC + 1];
     const int iv = blockIdx.z * ZW_BR + threadIdx.x;
     const int a = vorder[blockIdx.y];
     const int iu = blockIdx.x * ZW_BC + threadIdx.y;
-    float out = 0.f;
+    float out = 0.f, out2 = 0.f;
     const bool live = iu < g.nu && iv < g.nv;
     if (live) {
         const int c = a * g.nu + iu;
@@ -71,6 +77,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             WalkF w;
             walk_generic(g, tr.x, tr.y, iu, iv, w);
             out = march_generic(g, w, xs);
+            if (DUAL) out2 = march_generic(g, w, xs2);
         } else {
             const float4 cd = g.col[c];
             const int A = g.colaxis[c];
@@ -79,6 +86,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             const Off pz = g.nz + 2;
             const Off plane = pz * Off(nh + 2);
             const float* base = (A ? wy : wx) + pz + 1;  // tap (h, z) of slice s at base[s*plane + h*pz + z]
+            const float* base2 = DUAL ? (A ? w2y : w2x) + pz + 1 : nullptr;
             const float vd = float(v);
             const float czf = 0.5f * float(g.nz - 1);
             const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
@@ -103,34 +111,48 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                 while (s0 > 0 && inside(s0 - 1)) --s0;
                 while (s1 < ns - 1 && inside(s1 + 1)) ++s1;
             }
-            float acc = 0.f;
-            const float* ps = base + Off(s0) * plane;
+            float acc = 0.f, acc2 = 0.f;
+            const Off start = Off(s0) * plane;
 #pragma unroll 4
-            for (int s = s0; s <= s1; ++s, ps += plane) {
+            for (int s = s0; s <= s1; ++s) {
                 const float fs = float(s);
                 int ih, iz;
                 float th, tz;
                 split(fmaf(fs, cd.y, cd.x), ih, th);
                 split(fmaf(vd, fmaf(fs, cd.w, cd.z), czf), iz, tz);
-                const float* p = ps + (ih * int(pz) + iz);
-                const float v00 = __ldg(p), v01 = __ldg(p + 1);          // (ih, iz), (ih, iz+1)
-                const float v10 = __ldg(p + pz), v11 = __ldg(p + pz + 1);  // (ih+1, iz), (ih+1, iz+1)
-                const float a0 = fmaf(th, v10 - v00, v00);
-                const float a1 = fmaf(th, v11 - v01, v01);
-                acc += fmaf(tz, a1 - a0, a0);
+                const Off off = start + Off(s - s0) * plane + Off(ih * int(pz) + iz);
+                {
+                    const float* p = base + off;
+                    const float v00 = __ldg(p), v01 = __ldg(p + 1);          // (ih, iz), (ih, iz+1)
+                    const float v10 = __ldg(p + pz), v11 = __ldg(p + pz + 1);  // (ih+1, iz), (ih+1, iz+1)
+                    const float a0 = fmaf(th, v10 - v00, v00);
+                    const float a1 = fmaf(th, v11 - v01, v01);
+                    acc += fmaf(tz, a1 - a0, a0);
+                }
+                if (DUAL) {
+                    const float* p = base2 + off;
+                    const float v00 = __ldg(p), v01 = __ldg(p + 1);
+                    const float v10 = __ldg(p + pz), v11 = __ldg(p + pz + 1);
+                    const float a0 = fmaf(th, v10 - v00, v00);
+                    const float a1 = fmaf(th, v11 - v01, v01);
+                    acc2 += fmaf(tz, a1 - a0, a0);
+                }
             }
-            out = ray_step(g, cs, v) * acc;
+            const float stp = ray_step(g, cs, v);
+            out = stp * acc;
+            out2 = stp * acc2;
         }
     }
-    if (!RESID) {
+    if (MODE == 0 || DUAL) {
         // transpose through shared memory so the stores run along detector columns
-        outs[threadIdx.x][threadIdx.y] = out;
+        outs[threadIdx.x][threadIdx.y] = DUAL ? out2 : out;
         __syncthreads();
         const int t = threadIdx.x + ZW_BR * threadIdx.y;
         const int r = t / ZW_BC, cc = t % ZW_BC;
         const int ivw = blockIdx.z * ZW_BR + r, iuw = blockIdx.x * ZW_BC + cc;
         if (ivw < g.nv && iuw < g.nu) y[size_t(a) * g.nu * g.nv + size_t(ivw) * g.nu + iuw] = outs[r][cc];
-    } else {
+    }
+    if (MODE != 0) {
         double rr = 0.0;
         if (live) {
             const double d = double(out) - double(__ldg(b + size_t(a) * g.nu * g.nv + size_t(iv) * g.nu + iu));
@@ -142,13 +164,13 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
     }
 }
 
-void relayout_zfast(Geometry& g, const float* x, cudaStream_t s) {
+void relayout_zfast(Geometry& g, const float* x, DevBuf& wx, DevBuf& wy, cudaStream_t s) {
     const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
     const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
-    if (g.vx.ensure(nwx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vx.p, 0, nwx * sizeof(float), s));
-    if (g.vy.ensure(nwy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(g.vy.p, 0, nwy * sizeof(float), s));
+    if (wx.ensure(nwx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(wx.p, 0, nwx * sizeof(float), s));
+    if (wy.ensure(nwy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(wy.p, 0, nwy * sizeof(float), s));
     dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.nz + 31) / 32, g.ny);
-    k_relayout_zfast<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.vx.as<float>(), g.vy.as<float>());
+    k_relayout_zfast<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, wx.as<float>(), wy.as<float>());
     after_launch("k_relayout_zfast");
 }
 
@@ -159,37 +181,54 @@ bool wide_offsets(const Geometry& g) {
     return mx >= 2147483000.0;
 }
 
-template <bool RESID>
-void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s) {
+template <int MODE>
+void launch_ax(Geometry& g, const float* x, const float* x2, float* y, const float* b, double* partials,
+               cudaStream_t s) {
     const KGeom k = g.kgeom();
     const int* vo = g.d_vorder.as<int>();
-    const float* v0 = g.vx.as<float>();
-    const float* v1 = g.vy.as<float>();
+    const float *a0 = g.vx.as<float>(), *a1 = g.vy.as<float>();
+    const float *c0 = MODE == 2 ? g.vx2.as<float>() : nullptr, *c1 = MODE == 2 ? g.vy2.as<float>() : nullptr;
     const dim3 blk(ZW_BR, ZW_BC);
-    if (wide_offsets(g)) k_ax_zfast_f32<RESID, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
-    else k_ax_zfast_f32<RESID, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, v0, v1, x, y, b, partials);
-    after_launch(RESID ? "k_ax_zfast_f32_residual" : "k_ax_zfast_f32");
+    if (wide_offsets(g))
+        k_ax_zfast_f32<MODE, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, c0, c1, x, x2, y, b, partials);
+    else
+        k_ax_zfast_f32<MODE, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, c0, c1, x, x2, y, b, partials);
+    after_launch(MODE == 0 ? "k_ax_zfast_f32" : (MODE == 1 ? "k_ax_zfast_f32_residual" : "k_ax_zfast_f32_dual"));
 }
 
-void prepare(Geometry& g, const float* x, cudaStream_t s) { relayout_zfast(g, x, s); }
+double* residual_partials(Geometry& g, size_t& nblk) {
+    const dim3 grd = fwd_grid(g);
+    nblk = size_t(grd.x) * grd.y * grd.z;
+    g.proj_t.ensure(std::max(g.range() * sizeof(float), nblk * sizeof(double)));
+    return g.proj_t.as<double>();
+}
 
 }  // namespace
 
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
-    prepare(g, x, s);
+    relayout_zfast(g, x, g.vx, g.vy, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    launch_ax<false>(g, x, y, nullptr, nullptr, s);
+    launch_ax<0>(g, x, nullptr, y, nullptr, nullptr, s);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
 }
 
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
-    prepare(g, x, s);
-    const dim3 grd = fwd_grid(g);
-    const size_t nblk = size_t(grd.x) * grd.y * grd.z;
-    g.proj_t.ensure(std::max(g.range() * sizeof(float), nblk * sizeof(double)));
-    double* partials = g.proj_t.as<double>();
+    relayout_zfast(g, x, g.vx, g.vy, s);
+    size_t nblk;
+    double* partials = residual_partials(g, nblk);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    launch_ax<true>(g, x, nullptr, b, partials, s);
+    launch_ax<1>(g, x, nullptr, nullptr, b, partials, s);
+    CTK_CUDA(cudaEventRecord(g.ev1, s));
+    finish_sum(partials, int(nblk), d_out, s);
+}
+
+void ax_dual_f32(Geometry& g, const float* x, const float* b, double* d_out, const float* v, float* yv, cudaStream_t s) {
+    relayout_zfast(g, x, g.vx, g.vy, s);
+    relayout_zfast(g, v, g.vx2, g.vy2, s);
+    size_t nblk;
+    double* partials = residual_partials(g, nblk);
+    CTK_CUDA(cudaEventRecord(g.ev0, s));
+    launch_ax<2>(g, x, v, yv, b, partials, s);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
     finish_sum(partials, int(nblk), d_out, s);
 }
