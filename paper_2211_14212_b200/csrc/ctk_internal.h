@@ -79,8 +79,7 @@ struct Geometry {
     DevBuf d_ctst, d_col, d_colaxis, d_colstep;
     DevBuf d_vorder;  // views grouped by ray class (x-dominant first) for L2 reuse in Ax
     // workspaces (grown lazily)
-    DevBuf vx, vy;      // z-fast padded f32 relayouts for x- / y-dominant rays
-    DevBuf vx2, vy2;    // same, second volume of the dual forward
+    DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
     DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers
     DevBuf host_x, host_y;  // device staging for host-pointer entry points
     DevBuf red;         // reduction scratch (partials + results)
@@ -103,8 +102,6 @@ void launch_atb_voxel_f64(const Geometry& g, const double* y, double* x, cudaStr
 // f32 performance path (kernels_f32.cu)
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s);
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s);
-// one walk: *d_out = ||A x - b||^2 and yv = A v
-void ax_dual_f32(Geometry& g, const float* x, const float* b, double* d_out, const float* v, float* yv, cudaStream_t s);
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
 void atb_voxel_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
 

@@ -132,15 +132,17 @@ __device__ __forceinline__ double proj_u(const KGeom& g, double ct, double st, d
     return (-x * st + y * ct) / g.du + 0.5 * (g.nu - 1);
 }
 
-// floor without the conversion pipe: t = (f - 0.5) + 1.5*2^23 rounds to an integer n with
-// n = floor(f) except at exact integers, where n may be f - 1 with frac 1.0 -- the same
-// bilinear weights (weight 1 on tap f).  Valid for |f| < 2^22.
+// floor without the conversion pipe: t = f + 1.5*2^23 rounded toward -inf (one FADD.RM) is
+// exactly 1.5*2^23 + floor(f) for |f| < 2^22, so its bit pattern minus that of 1.5*2^23 is
+// floor(f) and f - (t - 1.5*2^23) the exact fraction in [0, 1).
+constexpr float kSplitM = 12582912.0f;
+constexpr int kSplitBias = 0x4B400000;  // __float_as_int(kSplitM)
+__device__ __forceinline__ float split_t(float f) { return __fadd_rd(f, kSplitM); }
+__device__ __forceinline__ float split_frac(float f, float t) { return __fsub_rn(f, __fsub_rn(t, kSplitM)); }
 __device__ __forceinline__ void split(float f, int& i, float& frac) {
-    const float M = 12582912.0f;
-    const float t = __fadd_rn(__fadd_rn(f, -0.5f), M);
-    const float fi = __fadd_rn(t, -M);
-    i = __float_as_int(t) - __float_as_int(M);
-    frac = __fadd_rn(f, -fi);
+    const float t = split_t(f);
+    i = __float_as_int(t) - kSplitBias;
+    frac = split_frac(f, t);
 }
 
 }  // namespace

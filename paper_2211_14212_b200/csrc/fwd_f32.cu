@@ -30,6 +30,11 @@ namespace {
 // of two partial rows of a y/x-fastest plane.
 constexpr int ZW_BR = 32, ZW_BC = 8;  // block: 32 detector rows (lanes) x 8 columns
 
+__device__ __forceinline__ const float* opaque_ptr(const float* p) {
+    asm("" : "+l"(p));
+    return p;
+}
+
 // x[i + nx(j + ny k)] -> wx[i][j+1][k+1] and wy[j][i+1][k+1]: 32x32 (i, k) tile transposes
 __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ wx,
                                  float* __restrict__ wy) {
@@ -51,22 +56,17 @@ __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict
     }
 }
 
-// MODE 0: y = A x1.   MODE 1: per-block partial of sum (A x1 - b)^2 (y never stored).
-// MODE 2 (dual): partials of (A x1 - b)^2 AND y = A x2 in one walk -- the solvers' explicit
-// residual of x_k (solve_log.hpp:111-115) fused with the next iteration's A v_{k+1}: the
-// ray setup, slice walk, floors and offsets are shared, only the taps are read twice.
+// MODE 0: y = A x.   MODE 1: per-block partial of sum (A x - b)^2 (y never stored).
 template <int MODE, class Off>
 __global__ void __launch_bounds__(ZW_BR * ZW_BC)
 k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
-               const float* __restrict__ w2x, const float* __restrict__ w2y, const float* __restrict__ xs,
-               const float* __restrict__ xs2, float* __restrict__ y, const float* __restrict__ b,
+               const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
                double* __restrict__ partials) {
-    constexpr bool DUAL = MODE == 2;
     __shared__ float outs[ZW_BR][ZW_BC + 1];
     const int iv = blockIdx.z * ZW_BR + threadIdx.x;
     const int a = vorder[blockIdx.y];
     const int iu = blockIdx.x * ZW_BC + threadIdx.y;
-    float out = 0.f, out2 = 0.f;
+    float out = 0.f;
     const bool live = iu < g.nu && iv < g.nv;
     if (live) {
         const int c = a * g.nu + iu;
@@ -77,7 +77,6 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             WalkF w;
             walk_generic(g, tr.x, tr.y, iu, iv, w);
             out = march_generic(g, w, xs);
-            if (DUAL) out2 = march_generic(g, w, xs2);
         } else {
             const float4 cd = g.col[c];
             const int A = g.colaxis[c];
@@ -86,7 +85,6 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             const Off pz = g.nz + 2;
             const Off plane = pz * Off(nh + 2);
             const float* base = (A ? wy : wx) + pz + 1;  // tap (h, z) of slice s at base[s*plane + h*pz + z]
-            const float* base2 = DUAL ? (A ? w2y : w2x) + pz + 1 : nullptr;
             const float vd = float(v);
             const float czf = 0.5f * float(g.nz - 1);
             const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
@@ -111,41 +109,43 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                 while (s0 > 0 && inside(s0 - 1)) --s0;
                 while (s1 < ns - 1 && inside(s1 + 1)) ++s1;
             }
-            float acc = 0.f, acc2 = 0.f;
-            const Off start = Off(s0) * plane;
+            float acc = 0.f;
+            // Offsets are formed from the raw bit patterns of the split sums (ih + bias,
+            // iz + bias); the bias term is folded into the running slice offset, in unsigned
+            // (modular) arithmetic, so a sample costs one IMAD and no float->int conversion.
+            using U = typename std::conditional<sizeof(Off) == 4, unsigned, unsigned long long>::type;
+            const U upz = U(pz), uplane = U(plane);
+            U sb = U(s0) * uplane - U(kSplitBias) * (upz + 1u);
+            // tap row ih+1; opaque so each tap row costs one IMAD.WIDE rather than a
+            // sign-extended 64-bit add chain on (off + pz)
+            const float* base1 = opaque_ptr(base + pz);
+            float fs = float(s0);
 #pragma unroll 4
-            for (int s = s0; s <= s1; ++s) {
-                const float fs = float(s);
-                int ih, iz;
-                float th, tz;
-                split(fmaf(fs, cd.y, cd.x), ih, th);
-                split(fmaf(vd, fmaf(fs, cd.w, cd.z), czf), iz, tz);
-                const Off off = start + Off(s - s0) * plane + Off(ih * int(pz) + iz);
+            for (int n = s1 - s0; n >= 0; --n) {
+                const float fh = fmaf(fs, cd.y, cd.x);
+                const float fz = fmaf(vd, fmaf(fs, cd.w, cd.z), czf);
+                const float tht = split_t(fh), tzt = split_t(fz);
+                const float th = split_frac(fh, tht), tz = split_frac(fz, tzt);
+                const Off off = Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt)))));
+                fs += 1.f;
+                sb += uplane;
                 {
                     const float* p = base + off;
-                    const float v00 = __ldg(p), v01 = __ldg(p + 1);          // (ih, iz), (ih, iz+1)
-                    const float v10 = __ldg(p + pz), v11 = __ldg(p + pz + 1);  // (ih+1, iz), (ih+1, iz+1)
+                    const float* q = base1 + off;
+                    const float v00 = __ldg(p), v01 = __ldg(p + 1);  // (ih, iz), (ih, iz+1)
+                    const float v10 = __ldg(q), v11 = __ldg(q + 1);  // (ih+1, iz), (ih+1, iz+1)
                     const float a0 = fmaf(th, v10 - v00, v00);
                     const float a1 = fmaf(th, v11 - v01, v01);
                     acc += fmaf(tz, a1 - a0, a0);
                 }
-                if (DUAL) {
-                    const float* p = base2 + off;
-                    const float v00 = __ldg(p), v01 = __ldg(p + 1);
-                    const float v10 = __ldg(p + pz), v11 = __ldg(p + pz + 1);
-                    const float a0 = fmaf(th, v10 - v00, v00);
-                    const float a1 = fmaf(th, v11 - v01, v01);
-                    acc2 += fmaf(tz, a1 - a0, a0);
-                }
             }
             const float stp = ray_step(g, cs, v);
             out = stp * acc;
-            out2 = stp * acc2;
         }
     }
-    if (MODE == 0 || DUAL) {
+    if (MODE == 0) {
         // transpose through shared memory so the stores run along detector columns
-        outs[threadIdx.x][threadIdx.y] = DUAL ? out2 : out;
+        outs[threadIdx.x][threadIdx.y] = out;
         __syncthreads();
         const int t = threadIdx.x + ZW_BR * threadIdx.y;
         const int r = t / ZW_BC, cc = t % ZW_BC;
@@ -182,18 +182,16 @@ bool wide_offsets(const Geometry& g) {
 }
 
 template <int MODE>
-void launch_ax(Geometry& g, const float* x, const float* x2, float* y, const float* b, double* partials,
-               cudaStream_t s) {
+void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s) {
     const KGeom k = g.kgeom();
     const int* vo = g.d_vorder.as<int>();
     const float *a0 = g.vx.as<float>(), *a1 = g.vy.as<float>();
-    const float *c0 = MODE == 2 ? g.vx2.as<float>() : nullptr, *c1 = MODE == 2 ? g.vy2.as<float>() : nullptr;
     const dim3 blk(ZW_BR, ZW_BC);
     if (wide_offsets(g))
-        k_ax_zfast_f32<MODE, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, c0, c1, x, x2, y, b, partials);
+        k_ax_zfast_f32<MODE, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials);
     else
-        k_ax_zfast_f32<MODE, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, c0, c1, x, x2, y, b, partials);
-    after_launch(MODE == 0 ? "k_ax_zfast_f32" : (MODE == 1 ? "k_ax_zfast_f32_residual" : "k_ax_zfast_f32_dual"));
+        k_ax_zfast_f32<MODE, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials);
+    after_launch(MODE == 0 ? "k_ax_zfast_f32" : "k_ax_zfast_f32_residual");
 }
 
 double* residual_partials(Geometry& g, size_t& nblk) {
@@ -208,7 +206,7 @@ double* residual_partials(Geometry& g, size_t& nblk) {
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
     relayout_zfast(g, x, g.vx, g.vy, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    launch_ax<0>(g, x, nullptr, y, nullptr, nullptr, s);
+    launch_ax<0>(g, x, y, nullptr, nullptr, s);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
 }
 
@@ -217,18 +215,7 @@ void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out,
     size_t nblk;
     double* partials = residual_partials(g, nblk);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    launch_ax<1>(g, x, nullptr, nullptr, b, partials, s);
-    CTK_CUDA(cudaEventRecord(g.ev1, s));
-    finish_sum(partials, int(nblk), d_out, s);
-}
-
-void ax_dual_f32(Geometry& g, const float* x, const float* b, double* d_out, const float* v, float* yv, cudaStream_t s) {
-    relayout_zfast(g, x, g.vx, g.vy, s);
-    relayout_zfast(g, v, g.vx2, g.vy2, s);
-    size_t nblk;
-    double* partials = residual_partials(g, nblk);
-    CTK_CUDA(cudaEventRecord(g.ev0, s));
-    launch_ax<2>(g, x, v, yv, b, partials, s);
+    launch_ax<1>(g, x, nullptr, b, partials, s);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
     finish_sum(partials, int(nblk), d_out, s);
 }

@@ -12,7 +12,6 @@
 // volume is sum-reduced, so all ranks hold identical domain vectors.
 #include <algorithm>
 #include <cmath>
-#include <cstdlib>
 #include <string>
 #include <utility>
 #include <vector>
@@ -94,26 +93,6 @@ struct Dev {
             return diff_nrm2sq(tmp_range.p, b, g.range(), true);
         }
     }
-    // ||A x - b||^2 and yv = A v.  On the f32 Joseph path one walk samples both volumes
-    // (ax_dual_f32); the residual is still a genuine forward application of x.
-    double resid2_and_ax(const T* x, const T* b, const T* v, T* yv) {
-        if constexpr (sizeof(T) == 4) {
-            if (g.projector == CTK_PROJ_JOSEPH && !dual_off()) {
-                ax_dual_f32(g, x, b, w.results, v, yv, s);
-                return range_sum(fetch(0));
-            }
-        }
-        const double r2 = resid2(x, b);
-        ax(v, yv);
-        return r2;
-    }
-    static bool dual_off() {
-        static const bool off = [] {
-            const char* e = std::getenv("CTK_NO_DUAL");
-            return e && e[0] == '1';
-        }();
-        return off;
-    }
 };
 
 template <class T>
@@ -142,11 +121,8 @@ struct Monitor {
     }
 
     // IterationMonitor::record; returns true when the solver should stop
-    // resid_sq: ||A x - b||^2 when the caller already computed it with a genuine forward
-    // application of this x (the fused dual walk), else computed here.
-    bool record(int k, const T* x, double implicit, bool has_lambda = false, double lambda = 0.0,
-                const double* resid_sq = nullptr) {
-        const double expl = std::sqrt(resid_sq ? *resid_sq : d.resid2(x, b)) / bnorm;
+    bool record(int k, const T* x, double implicit, bool has_lambda = false, double lambda = 0.0) {
+        const double expl = std::sqrt(d.resid2(x, b)) / bnorm;
         if (!std::isfinite(expl) || !std::isfinite(implicit))
             fail(CTK_E_NUMERICAL, "non-finite residual at iteration " + std::to_string(k), k);
         if (log->iterations >= log->capacity) fail(CTK_E_PARAMETER, "solve log capacity exceeded");
@@ -204,7 +180,6 @@ void cgls(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
     CTK_CUDA(cudaMemcpyAsync(p.p, s.p, sizeof(T) * nd, cudaMemcpyDeviceToDevice, d.s));
     double gamma = d.nrm2sq(s.p, nd, false);
     int k = 0;
-    bool have_q = false;  // q already holds A p (from the previous iteration's dual walk)
     while (k < o.max_iters) {
         ++k;
         if (!(gamma > 0.0)) {
@@ -212,8 +187,7 @@ void cgls(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
             --k;
             break;
         }
-        if (!have_q) d.ax(p.p, q.p);
-        have_q = false;
+        d.ax(p.p, q.p);
         const double delta = d.nrm2sq(q.p, nr, true);
         if (!std::isfinite(delta)) fail(CTK_E_NUMERICAL, "cgls: non-finite curvature at iteration " + std::to_string(k), k);
         if (!(delta > 0.0)) {
@@ -224,17 +198,12 @@ void cgls(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
         const double alpha = gamma / delta;
         axpy<T>(nd, alpha, p.p, x, d.s);
         const double rr = d.axpy_n2(-alpha, q.p, r.p, nr, true);
-        // The reference records x_k and then forms s = B r, p = s + beta p.  Forming them
-        // first lets the explicit residual of x_k share one walk with A p_{k+1}; every
-        // value is unchanged (only the last iteration does one unused A^T b + forward).
+        if (mon.record(k, x, std::sqrt(rr) / bnorm)) break;
         d.atb(r.p, s.p);
         const double gnew = d.nrm2sq(s.p, nd, false);
         const double beta = gnew / gamma;
         gamma = gnew;
         xpby<T>(nd, s.p, beta, p.p, d.s);
-        const double r2 = d.resid2_and_ax(x, b, p.p, q.p);
-        have_q = true;
-        if (mon.record(k, x, std::sqrt(rr) / bnorm, false, 0.0, &r2)) break;
     }
     mon.finish(k);
 }
@@ -257,11 +226,9 @@ void lsqr(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
     fill<T>(nd, T(0), x, d.s);
     double phibar = beta1, rhobar = alpha;
     int k = 0;
-    bool have_un = false;  // un already holds A v (from the previous iteration's dual walk)
     while (k < o.max_iters) {
         ++k;
-        if (!have_un) d.ax(v.p, un.p);
-        have_un = false;
+        d.ax(v.p, un.p);
         double beta = std::sqrt(d.axpy_n2(-alpha, u.p, un.p, nr, true));
         bool down = beta <= tol;
         if (beta > 0.0) {
@@ -284,11 +251,7 @@ void lsqr(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
         const double phi = c * phibar;
         phibar = sn * phibar;
         lsqr_update<T>(nd, phi / rho, theta / rho, x, w.p, v.p, d.s);
-        // explicit residual of x_k and the next iteration's A v_{k+1} in one walk (un is free:
-        // its old content was swapped into u or is no longer used)
-        const double r2 = d.resid2_and_ax(x, b, v.p, un.p);
-        have_un = true;
-        if (mon.record(k, x, phibar / beta1, false, 0.0, &r2)) break;
+        if (mon.record(k, x, phibar / beta1)) break;
         if (down) {
             mon.reason = CTK_STOP_BREAKDOWN;
             break;
@@ -320,11 +283,9 @@ void lsmr(Dev<T>& d, const T* b, double lambda, const ctk_solver_opts& o, T* x, 
     fill<T>(nd, T(0), x, d.s);
     double betadd = beta1, betad = 0, rhodold = 1, tautildeold = 0, thetatilde = 0, zeta = 0, dsq = 0;
     int k = 0;
-    bool have_un = false;  // un already holds A v (from the previous iteration's dual walk)
     while (k < o.max_iters) {
         ++k;
-        if (!have_un) d.ax(v.p, un.p);
-        have_un = false;
+        d.ax(v.p, un.p);
         double beta = std::sqrt(d.axpy_n2(-alpha, u.p, un.p, nr, true));
         bool down = beta <= tol;
         if (beta > 0.0) {
@@ -371,9 +332,7 @@ void lsmr(Dev<T>& d, const T* b, double lambda, const ctk_solver_opts& o, T* x, 
         const double taud = (zeta - thetatilde * tautildeold) / rhodold;
         dsq += betacheck * betacheck;
         const double normr = std::sqrt(dsq + (betad - taud) * (betad - taud) + betadd * betadd);
-        const double r2 = d.resid2_and_ax(x, b, v.p, un.p);
-        have_un = true;
-        if (mon.record(k, x, normr / beta1, true, lambda, &r2)) break;
+        if (mon.record(k, x, normr / beta1, true, lambda)) break;
         if (down) {
             mon.reason = CTK_STOP_BREAKDOWN;
             break;
