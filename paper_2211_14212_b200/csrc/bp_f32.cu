@@ -45,17 +45,18 @@ __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __
 // Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
 // their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
 constexpr int BP_PB = 256, BP_KB = 32, BP_SL = 8;
+constexpr int BP_ZG = 2;  // guard rows of Z on each side: out-of-band entries land there, unread
 
 template <int CLASS>
 __global__ void __launch_bounds__(BP_PB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, int ptiles) {
     extern __shared__ __align__(16) float sm[];
-    float* Z = sm;                                              // [BP_KB][BP_PB]
-    int* lists = reinterpret_cast<int*>(Z + BP_KB * BP_PB);     // [BP_PB][BP_SL]
+    float* Z = sm + BP_ZG * BP_PB;                              // [-BP_ZG, BP_KB+BP_ZG) x [BP_PB]
+    int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG) * BP_PB);  // [BP_PB][BP_SL]
     int* cnt = lists + BP_PB * BP_SL;                           // [BP_PB]
     float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_PB]
-    int2* urange = reinterpret_cast<int2*>(eth + BP_PB);        // [na]
-    float* vdtab = reinterpret_cast<float*>(urange + g.na);     // [nv]
+    float* vdtab = eth + BP_PB;                                 // [nv rounded up to 4], 16-byte aligned
+    int2* urange = reinterpret_cast<int2*>(vdtab + ((g.nv + 3) & ~3));  // [na]
 
     const int t = threadIdx.x;
     // plane index fastest: a wave of resident CTAs shares one (row tile, z band), so per
@@ -136,36 +137,55 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                         float* zc = Z + t;
                         if (gs > 0.f) {
                             // fz increases with iv, so each Z[k] is final once the march passes
-                            // it: accumulate in registers (A -> Z[cur], B -> Z[cur+1]) and
-                            // store each entry once, branch-free
+                            // it: accumulate in registers (A -> Z[cur], B -> Z[cur+1]) and store
+                            // both every row, unconditionally -- a later row either overwrites
+                            // them with a larger partial or has moved on.  Out-of-band k are
+                            // clamped into the guard rows.  Branch-free: no per-row divergence.
                             int cur = -(1 << 20);
                             float A = 0.f, B = 0.f;
-                            auto add = [&](int iv, float yv) {
-                                int iz;
-                                float tz;
-                                split(fmaf(vdtab[iv], gs, czf), iz, tz);
-                                const int kk = iz - k0;
-                                const int adv = kk - cur;
-                                if (adv >= 1 && unsigned(cur) < unsigned(BP_KB)) zc[cur * BP_PB] = A;
-                                if (adv >= 2 && unsigned(cur + 1) < unsigned(BP_KB)) zc[(cur + 1) * BP_PB] = B;
+                            auto step = [&](float vd, float yv) {
+                                const float fz = fmaf(vd, gs, czf);
+                                const float tt = split_t(fz);
+                                const int kk = __float_as_int(tt) - (kSplitBias + k0);
+                                const float tz = split_frac(fz, tt);
                                 const float w0 = (1.f - tz) * yv, w1 = tz * yv;
-                                A = (adv == 0) ? A + w0 : ((adv == 1) ? B + w0 : w0);
-                                B = (adv == 0) ? B + w1 : w1;
+                                const int adv = kk - cur;
+                                float ak = adv == 1 ? B : 0.f;  // two selects, no branch
+                                ak = adv == 0 ? A : ak;
+                                const float bk = adv == 0 ? B : 0.f;
+                                A = ak + w0;
+                                B = bk + w1;
                                 cur = kk;
+                                float* zp = zc + min(max(kk, -BP_ZG), BP_KB + BP_ZG - 2) * BP_PB;
+                                zp[0] = A;
+                                zp[BP_PB] = B;
                             };
                             if (vec4) {
-                                for (int b4 = v0 & ~3; b4 <= v1; b4 += 4) {
-                                    const float4 y4 = __ldg(reinterpret_cast<const float4*>(pc + b4));
-                                    if (b4 >= v0) add(b4, y4.x);
-                                    if (b4 + 1 >= v0 && b4 + 1 <= v1) add(b4 + 1, y4.y);
-                                    if (b4 + 2 >= v0 && b4 + 2 <= v1) add(b4 + 2, y4.z);
-                                    if (b4 + 3 <= v1) add(b4 + 3, y4.w);
-                                }
+                                // whole 4-row groups; only the first and last are masked to [v0, v1]
+                                const float4* pc4 = reinterpret_cast<const float4*>(pc);
+                                const float4* vd4 = reinterpret_cast<const float4*>(vdtab);
+                                const int q0 = v0 >> 2, q1 = v1 >> 2;
+                                auto group = [&](int q, bool mask) {
+                                    float4 y4 = __ldg(pc4 + q);
+                                    const float4 d4 = vd4[q];
+                                    if (mask) {
+                                        const int b = 4 * q;
+                                        y4.x = (b >= v0 && b <= v1) ? y4.x : 0.f;
+                                        y4.y = (b + 1 >= v0 && b + 1 <= v1) ? y4.y : 0.f;
+                                        y4.z = (b + 2 >= v0 && b + 2 <= v1) ? y4.z : 0.f;
+                                        y4.w = (b + 3 >= v0 && b + 3 <= v1) ? y4.w : 0.f;
+                                    }
+                                    step(d4.x, y4.x);
+                                    step(d4.y, y4.y);
+                                    step(d4.z, y4.z);
+                                    step(d4.w, y4.w);
+                                };
+                                if (q0 <= q1) group(q0, true);
+                                for (int q = q0 + 1; q < q1; ++q) group(q, false);
+                                if (q1 > q0) group(q1, true);
                             } else {
-                                for (int iv = v0; iv <= v1; ++iv) add(iv, __ldg(pc + iv));
+                                for (int iv = v0; iv <= v1; ++iv) step(vdtab[iv], __ldg(pc + iv));
                             }
-                            if (unsigned(cur) < unsigned(BP_KB)) zc[cur * BP_PB] = A;
-                            if (unsigned(cur + 1) < unsigned(BP_KB)) zc[(cur + 1) * BP_PB] = B;
                         } else {
                             // degenerate geometry (stencil point not in front of the source)
                             for (int iv = v0; iv <= v1; ++iv) {
@@ -406,8 +426,9 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz + BP_KB - 1) / BP_KB;
-    const size_t smem =
-        sizeof(float) * (size_t(BP_PB) * BP_KB + size_t(BP_PB) * BP_SL + 2 * BP_PB + g.nv) + sizeof(int2) * g.na;
+    const size_t smem = sizeof(float) * (size_t(BP_PB) * (BP_KB + 2 * BP_ZG) + size_t(BP_PB) * BP_SL + 2 * BP_PB +
+                                         ((size_t(g.nv) + 3) & ~size_t(3))) +
+                        sizeof(int2) * g.na;
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     static size_t configured = 0;
     if (smem > configured) {
