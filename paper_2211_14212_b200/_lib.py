@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libctk_b200.so")
+# CTK_B200_LIB: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("CTK_B200_LIB") or os.path.join(HERE, "lib", "libctk_b200.so")
 
 CTK_OK, CTK_E_DIMENSION, CTK_E_GEOMETRY, CTK_E_PARAMETER, CTK_E_DEGENERATE, CTK_E_NUMERICAL, CTK_E_CUDA, CTK_E_UNSUPPORTED = range(8)
 

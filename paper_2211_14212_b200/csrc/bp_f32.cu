@@ -1,14 +1,14 @@
 // A^T b for T = float on sm_100a: the exact transpose of fwd_f32.cu (matched) and the
-// voxel-driven backprojection (projector.hpp:204-279).  Both gather from the projections
-// transposed to pt[a][iu][iv] (detector columns contiguous; step-scaled for matched), so
-// no float atomics are used and every voxel sums its contributions in a fixed order.
+// voxel-driven backprojection (projector.hpp:204-279).  Both gather -- the matched one from
+// the step-scaled projections in 4-row groups pg[a][iv/4][iu][iv%4], the voxel-driven one
+// from the projections transposed to pt[a][iu][iv] -- so no float atomics are used and
+// every voxel sums its contributions in a fixed order.
 #include "f32_common.cuh"
 
 namespace ctkb {
 namespace {
 
 // ---- projection transpose for the gathers: pt[a][iu][iv] = (step?) * y[a][iv][iu] ------
-template <bool SCALE>
 __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __restrict__ pt) {
     __shared__ float tile[32][33];
     const int a = blockIdx.z;
@@ -22,14 +22,37 @@ __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int iu = u0 + r, iv = v0 + threadIdx.x;
         if (iu < g.nu && iv < g.nv) {
-            float val = tile[threadIdx.x][r];
-            const int c = a * g.nu + iu;
-            if (SCALE) val *= ray_step(g, g.colstep[c], row_coord(g, iv));
-            pt[size_t(c) * g.nv + iv] = val;
+            pt[(size_t(a) * g.nu + iu) * g.nv + iv] = tile[threadIdx.x][r];
         }
     }
 }
 
+// ---- grouped projection layout for the matched gather: pg[a][iv/4][iu][iv%4] = step * y ----
+// A warp of the plane kernel = 32 consecutive detector columns marching their rows in 4-row
+// groups (one 16-byte load per lane): with the columns of a row group contiguous, the warp's
+// load is one contiguous 512-byte run instead of 32 scattered 16-byte pieces.  Rows are
+// zero-padded to a multiple of 4.
+__device__ __forceinline__ size_t pg_index(const KGeom& g, int a, int iu, int iv) {
+    return ((size_t(a) * ((g.nv + 3) >> 2) + (iv >> 2)) * g.nu + iu) * 4 + (iv & 3);
+}
+
+__global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __restrict__ pg) {
+    // block: 32 columns x 8 row groups; thread (u, q) writes one float4
+    const int a = blockIdx.z;
+    const int iu = blockIdx.x * 32 + threadIdx.x, q = blockIdx.y * 8 + threadIdx.y;
+    const int nq = (g.nv + 3) >> 2;
+    if (iu >= g.nu || q >= nq) return;
+    const int c = a * g.nu + iu;
+    const double2 cs = g.colstep[c];
+    const float* fr = y + size_t(a) * g.nu * g.nv;
+    float r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int iv = 4 * q + j;
+        r[j] = iv < g.nv ? __ldg(fr + size_t(iv) * g.nu + iu) * ray_step(g, cs, row_coord(g, iv)) : 0.f;
+    }
+    reinterpret_cast<float4*>(pg)[(size_t(a) * nq + q) * g.nu + iu] = make_float4(r[0], r[1], r[2], r[3]);
+}
 
 // ---- matched A^T b, plane-driven ------------------------------------------------------
 // Pass CLASS (0: x-dominant columns, planes x = s, rows p = y; 1: y-dominant columns,
@@ -49,7 +72,7 @@ constexpr int BP_ZG = 2;  // guard rows of Z on each side: out-of-band entries l
 
 template <int CLASS>
 __global__ void __launch_bounds__(BP_PB)
-k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, int ptiles) {
+k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles) {
     extern __shared__ __align__(16) float sm[];
     float* Z = sm + BP_ZG * BP_PB;                              // [-BP_ZG, BP_KB+BP_ZG) x [BP_PB]
     int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG) * BP_PB);  // [BP_PB][BP_SL]
@@ -66,13 +89,13 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     const int p0 = ptile * BP_PB, k0 = kband * BP_KB;
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
-    for (int q = t; q < g.nv; q += BP_PB) vdtab[q] = float(row_coord(g, q));
+    for (int q = t; q < 4 * ((g.nv + 3) >> 2); q += BP_PB) vdtab[q] = float(row_coord(g, q));
     const float czf = 0.5f * float(g.nz - 1);
     const float cvf = 0.5f * float(g.nv - 1);
     const float invdu = float(1.0 / g.du);
     const float fs = float(s);
     const double h = g.h;
-    const bool vec4 = (g.nv & 3) == 0;
+    const int nq = (g.nv + 3) >> 2;  // row groups of the grouped projection layout
     // world coordinates of the plane and of the tile's row segment ends
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
@@ -113,8 +136,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                     const int ih = int(fih);
                     const float th = fh - fih;
                     if (ih + 1 >= p0 && ih <= p0 + BP_PB - 1 && ih + 1 >= 0 && ih < nh) {
-#pragma unroll
-                        for (int m = 0; m < BP_KB; ++m) Z[m * BP_PB + t] = 0.f;
                         const float gs = fmaf(fs, cd.w, cd.z);
                         int v0 = 0, v1 = g.nv - 1;
                         if (gs > 0.f) {
@@ -133,14 +154,33 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                             v0 = lo;
                             v1 = hi;
                         }
-                        const float* pc = pt + size_t(c) * g.nv;
+                        // column iu of view a, row group q: pc4[q * nu] (grouped layout)
+                        const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
+                        const size_t qs = size_t(g.nu);
                         float* zc = Z + t;
-                        if (gs > 0.f) {
-                            // fz increases with iv, so each Z[k] is final once the march passes
-                            // it: accumulate in registers (A -> Z[cur], B -> Z[cur+1]) and store
-                            // both every row, unconditionally -- a later row either overwrites
-                            // them with a larger partial or has moved on.  Out-of-band k are
-                            // clamped into the guard rows.  Branch-free: no per-row divergence.
+                        auto zero_rows = [&](int lo, int hi) {  // Z rows [lo, hi) of this column
+                            for (int m = max(lo, 0); m < min(hi, BP_KB); ++m) zc[m * BP_PB] = 0.f;
+                        };
+                        if (gs > 0.f && v0 <= v1) {
+                            // fz increases with iv, so Z[k] is final once the march passes it:
+                            // accumulate in registers (A -> Z[cur], B -> Z[cur+1]) and store both
+                            // after every row, unconditionally (a later row either overwrites them
+                            // with a larger partial or has moved past; measured faster than
+                            // predicated once-only stores, which compile to branches).
+                            // Out-of-band k land in the guard rows.  With at least 0.75 rows per
+                            // slice fz advances < 1.34 per row, so k never skips an entry and
+                            // only the rows before the first / after the last k need zeroing;
+                            // sparser columns zero the whole band first.
+                            const float rg = invdu / gs;
+                            if (rg >= 0.75f) {
+                                int kf, kfi;
+                                float tf;
+                                split(fmaf(vdtab[v0], gs, czf), kfi, tf);
+                                kf = kfi - k0;
+                                zero_rows(0, kf);
+                            } else {
+                                zero_rows(0, BP_KB);
+                            }
                             int cur = -(1 << 20);
                             float A = 0.f, B = 0.f;
                             auto step = [&](float vd, float yv) {
@@ -160,36 +200,33 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                                 zp[0] = A;
                                 zp[BP_PB] = B;
                             };
-                            if (vec4) {
-                                // whole 4-row groups; only the first and last are masked to [v0, v1]
-                                const float4* pc4 = reinterpret_cast<const float4*>(pc);
-                                const float4* vd4 = reinterpret_cast<const float4*>(vdtab);
-                                const int q0 = v0 >> 2, q1 = v1 >> 2;
-                                auto group = [&](int q, bool mask) {
-                                    float4 y4 = __ldg(pc4 + q);
-                                    const float4 d4 = vd4[q];
-                                    if (mask) {
-                                        const int b = 4 * q;
-                                        y4.x = (b >= v0 && b <= v1) ? y4.x : 0.f;
-                                        y4.y = (b + 1 >= v0 && b + 1 <= v1) ? y4.y : 0.f;
-                                        y4.z = (b + 2 >= v0 && b + 2 <= v1) ? y4.z : 0.f;
-                                        y4.w = (b + 3 >= v0 && b + 3 <= v1) ? y4.w : 0.f;
-                                    }
-                                    step(d4.x, y4.x);
-                                    step(d4.y, y4.y);
-                                    step(d4.z, y4.z);
-                                    step(d4.w, y4.w);
-                                };
-                                if (q0 <= q1) group(q0, true);
-                                for (int q = q0 + 1; q < q1; ++q) group(q, false);
-                                if (q1 > q0) group(q1, true);
-                            } else {
-                                for (int iv = v0; iv <= v1; ++iv) step(vdtab[iv], __ldg(pc + iv));
-                            }
+                            // whole 4-row groups; only the first and last are masked to [v0, v1]
+                            const float4* vd4 = reinterpret_cast<const float4*>(vdtab);
+                            const int q0 = v0 >> 2, q1 = v1 >> 2;
+                            auto group = [&](int q, bool mask) {
+                                float4 y4 = __ldg(pc4 + q * qs);
+                                const float4 d4 = vd4[q];
+                                if (mask) {
+                                    const int b = 4 * q;
+                                    y4.x = (b >= v0 && b <= v1) ? y4.x : 0.f;
+                                    y4.y = (b + 1 >= v0 && b + 1 <= v1) ? y4.y : 0.f;
+                                    y4.z = (b + 2 >= v0 && b + 2 <= v1) ? y4.z : 0.f;
+                                    y4.w = (b + 3 >= v0 && b + 3 <= v1) ? y4.w : 0.f;
+                                }
+                                step(d4.x, y4.x);
+                                step(d4.y, y4.y);
+                                step(d4.z, y4.z);
+                                step(d4.w, y4.w);
+                            };
+                            if (q0 <= q1) group(q0, true);
+                            for (int q = q0 + 1; q < q1; ++q) group(q, false);
+                            if (q1 > q0) group(q1, true);
+                            zero_rows(cur + 2, BP_KB);
                         } else {
-                            // degenerate geometry (stencil point not in front of the source)
+                            // no rows, or degenerate geometry (stencil point not in front of the source)
+                            zero_rows(0, BP_KB);
                             for (int iv = v0; iv <= v1; ++iv) {
-                                const float yv = __ldg(pc + iv);
+                                const float yv = reinterpret_cast<const float*>(pc4 + (iv >> 2) * qs)[iv & 3];
                                 int iz;
                                 float tz;
                                 split(fmaf(vdtab[iv], gs, czf), iz, tz);
@@ -267,7 +304,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     }
 }
 
-__global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x) {
+__global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x) {
     const size_t nvox = size_t(g.nx) * g.ny * g.nz;
     const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
     if (id >= nvox) return;
@@ -314,7 +351,7 @@ __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pt, f
                 float wb, wc;
                 if (i == ib) wb = 1.f - tb; else if (i == ib + 1) wb = tb; else continue;
                 if (j == ic) wc = 1.f - tc; else if (j == ic + 1) wc = tc; else continue;
-                acc = fmaf(wb * wc, __ldg(pt + size_t(c) * g.nv + iv), acc);
+                acc = fmaf(wb * wc, __ldg(pg + pg_index(g, a, iu, iv)), acc);
             }
         }
     }
@@ -412,12 +449,19 @@ int pick_kz(int nz) {
     return 16;
 }
 
-template <bool SCALE>
 void transpose_proj(Geometry& g, const float* y, cudaStream_t s) {
     g.proj_t.ensure(g.range() * sizeof(float));
     dim3 blk(32, 8), grd((g.nu + 31) / 32, (g.nv + 31) / 32, g.na);
-    k_proj_transpose<SCALE><<<grd, blk, 0, s>>>(g.kgeom(), y, g.proj_t.as<float>());
+    k_proj_transpose<<<grd, blk, 0, s>>>(g.kgeom(), y, g.proj_t.as<float>());
     after_launch("k_proj_transpose");
+}
+
+void group_proj(Geometry& g, const float* y, cudaStream_t s) {
+    const int nq = (g.nv + 3) >> 2;
+    g.proj_t.ensure(size_t(g.na) * g.nu * nq * 4 * sizeof(float));
+    dim3 blk(32, 8), grd((g.nu + 31) / 32, (nq + 7) / 8, g.na);
+    k_proj_group4<<<grd, blk, 0, s>>>(g.kgeom(), y, g.proj_t.as<float>());
+    after_launch("k_proj_group4");
 }
 
 template <int CLASS>
@@ -453,7 +497,7 @@ void launch_voxel(Geometry& g, float* x, cudaStream_t s) {
 }  // namespace
 
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
-    transpose_proj<true>(g, y, s);
+    group_proj(g, y, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
     launch_plane<0>(g, x, s);
     launch_plane<1>(g, x, s);
@@ -466,7 +510,7 @@ void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
 }
 
 void atb_voxel_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
-    transpose_proj<false>(g, y, s);
+    transpose_proj(g, y, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
     switch (pick_kz(g.nz)) {
         case 1: launch_voxel<1>(g, x, s); break;
