@@ -28,7 +28,14 @@ namespace {
 //   wx[i][j+1][k+1]  (x-dominant rays: slice i, h = j)     wy[j][i+1][k+1]  (h = i)
 // each of the 4 tap loads of a warp covers one contiguous z run (1-2 cache lines) instead
 // of two partial rows of a y/x-fastest plane.
-constexpr int ZW_BR = 32, ZW_BC = 8;  // block: 32 detector rows (lanes) x 8 columns
+#ifndef CTK_FWD_BC
+#define CTK_FWD_BC 8
+#endif
+#ifndef CTK_FWD_UNROLL
+#define CTK_FWD_UNROLL 2  // measured: 2 (48 regs, 5 CTAs/SM) beats 1, 3, 4, 8 at 256^3 and 512^3
+#endif
+constexpr int ZW_BR = 32, ZW_BC = CTK_FWD_BC;  // block: 32 detector rows (lanes) x ZW_BC columns
+constexpr int kFwdUnroll = CTK_FWD_UNROLL;
 
 __device__ __forceinline__ const float* opaque_ptr(const float* p) {
     asm("" : "+l"(p));
@@ -120,7 +127,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             // sign-extended 64-bit add chain on (off + pz)
             const float* base1 = opaque_ptr(base + pz);
             float fs = float(s0);
-#pragma unroll 4
+#pragma unroll kFwdUnroll
             for (int n = s1 - s0; n >= 0; --n) {
                 const float fh = fmaf(fs, cd.y, cd.x);
                 const float fz = fmaf(vd, fmaf(fs, cd.w, cd.z), czf);
