@@ -67,11 +67,19 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 //           the columns registered in its row, sorted by column -> deterministic order.
 // Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
 // their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
+// measured at 512^3 / 360 views: 4 CTAs/SM (64 regs) without the software prefetch is best
+// (89 ms) -- prefetch at 3 CTAs/SM 111 ms, prefetch at 4 CTAs/SM 92 ms
+#ifndef CTK_BP_MINB
+#define CTK_BP_MINB 4
+#endif
+#ifndef CTK_BP_PREFETCH
+#define CTK_BP_PREFETCH 0
+#endif
 constexpr int BP_PB = 256, BP_KB = 32, BP_SL = 8;
 constexpr int BP_ZG = 2;  // guard rows of Z on each side: out-of-band entries land there, unread
 
 template <int CLASS>
-__global__ void __launch_bounds__(BP_PB)
+__global__ void __launch_bounds__(BP_PB, CTK_BP_MINB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles) {
     extern __shared__ __align__(16) float sm[];
     float* Z = sm + BP_ZG * BP_PB;                              // [-BP_ZG, BP_KB+BP_ZG) x [BP_PB]
@@ -203,8 +211,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             // whole 4-row groups; only the first and last are masked to [v0, v1]
                             const float4* vd4 = reinterpret_cast<const float4*>(vdtab);
                             const int q0 = v0 >> 2, q1 = v1 >> 2;
-                            auto group = [&](int q, bool mask) {
-                                float4 y4 = __ldg(pc4 + q * qs);
+                            auto group = [&](int q, float4 y4, bool mask) {
                                 const float4 d4 = vd4[q];
                                 if (mask) {
                                     const int b = 4 * q;
@@ -218,9 +225,23 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 step(d4.z, y4.z);
                                 step(d4.w, y4.w);
                             };
-                            if (q0 <= q1) group(q0, true);
-                            for (int q = q0 + 1; q < q1; ++q) group(q, false);
-                            if (q1 > q0) group(q1, true);
+                            // software pipelined: the next group's load is in flight while the
+                            // current group is marched
+#if CTK_BP_PREFETCH
+                            const float4 yfirst = __ldg(pc4 + q0 * qs);
+                            float4 ynext = q1 > q0 ? __ldg(pc4 + (q0 + 1) * qs) : yfirst;
+                            group(q0, yfirst, true);
+                            for (int q = q0 + 1; q < q1; ++q) {
+                                const float4 y4 = ynext;
+                                ynext = __ldg(pc4 + (q + 1) * qs);
+                                group(q, y4, false);
+                            }
+                            if (q1 > q0) group(q1, ynext, true);
+#else
+                            group(q0, __ldg(pc4 + q0 * qs), true);
+                            for (int q = q0 + 1; q < q1; ++q) group(q, __ldg(pc4 + q * qs), false);
+                            if (q1 > q0) group(q1, __ldg(pc4 + q1 * qs), true);
+#endif
                             zero_rows(cur + 2, BP_KB);
                         } else {
                             // no rows, or degenerate geometry (stencil point not in front of the source)
