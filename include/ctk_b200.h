@@ -173,9 +173,17 @@ int ctk_hybrid_lsqr_f32(ctk_geom* g, int variant, const float* h_b, const ctk_hy
 int ctk_hybrid_lsqr_f64(ctk_geom* g, int variant, const double* h_b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
 int ctk_cgls_tv_f32(ctk_geom* g, int variant, const float* h_b, double lambda, int outer_iters, int inner_iters, const ctk_solver_opts* o, int warm_start, float* h_x, ctk_solve_log* log);
 int ctk_cgls_tv_f64(ctk_geom* g, int variant, const double* h_b, double lambda, int outer_iters, int inner_iters, const ctk_solver_opts* o, int warm_start, double* h_x, ctk_solve_log* log);
+/* SIRT (solvers.hpp:233-287) and AB/BA-GMRES (gmres.hpp:101-114): same signature as cgls. */
+int ctk_sirt_f32(ctk_geom* g, int variant, const float* h_b, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_sirt_f64(ctk_geom* g, int variant, const double* h_b, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
+int ctk_ab_gmres_f32(ctk_geom* g, int variant, const float* h_b, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_ab_gmres_f64(ctk_geom* g, int variant, const double* h_b, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
+int ctk_ba_gmres_f32(ctk_geom* g, int variant, const float* h_b, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_ba_gmres_f64(ctk_geom* g, int variant, const double* h_b, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
 
 /* Device-resident variants: b and x are DEVICE pointers; identical semantics.
- * solver: 0 cgls, 1 lsqr, 2 lsmr, 3 hybrid_lsqr, 4 cgls_tv.  `lambda` is the LSMR
+ * solver: 0 cgls, 1 lsqr, 2 lsmr, 3 hybrid_lsqr, 4 cgls_tv, 5 sirt, 6 ab_gmres,
+ * 7 ba_gmres.  `lambda` is the LSMR
  * damping / TV weight; hybrid reads `s`; cgls_tv reads outer/inner/warm_start. */
 int ctk_solve_dev_f32(ctk_geom* g, int solver, int variant, const float* d_b, double lambda,
                       const ctk_hybrid_strategy* s, int outer_iters, int inner_iters, int warm_start,

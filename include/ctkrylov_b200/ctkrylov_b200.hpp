@@ -83,6 +83,9 @@ struct Ops<float> {
     static int atb(ctk_geom* g, int v, const float* y, float* x) { return ctk_atb_host_f32(g, v, y, x); }
     static int cgls(ctk_geom* g, int v, const float* b, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_cgls_f32(g, v, b, o, x, l); }
     static int lsqr(ctk_geom* g, int v, const float* b, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_lsqr_f32(g, v, b, o, x, l); }
+    static int sirt(ctk_geom* g, int v, const float* b, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_sirt_f32(g, v, b, o, x, l); }
+    static int ab_gmres(ctk_geom* g, int v, const float* b, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_ab_gmres_f32(g, v, b, o, x, l); }
+    static int ba_gmres(ctk_geom* g, int v, const float* b, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_ba_gmres_f32(g, v, b, o, x, l); }
     static int lsmr(ctk_geom* g, int v, const float* b, double lam, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_lsmr_f32(g, v, b, lam, o, x, l); }
     static int hybrid(ctk_geom* g, int v, const float* b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_hybrid_lsqr_f32(g, v, b, s, o, x, l); }
     static int tv(ctk_geom* g, int v, const float* b, double lam, int oi, int ii, const ctk_solver_opts* o, int w, float* x, ctk_solve_log* l) { return ctk_cgls_tv_f32(g, v, b, lam, oi, ii, o, w, x, l); }
@@ -93,6 +96,9 @@ struct Ops<double> {
     static int atb(ctk_geom* g, int v, const double* y, double* x) { return ctk_atb_host_f64(g, v, y, x); }
     static int cgls(ctk_geom* g, int v, const double* b, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_cgls_f64(g, v, b, o, x, l); }
     static int lsqr(ctk_geom* g, int v, const double* b, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_lsqr_f64(g, v, b, o, x, l); }
+    static int sirt(ctk_geom* g, int v, const double* b, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_sirt_f64(g, v, b, o, x, l); }
+    static int ab_gmres(ctk_geom* g, int v, const double* b, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_ab_gmres_f64(g, v, b, o, x, l); }
+    static int ba_gmres(ctk_geom* g, int v, const double* b, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_ba_gmres_f64(g, v, b, o, x, l); }
     static int lsmr(ctk_geom* g, int v, const double* b, double lam, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_lsmr_f64(g, v, b, lam, o, x, l); }
     static int hybrid(ctk_geom* g, int v, const double* b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_hybrid_lsqr_f64(g, v, b, s, o, x, l); }
     static int tv(ctk_geom* g, int v, const double* b, double lam, int oi, int ii, const ctk_solver_opts* o, int w, double* x, ctk_solve_log* l) { return ctk_cgls_tv_f64(g, v, b, lam, oi, ii, o, w, x, l); }
@@ -207,6 +213,35 @@ ctk::SolveResult<T> lsqr(const B200Pair<T>& pair, std::span<const T> b, const ct
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::lsqr(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "lsqr");
+}
+/// SIRT (solvers.hpp:236-287)
+template <class T>
+ctk::SolveResult<T> sirt(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
+    opts.validate();
+    pair.check_range(b.size());
+    detail::Call<T> c(opts, opts.max_iters, 1);
+    std::vector<T> x(pair.domain_size);
+    check(Ops<T>::sirt(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
+    return c.result(std::move(x), pair, "sirt");
+}
+/// AB-GMRES / BA-GMRES (gmres.hpp:101-113)
+template <class T>
+ctk::SolveResult<T> ab_gmres(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
+    opts.validate();
+    pair.check_range(b.size());
+    detail::Call<T> c(opts, opts.max_iters, 1);
+    std::vector<T> x(pair.domain_size);
+    check(Ops<T>::ab_gmres(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
+    return c.result(std::move(x), pair, "ab_gmres");
+}
+template <class T>
+ctk::SolveResult<T> ba_gmres(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
+    opts.validate();
+    pair.check_range(b.size());
+    detail::Call<T> c(opts, opts.max_iters, 1);
+    std::vector<T> x(pair.domain_size);
+    check(Ops<T>::ba_gmres(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
+    return c.result(std::move(x), pair, "ba_gmres");
 }
 template <class T>
 ctk::SolveResult<T> lsmr(const B200Pair<T>& pair, std::span<const T> b, double lambda,

@@ -228,7 +228,7 @@ class RefError(RuntimeError):
         self.iteration = iteration
 
 
-SOLVERS = {"cgls": 0, "lsqr": 1, "lsmr": 2, "sirt": 3, "hybrid_lsqr": 4, "cgls_tv": 5}
+SOLVERS = {"cgls": 0, "lsqr": 1, "lsmr": 2, "sirt": 3, "hybrid_lsqr": 4, "cgls_tv": 5, "ab_gmres": 6, "ba_gmres": 7}
 
 
 class Reference:
@@ -536,6 +536,83 @@ def lsmr(fwd, back, b, lam, max_iters, tol=1e-6, stop_inc=True, gt=None, bd=1e-1
             mon.reason = "breakdown"
             break
     return mon.result(x, k)
+
+
+def sirt(fwd, back, b, nd, max_iters, tol=1e-6, stop_inc=True, gt=None):
+    """solvers.hpp:233-287: x <- x + C B (R (b - A x)), R / C inverse row / column sums of the
+    pair applied to all-ones vectors, floored at 1e-6 of their maximum."""
+    if not float(np.linalg.norm(b)) > 0:
+        return {"x": np.zeros(nd), "implicit": np.array([]), "explicit": np.array([]), "relative_error": np.array([]),
+                "lambda": np.array([]), "iterations_run": 0, "stop_reason": "tolerance"}
+    mon = Monitor(fwd, b, max_iters, tol, stop_inc, gt)
+
+    def inverse_weights(w):
+        wmax = float(np.max(np.abs(w)))
+        if not wmax > 0:
+            raise ValueError("sirt: operator maps ones to zero")
+        return 1.0 / np.maximum(w, 1e-6 * wmax)
+
+    row_inv = inverse_weights(fwd(np.ones(nd)))
+    col_inv = inverse_weights(back(np.ones(b.size)))
+    x = np.zeros(nd)
+    r = b.copy()
+    k = 0
+    while k < max_iters:
+        k += 1
+        x = x + col_inv * back(row_inv * r)
+        r = b - fwd(x)
+        expl = float(np.linalg.norm(r)) / mon.bnorm
+        if mon.record(k, x, expl, explicit=expl):
+            break
+    return mon.result(x, k)
+
+
+def abba_gmres(fwd, back, b, max_iters, ab, tol=1e-6, stop_inc=True, gt=None, reorth=True, bd=1e-14):
+    """gmres.hpp:41-99 with arnoldi_init/arnoldi_expand (krylov.hpp:94-145): Arnoldi by
+    modified Gram-Schmidt (+ a classical second pass when reorth) on A B (AB) or B A (BA);
+    projected least squares on the (k+1) x k Hessenberg; x rebuilt from the whole basis."""
+    mon = Monitor(fwd, b, max_iters, tol, stop_inc, gt)
+    rhs = b.copy() if ab else back(b)
+    square = (lambda v: fwd(back(v))) if ab else (lambda v: back(fwd(v)))
+    beta1 = float(np.linalg.norm(rhs))
+    W = [rhs / beta1]
+    hcols = []
+    x = None
+    k = 0
+    while k < max_iters:
+        k += 1
+        j = len(hcols)
+        w = square(W[j])
+        h = np.zeros(j + 2)
+        for i in range(j + 1):
+            h[i] = float(W[i] @ w)
+            w = w - h[i] * W[i]
+        if reorth:
+            for i in range(j + 1):
+                c = float(W[i] @ w)
+                w = w - c * W[i]
+                h[i] += c
+        hnext = float(np.linalg.norm(w))
+        h[j + 1] = hnext
+        hcols.append(h)
+        breakdown = hnext <= bd * beta1
+        if not breakdown:
+            W.append(w / hnext)
+        H = np.zeros((k + 1, k))
+        for c, col in enumerate(hcols):
+            H[: min(len(col), k + 1), c] = col[: k + 1]
+        e1 = np.zeros(k + 1)
+        e1[0] = beta1
+        y = np.linalg.lstsq(H, e1, rcond=None)[0]
+        resid = float(np.linalg.norm(e1 - H @ y))
+        comb = sum(y[i] * W[i] for i in range(k))
+        x = back(comb) if ab else comb
+        if mon.record(k, x, resid / beta1):
+            break
+        if breakdown:
+            mon.reason = "breakdown"
+            break
+    return mon.result(x, k, stored_domain_basis=0 if ab else len(W), stored_range_basis=len(W) if ab else 0)
 
 
 def gcv_lambda(H, beta1):

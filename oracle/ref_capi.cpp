@@ -19,6 +19,7 @@
 #include "ctkrylov/phantom.hpp"
 #include "ctkrylov/solvers.hpp"
 #ifdef CTK_REF_WITH_EIGEN
+#include "ctkrylov/gmres.hpp"
 #include "ctkrylov/hybrid.hpp"
 #include "ctkrylov/regparam.hpp"
 #include "ctkrylov/tv.hpp"
@@ -136,7 +137,7 @@ void fill_log(const ctk::SolveResult<T>& r, ref_log* log) {
     log->stored_range_basis = r.stored_range_basis;
 }
 
-// solver: 0 cgls, 1 lsqr, 2 lsmr, 3 sirt, 4 hybrid_lsqr, 5 cgls_tv
+// solver: 0 cgls, 1 lsqr, 2 lsmr, 3 sirt, 4 hybrid_lsqr, 5 cgls_tv, 6 ab_gmres, 7 ba_gmres
 template <typename T>
 int solve_impl(const ref_geom* d, int variant, int solver, double lambda, int strategy,
                double noise_level, int outer, int inner, int warm, const T* b, int max_iters,
@@ -168,6 +169,8 @@ int solve_impl(const ref_geom* d, int variant, int solver, double lambda, int st
                 break;
             }
             case 5: r = ctk::cgls_tv(pair, bs, lambda, outer, inner, opts, warm != 0); break;
+            case 6: r = ctk::ab_gmres(pair, bs, opts); break;
+            case 7: r = ctk::ba_gmres(pair, bs, opts); break;
 #endif
             default: throw ctk::ParameterError("solver not available in this build");
         }

@@ -25,6 +25,8 @@ from .api import (  # noqa: F401
     StopReason,
     UnsupportedError,
     VolumeShape,
+    ab_gmres,
+    ba_gmres,
     back_project,
     canonical_angle,
     cgls,
@@ -38,6 +40,7 @@ from .api import (  # noqa: F401
     lsqr,
     projector_pair,
     shepp_logan_3d,
+    sirt,
 )
 from ._lib import LIB_PATH, load  # noqa: F401
 

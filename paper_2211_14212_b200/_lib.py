@@ -144,6 +144,8 @@ def load():
     for t in ("f32", "f64"):
         sig[f"ctk_cgls_{t}"] = (i, [vp, i, vp, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
         sig[f"ctk_lsqr_{t}"] = (i, [vp, i, vp, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
+        for nm in ("sirt", "ab_gmres", "ba_gmres"):
+            sig[f"ctk_{nm}_{t}"] = (i, [vp, i, vp, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
         sig[f"ctk_lsmr_{t}"] = (i, [vp, i, vp, d, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
         sig[f"ctk_hybrid_lsqr_{t}"] = (i, [vp, i, vp, C.POINTER(HybridStrategyC), C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
         sig[f"ctk_cgls_tv_{t}"] = (i, [vp, i, vp, d, i, i, C.POINTER(SolverOpts), i, vp, C.POINTER(SolveLog)])

@@ -456,7 +456,8 @@ class HybridStrategy:
         return HybridStrategy(LambdaStrategy.gcv, 0.0, 0.0)
 
 
-_SOLVER_ID = {"cgls": 0, "lsqr": 1, "lsmr": 2, "hybrid_lsqr": 3, "cgls_tv": 4}
+_SOLVER_ID = {"cgls": 0, "lsqr": 1, "lsmr": 2, "hybrid_lsqr": 3, "cgls_tv": 4, "sirt": 5, "ab_gmres": 6,
+              "ba_gmres": 7}
 
 
 def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=None, outer=1, inner=1, warm=False):
@@ -505,7 +506,7 @@ def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=N
         x = np.empty(pair.domain_size, dtype=ndt)
         bp, xp = bh.ctypes.data_as(C.c_void_p), x.ctypes.data_as(C.c_void_p)
         v = int(pair.variant)
-        if name in ("cgls", "lsqr"):
+        if name in ("cgls", "lsqr", "sirt", "ab_gmres", "ba_gmres"):
             rc = getattr(lib, f"ctk_{name}_{t}")(proj.handle, v, bp, C.byref(o), xp, C.byref(log))
         elif name == "lsmr":
             rc = getattr(lib, f"ctk_lsmr_{t}")(proj.handle, v, bp, lam, C.byref(o), xp, C.byref(log))
@@ -530,6 +531,21 @@ def cgls(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
 def lsqr(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
     """solvers.hpp:62-126."""
     return _solve("lsqr", pair, b, opts)
+
+
+def sirt(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
+    """solvers.hpp:233-287 (scaled Landweber with inverse row/column sums)."""
+    return _solve("sirt", pair, b, opts)
+
+
+def ab_gmres(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
+    """gmres.hpp:101-106: GMRES on min_u ||b - A B u||, x = B u."""
+    return _solve("ab_gmres", pair, b, opts)
+
+
+def ba_gmres(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
+    """gmres.hpp:108-113: GMRES on min_x ||B b - B A x||."""
+    return _solve("ba_gmres", pair, b, opts)
 
 
 def lsmr(pair: OperatorPair, b, lambda_: float, opts: SolverOptions) -> SolveResult:

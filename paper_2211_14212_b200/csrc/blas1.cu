@@ -69,6 +69,18 @@ __global__ void k_axpy_nrm2sq(size_t n, T alpha, const T* __restrict__ x, T* __r
     if (threadIdx.x == 0) part[blockIdx.x] = r;
 }
 
+// r = b - ax; partial of ||r||^2 (SIRT residual, solvers.hpp:280-282)
+template <class T>
+__global__ void k_sub_nrm2sq(size_t n, const T* __restrict__ b, const T* __restrict__ ax, T* __restrict__ r,
+                             double* __restrict__ part) {
+    const double v = chunk_reduce<T>(n, [&](size_t i) {
+        const T d = b[i] - ax[i];
+        r[i] = d;
+        return double(d) * double(d);
+    });
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+}
+
 template <class T>
 __global__ void k_absmax(size_t n, const T* __restrict__ x, double* __restrict__ part) {
     const Chunk c = my_chunk(n);
@@ -136,6 +148,26 @@ struct LsmrF {
         x[i] += c2 * hb;
         h[i] = v[i] - c3 * hi;
     }
+};
+template <class T>
+struct InvFloorF {  // x = 1 / max(x, floor)   (solvers.hpp:257-263)
+    T floor;
+    T* x;
+    __device__ void operator()(size_t i) const { x[i] = T(1) / (x[i] > floor ? x[i] : floor); }
+};
+template <class T>
+struct MulF {  // out = a .* b
+    const T* a;
+    const T* b;
+    T* out;
+    __device__ void operator()(size_t i) const { out[i] = a[i] * b[i]; }
+};
+template <class T>
+struct AddMulF {  // x += a .* b
+    const T* a;
+    const T* b;
+    T* x;
+    __device__ void operator()(size_t i) const { x[i] += a[i] * b[i]; }
 };
 template <class T>
 struct FillF {
@@ -216,6 +248,24 @@ void axpy_nrm2sq(size_t n, double alpha, const T* x, T* y, double* d_res, RedWor
     finish_sum(w.partials, kRedBlocks, d_res, s);
 }
 template <class T>
+void sub_nrm2sq(size_t n, const T* b, const T* ax, T* r, double* d_res, RedWork w, cudaStream_t s) {
+    k_sub_nrm2sq<T><<<kRedBlocks, kRedThreads, 0, s>>>(n, b, ax, r, w.partials);
+    after_launch("k_sub_nrm2sq");
+    finish_sum(w.partials, kRedBlocks, d_res, s);
+}
+template <class T>
+void inv_floor(size_t n, double floor, T* x, cudaStream_t s) {
+    run_map<T>(n, InvFloorF<T>{T(floor), x}, s, "k_inv_floor");
+}
+template <class T>
+void mul(size_t n, const T* a, const T* b, T* out, cudaStream_t s) {
+    run_map<T>(n, MulF<T>{a, b, out}, s, "k_mul");
+}
+template <class T>
+void add_mul(size_t n, const T* a, const T* b, T* x, cudaStream_t s) {
+    run_map<T>(n, AddMulF<T>{a, b, x}, s, "k_add_mul");
+}
+template <class T>
 void reduce_absmax(size_t n, const T* x, double* d_res, RedWork w, cudaStream_t s) {
     k_absmax<T><<<kRedBlocks, kRedThreads, 0, s>>>(n, x, w.partials);
     after_launch("k_absmax");
@@ -270,6 +320,10 @@ void block_axpy(size_t n, int m, double alpha, const double* d_coef, const T* ba
     template void reduce_diff_nrm2sq<T>(size_t, const T*, const T*, double*, RedWork, cudaStream_t);      \
     template void axpy_nrm2sq<T>(size_t, double, const T*, T*, double*, RedWork, cudaStream_t);           \
     template void reduce_absmax<T>(size_t, const T*, double*, RedWork, cudaStream_t);                     \
+    template void sub_nrm2sq<T>(size_t, const T*, const T*, T*, double*, RedWork, cudaStream_t);          \
+    template void inv_floor<T>(size_t, double, T*, cudaStream_t);                                         \
+    template void mul<T>(size_t, const T*, const T*, T*, cudaStream_t);                                   \
+    template void add_mul<T>(size_t, const T*, const T*, T*, cudaStream_t);                               \
     template void axpy<T>(size_t, double, const T*, T*, cudaStream_t);                                    \
     template void xpby<T>(size_t, const T*, double, T*, cudaStream_t);                                    \
     template void scal<T>(size_t, double, T*, cudaStream_t);                                              \

@@ -271,6 +271,12 @@ CTK_SOLVE_HOST(ctk_cgls_f32, float, 0)
 CTK_SOLVE_HOST(ctk_cgls_f64, double, 0)
 CTK_SOLVE_HOST(ctk_lsqr_f32, float, 1)
 CTK_SOLVE_HOST(ctk_lsqr_f64, double, 1)
+CTK_SOLVE_HOST(ctk_sirt_f32, float, 5)
+CTK_SOLVE_HOST(ctk_sirt_f64, double, 5)
+CTK_SOLVE_HOST(ctk_ab_gmres_f32, float, 6)
+CTK_SOLVE_HOST(ctk_ab_gmres_f64, double, 6)
+CTK_SOLVE_HOST(ctk_ba_gmres_f32, float, 7)
+CTK_SOLVE_HOST(ctk_ba_gmres_f64, double, 7)
 #undef CTK_SOLVE_HOST
 
 int ctk_lsmr_f32(ctk_geom* g, int variant, const float* b, double lambda, const ctk_solver_opts* o, float* x,

@@ -7,6 +7,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -78,8 +79,9 @@ void comm_allreduce(Comm* c, void* d_buf, size_t count, int dtype, cudaStream_t 
     if (c->cb.allreduce_sum(d_buf, count, dtype, s, c->cb.user) != 0) fail(CTK_E_CUDA, "allreduce_sum callback failed");
 }
 
-double comm_sum_scalar(Comm* c, double v) {
-    if (!c || c->cb.nranks <= 1) return v;
+namespace {
+// every rank's value, in rank order
+std::vector<double> comm_gather_scalar(Comm* c, double v) {
     std::vector<double> all(size_t(c->cb.nranks), 0.0);
     if (c->nccl_comm) {
         auto* st = static_cast<NcclState*>(c->nccl_comm);
@@ -93,9 +95,22 @@ double comm_sum_scalar(Comm* c, double v) {
         if (!c->cb.allgather_f64) fail(CTK_E_PARAMETER, "communicator lacks allgather_f64");
         if (c->cb.allgather_f64(v, all.data(), c->cb.user) != 0) fail(CTK_E_CUDA, "allgather_f64 callback failed");
     }
+    return all;
+}
+}  // namespace
+
+double comm_sum_scalar(Comm* c, double v) {
+    if (!c || c->cb.nranks <= 1) return v;
     double s = 0.0;
-    for (double x : all) s += x;  // rank order
+    for (double x : comm_gather_scalar(c, v)) s += x;  // rank order
     return s;
+}
+
+double comm_max_scalar(Comm* c, double v) {
+    if (!c || c->cb.nranks <= 1) return v;
+    double m = v;
+    for (double x : comm_gather_scalar(c, v)) m = std::max(m, x);
+    return m;
 }
 
 void nccl_unique_id(void* out128) {

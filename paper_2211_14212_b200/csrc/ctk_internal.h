@@ -152,6 +152,14 @@ template <class T>  // x += c1*w (old w); w = v - c2*w     (solvers.hpp:114-116)
 void lsqr_update(size_t n, double c1, double c2, T* x, T* w, const T* v, cudaStream_t s);
 template <class T>  // hbar = h - c1*hbar; x += c2*hbar; h = v - c3*h   (solvers.hpp:201-204)
 void lsmr_update(size_t n, double c1, double c2, double c3, T* x, T* h, T* hbar, const T* v, cudaStream_t s);
+template <class T>  // r = b - ax, res = ||r||^2
+void sub_nrm2sq(size_t n, const T* b, const T* ax, T* r, double* d_res, RedWork w, cudaStream_t s);
+template <class T>  // x = 1 / max(x, floor)
+void inv_floor(size_t n, double floor, T* x, cudaStream_t s);
+template <class T>  // out = a .* b
+void mul(size_t n, const T* a, const T* b, T* out, cudaStream_t s);
+template <class T>  // x += a .* b
+void add_mul(size_t n, const T* a, const T* b, T* x, cudaStream_t s);
 template <class T>  // out[i] = max|x|  (fp64)
 void reduce_absmax(size_t n, const T* x, double* d_res, RedWork w, cudaStream_t s);
 // block Gram-Schmidt pieces (krylov.hpp:21-31, gmres.hpp:33-39): coef[i] = <basis_i, w>
@@ -180,6 +188,7 @@ struct Comm {
 };
 void comm_allreduce(Comm* c, void* d_buf, size_t count, int dtype, cudaStream_t s);
 double comm_sum_scalar(Comm* c, double v);  // rank-ordered sum of per-rank partials
+double comm_max_scalar(Comm* c, double v);
 
 uint64_t launch_count();
 

@@ -222,4 +222,33 @@ double choose_lambda(const ctk_hybrid_strategy& st, const std::vector<double>& H
     return 0.0;
 }
 
+// gmres.hpp:24-31 solves with Eigen's colPivHouseholderQr().  For full column rank (every
+// Arnoldi step that did not break down) the least-squares solution is unique and this
+// SVD-based solve agrees with it to rounding; a numerically rank-deficient H takes the
+// minimum-norm solution over singular values above 1e-13 s_max.  The residual is formed
+// explicitly as || rhs - H y || like the reference.
+std::vector<double> projected_ls(const std::vector<double>& H, int k, double beta1, double* resid) {
+    std::vector<double> U, s, V;
+    thin_svd(H, k + 1, k, U, s, V);
+    const double tol = k > 0 ? s[0] * 1e-13 : 0.0;
+    std::vector<double> c(size_t(k), 0.0), y(size_t(k), 0.0);
+    for (int i = 0; i < k; ++i) c[size_t(i)] = s[size_t(i)] > tol ? U[size_t(i)] * beta1 / s[size_t(i)] : 0.0;
+    for (int r = 0; r < k; ++r) {
+        double acc = 0.0;
+        for (int i = 0; i < k; ++i) acc += V[size_t(r) * k + i] * c[size_t(i)];
+        y[size_t(r)] = acc;
+    }
+    if (resid) {
+        double sq = 0.0;
+        for (int r = 0; r <= k; ++r) {
+            double hy = 0.0;
+            for (int j = 0; j < k; ++j) hy += H[size_t(r) * k + j] * y[size_t(j)];
+            const double e = (r == 0 ? beta1 : 0.0) - hy;
+            sq += e * e;
+        }
+        *resid = std::sqrt(sq);
+    }
+    return y;
+}
+
 }  // namespace ctkb

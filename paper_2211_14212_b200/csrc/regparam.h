@@ -24,5 +24,7 @@ double gcv_lambda(const std::vector<double>& H, int k, double beta1);
 std::vector<double> projected_tikhonov(const std::vector<double>& H, int k, double beta1, double lambda,
                                        double* fit_resid);
 double choose_lambda(const ctk_hybrid_strategy& st, const std::vector<double>& H, int k, double beta1);
+// min || beta1 e1 - H y || for the (k+1) x k Hessenberg of Arnoldi (gmres.hpp:24-31)
+std::vector<double> projected_ls(const std::vector<double>& H, int k, double beta1, double* resid);
 
 }  // namespace ctkb

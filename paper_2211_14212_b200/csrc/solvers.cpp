@@ -120,9 +120,12 @@ struct Monitor {
         log->iterations = log->n_relative_error = log->n_lambda = 0;
     }
 
-    // IterationMonitor::record; returns true when the solver should stop
-    bool record(int k, const T* x, double implicit, bool has_lambda = false, double lambda = 0.0) {
-        const double expl = std::sqrt(d.resid2(x, b)) / bnorm;
+    // IterationMonitor::record; returns true when the solver should stop.  expl_override:
+    // the relative explicit residual when the caller already formed it from a genuine
+    // forward application of this iterate (solve_log.hpp:102-115; SIRT), else computed here.
+    bool record(int k, const T* x, double implicit, bool has_lambda = false, double lambda = 0.0,
+                const double* expl_override = nullptr) {
+        const double expl = expl_override ? *expl_override : std::sqrt(d.resid2(x, b)) / bnorm;
         if (!std::isfinite(expl) || !std::isfinite(implicit))
             fail(CTK_E_NUMERICAL, "non-finite residual at iteration " + std::to_string(k), k);
         if (log->iterations >= log->capacity) fail(CTK_E_PARAMETER, "solve log capacity exceeded");
@@ -529,6 +532,148 @@ void cgls_tv(Dev<T>& d, const T* b, double lambda, int outer_iters, int inner_it
     mon.finish(k);
 }
 
+// SIRT (solvers.hpp:233-287): x <- x + C B (R (b - A x)), R and C the inverse row / column
+// sums of the pair (A 1, B 1) floored at 1e-6 of their maximum.  One genuine forward per
+// iteration drives both the update and the logged residual.
+template <class T>
+void sirt(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* log) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    log->iterations = log->n_relative_error = log->n_lambda = 0;
+    if (!(std::sqrt(d.nrm2sq(b, nr, true)) > 0.0)) {
+        // zero data: x = 0 is already the fixed point (solvers.hpp:240-251)
+        fill<T>(nd, T(0), x, d.s);
+        log->iterations_run = 0;
+        log->stop_reason = CTK_STOP_TOLERANCE;
+        return;
+    }
+    Monitor<T> mon(d, b, o, log, "sirt");
+    Vec<T> row_inv, col_inv, r, corr, ax;
+    row_inv.alloc(nr); col_inv.alloc(nd); r.alloc(nr); corr.alloc(nd); ax.alloc(nr);
+    // inverse weights from the pair applied to all-ones vectors (solvers.hpp:257-267)
+    auto inverse_weights = [&](T* w, size_t n, bool range) {
+        reduce_absmax<T>(n, w, d.w.results, d.w, d.s);
+        double wmax = d.fetch(0);
+        if (range && g.comm) wmax = comm_max_scalar(g.comm, wmax);
+        if (!(T(wmax) > T(0))) fail(CTK_E_DEGENERATE, "sirt: operator maps ones to zero");
+        inv_floor<T>(n, double(T(1e-6) * T(wmax)), w, d.s);
+    };
+    fill<T>(nd, T(1), corr.p, d.s);
+    d.ax(corr.p, row_inv.p);
+    inverse_weights(row_inv.p, nr, true);
+    fill<T>(nr, T(1), r.p, d.s);
+    d.atb(r.p, col_inv.p);
+    inverse_weights(col_inv.p, nd, false);
+    fill<T>(nd, T(0), x, d.s);
+    CTK_CUDA(cudaMemcpyAsync(r.p, b, sizeof(T) * nr, cudaMemcpyDeviceToDevice, d.s));  // b - A x for x = 0
+    int k = 0;
+    while (k < o.max_iters) {
+        ++k;
+        mul<T>(nr, row_inv.p, r.p, ax.p, d.s);  // scaled = R r (ax is scratch here)
+        d.atb(ax.p, corr.p);
+        add_mul<T>(nd, col_inv.p, corr.p, x, d.s);
+        d.ax(x, ax.p);
+        sub_nrm2sq<T>(nr, b, ax.p, r.p, d.w.results, d.w, d.s);
+        const double expl = std::sqrt(d.range_sum(d.fetch(0))) / mon.bnorm;
+        if (mon.record(k, x, expl, false, 0.0, &expl)) break;
+    }
+    mon.finish(k);
+}
+
+// AB-GMRES (ab = true: Arnoldi on A B over the range, x = B u) and BA-GMRES (Arnoldi on
+// B A over the domain with right-hand side B b), gmres.hpp:41-114; Arnoldi with modified
+// Gram-Schmidt plus an optional classical second pass (krylov.hpp:94-145).  x is rebuilt
+// from the whole basis every iteration like the reference (basis_combination).
+template <class T>
+void abba_gmres(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* log, bool ab) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    const size_t n = ab ? nr : nd;  // Arnoldi space
+    Monitor<T> mon(d, b, o, log, ab ? "ab_gmres" : "ba_gmres");
+    const int cap = o.max_iters + 1;
+    DevBuf Wb, dyb;
+    Wb.ensure(sizeof(T) * n * size_t(cap));
+    dyb.ensure(sizeof(double) * size_t(cap));
+    T* W = Wb.as<T>();
+    auto Wi = [&](int i) { return W + size_t(i) * n; };
+    Vec<T> tmp, u;
+    tmp.alloc(ab ? nd : nr);  // the intermediate of the squared operator
+    if (ab) u.alloc(nr);
+    auto apply_square = [&](const T* in, T* out) {
+        if (ab) {
+            d.atb(in, tmp.p);
+            d.ax(tmp.p, out);
+        } else {
+            d.ax(in, tmp.p);
+            d.atb(tmp.p, out);
+        }
+    };
+    // arnoldi_init (krylov.hpp:107-117)
+    if (ab) CTK_CUDA(cudaMemcpyAsync(Wi(0), b, sizeof(T) * nr, cudaMemcpyDeviceToDevice, d.s));
+    else d.atb(b, Wi(0));
+    const double beta1 = std::sqrt(d.nrm2sq(Wi(0), n, ab));
+    if (!(beta1 > 0.0)) fail(CTK_E_DEGENERATE, "arnoldi_init: zero right-hand side");
+    scal<T>(n, 1.0 / beta1, Wi(0), d.s);
+    const double tol = breakdown_factor<T>() * beta1;
+    std::vector<std::vector<double>> hcols;
+    int nbasis = 1;
+    int k = 0;
+    while (k < o.max_iters) {
+        ++k;
+        // arnoldi_expand (krylov.hpp:119-145)
+        const int j = int(hcols.size());
+        T* w = Wi(j + 1);
+        apply_square(Wi(j), w);
+        std::vector<double> h(size_t(j + 2), 0.0);
+        for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, in order
+            reduce_dot<T>(n, Wi(i), w, d.w.results, d.w, d.s);
+            double hi = d.fetch(0);
+            if (ab) hi = d.range_sum(hi);
+            h[size_t(i)] = double(T(hi));
+            axpy<T>(n, -h[size_t(i)], Wi(i), w, d.s);
+        }
+        if (o.reorth) {
+            for (int i = 0; i <= j; ++i) {
+                reduce_dot<T>(n, Wi(i), w, d.w.results, d.w, d.s);
+                double c = d.fetch(0);
+                if (ab) c = d.range_sum(c);
+                c = double(T(c));
+                axpy<T>(n, -c, Wi(i), w, d.s);
+                h[size_t(i)] = double(T(h[size_t(i)]) + T(c));
+            }
+        }
+        const double hnext = double(T(std::sqrt(d.nrm2sq(w, n, ab))));
+        h[size_t(j + 1)] = hnext;
+        hcols.push_back(h);
+        const bool breakdown = hnext <= tol;
+        if (!breakdown) {
+            scal<T>(n, 1.0 / hnext, w, d.s);
+            ++nbasis;
+        }
+        // projected least squares on the (k+1) x k Hessenberg (gmres.hpp:14-31)
+        std::vector<double> H(size_t(k + 1) * k, 0.0);
+        for (int c = 0; c < k; ++c)
+            for (int r = 0; r < int(hcols[size_t(c)].size()) && r <= k; ++r) H[size_t(r) * k + c] = hcols[size_t(c)][size_t(r)];
+        double resid = 0.0;
+        const std::vector<double> y = projected_ls(H, k, beta1, &resid);
+        // basis_combination (gmres.hpp:33-39) over the first k basis vectors
+        CTK_CUDA(cudaMemcpyAsync(dyb.p, y.data(), sizeof(double) * y.size(), cudaMemcpyHostToDevice, d.s));
+        T* comb = ab ? u.p : x;
+        fill<T>(n, T(0), comb, d.s);
+        block_axpy<T>(n, k, 1.0, dyb.as<double>(), W, n, comb, d.s);
+        CTK_CUDA(cudaStreamSynchronize(d.s));  // y (host) must outlive the async copy
+        if (ab) d.atb(u.p, x);
+        if (mon.record(k, x, resid / beta1)) break;
+        if (breakdown) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            break;
+        }
+    }
+    mon.finish(k);
+    log->stored_domain_basis = ab ? 0 : nbasis;
+    log->stored_range_basis = ab ? nbasis : 0;
+}
+
 }  // namespace
 
 template <class T>
@@ -548,6 +693,9 @@ void solve_device(Geometry& g, int solver, int variant, const T* d_b, double lam
             hybrid_lsqr<T>(d, d_b, *st, *o, d_x, log);
             break;
         case 4: cgls_tv<T>(d, d_b, lambda, outer, inner, warm != 0, *o, d_x, log); break;
+        case 5: sirt<T>(d, d_b, *o, d_x, log); break;
+        case 6: abba_gmres<T>(d, d_b, *o, d_x, log, true); break;
+        case 7: abba_gmres<T>(d, d_b, *o, d_x, log, false); break;
         default: fail(CTK_E_PARAMETER, "unknown solver");
     }
     CTK_CUDA(cudaStreamSynchronize(g.stream));

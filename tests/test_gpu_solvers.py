@@ -95,6 +95,34 @@ def test_cgls_tv_parity(ctk, reference, problem, dtype):
     assert list(res.outer_starts) == list(want["outer_starts"])
 
 
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_sirt_parity(ctk, reference, problem, dtype):
+    g, gt, b = problem
+    k = 10
+    want = reference.solve(g, b, "sirt", k, tol=0.0, stop_inc=False, gt=gt)
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    res = ctk.sirt(pair, b.astype(dtype), _opts(ctk, k, gt.astype(dtype)))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+    assert res.log.lambda_ == []
+    z = ctk.sirt(pair, np.zeros_like(b, dtype=dtype), _opts(ctk, k))
+    assert z.iterations_run == 0 and z.stop_reason.name == "tolerance" and not np.any(z.x)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("variant", ["ab_gmres", "ba_gmres"])
+def test_gmres_parity(ctk, reference, problem, dtype, variant):
+    g, gt, b = problem
+    k = 8
+    want = reference.solve(g, b, variant, k, tol=0.0, stop_inc=False, gt=gt)
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    res = getattr(ctk, variant)(pair, b.astype(dtype), _opts(ctk, k, gt.astype(dtype)))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+    assert res.stored_domain_basis == want["stored_domain_basis"]
+    assert res.stored_range_basis == want["stored_range_basis"]
+
+
 def test_voxel_driven_lsqr_parity(ctk, reference, problem):
     g, gt, b = problem
     k = 6

@@ -12,8 +12,8 @@ import pytest
 from geoms import ALL, cone_adjoint, parallel2d
 from conftest import rel_l2
 
-from oracle.oracle import (Geom, adjoint_discrepancy, cgls, cgls_tv, dp_lambda, gcv_lambda, hybrid_lsqr, lsmr, lsqr,
-                           ray_box_chord)
+from oracle.oracle import (Geom, abba_gmres, adjoint_discrepancy, cgls, cgls_tv, dp_lambda, gcv_lambda, hybrid_lsqr,
+                           lsmr, lsqr, ray_box_chord, sirt)
 
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
 
@@ -191,6 +191,36 @@ def test_numpy_cgls_tv_vs_reference(restated, reference, small_problem):
     assert rel_l2(got["x"], want["x"]) < 1e-9
     assert np.allclose(got["explicit"], want["explicit"], rtol=1e-9)
     assert list(got["outer_starts"]) == list(want["outer_starts"])
+
+
+def test_numpy_sirt_vs_reference(restated, reference, small_problem):
+    g, gt, b = small_problem
+    f = lambda v: restated.forward(g, v)  # noqa: E731
+    bk = lambda v: restated.back(g, v)  # noqa: E731
+    want = reference.solve(g, b, "sirt", 10, tol=0.0, stop_inc=False, gt=gt)
+    got = sirt(f, bk, b, g.domain_size, 10, tol=0.0, stop_inc=False, gt=gt)
+    assert rel_l2(got["x"], want["x"]) < 1e-9
+    assert np.allclose(got["explicit"], want["explicit"], rtol=1e-9)
+    assert np.allclose(got["implicit"], want["implicit"], rtol=1e-9)
+    assert len(want["lambda"]) == 0  # SIRT logs no lambda (solve_log.hpp:120)
+    # zero data: x = 0 is the fixed point, no iterations logged (solvers.hpp:240-251)
+    z = reference.solve(g, np.zeros_like(b), "sirt", 5, tol=0.0, stop_inc=False)
+    assert z["iterations_run"] == 0 and z["stop_reason"] == "tolerance" and not np.any(z["x"])
+
+
+@pytest.mark.parametrize("variant", ["ab_gmres", "ba_gmres"])
+@pytest.mark.parametrize("reorth", [True, False])
+def test_numpy_gmres_vs_reference(restated, reference, small_problem, variant, reorth):
+    g, gt, b = small_problem
+    f = lambda v: restated.forward(g, v)  # noqa: E731
+    bk = lambda v: restated.back(g, v)  # noqa: E731
+    want = reference.solve(g, b, variant, 8, tol=0.0, stop_inc=False, reorth=reorth, gt=gt)
+    got = abba_gmres(f, bk, b, 8, variant == "ab_gmres", tol=0.0, stop_inc=False, gt=gt, reorth=reorth)
+    assert rel_l2(got["x"], want["x"]) < 1e-8
+    assert np.allclose(got["explicit"], want["explicit"], rtol=1e-8)
+    assert np.allclose(got["implicit"], want["implicit"], rtol=1e-6)
+    assert got["stored_domain_basis"] == want["stored_domain_basis"]
+    assert got["stored_range_basis"] == want["stored_range_basis"]
 
 
 def test_regparam_numpy_vs_reference(reference):
