@@ -218,9 +218,20 @@ int ctk_comm_create(const ctk_comm_callbacks* cb, ctk_comm** out);
 int ctk_nccl_get_unique_id(void* out128);
 int ctk_comm_create_nccl(const void* id128, int nranks, int rank, ctk_comm** out);
 void ctk_comm_destroy(ctk_comm* c);
-/* Attach a communicator: the handle's angles are this rank's shard; A^T b partial
- * volumes are sum-reduced and range-space dots are summed over ranks in rank order. */
+/* Attach a communicator.  Angle sharding (no slab set): the handle's angles are this
+ * rank's shard; A^T b partial volumes are sum-reduced and range-space dots are summed over
+ * ranks in rank order.  z-slab sharding (ctk_geom_set_slab): domain vectors are this
+ * rank's slab; A x partial projections are sum-reduced, domain-space dots are summed in
+ * rank order and the TV stencils exchange one-slice halos. */
 int ctk_geom_attach_comm(ctk_geom* g, ctk_comm* c);
+
+/* ---- z-slab sharding --------------------------------------- */
+/* Contiguous z-slab of rank r among G ranks: slices [z0, z0+count). */
+int ctk_shard_slabs(int nz, int nranks, int rank, int* z0, int* count);
+/* The handle's domain vectors hold slices [z0, z0+nz_local) of the geometry's nz (the
+ * geometry, angles and detector stay global); nz_local = 0 restores the whole volume.
+ * Implemented for the f32 Joseph operators (others return CTK_E_UNSUPPORTED at apply). */
+int ctk_geom_set_slab(ctk_geom* g, int z0, int nz_local);
 
 /* ---- instrumentation ----------------------------------------------------------------- */
 /* Number of this library's kernel launches since load (for bench gpu_launches). */

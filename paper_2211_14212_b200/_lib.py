@@ -107,6 +107,7 @@ def load():
         "ctk_geom_sizes": (i, [vp, C.POINTER(sz), C.POINTER(sz)]),
         "ctk_geom_set_projector": (i, [vp, i]),
         "ctk_geom_set_bp_partitions": (i, [vp, i]),
+        "ctk_geom_set_slab": (i, [vp, i, i]),
         "ctk_geom_set_stream": (i, [vp, vp]),
         "ctk_geom_attach_comm": (i, [vp, vp]),
         "ctk_geom_last_kernel_ms": (d, [vp]),
@@ -132,6 +133,7 @@ def load():
         "ctk_solve_dev_f32": (i, [vp, i, i, vp, d, C.POINTER(HybridStrategyC), i, i, i, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)]),
         "ctk_solve_dev_f64": (i, [vp, i, i, vp, d, C.POINTER(HybridStrategyC), i, i, i, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)]),
         "ctk_shard_angles": (i, [i, i, i, C.POINTER(i), C.POINTER(i)]),
+        "ctk_shard_slabs": (i, [i, i, i, C.POINTER(i), C.POINTER(i)]),
         "ctk_comm_create": (i, [C.POINTER(CommCallbacks), C.POINTER(vp)]),
         "ctk_nccl_get_unique_id": (i, [vp]),
         "ctk_comm_create_nccl": (i, [vp, i, i, C.POINTER(vp)]),

@@ -31,7 +31,7 @@ import ctypes as C
 import math
 from dataclasses import dataclass, field
 from enum import IntEnum
-from typing import Callable, Optional, Sequence
+from typing import Callable, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -259,6 +259,14 @@ class Projector:
             self.lib.ctk_geom_destroy(h)
             self.handle = None
 
+    def set_slab(self, z0: int, nz_local: int):
+        """Domain vectors hold slices [z0, z0 + nz_local) of the volume (z-slab sharding);
+        nz_local = 0 restores the whole volume."""
+        _check(self.lib.ctk_geom_set_slab(self.handle, int(z0), int(nz_local)))
+        ds, rs = C.c_size_t(), C.c_size_t()
+        _check(self.lib.ctk_geom_sizes(self.handle, C.byref(ds), C.byref(rs)))
+        self.domain_size, self.range_size = ds.value, rs.value
+
     def attach_comm(self, comm):
         _check(self.lib.ctk_geom_attach_comm(self.handle, comm.handle))
         self._comm = comm
@@ -354,14 +362,20 @@ class OperatorPair:
 
 def projector_pair(geom: ConeGeometry, variant: BackprojectVariant = BackprojectVariant.matched,
                    dtype=np.float32, projector: ProjectorKind = ProjectorKind.joseph,
-                   bp_partitions: int = 1) -> OperatorPair:
-    """operators.hpp:91-115 -- the projector pair of a geometry, backed by the sm_100a kernels."""
+                   bp_partitions: int = 1, slab: Optional[Tuple[int, int]] = None) -> OperatorPair:
+    """operators.hpp:91-115 -- the projector pair of a geometry, backed by the sm_100a kernels.
+    slab = (z0, nz_local): the pair acts on slices [z0, z0 + nz_local) of the volume
+    (z-slab sharding; f32 Joseph operators)."""
     geom.validate()
     canon = ConeGeometry(geom.mode, geom.source_to_origin, geom.origin_to_detector, geom.detector_pixel_size,
                          geom.nu, geom.nv, geom.vol, [canonical_angle(a) for a in geom.angles])
     proj = Projector(canon, projector, bp_partitions)
+    shape = canon.vol
+    if slab is not None:
+        proj.set_slab(*slab)
+        shape = VolumeShape(canon.vol.nx, canon.vol.ny, int(slab[1]), canon.vol.spacing)
     v = BackprojectVariant(variant)
-    return OperatorPair(proj.domain_size, proj.range_size, v == BackprojectVariant.matched, canon.vol,
+    return OperatorPair(proj.domain_size, proj.range_size, v == BackprojectVariant.matched, shape,
                         lambda x, y: proj.forward(x, y), lambda y, x: proj.back(y, x, v), np.dtype(dtype), proj, v)
 
 

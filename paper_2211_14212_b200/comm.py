@@ -25,6 +25,14 @@ def shard_angles(n_angles: int, nranks: int, rank: int):
     return f.value, c.value
 
 
+def shard_slabs(nz: int, nranks: int, rank: int):
+    """Contiguous z-slab [z0, z0 + count) of `rank` (z-slab sharding)."""
+    lib = L.load()
+    z, c = C.c_int(), C.c_int()
+    _check(lib.ctk_shard_slabs(nz, nranks, rank, C.byref(z), C.byref(c)))
+    return z.value, c.value
+
+
 class NcclComm:
     def __init__(self, rank: int, nranks: int, group=None):
         import torch
@@ -99,8 +107,16 @@ class TorchComm:
             if self.device != "cpu":
                 import torch
 
-                torch.cuda.current_stream().synchronize()
+                # the library's kernels ran on `stream`: finish them before reducing
+                if stream:
+                    torch.cuda.ExternalStream(stream).synchronize()
+                else:
+                    torch.cuda.synchronize()
             dist.all_reduce(t, group=self.group)
+            if self.device != "cpu" and dist.get_backend(self.group) != "nccl":
+                import torch
+
+                torch.cuda.synchronize()  # host-staged (gloo) result visible before the next kernel
             return 0
         except Exception:  # surfaced by the library as CTK_E_CUDA
             return 1

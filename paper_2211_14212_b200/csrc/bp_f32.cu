@@ -104,7 +104,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
     for (int q = t; q < 4 * ((g.nv + 3) >> 2); q += BP_PB) vdtab[q] = float(row_coord(g, q));
-    const float czf = 0.5f * float(g.nz - 1);
+    const float czf = 0.5f * float(g.nzg - 1);  // global z centre; this handle's slices start at z0
+    const int kg0 = k0 + g.z0;                   // global index of the band's first slice
     const float cvf = 0.5f * float(g.nv - 1);
     const float invdu = float(1.0 / g.du);
     const float fs = float(s);
@@ -154,8 +155,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         int v0 = 0, v1 = g.nv - 1;
                         if (gs > 0.f) {
                             const float rg = invdu / gs;
-                            v0 = max(v0, int(floorf(fmaf(float(k0) - 1.f - czf, rg, cvf))) - 1);
-                            v1 = min(v1, int(ceilf(fmaf(float(k0 + BP_KB) - czf, rg, cvf))) + 1);
+                            v0 = max(v0, int(floorf(fmaf(float(kg0) - 1.f - czf, rg, cvf))) - 1);
+                            v1 = min(v1, int(ceilf(fmaf(float(kg0 + BP_KB) - czf, rg, cvf))) + 1);
                         }
                         if (g.has_zrays) {
                             // rows whose ray is z-dominant (|v| > |d_A|) belong to the generic
@@ -190,7 +191,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 int kf, kfi;
                                 float tf;
                                 split(fmaf(vdtab[v0], gs, czf), kfi, tf);
-                                kf = kfi - k0;
+                                kf = kfi - kg0;
                                 zero_rows(0, kf);
                             } else {
                                 zero_rows(0, BP_KB);
@@ -200,7 +201,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             auto step = [&](float vd, float yv) {
                                 const float fz = fmaf(vd, gs, czf);
                                 const float tt = split_t(fz);
-                                const int kk = __float_as_int(tt) - (kSplitBias + k0);
+                                const int kk = __float_as_int(tt) - (kSplitBias + kg0);
                                 const float tz = split_frac(fz, tt);
                                 const float w0 = (1.f - tz) * yv, w1 = tz * yv;
                                 const int adv = kk - cur;
@@ -272,7 +273,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 int iz;
                                 float tz;
                                 split(fmaf(vdtab[iv], gs, czf), iz, tz);
-                                const int kk = iz - k0;
+                                const int kk = iz - kg0;
                                 if (unsigned(kk) < unsigned(BP_KB)) zc[kk * BP_PB] = fmaf(1.f - tz, yv, zc[kk * BP_PB]);
                                 if (unsigned(kk + 1) < unsigned(BP_KB)) zc[(kk + 1) * BP_PB] = fmaf(tz, yv, zc[(kk + 1) * BP_PB]);
                             }
@@ -352,7 +353,8 @@ __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, f
     if (id >= nvox) return;
     const int i = int(id % g.nx), j = int((id / g.nx) % g.ny), k = int(id / (size_t(g.nx) * g.ny));
     const double h = g.h;
-    const double xc = (i - 0.5 * (g.nx - 1)) * h, yc = (j - 0.5 * (g.ny - 1)) * h, zc = (k - 0.5 * (g.nz - 1)) * h;
+    const int kg = k + g.z0;  // global slice
+    const double xc = (i - 0.5 * (g.nx - 1)) * h, yc = (j - 0.5 * (g.ny - 1)) * h, zc = (kg - 0.5 * (g.nzg - 1)) * h;
     float acc = 0.f;
     for (int a = 0; a < g.na; ++a) {
         const double2 tr = g.ctst[a];
@@ -385,7 +387,7 @@ __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, f
                 WalkF w;
                 walk_generic(g, tr.x, tr.y, iu, iv, w);
                 // axis is z: slice k, b = x (i), c = y (j)
-                const float fs = float(k);
+                const float fs = float(kg);
                 const float fb = fmaf(fs, w.fbd, w.fb0), fc = fmaf(fs, w.fcd, w.fc0);
                 const float fib = floorf(fb), fic = floorf(fc);
                 const int ib = int(fib), ic = int(fic);
@@ -420,7 +422,7 @@ k_atb_voxel_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
 #pragma unroll
     for (int m = 0; m < KZ; ++m) {
         const int k = kb + lane + 32 * m;
-        zk[m] = float((k - 0.5 * (g.nz - 1)) * g.h);
+        zk[m] = float((k + g.z0 - 0.5 * (g.nzg - 1)) * g.h);
         acc[m] = 0.f;
     }
     for (int a = 0; a < g.na; ++a) {
@@ -511,7 +513,7 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int nh = CLASS ? g.nx : g.ny;
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
-    const int kbands = (g.nz + BP_KB - 1) / BP_KB;
+    const int kbands = (g.nz_local() + BP_KB - 1) / BP_KB;
     const size_t smem = sizeof(float) * (size_t(BP_PB) * (BP_KB + 2 * BP_ZG) + size_t(BP_PB) * BP_SL + 2 * BP_PB +
                                          ((size_t(g.nv) + 3) & ~size_t(3))) +
                         sizeof(int2) * g.na;
@@ -528,7 +530,7 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
 
 template <int KZ>
 void launch_voxel(Geometry& g, float* x, cudaStream_t s) {
-    const int kblocks = (g.nz + 32 * KZ - 1) / (32 * KZ);
+    const int kblocks = (g.nz_local() + 32 * KZ - 1) / (32 * KZ);
     const long warps = long(g.nx) * g.ny * kblocks;
     dim3 blk(32, 4);
     const unsigned grd = unsigned((warps + 3) / 4);
@@ -554,7 +556,7 @@ void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
 void atb_voxel_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
     transpose_proj(g, y, s);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    switch (pick_kz(g.nz)) {
+    switch (pick_kz(g.nz_local())) {
         case 1: launch_voxel<1>(g, x, s); break;
         case 2: launch_voxel<2>(g, x, s); break;
         case 4: launch_voxel<4>(g, x, s); break;

@@ -163,6 +163,23 @@ int ctk_geom_set_projector(ctk_geom* g, int p) {
         G(g).projector = p;
     });
 }
+int ctk_geom_set_slab(ctk_geom* g, int z0, int nz_local) {
+    return guard([&] {
+        auto& gg = G(g);
+        if (nz_local == 0) {
+            gg.slab = false;
+            gg.z0 = 0;
+            gg.nzl = 0;
+        } else {
+            if (z0 < 0 || nz_local < 1 || z0 + nz_local > gg.nz) ctkb::fail(CTK_E_PARAMETER, "slab outside the volume");
+            gg.slab = true;
+            gg.z0 = z0;
+            gg.nzl = nz_local;
+        }
+        gg.vx.release();  // padded relayouts depend on the slab height
+        gg.vy.release();
+    });
+}
 int ctk_geom_set_bp_partitions(ctk_geom* g, int n) {
     return guard([&] {
         if (n < 1) ctkb::fail(CTK_E_PARAMETER, "partitions must be >= 1");
@@ -333,6 +350,9 @@ int ctk_projected_tikhonov(const double* H, int k, double beta1, double lambda, 
     });
 }
 
+int ctk_shard_slabs(int nz, int nranks, int rank, int* z0, int* count) {
+    return ctk_shard_angles(nz, nranks, rank, z0, count);  // the same contiguous block partition
+}
 int ctk_shard_angles(int n_angles, int nranks, int rank, int* first, int* count) {
     return guard([&] {
         if (n_angles < 1 || nranks < 1 || rank < 0 || rank >= nranks) ctkb::fail(CTK_E_PARAMETER, "invalid sharding");

@@ -49,6 +49,7 @@ struct DevBuf {
 // ---- kernel-side geometry (passed by value) --------------------------------------------
 struct KGeom {
     int mode, nu, nv, nx, ny, nz, na;
+    int nzg, z0;                  // z-slab: the handle holds slices [z0, z0 + nz) of nzg
     int has_zrays;
     double dso, dod, du, h;
     const double2* ctst;          // per view (cos, sin), host libm values
@@ -70,6 +71,9 @@ struct Geometry {
     bool has_zrays = false;      // any cone ray with |d_z| dominant
     int projector = CTK_PROJ_JOSEPH;
     int bp_parts = 1;
+    // z-slab sharding: domain vectors hold slices [z0, z0 + nzl) of nz
+    bool slab = false;
+    int z0 = 0, nzl = 0;
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -86,7 +90,8 @@ struct Geometry {
     double* pinned = nullptr;  // host-side reduction results
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
-    size_t domain() const { return size_t(nx) * ny * nz; }
+    size_t domain() const { return size_t(nx) * ny * (slab ? nzl : nz); }
+    int nz_local() const { return slab ? nzl : nz; }
     size_t range() const { return size_t(na) * nu * nv; }
     KGeom kgeom() const;
     void require_angles() const;
@@ -174,12 +179,16 @@ void finish_sum(const double* partials, int n, double* d_out, cudaStream_t s);
 void finish_max(const double* partials, int n, double* d_out, cudaStream_t s);
 
 // gradient / TV stencils (stencils.cu)
+// z-slab halos: x_above = the next rank's first slice (null: this slab ends the volume);
+// gzw_below = the previous rank's last slice of (lam w .* gz); has_above = not the last slab
 template <class T>  // out{x,y,z} = scale[i] * (D x)_axis ; scale may be null (=1)
-void gradient_scaled(int nx, int ny, int nz, const T* x, const T* scale, double lam, T* gx, T* gy, T* gz, cudaStream_t s);
+void gradient_scaled(int nx, int ny, int nz, const T* x, const T* scale, double lam, T* gx, T* gy, T* gz, cudaStream_t s,
+                     const T* x_above = nullptr);
 template <class T>  // out += D^T (lam * w .* g)
-void gradient_adjoint_scaled_add(int nx, int ny, int nz, const T* gx, const T* gy, const T* gz, const T* w, double lam, T* out, cudaStream_t s);
+void gradient_adjoint_scaled_add(int nx, int ny, int nz, const T* gx, const T* gy, const T* gz, const T* w, double lam,
+                                 T* out, cudaStream_t s, const T* gzw_below = nullptr, bool has_above = false);
 template <class T>  // w = (|Dx|^2 + eps^2)^(-1/4)
-void tv_weights(int nx, int ny, int nz, const T* x, double eps, T* w, cudaStream_t s);
+void tv_weights(int nx, int ny, int nz, const T* x, double eps, T* w, cudaStream_t s, const T* x_above = nullptr);
 
 // ---- communicator ----------------------------------------------------------------------
 struct Comm {

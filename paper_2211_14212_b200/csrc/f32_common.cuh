@@ -74,7 +74,7 @@ __device__ void walk_generic(const KGeom& g, double ct, double st, int iu, int i
     double adm = ad0;
     if (ad1 > adm) { axis = 1; adm = ad1; }
     if (ad2 > adm) { axis = 2; adm = ad2; }
-    const int n3[3] = {g.nx, g.ny, g.nz};
+    const int n3[3] = {g.nx, g.ny, g.nzg};  // global geometry; a slab is applied in the march
     const int s3[3] = {1, g.nx, g.nx * g.ny};
     const int b = axis == 2 ? 0 : axis + 1, c = axis == 0 ? 2 : axis - 1;
     const double h = g.h;
@@ -94,8 +94,9 @@ __device__ void walk_generic(const KGeom& g, double ct, double st, int iu, int i
     w.fcd = float(dt * d[c] / h);
 }
 
+// z-rays only (axis 2): slices are global z, restricted to the handle's slab
 __device__ float march_generic(const KGeom& g, const WalkF& w, const float* __restrict__ vol) {
-    int s0 = 0, s1 = w.ns - 1;
+    int s0 = g.z0, s1 = g.z0 + g.nz - 1;
     clip_affine(w.fb0, w.fbd, -1.0, w.nb, s0, s1);
     clip_affine(w.fc0, w.fcd, -1.0, w.nc, s0, s1);
     float acc = 0.f;
@@ -105,7 +106,7 @@ __device__ float march_generic(const KGeom& g, const WalkF& w, const float* __re
         const float fib = floorf(fb), fic = floorf(fc);
         const int ib = int(fib), ic = int(fic);
         const float tb = fb - fib, tc = fc - fic;
-        const float* p = vol + size_t(s) * w.sa;
+        const float* p = vol + size_t(s - g.z0) * w.sa;
         const bool b0 = ib >= 0 && ib < w.nb, b1 = ib + 1 >= 0 && ib + 1 < w.nb;
         const bool c0 = ic >= 0 && ic < w.nc, c1 = ic + 1 >= 0 && ic + 1 < w.nc;
         const float v00 = (b0 && c0) ? __ldg(p + ib * w.sb + ic * w.sc) : 0.f;

@@ -93,7 +93,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             const Off plane = pz * Off(nh + 2);
             const float* base = (A ? wy : wx) + pz + 1;  // tap (h, z) of slice s at base[s*plane + h*pz + z]
             const float vd = float(v);
-            const float czf = 0.5f * float(g.nz - 1);
+            const float czf = 0.5f * float(g.nzg - 1);  // global z centre; slab slices start at z0
             const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
             // a sample contributes iff some tap is inside the volume: ih in [-1, nh-1] and
             // iz in [-1, nz-1].  ih(s) and iz(s) are monotone in s (monotone roundings of
@@ -105,11 +105,11 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                 float th, tz;
                 split(fmaf(fs, cd.y, cd.x), ih, th);
                 split(fmaf(vd, fmaf(fs, cd.w, cd.z), czf), iz, tz);
-                return unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
+                return unsigned(ih + 1) <= unh && unsigned(iz - g.z0 + 1) <= unz;
             };
             int s0 = 0, s1 = ns - 1;
             clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
-            clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
+            clip_affine(double(vd) * cd.z + czf - g.z0, double(vd) * cd.w, -1.0, g.nz, s0, s1);
             while (s0 <= s1 && !inside(s0)) ++s0;
             while (s1 >= s0 && !inside(s1)) --s1;
             if (s0 <= s1) {
@@ -122,7 +122,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             // (modular) arithmetic, so a sample costs one IMAD and no float->int conversion.
             using U = typename std::conditional<sizeof(Off) == 4, unsigned, unsigned long long>::type;
             const U upz = U(pz), uplane = U(plane);
-            U sb = U(s0) * uplane - U(kSplitBias) * (upz + 1u);
+            U sb = U(s0) * uplane - U(kSplitBias) * (upz + 1u) - U(unsigned(g.z0));
             // tap row ih+1; opaque so each tap row costs one IMAD.WIDE rather than a
             // sign-extended 64-bit add chain on (off + pz)
             const float* base1 = opaque_ptr(base + pz);
@@ -172,19 +172,19 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
 }
 
 void relayout_zfast(Geometry& g, const float* x, DevBuf& wx, DevBuf& wy, cudaStream_t s) {
-    const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz) + 2);
-    const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz) + 2);
+    const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz_local()) + 2);
+    const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz_local()) + 2);
     if (wx.ensure(nwx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(wx.p, 0, nwx * sizeof(float), s));
     if (wy.ensure(nwy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(wy.p, 0, nwy * sizeof(float), s));
-    dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.nz + 31) / 32, g.ny);
-    k_relayout_zfast<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, wx.as<float>(), wy.as<float>());
+    dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.nz_local() + 31) / 32, g.ny);
+    k_relayout_zfast<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz_local(), x, wx.as<float>(), wy.as<float>());
     after_launch("k_relayout_zfast");
 }
 
 dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + ZW_BC - 1) / ZW_BC, g.na, (g.nv + ZW_BR - 1) / ZW_BR); }
 
 bool wide_offsets(const Geometry& g) {
-    const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz + 2);
+    const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz_local() + 2);
     return mx >= 2147483000.0;
 }
 

@@ -41,7 +41,9 @@ KGeom Geometry::kgeom() const {
     k.nv = nv;
     k.nx = nx;
     k.ny = ny;
-    k.nz = nz;
+    k.nz = nz_local();
+    k.nzg = nz;
+    k.z0 = slab ? z0 : 0;
     k.na = na;
     k.has_zrays = has_zrays ? 1 : 0;
     k.dso = dso;

@@ -5,8 +5,16 @@
 
 namespace ctkb {
 
+// z-slab sharding is implemented for the f32 Joseph operators (the C5 path of SURVEY.md 8(d))
+template <class T>
+void require_slab_support(const Geometry& g) {
+    if (g.slab && (sizeof(T) != 4 || g.projector != CTK_PROJ_JOSEPH))
+        fail(CTK_E_UNSUPPORTED, "z-slab sharding is implemented for the f32 Joseph operators only");
+}
+
 template <class T>
 void op_ax(Geometry& g, const T* x, T* y, cudaStream_t s) {
+    require_slab_support<T>(g);
     if (g.projector == CTK_PROJ_SIDDON) {
         CTK_CUDA(cudaEventRecord(g.ev0, s));
         siddon_ax<T>(g, x, y, s);
@@ -23,6 +31,7 @@ void op_ax(Geometry& g, const T* x, T* y, cudaStream_t s) {
 template <class T>
 void op_atb(Geometry& g, int variant, const T* y, T* x, cudaStream_t s) {
     if (variant != CTK_BP_MATCHED && variant != CTK_BP_VOXEL_DRIVEN) fail(CTK_E_PARAMETER, "unknown backprojector variant");
+    require_slab_support<T>(g);
     if (variant == CTK_BP_MATCHED && g.projector == CTK_PROJ_SIDDON) {
         CTK_CUDA(cudaEventRecord(g.ev0, s));
         siddon_atb<T>(g, y, x, s);

@@ -7,9 +7,15 @@
 //   lsqr               solvers.hpp:62-126       lsmr         solvers.hpp:128-231
 //   hybrid_lsqr        hybrid.hpp:76-116 (gk_init/gk_expand krylov.hpp:50-92, cgs2 :21-31)
 //   cgls_tv            tv.hpp:45-110 (stack_weighted_gradient operators.hpp:141-186)
-// With a communicator attached (angle sharding), range vectors are this rank's angle
-// block: range reductions are summed over ranks in rank order and every A^T b partial
-// volume is sum-reduced, so all ranks hold identical domain vectors.
+// With a communicator attached the vectors of one space are sharded and the other is
+// replicated:
+//   angle sharding  range vectors are this rank's angle block; range reductions are summed
+//                   over ranks in rank order and every A^T b partial volume is sum-reduced,
+//                   so all ranks hold identical domain vectors;
+//   z-slab          domain vectors are this rank's slab of z-slices; domain reductions are
+//                   summed in rank order and every A x partial projection set is
+//                   sum-reduced (by linearity A x = sum_r A x_r), so all ranks hold
+//                   identical range vectors; the TV stencils exchange one-slice halos.
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -51,40 +57,83 @@ struct Dev {
 
     Dev(Geometry& g_, int v) : g(g_), variant(v), s(g_.stream), w(red_work(&g_)) {}
 
-    void ax(const T* x, T* y) { op_ax<T>(g, x, y, s); }
+    bool slab_mode() const { return g.comm && g.slab; }
+    // are vectors of this space split across ranks (their reductions summed)?
+    bool sharded(bool range) const { return g.comm && (g.slab ? !range : range); }
+    void ax(const T* x, T* y) {
+        op_ax<T>(g, x, y, s);
+        if (slab_mode()) comm_allreduce(g.comm, y, g.range(), sizeof(T) == 8 ? 1 : 0, s);
+    }
     void atb(const T* y, T* x) {
         op_atb<T>(g, variant, y, x, s);
-        if (g.comm) comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
+        if (g.comm && !g.slab) comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
     }
     double fetch(int slot) {
         CTK_CUDA(cudaMemcpyAsync(g.pinned + slot, w.results + slot, sizeof(double), cudaMemcpyDeviceToHost, s));
         CTK_CUDA(cudaStreamSynchronize(s));
         return g.pinned[slot];
     }
-    double range_sum(double v) { return g.comm ? comm_sum_scalar(g.comm, v) : v; }
+    double part_sum(double v, bool range) { return sharded(range) ? comm_sum_scalar(g.comm, v) : v; }
+    double domain_max(double v) { return sharded(false) ? comm_max_scalar(g.comm, v) : v; }
+
+    // ---- one-slice halos of z-slab sharding (gradient.hpp:19-21 and its transpose) ----
+    // Every rank's chosen slice is gathered by a sum-allreduce of a zeroed [nranks][nx*ny]
+    // buffer in which each rank fills only its own row: one nonzero term per entry, exact.
+    DevBuf halo;
+    bool last_slab() const { return g.comm->cb.rank == g.comm->cb.nranks - 1; }
+    const T* gather_slices(const T* slice) {
+        const size_t S = size_t(g.nx) * g.ny, R = size_t(g.comm->cb.nranks);
+        halo.ensure(sizeof(T) * S * R);
+        fill<T>(S * R, T(0), halo.as<T>(), s);
+        CTK_CUDA(cudaMemcpyAsync(halo.as<T>() + size_t(g.comm->cb.rank) * S, slice, sizeof(T) * S,
+                                 cudaMemcpyDeviceToDevice, s));
+        comm_allreduce(g.comm, halo.p, S * R, sizeof(T) == 8 ? 1 : 0, s);
+        return halo.as<T>();
+    }
+    // the next rank's first slice of x (null when unsharded or on the last slab)
+    const T* slice_above(const T* x) {
+        if (!slab_mode()) return nullptr;
+        const T* all = gather_slices(x);
+        return last_slab() ? nullptr : all + size_t(g.comm->cb.rank + 1) * size_t(g.nx) * g.ny;
+    }
+    // the previous rank's last slice of lam * w .* gz (null when unsharded or on the first slab)
+    Vec<T> wtop;
+    const T* weighted_slice_below(const T* gz, const T* wts, double lam) {
+        if (!slab_mode()) return nullptr;
+        const size_t S = size_t(g.nx) * g.ny, top = size_t(g.nz_local() - 1) * S;
+        if (!wtop.p) wtop.alloc(S);
+        if (wts) {
+            scale_copy<T>(S, lam, wts + top, wtop.p, s);  // sc = lam * w   (operators.hpp:176-181)
+            mul<T>(S, wtop.p, gz + top, wtop.p, s);
+        } else {
+            CTK_CUDA(cudaMemcpyAsync(wtop.p, gz + top, sizeof(T) * S, cudaMemcpyDeviceToDevice, s));
+        }
+        const T* all = gather_slices(wtop.p);
+        return g.comm->cb.rank == 0 ? nullptr : all + size_t(g.comm->cb.rank - 1) * S;
+    }
 
     double nrm2sq(const T* x, size_t n, bool range) {
         reduce_dot<T>(n, x, x, w.results, w, s);
         const double v = fetch(0);
-        return range ? range_sum(v) : v;
+        return part_sum(v, range);
     }
     double diff_nrm2sq(const T* a, const T* b, size_t n, bool range) {
         reduce_diff_nrm2sq<T>(n, a, b, w.results, w, s);
         const double v = fetch(0);
-        return range ? range_sum(v) : v;
+        return part_sum(v, range);
     }
     // y += alpha x, returns ||y||^2
     double axpy_n2(double alpha, const T* x, T* y, size_t n, bool range) {
         axpy_nrm2sq<T>(n, alpha, x, y, w.results, w, s);
         const double v = fetch(0);
-        return range ? range_sum(v) : v;
+        return part_sum(v, range);
     }
     // ||A x - b||^2 over all ranks (solve_log.hpp:111-115), never storing A x in T=float
     double resid2(const T* x, const T* b) {
         if constexpr (sizeof(T) == 4) {
-            if (g.projector == CTK_PROJ_JOSEPH) {
+            if (g.projector == CTK_PROJ_JOSEPH && !slab_mode()) {
                 ax_residual_f32(g, x, b, w.results, s);
-                return range_sum(fetch(0));
+                return part_sum(fetch(0), true);
             }
         }
         {
@@ -350,7 +399,7 @@ template <class T>
 void cgs2(Dev<T>& d, const T* basis, size_t ld, int m, T* wv, size_t n, bool range, double* d_coef, double* scratch) {
     for (int pass = 0; pass < 2; ++pass) {
         block_dot<T>(n, m, basis, ld, wv, d_coef, scratch, d.s);
-        if (range && d.g.comm) {
+        if (d.sharded(range)) {
             std::vector<double> c(static_cast<size_t>(m));
             CTK_CUDA(cudaMemcpyAsync(c.data(), d_coef, sizeof(double) * m, cudaMemcpyDeviceToHost, d.s));
             CTK_CUDA(cudaStreamSynchronize(d.s));
@@ -463,11 +512,14 @@ struct Stacked {
     size_t nd, nr;
     void fwd(const T* x, T* y) {
         d.ax(x, y);
-        gradient_scaled<T>(d.g.nx, d.g.ny, d.g.nz, x, w, lam, y + nr, y + nr + nd, y + nr + 2 * nd, d.s);
+        const T* above = d.slice_above(x);
+        gradient_scaled<T>(d.g.nx, d.g.ny, d.g.nz_local(), x, w, lam, y + nr, y + nr + nd, y + nr + 2 * nd, d.s, above);
     }
     void back(const T* y, T* x) {
         d.atb(y, x);
-        gradient_adjoint_scaled_add<T>(d.g.nx, d.g.ny, d.g.nz, y + nr, y + nr + nd, y + nr + 2 * nd, w, lam, x, d.s);
+        const T* below = d.weighted_slice_below(y + nr + 2 * nd, w, lam);
+        gradient_adjoint_scaled_add<T>(d.g.nx, d.g.ny, d.g.nz_local(), y + nr, y + nr + nd, y + nr + 2 * nd, w, lam, x,
+                                       d.s, below, d.slab_mode() && !d.last_slab());
     }
     // squared norm of a stacked vector: sharded range part + replicated gradient part
     double n2(const T* y) { return d.nrm2sq(y, nr, true) + d.nrm2sq(y + nr, 3 * nd, false); }
@@ -492,8 +544,8 @@ void cgls_tv(Dev<T>& d, const T* b, double lambda, int outer_iters, int inner_it
     for (int outer = 0; outer < outer_iters && !stopped; ++outer) {
         // tv_weights (tv.hpp:28-43): eps = 1e-4 max|x|
         reduce_absmax<T>(nd, x, d.w.results, d.w, d.s);
-        const double eps = 1e-4 * d.fetch(0);
-        tv_weights<T>(g.nx, g.ny, g.nz, x, eps, wts.p, d.s);
+        const double eps = 1e-4 * d.domain_max(d.fetch(0));
+        tv_weights<T>(g.nx, g.ny, g.nz_local(), x, eps, wts.p, d.s, d.slice_above(x));
         Stacked<T> K{d, wts.p, lambda, nd, nr};
         // rhs = [b; 0]
         if (log->outer_starts) log->outer_starts[log->n_outer_starts++] = k;
@@ -554,7 +606,7 @@ void sirt(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
     auto inverse_weights = [&](T* w, size_t n, bool range) {
         reduce_absmax<T>(n, w, d.w.results, d.w, d.s);
         double wmax = d.fetch(0);
-        if (range && g.comm) wmax = comm_max_scalar(g.comm, wmax);
+        if (d.sharded(range)) wmax = comm_max_scalar(g.comm, wmax);
         if (!(T(wmax) > T(0))) fail(CTK_E_DEGENERATE, "sirt: operator maps ones to zero");
         inv_floor<T>(n, double(T(1e-6) * T(wmax)), w, d.s);
     };
@@ -574,7 +626,7 @@ void sirt(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
         add_mul<T>(nd, col_inv.p, corr.p, x, d.s);
         d.ax(x, ax.p);
         sub_nrm2sq<T>(nr, b, ax.p, r.p, d.w.results, d.w, d.s);
-        const double expl = std::sqrt(d.range_sum(d.fetch(0))) / mon.bnorm;
+        const double expl = std::sqrt(d.part_sum(d.fetch(0), true)) / mon.bnorm;
         if (mon.record(k, x, expl, false, 0.0, &expl)) break;
     }
     mon.finish(k);
@@ -628,7 +680,7 @@ void abba_gmres(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve
         for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, in order
             reduce_dot<T>(n, Wi(i), w, d.w.results, d.w, d.s);
             double hi = d.fetch(0);
-            if (ab) hi = d.range_sum(hi);
+            hi = d.part_sum(hi, ab);
             h[size_t(i)] = double(T(hi));
             axpy<T>(n, -h[size_t(i)], Wi(i), w, d.s);
         }
@@ -636,7 +688,7 @@ void abba_gmres(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve
             for (int i = 0; i <= j; ++i) {
                 reduce_dot<T>(n, Wi(i), w, d.w.results, d.w, d.s);
                 double c = d.fetch(0);
-                if (ab) c = d.range_sum(c);
+                c = d.part_sum(c, ab);
                 c = double(T(c));
                 axpy<T>(n, -c, Wi(i), w, d.s);
                 h[size_t(i)] = double(T(h[size_t(i)]) + T(c));

@@ -16,7 +16,8 @@ __device__ __forceinline__ void unpack(size_t id, int nx, int ny, int& i, int& j
 
 template <class T>
 __global__ void k_gradient_scaled(int nx, int ny, int nz, const T* __restrict__ x, const T* __restrict__ w, T lam,
-                                  T* __restrict__ gx, T* __restrict__ gy, T* __restrict__ gz) {
+                                  T* __restrict__ gx, T* __restrict__ gy, T* __restrict__ gz,
+                                  const T* __restrict__ x_above) {
     const size_t n = size_t(nx) * ny * nz;
     for (size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x; id < n; id += size_t(gridDim.x) * blockDim.x) {
         int i, j, k;
@@ -24,7 +25,9 @@ __global__ void k_gradient_scaled(int nx, int ny, int nz, const T* __restrict__ 
         const T v = x[id];
         const T dx = (i + 1 < nx) ? x[id + 1] - v : T(0);
         const T dy = (j + 1 < ny) ? x[id + nx] - v : T(0);
-        const T dz = (k + 1 < nz) ? x[id + size_t(nx) * ny] - v : T(0);
+        // z-slab: the top slice differences against the next rank's first slice
+        const T dz = (k + 1 < nz) ? x[id + size_t(nx) * ny] - v
+                                  : (x_above ? x_above[size_t(i) + size_t(nx) * j] - v : T(0));
         const T s = w ? lam * w[id] : T(1);  // stack_weighted_gradient: s = lam * w_i (operators.hpp:167)
         gx[id] = s * dx;
         gy[id] = s * dy;
@@ -34,7 +37,8 @@ __global__ void k_gradient_scaled(int nx, int ny, int nz, const T* __restrict__ 
 
 template <class T>
 __global__ void k_gradient_adjoint_add(int nx, int ny, int nz, const T* __restrict__ gx, const T* __restrict__ gy,
-                                       const T* __restrict__ gz, const T* __restrict__ w, T lam, T* __restrict__ out) {
+                                       const T* __restrict__ gz, const T* __restrict__ w, T lam, T* __restrict__ out,
+                                       const T* __restrict__ gzw_below, int has_above) {
     const size_t n = size_t(nx) * ny * nz;
     const size_t sy = size_t(nx), sz = size_t(nx) * ny;
     for (size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x; id < n; id += size_t(gridDim.x) * blockDim.x) {
@@ -47,14 +51,18 @@ __global__ void k_gradient_adjoint_add(int nx, int ny, int nz, const T* __restri
         if (i + 1 < nx) acc -= sc(id) * gx[id];
         if (j > 0) acc += sc(id - sy) * gy[id - sy];
         if (j + 1 < ny) acc -= sc(id) * gy[id];
+        // z-slab: the previous rank's top-slice term (already weighted) and this rank's top
+        // slice, whose difference exists unless this is the last slab
         if (k > 0) acc += sc(id - sz) * gz[id - sz];
-        if (k + 1 < nz) acc -= sc(id) * gz[id];
+        else if (gzw_below) acc += gzw_below[size_t(i) + size_t(nx) * j];
+        if (k + 1 < nz || has_above) acc -= sc(id) * gz[id];
         out[id] += acc;
     }
 }
 
 template <class T>
-__global__ void k_tv_weights(int nx, int ny, int nz, const T* __restrict__ x, double eps, T* __restrict__ w) {
+__global__ void k_tv_weights(int nx, int ny, int nz, const T* __restrict__ x, double eps, T* __restrict__ w,
+                             const T* __restrict__ x_above) {
     const size_t n = size_t(nx) * ny * nz;
     for (size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x; id < n; id += size_t(gridDim.x) * blockDim.x) {
         if (eps == 0.0) {
@@ -66,7 +74,8 @@ __global__ void k_tv_weights(int nx, int ny, int nz, const T* __restrict__ x, do
         const T v = x[id];
         const T dx = (i + 1 < nx) ? x[id + 1] - v : T(0);
         const T dy = (j + 1 < ny) ? x[id + nx] - v : T(0);
-        const T dz = (k + 1 < nz) ? x[id + size_t(nx) * ny] - v : T(0);
+        const T dz = (k + 1 < nz) ? x[id + size_t(nx) * ny] - v
+                                  : (x_above ? x_above[size_t(i) + size_t(nx) * j] - v : T(0));
         const double m2 = double(dx) * dx + double(dy) * dy + double(dz) * dz;
         w[id] = T(pow(m2 + eps * eps, -0.25));
     }
@@ -137,30 +146,36 @@ void launch_shepp_logan_f32(int n, float* out, cudaStream_t s) { shepp_logan<flo
 void launch_shepp_logan_f64(int n, double* out, cudaStream_t s) { shepp_logan<double>(n, out, s); }
 
 template <class T>
-void gradient_scaled(int nx, int ny, int nz, const T* x, const T* scale, double lam, T* gx, T* gy, T* gz, cudaStream_t s) {
+void gradient_scaled(int nx, int ny, int nz, const T* x, const T* scale, double lam, T* gx, T* gy, T* gz, cudaStream_t s,
+                     const T* x_above) {
     const size_t n = size_t(nx) * ny * nz;
-    k_gradient_scaled<T><<<unsigned(grid_for(n)), 256, 0, s>>>(nx, ny, nz, x, scale, T(lam), gx, gy, gz);
+    k_gradient_scaled<T><<<unsigned(grid_for(n)), 256, 0, s>>>(nx, ny, nz, x, scale, T(lam), gx, gy, gz, x_above);
     after_launch("k_gradient_scaled");
 }
 template <class T>
 void gradient_adjoint_scaled_add(int nx, int ny, int nz, const T* gx, const T* gy, const T* gz, const T* w, double lam,
-                                 T* out, cudaStream_t s) {
+                                 T* out, cudaStream_t s, const T* gzw_below, bool has_above) {
     const size_t n = size_t(nx) * ny * nz;
-    k_gradient_adjoint_add<T><<<unsigned(grid_for(n)), 256, 0, s>>>(nx, ny, nz, gx, gy, gz, w, T(lam), out);
+    k_gradient_adjoint_add<T><<<unsigned(grid_for(n)), 256, 0, s>>>(nx, ny, nz, gx, gy, gz, w, T(lam), out, gzw_below,
+                                                                     has_above ? 1 : 0);
     after_launch("k_gradient_adjoint_add");
 }
 template <class T>
-void tv_weights(int nx, int ny, int nz, const T* x, double eps, T* w, cudaStream_t s) {
+void tv_weights(int nx, int ny, int nz, const T* x, double eps, T* w, cudaStream_t s, const T* x_above) {
     const size_t n = size_t(nx) * ny * nz;
-    k_tv_weights<T><<<unsigned(grid_for(n)), 256, 0, s>>>(nx, ny, nz, x, eps, w);
+    k_tv_weights<T><<<unsigned(grid_for(n)), 256, 0, s>>>(nx, ny, nz, x, eps, w, x_above);
     after_launch("k_tv_weights");
 }
 
-template void gradient_scaled<float>(int, int, int, const float*, const float*, double, float*, float*, float*, cudaStream_t);
-template void gradient_scaled<double>(int, int, int, const double*, const double*, double, double*, double*, double*, cudaStream_t);
-template void gradient_adjoint_scaled_add<float>(int, int, int, const float*, const float*, const float*, const float*, double, float*, cudaStream_t);
-template void gradient_adjoint_scaled_add<double>(int, int, int, const double*, const double*, const double*, const double*, double, double*, cudaStream_t);
-template void tv_weights<float>(int, int, int, const float*, double, float*, cudaStream_t);
-template void tv_weights<double>(int, int, int, const double*, double, double*, cudaStream_t);
+template void gradient_scaled<float>(int, int, int, const float*, const float*, double, float*, float*, float*, cudaStream_t,
+                                     const float*);
+template void gradient_scaled<double>(int, int, int, const double*, const double*, double, double*, double*, double*,
+                                      cudaStream_t, const double*);
+template void gradient_adjoint_scaled_add<float>(int, int, int, const float*, const float*, const float*, const float*,
+                                                 double, float*, cudaStream_t, const float*, bool);
+template void gradient_adjoint_scaled_add<double>(int, int, int, const double*, const double*, const double*,
+                                                  const double*, double, double*, cudaStream_t, const double*, bool);
+template void tv_weights<float>(int, int, int, const float*, double, float*, cudaStream_t, const float*);
+template void tv_weights<double>(int, int, int, const double*, double, double*, cudaStream_t, const double*);
 
 }  // namespace ctkb

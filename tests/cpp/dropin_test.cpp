@@ -3,13 +3,15 @@
 // (needs /root/reference at compile time only); run by tests/test_gpu_dropin.py.
 //  1. ctkb::projector_pair<double> is bit-identical to ctk::projector_pair<double>.
 //  2. The reference's own CPU lsqr accepts the B200 pair (OperatorPair compatibility).
-//  3. The device-resident ctkb::lsqr / lsmr / cgls match the reference solvers.
+//  3. The device-resident ctkb::lsqr / lsmr / cgls / sirt / ab_gmres / ba_gmres match the
+//     reference solvers (gmres.hpp compiled against the test-only Eigen shim).
 //  4. Errors come back as the reference's exception types.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
 
+#include "ctkrylov/gmres.hpp"
 #include "ctkrylov/operators.hpp"
 #include "ctkrylov/phantom.hpp"
 #include "ctkrylov/solvers.hpp"
@@ -67,6 +69,18 @@ int main() {
     const auto c_ref = ctk::cgls(ref, ctk::cspan(b), opts);
     const auto c_dev = ctkb::cgls(b200, ctk::cspan(b), opts);
     EXPECT(rel(c_dev.x, c_ref.x) < 1e-10);
+    const auto s_ref = ctk::sirt(ref, ctk::cspan(b), opts);
+    const auto s_dev = ctkb::sirt(b200, ctk::cspan(b), opts);
+    EXPECT(rel(s_dev.x, s_ref.x) < 1e-10);
+    EXPECT(s_dev.log.lambda.empty());
+    const auto ab_ref = ctk::ab_gmres(ref, ctk::cspan(b), opts);
+    const auto ab_dev = ctkb::ab_gmres(b200, ctk::cspan(b), opts);
+    EXPECT(rel(ab_dev.x, ab_ref.x) < 1e-9);
+    EXPECT(ab_dev.stored_range_basis == ab_ref.stored_range_basis);
+    const auto ba_ref = ctk::ba_gmres(ref, ctk::cspan(b), opts);
+    const auto ba_dev = ctkb::ba_gmres(b200, ctk::cspan(b), opts);
+    EXPECT(rel(ba_dev.x, ba_ref.x) < 1e-9);
+    EXPECT(ba_dev.stored_domain_basis == ba_ref.stored_domain_basis);
 
     // f32 pair through the same API
     auto b32 = ctkb::projector_pair<float>(g);
