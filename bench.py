@@ -42,6 +42,8 @@ def parse():
     p.add_argument("--angles", type=int, default=360)
     p.add_argument("--iters", type=int, default=50)
     p.add_argument("--lam", type=float, default=30.0)
+    p.add_argument("--shard", default="angle", choices=["angle", "slab"],
+                   help="multi-GPU partition (SURVEY.md 8(e)): angle blocks (C3/C4) or z-slabs (C5)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work for the cpu_baseline sample")
     return p.parse_args()
@@ -211,7 +213,7 @@ def main():
     import torch
 
     import paper_2211_14212_b200 as ctk
-    from paper_2211_14212_b200.comm import NcclComm, shard_angles
+    from paper_2211_14212_b200.comm import NcclComm, shard_angles, shard_slabs
 
     torch.cuda.set_device(local)
     dist = None
@@ -221,19 +223,25 @@ def main():
         dist.init_process_group("nccl")
     n, na = args.n, args.angles
     full = ctk.bench_geometry(n, na)
-    first, count = shard_angles(na, world, rank)
-    geom = full.subset(first, count)
-    pair = ctk.projector_pair(geom)
+    # synthetic inputs, resident in HBM: phantom rasterised on the device, b = A x
+    x_true = ctk.shepp_logan_3d(n)
+    if args.shard == "slab":
+        # z-slab: this rank's slices of x; b (replicated) from the whole-volume operator (setup)
+        z0, nzl = shard_slabs(n, world, rank)
+        b = torch.empty(ctk.projector_pair(full).range_size, dtype=torch.float32, device="cuda")
+        ctk.projector_pair(full).forward(x_true, b)
+        x_true = x_true[z0 * n * n:(z0 + nzl) * n * n].contiguous()
+        pair = ctk.projector_pair(full, slab=(z0, nzl))
+    else:
+        first, count = shard_angles(na, world, rank)
+        pair = ctk.projector_pair(full.subset(first, count))
+        b = torch.empty(pair.range_size, dtype=torch.float32, device="cuda")
+        pair.forward(x_true, b)
     proj = pair.projector
     comm = None
     if world > 1:
         comm = NcclComm(rank, world)
         proj.attach_comm(comm)
-
-    # synthetic inputs, resident in HBM: phantom rasterised on the device, b = A x
-    x_true = ctk.shepp_logan_3d(n)
-    b = torch.empty(pair.range_size, dtype=torch.float32, device="cuda")
-    pair.forward(x_true, b)
     torch.cuda.synchronize()
     opts = ctk.SolverOptions(max_iters=args.iters, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
 
@@ -305,8 +313,11 @@ def main():
     e2e_value = args.iters * e2e_steps / e2e_s
 
     hbm_peak, sm_mhz, peak_src = peaks()
-    nvox, nproj = n ** 3, count * n * n
-    samples = count * n * n * n  # Gray-voxel normaliser (rays x slices)
+    # this rank's share of the work: its angle block (angle) or its slab of slices (slab)
+    my_angles = count if args.shard == "angle" else na
+    my_slices = n if args.shard == "angle" else nzl
+    nvox, nproj = n * n * my_slices, my_angles * n * n
+    samples = my_angles * n * n * my_slices  # Gray-voxel normaliser (rays x slices)
     ax_gvox = 1e-9 * samples / (t_ax / 1e3)
     bt_gvox = 1e-9 * samples / (t_bt / 1e3)
     alg_bytes = 4.0 * (nvox + nproj)
@@ -330,7 +341,7 @@ def main():
         "data": "synthetic: Shepp-Logan 3D rasterised on device (phantom.hpp), b = A x (GPU Ax)",
         "config": {"workload": f"LSMR lambda={args.lam}, {args.iters} iters/step, {n}^3 volume, {n}^2 detector, "
                                f"{na} angles, cone DSO=2n DOD=n pixel 1.5, matched Joseph (BASELINE config 3)",
-                   "parallelism": f"angle-sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"{args.shard}-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (volume 512 MiB, projections 360 MiB)"},
         "ax_gvox_s": ax_gvox,
         "atb_gvox_s": bt_gvox,
