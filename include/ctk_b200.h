@@ -153,6 +153,11 @@ typedef struct {
     int stop_reason;    /* ctk_stop_reason */
     int stored_domain_basis;
     int stored_range_basis;
+    /* SolveResult::warnings (solve_log.hpp:69): flsqr_tv records the iterations whose inner
+     * CG did not converge ("tv preconditioner: inner CG not converged at iteration k",
+     * tv.hpp:170-172).  Caller-allocated, `capacity` entries, may be NULL. */
+    int* warning_iterations;
+    int n_warnings;
 } ctk_solve_log;
 
 /* HybridStrategy, hybrid.hpp:15-33 */
@@ -180,10 +185,14 @@ int ctk_ab_gmres_f32(ctk_geom* g, int variant, const float* h_b, const ctk_solve
 int ctk_ab_gmres_f64(ctk_geom* g, int variant, const double* h_b, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
 int ctk_ba_gmres_f32(ctk_geom* g, int variant, const float* h_b, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
 int ctk_ba_gmres_f64(ctk_geom* g, int variant, const double* h_b, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
+/* flsqr_tv (tv.hpp:177-185): flexible hybrid LSQR with the TV priorconditioner; the
+ * strategy must be fixed or gcv (dp -> CTK_E_PARAMETER, as in hybrid.hpp:135-136). */
+int ctk_flsqr_tv_f32(ctk_geom* g, int variant, const float* h_b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, float* h_x, ctk_solve_log* log);
+int ctk_flsqr_tv_f64(ctk_geom* g, int variant, const double* h_b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, double* h_x, ctk_solve_log* log);
 
 /* Device-resident variants: b and x are DEVICE pointers; identical semantics.
  * solver: 0 cgls, 1 lsqr, 2 lsmr, 3 hybrid_lsqr, 4 cgls_tv, 5 sirt, 6 ab_gmres,
- * 7 ba_gmres.  `lambda` is the LSMR
+ * 7 ba_gmres, 8 flsqr_tv (reads `s`).  `lambda` is the LSMR
  * damping / TV weight; hybrid reads `s`; cgls_tv reads outer/inner/warm_start. */
 int ctk_solve_dev_f32(ctk_geom* g, int solver, int variant, const float* d_b, double lambda,
                       const ctk_hybrid_strategy* s, int outer_iters, int inner_iters, int warm_start,

@@ -88,6 +88,7 @@ struct Ops<float> {
     static int ba_gmres(ctk_geom* g, int v, const float* b, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_ba_gmres_f32(g, v, b, o, x, l); }
     static int lsmr(ctk_geom* g, int v, const float* b, double lam, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_lsmr_f32(g, v, b, lam, o, x, l); }
     static int hybrid(ctk_geom* g, int v, const float* b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_hybrid_lsqr_f32(g, v, b, s, o, x, l); }
+    static int flsqr_tv(ctk_geom* g, int v, const float* b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, float* x, ctk_solve_log* l) { return ctk_flsqr_tv_f32(g, v, b, s, o, x, l); }
     static int tv(ctk_geom* g, int v, const float* b, double lam, int oi, int ii, const ctk_solver_opts* o, int w, float* x, ctk_solve_log* l) { return ctk_cgls_tv_f32(g, v, b, lam, oi, ii, o, w, x, l); }
 };
 template <>
@@ -101,6 +102,7 @@ struct Ops<double> {
     static int ba_gmres(ctk_geom* g, int v, const double* b, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_ba_gmres_f64(g, v, b, o, x, l); }
     static int lsmr(ctk_geom* g, int v, const double* b, double lam, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_lsmr_f64(g, v, b, lam, o, x, l); }
     static int hybrid(ctk_geom* g, int v, const double* b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_hybrid_lsqr_f64(g, v, b, s, o, x, l); }
+    static int flsqr_tv(ctk_geom* g, int v, const double* b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o, double* x, ctk_solve_log* l) { return ctk_flsqr_tv_f64(g, v, b, s, o, x, l); }
     static int tv(ctk_geom* g, int v, const double* b, double lam, int oi, int ii, const ctk_solver_opts* o, int w, double* x, ctk_solve_log* l) { return ctk_cgls_tv_f64(g, v, b, lam, oi, ii, o, w, x, l); }
 };
 
@@ -139,7 +141,7 @@ namespace detail {
 template <class T>
 struct Call {
     std::vector<double> impl, expl, err, lam;
-    std::vector<int> outer;
+    std::vector<int> outer, warn;
     std::vector<T> gt;
     ctk_solve_log log{};
     ctk_solver_opts o{};
@@ -151,12 +153,14 @@ struct Call {
         err.resize(size_t(cap));
         lam.resize(size_t(cap));
         outer.resize(size_t(outer_cap) + 1);
+        warn.resize(size_t(cap) + 1);
         log.capacity = cap;
         log.implicit_residual = impl.data();
         log.explicit_residual = expl.data();
         log.relative_error = err.data();
         log.lambda = lam.data();
         log.outer_starts = outer.data();
+        log.warning_iterations = warn.data();
         o.max_iters = so.max_iters;
         o.stop_on_explicit_residual_increase = so.stop_on_explicit_residual_increase;
         o.residual_tolerance = so.residual_tolerance;
@@ -189,6 +193,8 @@ struct Call {
         r.outer_starts.assign(outer.begin(), outer.begin() + log.n_outer_starts);
         r.stored_domain_basis = log.stored_domain_basis;
         r.stored_range_basis = log.stored_range_basis;
+        for (int i = 0; i < log.n_warnings; ++i)
+            r.warnings.push_back("tv preconditioner: inner CG not converged at iteration " + std::to_string(warn[size_t(i)]));
         return r;
     }
 };
@@ -265,6 +271,18 @@ ctk::SolveResult<T> hybrid_lsqr(const B200Pair<T>& pair, std::span<const T> b, c
     const ctk_hybrid_strategy cs{int(s.kind), s.lambda, s.noise_level};
     check(Ops<T>::hybrid(pair.native->get(), pair.variant, b.data(), &cs, &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "hybrid_lsqr");
+}
+/// flsqr_tv (tv.hpp:177-185); Strategy as for hybrid_lsqr (fixed or gcv)
+template <class T, class Strategy>
+ctk::SolveResult<T> flsqr_tv(const B200Pair<T>& pair, std::span<const T> b, const Strategy& s,
+                             const ctk::SolverOptions<T>& opts) {
+    opts.validate();
+    pair.check_range(b.size());
+    detail::Call<T> c(opts, opts.max_iters, 1);
+    std::vector<T> x(pair.domain_size);
+    const ctk_hybrid_strategy cs{int(s.kind), s.lambda, s.noise_level};
+    check(Ops<T>::flsqr_tv(pair.native->get(), pair.variant, b.data(), &cs, &c.o, x.data(), &c.log));
+    return c.result(std::move(x), pair, "flsqr_tv");
 }
 template <class T>
 ctk::SolveResult<T> cgls_tv(const B200Pair<T>& pair, std::span<const T> b, double lambda, int outer_iters,

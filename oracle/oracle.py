@@ -218,6 +218,8 @@ class _RefLog(C.Structure):
         ("n_outer_starts", C.c_int),
         ("stored_domain_basis", C.c_int),
         ("stored_range_basis", C.c_int),
+        ("warning_iterations", C.POINTER(C.c_int)),
+        ("n_warnings", C.c_int),
     ]
 
 
@@ -228,7 +230,8 @@ class RefError(RuntimeError):
         self.iteration = iteration
 
 
-SOLVERS = {"cgls": 0, "lsqr": 1, "lsmr": 2, "sirt": 3, "hybrid_lsqr": 4, "cgls_tv": 5, "ab_gmres": 6, "ba_gmres": 7}
+SOLVERS = {"cgls": 0, "lsqr": 1, "lsmr": 2, "sirt": 3, "hybrid_lsqr": 4, "cgls_tv": 5, "ab_gmres": 6, "ba_gmres": 7,
+           "flsqr_tv": 8}
 
 
 class Reference:
@@ -277,8 +280,9 @@ class Reference:
         cap = max(max_iters, outer * inner) + 2
         bufs = [np.zeros(cap) for _ in range(4)]
         outer_buf = np.zeros(outer + 2, dtype=np.int32)
+        warn_buf = np.zeros(cap, dtype=np.int32)
         log = _RefLog(*[_ptr(t, C.c_double) for t in bufs], 0, 0, 0, 0, 0, 0,
-                      _ptr(outer_buf, C.c_int), 0, 0, 0)
+                      _ptr(outer_buf, C.c_int), 0, 0, 0, _ptr(warn_buf, C.c_int), 0)
         x = np.zeros(g.domain_size, dtype=dt)
         gs = g.cstruct()
         gt_p = None
@@ -304,6 +308,7 @@ class Reference:
             "outer_starts": outer_buf[: log.n_outer_starts].copy(),
             "stored_domain_basis": log.stored_domain_basis,
             "stored_range_basis": log.stored_range_basis,
+            "warning_iterations": warn_buf[: log.n_warnings].copy(),
         }
 
     def phantom(self, kind, n, dtype=np.float64):
@@ -775,6 +780,115 @@ def hybrid_lsqr(fwd, back, b, max_iters, strategy="gcv", lam=0.0, nl=0.0, tol=1e
             mon.reason = "breakdown"
             break
     return mon.result(x, k, stored_domain_basis=len(V), stored_range_basis=len(U))
+
+
+def flsqr_tv(fwd, back, b, shape, max_iters, restated: Restated, strategy="gcv", lam=0.0, tol=1e-6, stop_inc=True,
+             gt=None, reorth=True, bd=1e-14, max_inner=50, inner_tol=1e-6):
+    """flsqr_tv (tv.hpp:112-185) = flexible_hybrid_lsqr (hybrid.hpp:118-168) with the TV
+    priorconditioner: flexible GK (krylov.hpp:147-224), z_j = CG solve of
+    (D^T diag(w^2) D + tau^2 I) z = v_j from zero (tau = 1e-3 lambda0), w = tv_weights(x)."""
+    # dots accumulate sequentially like the reference's dot() (types.hpp:137-142): the
+    # truncated inner CG amplifies summation-order differences (see DESIGN.md §2)
+    def sdot(a, b):
+        return float(np.cumsum(a * b)[-1]) if a.size else 0.0
+
+    def snrm(a):
+        return math.sqrt(sdot(a, a))
+
+    lambda0 = lam if strategy == "fixed" and lam > 0.0 else 1.0
+    tau2 = (1e-3 * lambda0) ** 2
+    mon = Monitor(fwd, b, max_iters, tol, stop_inc, gt)
+    beta1 = snrm(b)
+    tolb = bd * beta1
+    U = [b / beta1]
+    v = back(U[0])
+    V = [v / snrm(v)]
+    Z, mcols, warnings = [], [], []
+    x = np.zeros_like(V[0])
+
+    def mgs(basis, w, coef=None):
+        for i, q in enumerate(basis):
+            c = sdot(q, w)
+            w = w - c * q
+            if coef is not None:
+                coef[i] += c
+        return w
+
+    k = 0
+    while k < max_iters:
+        w2 = restated.tv_weights(shape, x) ** 2
+
+        def apply(p):
+            dx, dy, dz = restated.gradient(shape, p)
+            return restated.gradient_adjoint(shape, w2 * dx, w2 * dy, w2 * dz) + tau2 * p
+
+        j = len(mcols)
+        z = np.zeros_like(x)
+        r = V[j].copy()
+        p = r.copy()
+        rr = sdot(r, r)
+        target = inner_tol * math.sqrt(rr)
+        conv = not math.sqrt(rr) > 0
+        for _ in range(max_inner):
+            if conv:
+                break
+            ap = apply(p)
+            pap = sdot(p, ap)
+            if not pap > 0:
+                break
+            alpha = rr / pap
+            z = z + alpha * p
+            r = r - alpha * ap
+            rr_new = sdot(r, r)
+            if math.sqrt(rr_new) <= target:
+                conv = True
+                break
+            beta = rr_new / rr
+            rr = rr_new
+            p = r + beta * p
+        if not conv:
+            warnings.append(k + 1)
+        status = "ok"
+        if not snrm(z) > 0:
+            status = "breakdown"
+        else:
+            w = fwd(z)
+            m = np.zeros(j + 2)
+            w = mgs(U, w, m)
+            if reorth:
+                w = mgs(U, w, m)
+            mnext = snrm(w)
+            m[j + 1] = mnext
+            Z.append(z)
+            mcols.append(m)
+            if mnext <= tolb:
+                status = "breakdown"
+            else:
+                U.append(w / mnext)
+                vn = back(U[-1])
+                for _ in range(2 if reorth else 1):
+                    vn = mgs(V, vn)
+                nv = snrm(vn)
+                if nv <= tolb:
+                    status = "breakdown"
+                else:
+                    V.append(vn / nv)
+        if status == "breakdown" and len(mcols) < k + 1:
+            mon.reason = "breakdown"
+            break
+        k += 1
+        M = np.zeros((k + 1, k))
+        for c, col in enumerate(mcols):
+            M[: min(len(col), k + 1), c] = col[: k + 1]
+        lam_k = lam if strategy == "fixed" else math.sqrt(max(0.0, gcv_lambda(M, beta1)))
+        y, fit = projected_tikhonov(M, beta1, lam_k)
+        x = sum(float(y[i]) * Z[i] for i in range(len(y)))
+        if mon.record(k, x, fit / beta1, lam_k):
+            break
+        if status == "breakdown":
+            mon.reason = "breakdown"
+            break
+    return mon.result(x, k, stored_domain_basis=len(Z), stored_range_basis=len(U), warnings=warnings)
 
 
 def cgls_tv(fwd, back, b, shape, lam, outer, inner, restated: Restated, tol=1e-6, stop_inc=True,

@@ -6,7 +6,9 @@
 // the C restatement (oracle/ctk_oracle.c) and as the CPU baseline ("kind": "reference").
 // No reference source is copied here; the reference is #included from where it lies.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 #include <exception>
 #include <vector>
 
@@ -52,6 +54,8 @@ struct ref_log {
     int n_outer_starts;
     int stored_domain_basis;
     int stored_range_basis;
+    int* warning_iterations;  // SolveResult::warnings: the trailing iteration number of each
+    int n_warnings;
 };
 
 }  // extern "C"
@@ -135,9 +139,15 @@ void fill_log(const ctk::SolveResult<T>& r, ref_log* log) {
         for (std::size_t i = 0; i < r.outer_starts.size(); ++i) log->outer_starts[i] = r.outer_starts[i];
     log->stored_domain_basis = r.stored_domain_basis;
     log->stored_range_basis = r.stored_range_basis;
+    log->n_warnings = int(r.warnings.size());
+    if (log->warning_iterations)
+        for (std::size_t i = 0; i < r.warnings.size(); ++i) {
+            const std::string& w = r.warnings[i];
+            log->warning_iterations[i] = std::atoi(w.c_str() + w.find_last_of(' ') + 1);
+        }
 }
 
-// solver: 0 cgls, 1 lsqr, 2 lsmr, 3 sirt, 4 hybrid_lsqr, 5 cgls_tv, 6 ab_gmres, 7 ba_gmres
+// solver: 0 cgls, 1 lsqr, 2 lsmr, 3 sirt, 4 hybrid_lsqr, 5 cgls_tv, 6 ab_gmres, 7 ba_gmres, 8 flsqr_tv
 template <typename T>
 int solve_impl(const ref_geom* d, int variant, int solver, double lambda, int strategy,
                double noise_level, int outer, int inner, int warm, const T* b, int max_iters,
@@ -171,6 +181,11 @@ int solve_impl(const ref_geom* d, int variant, int solver, double lambda, int st
             case 5: r = ctk::cgls_tv(pair, bs, lambda, outer, inner, opts, warm != 0); break;
             case 6: r = ctk::ab_gmres(pair, bs, opts); break;
             case 7: r = ctk::ba_gmres(pair, bs, opts); break;
+            case 8: {
+                ctk::HybridStrategy s = strategy == 0 ? ctk::HybridStrategy::fixed(lambda) : ctk::HybridStrategy::gcv();
+                r = ctk::flsqr_tv(pair, bs, s, opts);
+                break;
+            }
 #endif
             default: throw ctk::ParameterError("solver not available in this build");
         }

@@ -33,6 +33,7 @@ from .api import (  # noqa: F401
     cgls_tv,
     default_geometry,
     equidistant_angles,
+    flsqr_tv,
     forward_project,
     hybrid_lsqr,
     launch_count,

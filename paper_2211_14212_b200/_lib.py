@@ -64,6 +64,8 @@ class SolveLog(C.Structure):
         ("stop_reason", C.c_int),
         ("stored_domain_basis", C.c_int),
         ("stored_range_basis", C.c_int),
+        ("warning_iterations", C.POINTER(C.c_int)),
+        ("n_warnings", C.c_int),
     ]
 
 
@@ -150,6 +152,7 @@ def load():
             sig[f"ctk_{nm}_{t}"] = (i, [vp, i, vp, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
         sig[f"ctk_lsmr_{t}"] = (i, [vp, i, vp, d, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
         sig[f"ctk_hybrid_lsqr_{t}"] = (i, [vp, i, vp, C.POINTER(HybridStrategyC), C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
+        sig[f"ctk_flsqr_tv_{t}"] = (i, [vp, i, vp, C.POINTER(HybridStrategyC), C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)])
         sig[f"ctk_cgls_tv_{t}"] = (i, [vp, i, vp, d, i, i, C.POINTER(SolverOpts), i, vp, C.POINTER(SolveLog)])
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

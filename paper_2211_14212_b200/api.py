@@ -471,7 +471,7 @@ class HybridStrategy:
 
 
 _SOLVER_ID = {"cgls": 0, "lsqr": 1, "lsmr": 2, "hybrid_lsqr": 3, "cgls_tv": 4, "sirt": 5, "ab_gmres": 6,
-              "ba_gmres": 7}
+              "ba_gmres": 7, "flsqr_tv": 8}
 
 
 def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=None, outer=1, inner=1, warm=False):
@@ -488,8 +488,10 @@ def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=N
     cap = outer * inner if name == "cgls_tv" else opts.max_iters
     bufs = [np.zeros(cap + 1) for _ in range(4)]
     starts = np.zeros(outer + 1, dtype=np.int32)
+    wits = np.zeros(cap + 1, dtype=np.int32)
     log = L.SolveLog(cap, *[a.ctypes.data_as(C.POINTER(C.c_double)) for a in bufs],
-                     starts.ctypes.data_as(C.POINTER(C.c_int)), 0, 0, 0, 0, 0, 0, 0, 0)
+                     starts.ctypes.data_as(C.POINTER(C.c_int)), 0, 0, 0, 0, 0, 0, 0, 0,
+                     wits.ctypes.data_as(C.POINTER(C.c_int)), 0)
     gt = None
     if opts.ground_truth is not None:
         gt = np.ascontiguousarray(np.asarray(opts.ground_truth), dtype=ndt).reshape(-1)
@@ -524,8 +526,8 @@ def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=N
             rc = getattr(lib, f"ctk_{name}_{t}")(proj.handle, v, bp, C.byref(o), xp, C.byref(log))
         elif name == "lsmr":
             rc = getattr(lib, f"ctk_lsmr_{t}")(proj.handle, v, bp, lam, C.byref(o), xp, C.byref(log))
-        elif name == "hybrid_lsqr":
-            rc = getattr(lib, f"ctk_hybrid_lsqr_{t}")(proj.handle, v, bp, C.byref(st), C.byref(o), xp, C.byref(log))
+        elif name in ("hybrid_lsqr", "flsqr_tv"):
+            rc = getattr(lib, f"ctk_{name}_{t}")(proj.handle, v, bp, C.byref(st), C.byref(o), xp, C.byref(log))
         else:
             rc = getattr(lib, f"ctk_cgls_tv_{t}")(proj.handle, v, bp, lam, outer, inner, C.byref(o), int(warm), xp,
                                                    C.byref(log))
@@ -533,8 +535,9 @@ def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=N
     it = log.iterations
     clog = ConvergenceLog(list(bufs[0][:it]), list(bufs[1][:it]), list(bufs[2][:log.n_relative_error]),
                           list(bufs[3][:log.n_lambda]), name, "single" if t == "f32" else "double", pair.matched)
+    warnings = [f"tv preconditioner: inner CG not converged at iteration {int(k)}" for k in wits[:log.n_warnings]]
     return SolveResult(x, pair.domain_shape, log.iterations_run, StopReason(log.stop_reason), clog,
-                       list(starts[:log.n_outer_starts]), log.stored_domain_basis, log.stored_range_basis)
+                       list(starts[:log.n_outer_starts]), log.stored_domain_basis, log.stored_range_basis, warnings)
 
 
 def cgls(pair: OperatorPair, b, opts: SolverOptions) -> SolveResult:
@@ -573,6 +576,13 @@ def lsmr(pair: OperatorPair, b, lambda_: float, opts: SolverOptions) -> SolveRes
 def hybrid_lsqr(pair: OperatorPair, b, strategy: HybridStrategy, opts: SolverOptions) -> SolveResult:
     """hybrid.hpp:76-116."""
     return _solve("hybrid_lsqr", pair, b, opts, strategy=strategy)
+
+
+def flsqr_tv(pair: OperatorPair, b, strategy: HybridStrategy, opts: SolverOptions) -> SolveResult:
+    """tv.hpp:177-185: flexible hybrid LSQR with the TV priorconditioner (fixed or gcv)."""
+    if strategy.kind == LambdaStrategy.dp:
+        raise ParameterError("flsqr_tv: dp strategy is not supported, use fixed or gcv")
+    return _solve("flsqr_tv", pair, b, opts, strategy=strategy)
 
 
 def cgls_tv(pair: OperatorPair, b, lambda_: float, outer_iters: int, inner_iters: int, opts: SolverOptions,

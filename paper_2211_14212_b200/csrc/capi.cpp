@@ -312,6 +312,14 @@ int ctk_hybrid_lsqr_f64(ctk_geom* g, int variant, const double* b, const ctk_hyb
                         const ctk_solver_opts* o, double* x, ctk_solve_log* log) {
     return guard([&] { solve_host<double>(G(g), 3, variant, b, 0.0, s, 1, 1, 0, o, x, log); });
 }
+int ctk_flsqr_tv_f32(ctk_geom* g, int variant, const float* b, const ctk_hybrid_strategy* s, const ctk_solver_opts* o,
+                     float* x, ctk_solve_log* log) {
+    return guard([&] { solve_host<float>(G(g), 8, variant, b, 0.0, s, 1, 1, 0, o, x, log); });
+}
+int ctk_flsqr_tv_f64(ctk_geom* g, int variant, const double* b, const ctk_hybrid_strategy* s,
+                     const ctk_solver_opts* o, double* x, ctk_solve_log* log) {
+    return guard([&] { solve_host<double>(G(g), 8, variant, b, 0.0, s, 1, 1, 0, o, x, log); });
+}
 int ctk_cgls_tv_f32(ctk_geom* g, int variant, const float* b, double lambda, int outer, int inner,
                     const ctk_solver_opts* o, int warm, float* x, ctk_solve_log* log) {
     return guard([&] { solve_host<float>(G(g), 4, variant, b, lambda, nullptr, outer, inner, warm, o, x, log); });

@@ -166,7 +166,7 @@ struct Monitor {
             gt_norm = std::sqrt(d.nrm2sq(gt.p, d.g.domain(), false));
             if (!(gt_norm > 0.0)) fail(CTK_E_DEGENERATE, "ground truth has zero norm");
         }
-        log->iterations = log->n_relative_error = log->n_lambda = 0;
+        log->iterations = log->n_relative_error = log->n_lambda = log->n_warnings = 0;
     }
 
     // IterationMonitor::record; returns true when the solver should stop.  expl_override:
@@ -591,7 +591,7 @@ template <class T>
 void sirt(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* log) {
     Geometry& g = d.g;
     const size_t nd = g.domain(), nr = g.range();
-    log->iterations = log->n_relative_error = log->n_lambda = 0;
+    log->iterations = log->n_relative_error = log->n_lambda = log->n_warnings = 0;
     if (!(std::sqrt(d.nrm2sq(b, nr, true)) > 0.0)) {
         // zero data: x = 0 is already the fixed point (solvers.hpp:240-251)
         fill<T>(nd, T(0), x, d.s);
@@ -726,6 +726,163 @@ void abba_gmres(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve
     log->stored_range_basis = ab ? nbasis : 0;
 }
 
+// Flexible hybrid LSQR with TV priorconditioning (hybrid.hpp:118-168, tv.hpp:112-185,
+// krylov.hpp:147-224): flexible Golub-Kahan A Z_k = U_{k+1} M_k where z_j = P_j v_j and P_j
+// is an inner CG solve of (D^T diag(w^2) D + tau^2 I) z = v with IRN weights w from the
+// current iterate (tau = 1e-3 lambda0, <= 50 CG steps to 1e-6); modified Gram-Schmidt
+// (+ a classical pass when reorth) on U, full re-orthogonalisation of V; projected
+// Tikhonov on the (k+1) x k Hessenberg M with lambda fixed or by GCV; x = Z_k y.
+template <class T>
+void flsqr_tv(Dev<T>& d, const T* b, const ctk_hybrid_strategy& strat, const ctk_solver_opts& o, T* x,
+              ctk_solve_log* log) {
+    Geometry& g = d.g;
+    const size_t nd = g.domain(), nr = g.range();
+    if (strat.kind == CTK_LAMBDA_DP) fail(CTK_E_PARAMETER, "flsqr_tv: dp strategy is not supported, use fixed or gcv");
+    if (strat.kind != CTK_LAMBDA_FIXED && strat.kind != CTK_LAMBDA_GCV) fail(CTK_E_PARAMETER, "unknown lambda strategy");
+    if (strat.kind == CTK_LAMBDA_FIXED && strat.lambda < 0.0) fail(CTK_E_PARAMETER, "fixed lambda must be nonnegative");
+    const double lambda0 = strat.kind == CTK_LAMBDA_FIXED && strat.lambda > 0.0 ? strat.lambda : 1.0;
+    const double tau = 1e-3 * lambda0;
+    const T tau2 = T(tau * tau);
+    constexpr int kMaxInner = 50;
+    constexpr double kInnerTol = 1e-6;
+    Monitor<T> mon(d, b, o, log, "flsqr_tv");
+    log->n_warnings = 0;
+    const int cap = o.max_iters + 2;
+    DevBuf Ub, Vb, Zb, coefb;
+    Ub.ensure(sizeof(T) * nr * size_t(cap));
+    Vb.ensure(sizeof(T) * nd * size_t(cap));
+    Zb.ensure(sizeof(T) * nd * size_t(cap));
+    coefb.ensure(sizeof(double) * size_t(cap));
+    auto Ui = [&](int i) { return Ub.as<T>() + size_t(i) * nr; };
+    auto Vi = [&](int i) { return Vb.as<T>() + size_t(i) * nd; };
+    auto Zi = [&](int i) { return Zb.as<T>() + size_t(i) * nd; };
+    Vec<T> w2, r, p, ap, gx, gy, gz;
+    w2.alloc(nd); r.alloc(nd); p.alloc(nd); ap.alloc(nd); gx.alloc(nd); gy.alloc(nd); gz.alloc(nd);
+    // flexible_gk_init (krylov.hpp:161-177)
+    const double beta1 = mon.bnorm;
+    const double tol = breakdown_factor<T>() * beta1;
+    scale_copy<T>(nr, 1.0 / beta1, b, Ui(0), d.s);
+    d.atb(Ui(0), Vi(0));
+    const double nv0 = std::sqrt(d.nrm2sq(Vi(0), nd, false));
+    if (!(nv0 > 0.0)) fail(CTK_E_DEGENERATE, "flexible_gk_init: B u_1 vanished");
+    scal<T>(nd, 1.0 / nv0, Vi(0), d.s);
+    int nu_ = 1, nv_ = 1, nz_ = 0;
+    std::vector<std::vector<double>> mcols;
+    fill<T>(nd, T(0), x, d.s);
+    // the TV operator D^T diag(w^2) D + tau^2 I of the preconditioner (tv.hpp:134-143)
+    auto apply_tv = [&](const T* in, T* out) {
+        scale_copy<T>(nd, double(tau2), in, out, d.s);
+        gradient_scaled<T>(g.nx, g.ny, g.nz_local(), in, w2.p, 1.0, gx.p, gy.p, gz.p, d.s, d.slice_above(in));
+        const T* below = d.weighted_slice_below(gz.p, nullptr, 1.0);
+        gradient_adjoint_scaled_add<T>(g.nx, g.ny, g.nz_local(), gx.p, gy.p, gz.p, nullptr, 1.0, out, d.s, below,
+                                       d.slab_mode() && !d.last_slab());
+    };
+    // inner CG from zero on the SPD system (tv.hpp:145-168); returns false if not converged
+    auto precond = [&](const T* v, T* z) {
+        fill<T>(nd, T(0), z, d.s);
+        CTK_CUDA(cudaMemcpyAsync(r.p, v, sizeof(T) * nd, cudaMemcpyDeviceToDevice, d.s));
+        CTK_CUDA(cudaMemcpyAsync(p.p, v, sizeof(T) * nd, cudaMemcpyDeviceToDevice, d.s));
+        double rr = d.nrm2sq(r.p, nd, false);
+        const double target = kInnerTol * std::sqrt(rr);
+        bool converged = !(std::sqrt(rr) > 0.0);
+        for (int it = 0; it < kMaxInner && !converged; ++it) {
+            apply_tv(p.p, ap.p);
+            reduce_dot<T>(nd, p.p, ap.p, d.w.results, d.w, d.s);
+            const double pap = d.part_sum(d.fetch(0), false);
+            if (!(pap > 0.0)) break;
+            const double alpha = rr / pap;
+            axpy<T>(nd, alpha, p.p, z, d.s);
+            const double rr_new = d.axpy_n2(-alpha, ap.p, r.p, nd, false);
+            if (std::sqrt(rr_new) <= target) {
+                converged = true;
+                break;
+            }
+            const double beta = rr_new / rr;
+            rr = rr_new;
+            xpby<T>(nd, r.p, beta, p.p, d.s);
+        }
+        return converged;
+    };
+    // modified Gram-Schmidt of w against the first m vectors of a basis, in order
+    auto mgs = [&](auto basis, int m, T* wv, size_t n, bool range, std::vector<double>* coef) {
+        for (int i = 0; i < m; ++i) {
+            reduce_dot<T>(n, basis(i), wv, d.w.results, d.w, d.s);
+            const double c = double(T(d.part_sum(d.fetch(0), range)));
+            axpy<T>(n, -c, basis(i), wv, d.s);
+            if (coef) (*coef)[size_t(i)] = double(T((*coef)[size_t(i)]) + T(c));
+        }
+    };
+    int k = 0;
+    while (k < o.max_iters) {
+        // the preconditioner of iteration k+1, from the current iterate: w^2 of tv_weights
+        reduce_absmax<T>(nd, x, d.w.results, d.w, d.s);
+        const double eps = 1e-4 * d.domain_max(d.fetch(0));
+        tv_weights<T>(g.nx, g.ny, g.nz_local(), x, eps, w2.p, d.s, d.slice_above(x));
+        mul<T>(nd, w2.p, w2.p, w2.p, d.s);
+        // flexible_gk_expand (krylov.hpp:179-223)
+        bool breakdown = false;
+        {
+            const int j = int(mcols.size());
+            T* z = Zi(j);
+            if (!precond(Vi(j), z) && log->warning_iterations && log->n_warnings < log->capacity)
+                log->warning_iterations[log->n_warnings++] = k + 1;
+            if (!(std::sqrt(d.nrm2sq(z, nd, false)) > 0.0)) {
+                breakdown = true;
+            } else {
+                T* wv = Ui(nu_);
+                d.ax(z, wv);
+                std::vector<double> m(size_t(j + 2), 0.0);
+                mgs(Ui, j + 1, wv, nr, true, &m);
+                if (o.reorth) mgs(Ui, j + 1, wv, nr, true, &m);
+                const double mnext = double(T(std::sqrt(d.nrm2sq(wv, nr, true))));
+                m[size_t(j + 1)] = mnext;
+                ++nz_;
+                mcols.push_back(m);
+                if (mnext <= tol) {
+                    breakdown = true;
+                } else {
+                    scal<T>(nr, 1.0 / mnext, wv, d.s);
+                    ++nu_;
+                    T* v = Vi(nv_);
+                    d.atb(wv, v);
+                    for (int pass = 0; pass < (o.reorth ? 2 : 1); ++pass) mgs(Vi, nv_, v, nd, false, nullptr);
+                    const double nvn = std::sqrt(d.nrm2sq(v, nd, false));
+                    if (nvn <= tol) {
+                        breakdown = true;
+                    } else {
+                        scal<T>(nd, 1.0 / nvn, v, d.s);
+                        ++nv_;
+                    }
+                }
+            }
+        }
+        if (breakdown && int(mcols.size()) < k + 1) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            break;
+        }
+        ++k;
+        std::vector<double> M(size_t(k + 1) * k, 0.0);
+        for (int c = 0; c < k; ++c)
+            for (int rr = 0; rr < int(mcols[size_t(c)].size()) && rr <= k; ++rr)
+                M[size_t(rr) * k + c] = mcols[size_t(c)][size_t(rr)];
+        const double lambda_k = choose_lambda(strat, M, k, beta1);
+        double fit = 0.0;
+        const std::vector<double> y = projected_tikhonov(M, k, beta1, lambda_k, &fit);
+        CTK_CUDA(cudaMemcpyAsync(coefb.p, y.data(), sizeof(double) * y.size(), cudaMemcpyHostToDevice, d.s));
+        fill<T>(nd, T(0), x, d.s);
+        block_axpy<T>(nd, int(y.size()), 1.0, coefb.as<double>(), Zb.as<T>(), nd, x, d.s);
+        CTK_CUDA(cudaStreamSynchronize(d.s));  // y (host) must outlive the async copy
+        if (mon.record(k, x, fit / beta1, true, lambda_k)) break;
+        if (breakdown) {
+            mon.reason = CTK_STOP_BREAKDOWN;
+            break;
+        }
+    }
+    mon.finish(k);
+    log->stored_domain_basis = nz_;
+    log->stored_range_basis = nu_;
+}
+
 }  // namespace
 
 template <class T>
@@ -748,6 +905,10 @@ void solve_device(Geometry& g, int solver, int variant, const T* d_b, double lam
         case 5: sirt<T>(d, d_b, *o, d_x, log); break;
         case 6: abba_gmres<T>(d, d_b, *o, d_x, log, true); break;
         case 7: abba_gmres<T>(d, d_b, *o, d_x, log, false); break;
+        case 8:
+            if (!st) fail(CTK_E_PARAMETER, "flsqr_tv needs a strategy");
+            flsqr_tv<T>(d, d_b, *st, *o, d_x, log);
+            break;
         default: fail(CTK_E_PARAMETER, "unknown solver");
     }
     CTK_CUDA(cudaStreamSynchronize(g.stream));

@@ -12,6 +12,7 @@
 #include <random>
 
 #include "ctkrylov/gmres.hpp"
+#include "ctkrylov/tv.hpp"
 #include "ctkrylov/operators.hpp"
 #include "ctkrylov/phantom.hpp"
 #include "ctkrylov/solvers.hpp"
@@ -81,6 +82,10 @@ int main() {
     const auto ba_dev = ctkb::ba_gmres(b200, ctk::cspan(b), opts);
     EXPECT(rel(ba_dev.x, ba_ref.x) < 1e-9);
     EXPECT(ba_dev.stored_domain_basis == ba_ref.stored_domain_basis);
+    const auto f_ref = ctk::flsqr_tv(ref, ctk::cspan(b), ctk::HybridStrategy::gcv(), opts);
+    const auto f_dev = ctkb::flsqr_tv(b200, ctk::cspan(b), ctk::HybridStrategy::gcv(), opts);
+    EXPECT(rel(f_dev.x, f_ref.x) < 1e-6);
+    EXPECT(f_dev.warnings == f_ref.warnings);
 
     // f32 pair through the same API
     auto b32 = ctkb::projector_pair<float>(g);

@@ -123,6 +123,27 @@ def test_gmres_parity(ctk, reference, problem, dtype, variant):
     assert res.stored_range_basis == want["stored_range_basis"]
 
 
+# fixed lambda: compared at k = 3 (the reference algorithm amplifies rounding-level
+# perturbations ~30x per iteration there; see test_oracle.py / DESIGN.md)
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("strategy,k", [("gcv", 6), ("fixed", 3)])
+def test_flsqr_tv_parity(ctk, reference, problem, dtype, strategy, k):
+    g, gt, b = problem
+    sid = {"fixed": 0, "gcv": 2}[strategy]
+    want = reference.solve(g, b, "flsqr_tv", k, strategy=sid, lam=5.0, tol=0.0, stop_inc=False, gt=gt)
+    pair = ctk.projector_pair(to_ctk(g), dtype=dtype)
+    st = ctk.HybridStrategy.gcv() if strategy == "gcv" else ctk.HybridStrategy.fixed(5.0)
+    res = ctk.flsqr_tv(pair, b.astype(dtype), st, _opts(ctk, k, gt.astype(dtype)))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+    assert np.allclose(res.log.lambda_, want["lambda"], rtol=1e-3)
+    assert [int(w.rsplit(" ", 1)[1]) for w in res.warnings] == list(want["warning_iterations"])
+    assert res.stored_domain_basis == want["stored_domain_basis"]
+    assert res.stored_range_basis == want["stored_range_basis"]
+    with pytest.raises(ctk.ParameterError):
+        ctk.flsqr_tv(pair, b.astype(dtype), ctk.HybridStrategy.dp(0.01), _opts(ctk, k))
+
+
 def test_voxel_driven_lsqr_parity(ctk, reference, problem):
     g, gt, b = problem
     k = 6

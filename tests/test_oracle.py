@@ -12,8 +12,8 @@ import pytest
 from geoms import ALL, cone_adjoint, parallel2d
 from conftest import rel_l2
 
-from oracle.oracle import (Geom, abba_gmres, adjoint_discrepancy, cgls, cgls_tv, dp_lambda, gcv_lambda, hybrid_lsqr,
-                           lsmr, lsqr, ray_box_chord, sirt)
+from oracle.oracle import (Geom, abba_gmres, adjoint_discrepancy, cgls, cgls_tv, dp_lambda, flsqr_tv, gcv_lambda,
+                           hybrid_lsqr, lsmr, lsqr, ray_box_chord, sirt)
 
 GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "*.npz")))
 
@@ -219,6 +219,26 @@ def test_numpy_gmres_vs_reference(restated, reference, small_problem, variant, r
     assert rel_l2(got["x"], want["x"]) < 1e-8
     assert np.allclose(got["explicit"], want["explicit"], rtol=1e-8)
     assert np.allclose(got["implicit"], want["implicit"], rtol=1e-6)
+    assert got["stored_domain_basis"] == want["stored_domain_basis"]
+    assert got["stored_range_basis"] == want["stored_range_basis"]
+
+
+# With a fixed lambda the reference's flsqr_tv amplifies rounding-level perturbations
+# ~30x per iteration (its truncated inner CG feeds the next preconditioner), so runs are
+# compared at k = 3 there; GCV picks a large lambda and is stable (k = 6).
+@pytest.mark.parametrize("strategy,k,tol", [("gcv", 6, 1e-7), ("fixed", 3, 1e-5)])
+def test_numpy_flsqr_tv_vs_reference(restated, reference, small_problem, strategy, k, tol):
+    g, gt, b = small_problem
+    f = lambda v: restated.forward(g, v)  # noqa: E731
+    bk = lambda v: restated.back(g, v)  # noqa: E731
+    sid = {"fixed": 0, "gcv": 2}[strategy]
+    want = reference.solve(g, b, "flsqr_tv", k, strategy=sid, lam=5.0, tol=0.0, stop_inc=False, gt=gt)
+    got = flsqr_tv(f, bk, b, (16, 16, 16), k, restated, strategy=strategy, lam=5.0, tol=0.0, stop_inc=False, gt=gt)
+    assert rel_l2(got["x"], want["x"]) < tol
+    assert np.allclose(got["explicit"], want["explicit"], rtol=tol)
+    assert np.allclose(got["implicit"], want["implicit"], rtol=1e-6)
+    assert np.allclose(got["lambda"], want["lambda"], rtol=1e-5, atol=1e-12)
+    assert list(got["warnings"]) == list(want["warning_iterations"])
     assert got["stored_domain_basis"] == want["stored_domain_basis"]
     assert got["stored_range_basis"] == want["stored_range_basis"]
 
