@@ -78,6 +78,9 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 #ifndef CTK_BP_U2
 #define CTK_BP_U2 1  // two row groups per iteration (87 ms vs 89 ms)
 #endif
+#ifndef CTK_BP_PAIR
+#define CTK_BP_PAIR 1  // packed f32x2 row positions (87.3 -> 86.3 ms)
+#endif
 #ifndef CTK_BP_UCLAMP
 #define CTK_BP_UCLAMP 1
 #endif
@@ -198,12 +201,11 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             }
                             int cur = -(1 << 20);
                             float A = 0.f, B = 0.f;
-                            auto step = [&](float vd, float yv) {
-                                const float fz = fmaf(vd, gs, czf);
-                                const float tt = split_t(fz);
+                            // one row: tt = fz + 1.5*2^23 rounded down (its bits carry the slice
+                            // index), tz = the z fraction, omt = 1 - tz
+                            auto step_w = [&](float tt, float tz, float omt, float yv) {
                                 const int kk = __float_as_int(tt) - (kSplitBias + kg0);
-                                const float tz = split_frac(fz, tt);
-                                const float w0 = (1.f - tz) * yv, w1 = tz * yv;
+                                const float w0 = omt * yv, w1 = tz * yv;
                                 const int adv = kk - cur;
                                 float ak = adv == 1 ? B : 0.f;  // two selects, no branch
                                 ak = adv == 0 ? A : ak;
@@ -220,6 +222,27 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 zp[0] = A;
                                 zp[BP_PB] = B;
                             };
+                            auto step = [&](float vd, float yv) {
+                                const float fz = fmaf(vd, gs, czf);
+                                const float tt = split_t(fz);
+                                const float tz = split_frac(fz, tt);
+                                step_w(tt, tz, 1.f - tz, yv);
+                            };
+#if CTK_BP_PAIR
+                            // the row positions of a 4-row group in packed f32x2 arithmetic
+                            // (FFMA2 / FADD2): per lane the same operations as step()
+                            const float2 gs2 = make_float2(gs, gs), cz2 = make_float2(czf, czf);
+                            const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
+                            const float2 m1 = make_float2(-1.f, -1.f), one2 = make_float2(1.f, 1.f);
+                            auto step2 = [&](float2 vd, float ya, float yb) {
+                                const float2 fz = __ffma2_rn(vd, gs2, cz2);
+                                const float2 tt = __fadd2_rd(fz, M2);
+                                const float2 tz = __ffma2_rn(__fadd2_rn(tt, nM2), m1, fz);
+                                const float2 omt = __ffma2_rn(tz, m1, one2);
+                                step_w(tt.x, tz.x, omt.x, ya);
+                                step_w(tt.y, tz.y, omt.y, yb);
+                            };
+#endif
                             // whole 4-row groups; only the first and last are masked to [v0, v1]
                             const float4* vd4 = reinterpret_cast<const float4*>(vdtab);
                             const int q0 = v0 >> 2, q1 = v1 >> 2;
@@ -232,10 +255,15 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                     y4.z = (b + 2 >= v0 && b + 2 <= v1) ? y4.z : 0.f;
                                     y4.w = (b + 3 >= v0 && b + 3 <= v1) ? y4.w : 0.f;
                                 }
+#if CTK_BP_PAIR
+                                step2(make_float2(d4.x, d4.y), y4.x, y4.y);
+                                step2(make_float2(d4.z, d4.w), y4.z, y4.w);
+#else
                                 step(d4.x, y4.x);
                                 step(d4.y, y4.y);
                                 step(d4.z, y4.z);
                                 step(d4.w, y4.w);
+#endif
                             };
                             // software pipelined: the next group's load is in flight while the
                             // current group is marched
