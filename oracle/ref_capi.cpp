@@ -16,6 +16,7 @@
 #include <omp.h>
 #endif
 
+#include "ctkrylov/io.hpp"
 #include "ctkrylov/noise.hpp"
 #include "ctkrylov/operators.hpp"
 #include "ctkrylov/phantom.hpp"
@@ -330,4 +331,46 @@ double ref_dp_lambda(const double* H, int k, double beta1, double nl) {
 }
 #endif
 
+}  // extern "C"
+
+// ---- raw f32 + .hdr I/O and 16-bit PGM (src/io.cpp, compiled from where it lies) ----------
+extern "C" {
+int ref_save_volume(const char* path, int nx, int ny, int nz, double spacing, const float* data) {
+    return guarded([&] {
+        ctk::Volume<float> v(nx, ny, nz, spacing);
+        std::memcpy(v.data.data(), data, v.data.size() * sizeof(float));
+        ctk::save_volume(path, v);
+    });
+}
+// shape[4] = nx ny nz + spacing in *spacing; data may be NULL (header only)
+int ref_load_volume(const char* path, int* shape, double* spacing, float* data, size_t cap) {
+    return guarded([&] {
+        const auto v = ctk::load_volume(path);
+        shape[0] = v.nx;
+        shape[1] = v.ny;
+        shape[2] = v.nz;
+        *spacing = v.spacing;
+        if (data && cap >= v.data.size()) std::memcpy(data, v.data.data(), v.data.size() * sizeof(float));
+    });
+}
+int ref_save_projections(const char* path, int na, int nu, int nv, const double* angles, const float* data) {
+    return guarded([&] {
+        ctk::ProjectionSet<float> p(std::vector<double>(angles, angles + na), nu, nv);
+        std::memcpy(p.data.data(), data, p.data.size() * sizeof(float));
+        ctk::save_projections(path, p);
+    });
+}
+int ref_load_projections(const char* path, int* dims, double* angles, size_t angle_cap, float* data, size_t cap) {
+    return guarded([&] {
+        const auto p = ctk::load_projections(path);
+        dims[0] = p.n_angles;
+        dims[1] = p.nu;
+        dims[2] = p.nv;
+        if (angles && angle_cap >= p.angles.size()) std::memcpy(angles, p.angles.data(), p.angles.size() * sizeof(double));
+        if (data && cap >= p.data.size()) std::memcpy(data, p.data.data(), p.data.size() * sizeof(float));
+    });
+}
+int ref_write_pgm16(const char* path, int w, int h, const float* values, double wmin, double wmax) {
+    return guarded([&] { ctk::write_pgm16(path, w, h, values, wmin, wmax); });
+}
 }  // extern "C"
