@@ -67,10 +67,11 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 //           the columns registered in its row, sorted by column -> deterministic order.
 // Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
 // their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
-// measured at 512^3 / 360 views: 4 CTAs/SM (64 regs) without the software prefetch is best
-// (89 ms) -- prefetch at 3 CTAs/SM 111 ms, prefetch at 4 CTAs/SM 92 ms
+// measured at 512^3 / 360 views: without view batching 4 CTAs/SM (64 regs) was best (89 ms;
+// prefetch at 3 CTAs/SM 111 ms, at 4 CTAs/SM 92 ms); with batching and 12-entry row lists
+// (60 KB of shared memory) 3 CTAs/SM: 82.4 ms
 #ifndef CTK_BP_MINB
-#define CTK_BP_MINB 4
+#define CTK_BP_MINB 3
 #endif
 #ifndef CTK_BP_PREFETCH
 #define CTK_BP_PREFETCH 0
@@ -84,7 +85,10 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 #ifndef CTK_BP_UCLAMP
 #define CTK_BP_UCLAMP 1
 #endif
-constexpr int BP_PB = 256, BP_KB = 32, BP_SL = 8;
+#ifndef CTK_BP_SL
+#define CTK_BP_SL 12  // row list capacity: a batch can register entries of two views in a row
+#endif
+constexpr int BP_PB = 256, BP_KB = 32, BP_SL = CTK_BP_SL;
 constexpr int BP_ZG = 2;  // guard rows of Z on each side: out-of-band entries land there, unread
 
 template <int CLASS>
@@ -97,6 +101,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_PB]
     float* vdtab = eth + BP_PB;                                 // [nv rounded up to 4], 16-byte aligned
     int2* urange = reinterpret_cast<int2*>(vdtab + ((g.nv + 3) & ~3));  // [na]
+    int* pref = reinterpret_cast<int*>(urange + g.na);          // [na + 1] candidate prefix sums
+    int* slotcol = pref + g.na + 1;                             // [BP_PB] (view, column) of a slot
 
     const int t = threadIdx.x;
     // plane index fastest: a wave of resident CTAs shares one (row tile, z band), so per
@@ -134,18 +140,55 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
             i0 = max(i0, int(floor(fmax(fmin(u1, u2), -1e9))) - 1);
             i1 = min(i1, int(ceil(fmin(fmax(u1, u2), 1e9))) + 1);
         }
+        // only this pass's ray class: intersect with the hull of the view's CLASS columns
+        const int4 vc = g.vclass[a];
+        i0 = max(i0, CLASS ? vc.z : vc.x);
+        i1 = min(i1, CLASS ? vc.w : vc.y);
         urange[a] = make_int2(i0, i1);
     }
     __syncthreads();
+    // Candidate (view, column) pairs of all views are packed into batches of BP_PB slots
+    // (view-major, columns ascending), so a batch mixes the tail of one view with the head
+    // of the next and no thread idles on a half-empty chunk.  Per voxel the summation order
+    // is unchanged: entries are still added in (view, column) order.
+    if (t < 32) {  // exclusive prefix sum of the candidate counts, one warp
+        int run = 0;
+        for (int a0 = 0; a0 < g.na; a0 += 32) {
+            const int a = a0 + t;
+            const int n = a < g.na ? max(0, urange[a].y - urange[a].x + 1) : 0;
+            int incl = n;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, incl, d);
+                if (t >= d) incl += o;
+            }
+            if (a < g.na) pref[a] = run + incl - n;
+            run += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (t == 0) pref[g.na] = run;
+    }
+    __syncthreads();
+    const int total = pref[g.na];
 
-    for (int a = 0; a < g.na; ++a) {
-        const int iu0 = urange[a].x, iu1 = urange[a].y;
-        for (int cbase = iu0; cbase <= iu1; cbase += BP_PB) {
+    for (int b0 = 0; b0 < total; b0 += BP_PB) {
+        {
             // ---- phase 1 ----
             cnt[t] = 0;
+            int a = -1, iu = 0;
+            const int gidx = b0 + t;
+            if (gidx < total) {  // the view of this slot: last a with pref[a] <= gidx
+                int lo = 0, hi = g.na - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if (pref[mid] <= gidx) lo = mid;
+                    else hi = mid - 1;
+                }
+                a = lo;
+                iu = urange[a].x + (gidx - pref[a]);
+            }
+            slotcol[t] = a >= 0 ? a * g.nu + iu : -1;
             __syncthreads();
-            const int iu = cbase + t;
-            if (iu <= iu1) {
+            if (a >= 0) {
                 const int c = a * g.nu + iu;
                 if (g.colaxis[c] == CLASS) {
                     const float4 cd = g.col[c];
@@ -341,10 +384,10 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_PB + e], acc[m]);
                     }
                 } else {
-                    // overflow (very fine detector sampling): scan every column of the chunk in order
-                    for (int e = 0; e < BP_PB && cbase + e <= iu1; ++e) {
-                        const int c = a * g.nu + cbase + e;
-                        if (g.colaxis[c] != CLASS) continue;
+                    // overflow (very fine detector sampling): scan every slot of the batch in order
+                    for (int e = 0; e < BP_PB; ++e) {
+                        const int c = slotcol[e];
+                        if (c < 0 || g.colaxis[c] != CLASS) continue;
                         const float4 cd = g.col[c];
                         const float fh = fmaf(fs, cd.y, cd.x);
                         const float fih = floorf(fh);
@@ -544,7 +587,7 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int kbands = (g.nz_local() + BP_KB - 1) / BP_KB;
     const size_t smem = sizeof(float) * (size_t(BP_PB) * (BP_KB + 2 * BP_ZG) + size_t(BP_PB) * BP_SL + 2 * BP_PB +
                                          ((size_t(g.nv) + 3) & ~size_t(3))) +
-                        sizeof(int2) * g.na;
+                        sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     static size_t configured = 0;
     if (smem > configured) {

@@ -56,6 +56,7 @@ struct KGeom {
     const float4* col;            // per (view, iu): fh0, fhd, g0, gd   (f32 separable model)
     const unsigned char* colaxis; // per (view, iu): 0 = x-dominant, 1 = y-dominant
     const double2* colstep;       // per (view, iu): (dx^2+dy^2, |d_A|) of the unnormalised ray
+    const int4* vclass;           // per view: column hull [x.. y] of x-dominant, [z.. w] of y-dominant columns
 };
 
 // ---- the geometry handle ---------------------------------------------------------------
@@ -82,6 +83,7 @@ struct Geometry {
     // device tables
     DevBuf d_ctst, d_col, d_colaxis, d_colstep;
     DevBuf d_vorder;  // views grouped by ray class (x-dominant first) for L2 reuse in Ax
+    DevBuf d_vclass;  // per view: hull of the columns of each ray class (matched A^T b batching)
     // workspaces (grown lazily)
     DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
     DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers

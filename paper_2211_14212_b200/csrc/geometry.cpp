@@ -53,6 +53,7 @@ KGeom Geometry::kgeom() const {
     k.ctst = d_ctst.as<double2>();
     k.col = d_col.as<float4>();
     k.colaxis = d_colaxis.as<unsigned char>();
+    k.vclass = d_vclass.as<int4>();
     k.colstep = d_colstep.as<double2>();
     return k;
 }
@@ -203,6 +204,21 @@ Geometry* geometry_create(const ctk_geom_desc* d) {
                 for (int iu = 0; iu < g->nu; ++iu) nxd += cax[size_t(a) * g->nu + iu] == 0;
                 if ((2 * nxd >= g->nu) == (pass == 0)) vorder.push_back(a);
             }
+        // per view and ray class, the hull of that class's detector columns (empty: lo > hi)
+        std::vector<int4> vcls(size_t(g->na), make_int4(g->nu, -1, g->nu, -1));
+        for (int a = 0; a < g->na; ++a)
+            for (int iu = 0; iu < g->nu; ++iu) {
+                int4& h = vcls[size_t(a)];
+                if (cax[size_t(a) * g->nu + iu] == 0) {
+                    h.x = std::min(h.x, iu);
+                    h.y = std::max(h.y, iu);
+                } else {
+                    h.z = std::min(h.z, iu);
+                    h.w = std::max(h.w, iu);
+                }
+            }
+        g->d_vclass.ensure(sizeof(int4) * vcls.size());
+        CTK_CUDA(cudaMemcpy(g->d_vclass.p, vcls.data(), sizeof(int4) * vcls.size(), cudaMemcpyHostToDevice));
         g->d_vorder.ensure(sizeof(int) * vorder.size());
         CTK_CUDA(cudaMemcpy(g->d_vorder.p, vorder.data(), sizeof(int) * vorder.size(), cudaMemcpyHostToDevice));
         g->d_ctst.ensure(sizeof(double2) * ctst.size());
