@@ -84,6 +84,10 @@ struct Geometry {
     DevBuf d_ctst, d_col, d_colaxis, d_colstep;
     DevBuf d_vorder;  // views grouped by ray class (x-dominant first) for L2 reuse in Ax
     DevBuf d_vclass;  // per view: hull of the columns of each ray class (matched A^T b batching)
+    DevBuf d_rayinv;  // per ray: 1/d of make_ray, for the exact gathers (built on first use)
+    bool rayinv_ready = false;
+    DevBuf d_walk;    // per ray: the plan_walk parameters of the exact f64 path (built on first use)
+    bool walk_ready = false;
     // workspaces (grown lazily)
     DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
     DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers
@@ -103,7 +107,7 @@ struct Geometry {
 // ---- kernels (launch wrappers) ---------------------------------------------------------
 // exact f64 path (kernels_f64.cu, compiled with --fmad=false)
 void launch_ax_exact_f64(const Geometry& g, const double* x, double* y, cudaStream_t s);
-void launch_atb_matched_exact_f64(const Geometry& g, const double* y, double* x, cudaStream_t s);
+void launch_atb_matched_exact_f64(Geometry& g, const double* y, double* x, cudaStream_t s);
 void launch_atb_voxel_f64(const Geometry& g, const double* y, double* x, cudaStream_t s);
 
 // f32 performance path (kernels_f32.cu)
@@ -122,7 +126,7 @@ void op_atb(Geometry& g, int variant, const T* y, T* x, cudaStream_t s);
 template <class T>
 void siddon_ax(const Geometry& g, const T* x, T* y, cudaStream_t s);
 template <class T>
-void siddon_atb(const Geometry& g, const T* y, T* x, cudaStream_t s);
+void siddon_atb(Geometry& g, const T* y, T* x, cudaStream_t s);
 
 // phantom (stencils.cu)
 void launch_shepp_logan_f32(int n, float* out, cudaStream_t s);

@@ -132,22 +132,48 @@ __device__ __forceinline__ bool project_point(const KGeom& g, double ct, double 
     return true;
 }
 
-// Exact transpose as a gather: voxel (i,j,k) sums w * (step * y) over every ray whose
-// Joseph stencil touches it, in the reference's scatter order.  Candidate rays are the
-// pixels whose centres fall in the detector footprint of the cube [voxel +- h]^3 (every
-// stencil point of the voxel lies in that cube), widened by one pixel.
-__global__ void k_atb_matched_exact(KGeom g, int nparts, const double* __restrict__ proj,
-                                    double* __restrict__ vol) {
-    const size_t nvox = size_t(g.nx) * g.ny * g.nz;
-    const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= nvox) return;
-    const int i = int(id % g.nx);
-    const int j = int((id / g.nx) % g.ny);
-    const int k = int(id / (size_t(g.nx) * g.ny));
+// plan_walk of every ray, once per geometry: {axis, fb0, fb_d, fc0, fc_d, step}, so the
+// transpose's candidates cost a 48-byte load instead of make_ray's sqrt and divisions.
+// Layout [a][iu][iv] (detector columns contiguous, as the gather's lanes read them).
+__global__ void k_walk_table(KGeom g, double* __restrict__ tab) {
+    const int iu = blockIdx.x * blockDim.x + threadIdx.x;
+    const int iv = blockIdx.y * blockDim.y + threadIdx.y;
+    const int a = blockIdx.z;
+    if (iu >= g.nu || iv >= g.nv) return;
+    const double2 cs = g.ctst[a];
+    Walk w;
+    make_walk(g, cs.x, cs.y, iu, iv, w);
+    double* o = tab + 6 * ((size_t(a) * g.nu + iu) * g.nv + iv);
+    o[0] = double(w.axis);
+    o[1] = w.fb0;
+    o[2] = w.fb_d;
+    o[3] = w.fc0;
+    o[4] = w.fc_d;
+    o[5] = w.step;
+}
+
+// Exact transpose as a gather, warp = 32 consecutive z voxels of one (i, j) column: voxel
+// (i,j,k) sums w * (step * y) over every ray whose Joseph stencil touches it, in the
+// reference's scatter order (angle partition, angle, iv, iu).  A ray touches the voxel only
+// if it crosses the cube [voxel +- h]^3 (its stencil point in the voxel's slice lies within
+// one voxel of it), i.e. only pixel centres inside the bounding box of the cube's 8 corner
+// projections (1e-6-pixel slack) are candidates.  Bit-identical to the scatter: the same
+// plan_walk values (tabulated) and the same per-voxel summation order.
+__global__ void __launch_bounds__(128) k_atb_matched_exact(KGeom g, int nparts, const double* __restrict__ walk,
+                                                           const double* __restrict__ pt, double* __restrict__ vol,
+                                                           int kblocks) {
+    const long wid = long(blockIdx.x) * blockDim.y + threadIdx.y;
+    const long ncol = long(g.nx) * g.ny;
+    if (wid >= ncol * kblocks) return;
+    const int kb = int(wid / ncol) * 32;
+    const long col = wid % ncol;
+    const int i = int(col % g.nx), j = int(col / g.nx), k = kb + int(threadIdx.x);
+    if (k >= g.nz) return;
     const double h = g.h;
     const double xc = (i - 0.5 * (g.nx - 1)) * h, yc = (j - 0.5 * (g.ny - 1)) * h, zc = (k - 0.5 * (g.nz - 1)) * h;
     const int vidx[3] = {i, j, k};
     const size_t frame = size_t(g.nu) * g.nv;
+    const double cu = 0.5 * (g.nu - 1), cvv = 0.5 * (g.nv - 1), eps = 1e-6;
     double out = 0;
     for (int t = 0; t < nparts; ++t) {
         double part = 0;
@@ -155,37 +181,45 @@ __global__ void k_atb_matched_exact(KGeom g, int nparts, const double* __restric
             const double2 cs = g.ctst[a];
             double umin = DBL_MAX, umax = -DBL_MAX, vmin = DBL_MAX, vmax = -DBL_MAX;
             bool all = false;
-            for (int q = 0; q < 8 && !all; ++q) {
-                double fu, fv;
-                if (!project_point(g, cs.x, cs.y, xc + ((q & 1) ? h : -h), yc + ((q & 2) ? h : -h),
-                                   zc + ((q & 4) ? h : -h), fu, fv)) {
-                    all = true;
-                    break;
+            for (int q = 0; q < 4; ++q) {  // the cube's 4 (x, y) corners, each with z = zc -+ h
+                const double x = xc + ((q & 1) ? h : -h), y = yc + ((q & 2) ? h : -h);
+                double u, tz;
+                if (g.mode == CTK_CONE3D) {
+                    const double depth = g.dso - (x * cs.x + y * cs.y);
+                    if (!(depth > 1e-9 * g.dso)) { all = true; break; }
+                    tz = (g.dso + g.dod) / depth;
+                    u = (-x * cs.y + y * cs.x) * tz;
+                } else {
+                    tz = 1.0;
+                    u = -x * cs.y + y * cs.x;
                 }
-                umin = fmin(umin, fu); umax = fmax(umax, fu);
-                vmin = fmin(vmin, fv); vmax = fmax(vmax, fv);
+                umin = fmin(umin, u); umax = fmax(umax, u);
+                vmin = fmin(vmin, fmin((zc - h) * tz, (zc + h) * tz));
+                vmax = fmax(vmax, fmax((zc - h) * tz, (zc + h) * tz));
             }
             int iu0 = 0, iu1 = g.nu - 1, iv0 = 0, iv1 = g.nv - 1;
             if (!all) {
-                iu0 = max(iu0, int(floor(fmax(umin, -1e9))) - 1);
-                iu1 = min(iu1, int(ceil(fmin(umax, 1e9))) + 1);
+                iu0 = max(iu0, int(ceil(fmax(umin / g.du + cu - eps, -1e9))));
+                iu1 = min(iu1, int(floor(fmin(umax / g.du + cu + eps, 1e9))));
                 if (g.nv > 1) {
-                    iv0 = max(iv0, int(floor(fmax(vmin, -1e9))) - 1);
-                    iv1 = min(iv1, int(ceil(fmin(vmax, 1e9))) + 1);
+                    iv0 = max(iv0, int(ceil(fmax(vmin / g.du + cvv - eps, -1e9))));
+                    iv1 = min(iv1, int(floor(fmin(vmax / g.du + cvv + eps, 1e9))));
                 }
             }
-            const double* fr = proj + size_t(a) * frame;
+            const double* fa = pt + size_t(a) * frame;
+            const double* wa = walk + 6 * size_t(a) * frame;
             for (int iv = iv0; iv <= iv1; ++iv) {
                 for (int iu = iu0; iu <= iu1; ++iu) {
-                    const double value = __ldg(fr + size_t(iu) + size_t(g.nu) * iv);
+                    const size_t q = size_t(iu) * g.nv + iv;  // [a][iu][iv]
+                    const double value = __ldg(fa + q);
                     if (value == 0.0) continue;
-                    Walk w;
-                    make_walk(g, cs.x, cs.y, iu, iv, w);
-                    const int s = vidx[w.axis];
-                    const int pb = vidx[w.axis == 2 ? 0 : w.axis + 1];
-                    const int pc = vidx[w.axis == 0 ? 2 : w.axis - 1];
-                    const double fb = w.fb0 + s * w.fb_d;
-                    const double fc = w.fc0 + s * w.fc_d;
+                    const double* wr = wa + 6 * q;
+                    const int axis = int(__ldg(wr));
+                    const int s = vidx[axis];
+                    const int pb = vidx[axis == 2 ? 0 : axis + 1];
+                    const int pc = vidx[axis == 0 ? 2 : axis - 1];
+                    const double fb = __ldg(wr + 1) + s * __ldg(wr + 2);
+                    const double fc = __ldg(wr + 3) + s * __ldg(wr + 4);
                     const int ib = int(floor(fb));
                     const int ic = int(floor(fc));
                     const int ob = pb - ib, oc = pc - ic;
@@ -199,14 +233,30 @@ __global__ void k_atb_matched_exact(KGeom g, int nparts, const double* __restric
                         default: wq = tb * tc; break;
                     }
                     if (wq == 0.0) continue;
-                    const double scaled = w.step * value;
+                    const double scaled = __ldg(wr + 5) * value;
                     part += wq * scaled;
                 }
             }
         }
         out += 1.0 * part;
     }
-    vol[id] = out;
+    vol[size_t(i) + size_t(g.nx) * (size_t(j) + size_t(g.ny) * k)] = out;
+}
+
+// y[a][iv][iu] -> pt[a][iu][iv]
+__global__ void k_transpose_f64(int nu, int nv, const double* __restrict__ y, double* __restrict__ pt) {
+    __shared__ double tile[32][33];
+    const int a = blockIdx.z, u0 = blockIdx.x * 32, v0 = blockIdx.y * 32;
+    const size_t frame = size_t(nu) * nv;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int iu = u0 + threadIdx.x, iv = v0 + r;
+        tile[r][threadIdx.x] = (iu < nu && iv < nv) ? y[a * frame + size_t(iv) * nu + iu] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int iu = u0 + r, iv = v0 + threadIdx.x;
+        if (iu < nu && iv < nv) pt[a * frame + size_t(iu) * nv + iv] = tile[threadIdx.x][r];
+    }
 }
 
 // back_project_voxel_driven, per voxel over views in order (projector.hpp:208-279).
@@ -273,10 +323,23 @@ void launch_ax_exact_f64(const Geometry& g, const double* x, double* y, cudaStre
     after_launch("k_ax_exact");
 }
 
-void launch_atb_matched_exact_f64(const Geometry& g, const double* y, double* x, cudaStream_t s) {
-    const size_t n = g.domain();
+void launch_atb_matched_exact_f64(Geometry& g, const double* y, double* x, cudaStream_t s) {
+    const size_t nrays = g.range();
+    dim3 rb(32, 8), rg((g.nu + 31) / 32, (g.nv + 31) / 32, g.na);
+    if (g.d_walk.ensure(6 * nrays * sizeof(double)) || !g.walk_ready) {
+        dim3 wb(32, 4), wg((g.nu + 31) / 32, (g.nv + 3) / 4, g.na);
+        k_walk_table<<<wg, wb, 0, s>>>(g.kgeom(), g.d_walk.as<double>());
+        after_launch("k_walk_table");
+        g.walk_ready = true;
+    }
+    g.proj_t.ensure(nrays * sizeof(double));
+    k_transpose_f64<<<rg, rb, 0, s>>>(g.nu, g.nv, y, g.proj_t.as<double>());
+    after_launch("k_transpose_f64");
     const int nparts = std::max(1, std::min(g.bp_parts, g.na));
-    k_atb_matched_exact<<<unsigned((n + 127) / 128), 128, 0, s>>>(g.kgeom(), nparts, y, x);
+    const int kblocks = (g.nz + 31) / 32;
+    const long warps = long(g.nx) * g.ny * kblocks;
+    k_atb_matched_exact<<<unsigned((warps + 3) / 4), dim3(32, 4), 0, s>>>(g.kgeom(), nparts, g.d_walk.as<double>(),
+                                                                        g.proj_t.as<double>(), x, kblocks);
     after_launch("k_atb_matched_exact");
 }
 

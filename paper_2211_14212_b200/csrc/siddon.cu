@@ -120,79 +120,125 @@ __global__ void k_siddon_ax(KGeom g, const T* __restrict__ vol, T* __restrict__ 
     proj[size_t(a) * g.nu * g.nv + size_t(iu) + size_t(g.nu) * iv] = acc;
 }
 
-// projection of a point onto continuous detector coordinates; false if not in front of
-// the cone source (then every pixel is a candidate)
-__device__ __forceinline__ bool s_project(const KGeom& g, double ct, double st, double x, double y, double z,
-                                          double& fu, double& fv) {
-    double u, v;
-    if (g.mode == CTK_CONE3D) {
-        const double sx = g.dso * ct, sy = g.dso * st;
-        const double rx = x - sx, ry = y - sy;
-        const double depth = -(rx * ct + ry * st);
-        if (!(depth > 1e-9 * g.dso)) return false;
-        const double t = (g.dso + g.dod) / depth;
-        u = -(sx + t * rx) * st + (sy + t * ry) * ct;
-        v = t * z;
-    } else {
-        u = -x * st + y * ct;
-        v = z;
+// 1/d of every ray (make_ray, then the reciprocal exactly as s_make_ray forms it), so the
+// transpose's candidates cost a 24-byte load instead of a sqrt and six divisions
+__global__ void k_siddon_rayinv(KGeom g, double* __restrict__ inv) {
+    const int iu = blockIdx.x * blockDim.x + threadIdx.x;
+    const int iv = blockIdx.y * blockDim.y + threadIdx.y;
+    const int a = blockIdx.z;
+    if (iu >= g.nu || iv >= g.nv) return;
+    const double2 cs = g.ctst[a];
+    SRay r;
+    s_make_ray(g, cs.x, cs.y, iu, iv, r);
+    double* o = inv + 3 * ((size_t(a) * g.nu + iu) * g.nv + iv);  // [a][iu][iv]
+    o[0] = r.inv[0];
+    o[1] = r.inv[1];
+    o[2] = r.inv[2];
+}
+
+// Detector window of the box [lo3, lo3 + h]^3 for one view: the pixel centres inside the
+// bounding box of the 8 corner projections (a ray meets the box iff its detector point lies
+// in the box's projection; the 1e-6-pixel slack absorbs rounding).  For a cone the four
+// (x, y) corners share one depth each: u = w D / depth, v = z D / depth -- four divisions.
+// false: the box is not strictly in front of the source (every pixel is a candidate).
+__device__ __forceinline__ bool s_window(const KGeom& g, double ct, double st, const double lo3[3], double h,
+                                         int& iu0, int& iu1, int& iv0, int& iv1) {
+    double umin = DBL_MAX, umax = -DBL_MAX, vmin = DBL_MAX, vmax = -DBL_MAX;
+    const double z0 = lo3[2], z1 = lo3[2] + h;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double x = lo3[0] + ((q & 1) ? h : 0.0), y = lo3[1] + ((q & 2) ? h : 0.0);
+        const double w = -x * st + y * ct;
+        if (g.mode == CTK_CONE3D) {
+            const double depth = g.dso - (x * ct + y * st);
+            if (!(depth > 1e-9 * g.dso)) return false;
+            const double t = (g.dso + g.dod) / depth;
+            umin = fmin(umin, w * t);
+            umax = fmax(umax, w * t);
+            vmin = fmin(vmin, fmin(z0 * t, z1 * t));
+            vmax = fmax(vmax, fmax(z0 * t, z1 * t));
+        } else {
+            umin = fmin(umin, w);
+            umax = fmax(umax, w);
+            vmin = z0;
+            vmax = z1;
+        }
     }
-    fu = u / g.du + 0.5 * (g.nu - 1);
-    fv = v / g.du + 0.5 * (g.nv - 1);
+    const double cu = 0.5 * (g.nu - 1), cv = 0.5 * (g.nv - 1), eps = 1e-6;
+    iu0 = max(0, int(ceil(fmax(umin / g.du + cu - eps, -1e9))));
+    iu1 = min(g.nu - 1, int(floor(fmin(umax / g.du + cu + eps, 1e9))));
+    iv0 = 0;
+    iv1 = g.nv - 1;
+    if (g.nv > 1) {
+        iv0 = max(0, int(ceil(fmax(vmin / g.du + cv - eps, -1e9))));
+        iv1 = min(g.nv - 1, int(floor(fmin(vmax / g.du + cv + eps, 1e9))));
+    }
     return true;
 }
 
+// Transpose as a gather, warp = 32 consecutive z voxels of one (i, j) column (lanes along
+// z): a cone view's detector COLUMN window depends on (x, y) only, so the warp walks one
+// column range together, each lane its own row window; the projections (transposed to
+// pt[a][iu][iv]) and the ray table (same order) are read along detector columns, i.e.
+// coalesced across the lanes.  Per voxel the contributions are added in the reference's
+// scatter order (view, row, column) -- the lane's row loop is inside the column loop here,
+// so the order is kept by iterating rows outermost per lane.
 template <class T>
-__global__ void k_siddon_atb(KGeom g, const T* __restrict__ proj, T* __restrict__ vol) {
-    const size_t nvox = size_t(g.nx) * g.ny * g.nz;
-    const size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (id >= nvox) return;
-    const int idx3[3] = {int(id % g.nx), int((id / g.nx) % g.ny), int(id / (size_t(g.nx) * g.ny))};
+__global__ void __launch_bounds__(128) k_siddon_atb(KGeom g, const double* __restrict__ rayinv,
+                                                    const T* __restrict__ pt, T* __restrict__ vol, int kblocks) {
+    const long wid = long(blockIdx.x) * blockDim.y + threadIdx.y;
+    const long ncol = long(g.nx) * g.ny;
+    if (wid >= ncol * kblocks) return;
+    const int kb = int(wid / ncol) * 32;
+    const long col = wid % ncol;
+    const int idx3[3] = {int(col % g.nx), int(col / g.nx), kb + int(threadIdx.x)};
+    const bool live = idx3[2] < g.nz;
     const int n3[3] = {g.nx, g.ny, g.nz};
     const double h = g.h;
     const double lo3[3] = {(idx3[0] - 0.5 * g.nx) * h, (idx3[1] - 0.5 * g.ny) * h, (idx3[2] - 0.5 * g.nz) * h};
+    double plo[3], phi[3];  // the voxel's six crossing planes, (q - n/2) h exactly as s_alpha forms them
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        plo[ax] = (idx3[ax] - 0.5 * n3[ax]) * h;
+        phi[ax] = (idx3[ax] + 1 - 0.5 * n3[ax]) * h;
+    }
     const size_t frame = size_t(g.nu) * g.nv;
+    const bool cone = g.mode == CTK_CONE3D;
     T acc = 0;
-    for (int a = 0; a < g.na; ++a) {
+    for (int a = 0; a < g.na && live; ++a) {
         const double2 cs = g.ctst[a];
-        double umin = DBL_MAX, umax = -DBL_MAX, vmin = DBL_MAX, vmax = -DBL_MAX;
-        bool all = false;
-        for (int q = 0; q < 8; ++q) {
-            double fu, fv;
-            if (!s_project(g, cs.x, cs.y, lo3[0] + ((q & 1) ? h : 0.0), lo3[1] + ((q & 2) ? h : 0.0),
-                           lo3[2] + ((q & 4) ? h : 0.0), fu, fv)) {
-                all = true;
-                break;
-            }
-            umin = fmin(umin, fu); umax = fmax(umax, fu);
-            vmin = fmin(vmin, fv); vmax = fmax(vmax, fv);
-        }
         int iu0 = 0, iu1 = g.nu - 1, iv0 = 0, iv1 = g.nv - 1;
-        if (!all) {
-            iu0 = max(iu0, int(floor(fmax(umin, -1e9))) - 1);
-            iu1 = min(iu1, int(ceil(fmin(umax, 1e9))) + 1);
-            if (g.nv > 1) {
-                iv0 = max(iv0, int(floor(fmax(vmin, -1e9))) - 1);
-                iv1 = min(iv1, int(ceil(fmin(vmax, 1e9))) + 1);
-            }
+        if (!s_window(g, cs.x, cs.y, lo3, h, iu0, iu1, iv0, iv1)) {
+            iu0 = 0; iu1 = g.nu - 1; iv0 = 0; iv1 = g.nv - 1;
         }
-        const T* fr = proj + size_t(a) * frame;
+        const double sx = g.dso * cs.x, sy = g.dso * cs.y;  // cone: every ray starts at the source
+        const T* fa = pt + size_t(a) * frame;
+        const double* ra = rayinv + 3 * size_t(a) * frame;
         for (int iv = iv0; iv <= iv1; ++iv)
             for (int iu = iu0; iu <= iu1; ++iu) {
-                const T value = __ldg(fr + size_t(iu) + size_t(g.nu) * iv);
+                const size_t q = size_t(iu) * g.nv + iv;  // [a][iu][iv]
+                const T value = __ldg(fa + q);
                 if (value == T(0)) continue;
-                SRay r;
-                s_make_ray(g, cs.x, cs.y, iu, iv, r);
+                const double inv[3] = {__ldg(ra + 3 * q), __ldg(ra + 3 * q + 1), __ldg(ra + 3 * q + 2)};
+                double o[3];
+                if (cone) {
+                    o[0] = sx; o[1] = sy; o[2] = 0.0;
+                } else {  // make_ray's parallel origin, operation for operation
+                    const double u = (iu - 0.5 * (g.nu - 1)) * g.du;
+                    const double v = (iv - 0.5 * (g.nv - 1)) * g.du;
+                    const double cx = -g.dod * cs.x, cy = -g.dod * cs.y, cz = 0.0;
+                    o[0] = cx - u * cs.y; o[1] = cy + u * cs.x; o[2] = cz + v;
+                }
                 double lo = -DBL_MAX, hi = DBL_MAX;
                 bool miss = false;
 #pragma unroll
                 for (int ax = 0; ax < 3; ++ax) {
-                    if (r.d[ax] == 0.0) {
-                        if (s_slab(r.o[ax], n3[ax], h) != idx3[ax]) miss = true;
+                    if (inv[ax] == 0.0) {  // d_ax == 0
+                        if (s_slab(o[ax], n3[ax], h) != idx3[ax]) miss = true;
                         continue;
                     }
-                    const double a0 = s_alpha(r, ax, idx3[ax], n3[ax], h);
-                    const double a1 = s_alpha(r, ax, idx3[ax] + 1, n3[ax], h);
+                    const double a0 = (plo[ax] - o[ax]) * inv[ax];
+                    const double a1 = (phi[ax] - o[ax]) * inv[ax];
                     lo = fmax(lo, fmin(a0, a1));
                     hi = fmin(hi, fmax(a0, a1));
                 }
@@ -200,7 +246,24 @@ __global__ void k_siddon_atb(KGeom g, const T* __restrict__ proj, T* __restrict_
                 acc += T(hi - lo) * value;
             }
     }
-    vol[id] = acc;
+    if (live) vol[size_t(idx3[0]) + size_t(g.nx) * (size_t(idx3[1]) + size_t(g.ny) * idx3[2])] = acc;
+}
+
+// y[a][iv][iu] -> pt[a][iu][iv]
+template <class T>
+__global__ void k_siddon_transpose(int nu, int nv, const T* __restrict__ y, T* __restrict__ pt) {
+    __shared__ T tile[32][33];
+    const int a = blockIdx.z, u0 = blockIdx.x * 32, v0 = blockIdx.y * 32;
+    const size_t frame = size_t(nu) * nv;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int iu = u0 + threadIdx.x, iv = v0 + r;
+        tile[r][threadIdx.x] = (iu < nu && iv < nv) ? y[a * frame + size_t(iv) * nu + iu] : T(0);
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int iu = u0 + r, iv = v0 + threadIdx.x;
+        if (iu < nu && iv < nv) pt[a * frame + size_t(iu) * nv + iv] = tile[threadIdx.x][r];
+    }
 }
 
 }  // namespace
@@ -213,15 +276,31 @@ void siddon_ax(const Geometry& g, const T* x, T* y, cudaStream_t s) {
 }
 
 template <class T>
-void siddon_atb(const Geometry& g, const T* y, T* x, cudaStream_t s) {
-    const size_t n = g.domain();
-    k_siddon_atb<T><<<unsigned((n + 127) / 128), 128, 0, s>>>(g.kgeom(), y, x);
+void siddon_atb(Geometry& g, const T* y, T* x, cudaStream_t s) {
+    const size_t nrays = g.range();
+    if (g.d_rayinv.ensure(3 * nrays * sizeof(double)) || !g.rayinv_ready) {
+        dim3 blk(32, 4), grd((g.nu + 31) / 32, (g.nv + 3) / 4, g.na);
+        k_siddon_rayinv<<<grd, blk, 0, s>>>(g.kgeom(), g.d_rayinv.as<double>());
+        after_launch("k_siddon_rayinv");
+        g.rayinv_ready = true;
+    }
+    g.proj_t.ensure(nrays * sizeof(T));
+    {
+        dim3 blk(32, 8), grd((g.nu + 31) / 32, (g.nv + 31) / 32, g.na);
+        k_siddon_transpose<T><<<grd, blk, 0, s>>>(g.nu, g.nv, y, g.proj_t.as<T>());
+        after_launch("k_siddon_transpose");
+    }
+    const int kblocks = (g.nz + 31) / 32;
+    const long warps = long(g.nx) * g.ny * kblocks;
+    dim3 blk(32, 4);
+    k_siddon_atb<T><<<unsigned((warps + 3) / 4), blk, 0, s>>>(g.kgeom(), g.d_rayinv.as<double>(), g.proj_t.as<T>(), x,
+                                                            kblocks);
     after_launch("k_siddon_atb");
 }
 
 template void siddon_ax<float>(const Geometry&, const float*, float*, cudaStream_t);
 template void siddon_ax<double>(const Geometry&, const double*, double*, cudaStream_t);
-template void siddon_atb<float>(const Geometry&, const float*, float*, cudaStream_t);
-template void siddon_atb<double>(const Geometry&, const double*, double*, cudaStream_t);
+template void siddon_atb<float>(Geometry&, const float*, float*, cudaStream_t);
+template void siddon_atb<double>(Geometry&, const double*, double*, cudaStream_t);
 
 }  // namespace ctkb
