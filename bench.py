@@ -42,6 +42,10 @@ def parse():
     p.add_argument("--angles", type=int, default=360)
     p.add_argument("--iters", type=int, default=50)
     p.add_argument("--lam", type=float, default=30.0)
+    p.add_argument("--solver", default="lsmr", choices=["lsmr", "lsqr", "cgls"],
+                   help="lsmr (C3, the headline), lsqr (C2) or cgls (C1)")
+    p.add_argument("--projector", default="joseph", choices=["joseph", "siddon"],
+                   help="joseph (C1, C3) or siddon (C2: exact-length projector and its transpose)")
     p.add_argument("--shard", default="angle", choices=["angle", "slab"],
                    help="multi-GPU partition (SURVEY.md 8(e)): angle blocks (C3/C4) or z-slabs (C5)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -223,6 +227,12 @@ def main():
         dist.init_process_group("nccl")
     n, na = args.n, args.angles
     full = ctk.bench_geometry(n, na)
+    proj_kind = ctk.ProjectorKind.siddon if args.projector == "siddon" else ctk.ProjectorKind.joseph
+
+    def solve(bb):
+        if args.solver == "lsmr":
+            return ctk.lsmr(pair, bb, args.lam, opts)
+        return getattr(ctk, args.solver)(pair, bb, opts)
     # synthetic inputs, resident in HBM: phantom rasterised on the device, b = A x
     x_true = ctk.shepp_logan_3d(n)
     if args.shard == "slab":
@@ -231,10 +241,10 @@ def main():
         b = torch.empty(ctk.projector_pair(full).range_size, dtype=torch.float32, device="cuda")
         ctk.projector_pair(full).forward(x_true, b)
         x_true = x_true[z0 * n * n:(z0 + nzl) * n * n].contiguous()
-        pair = ctk.projector_pair(full, slab=(z0, nzl))
+        pair = ctk.projector_pair(full, slab=(z0, nzl), projector=proj_kind)
     else:
         first, count = shard_angles(na, world, rank)
-        pair = ctk.projector_pair(full.subset(first, count))
+        pair = ctk.projector_pair(full.subset(first, count), projector=proj_kind)
         b = torch.empty(pair.range_size, dtype=torch.float32, device="cuda")
         pair.forward(x_true, b)
     proj = pair.projector
@@ -280,14 +290,14 @@ def main():
     # sampler starts before the warmup so its start-up never overlaps the timed region.
     with Clocks(local) as clk:
         for _ in range(args.warmup):
-            ctk.lsmr(pair, b, args.lam, opts)
+            solve(b)
         barrier()
         launches0 = ctk.launch_count()
         t0 = time.perf_counter()
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record()
         for _ in range(args.steps):
-            res = ctk.lsmr(pair, b, args.lam, opts)
+            res = solve(b)
         s1.record()
         barrier()
         t1 = time.perf_counter()
@@ -307,12 +317,15 @@ def main():
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        r = ctk.lsmr(pair, b_np, args.lam, opts)  # H2D b, solve, D2H x inside the call
+        r = solve(b_np)  # H2D b, solve, D2H x inside the call
     barrier()
     e2e_s = maxed(time.perf_counter() - t0)
     e2e_value = args.iters * e2e_steps / e2e_s
 
     hbm_peak, sm_mhz, peak_src = peaks()
+    solver_desc = f"LSMR lambda={args.lam}" if args.solver == "lsmr" else args.solver.upper()
+    config_name = {("lsmr", "joseph"): "BASELINE config 3", ("lsqr", "siddon"): "BASELINE config 2",
+                   ("cgls", "joseph"): "BASELINE config 1"}.get((args.solver, args.projector), "custom")
     # this rank's share of the work: its angle block (angle) or its slab of slices (slab)
     my_angles = count if args.shard == "angle" else na
     my_slices = n if args.shard == "angle" else nzl
@@ -339,8 +352,9 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic: Shepp-Logan 3D rasterised on device (phantom.hpp), b = A x (GPU Ax)",
-        "config": {"workload": f"LSMR lambda={args.lam}, {args.iters} iters/step, {n}^3 volume, {n}^2 detector, "
-                               f"{na} angles, cone DSO=2n DOD=n pixel 1.5, matched Joseph (BASELINE config 3)",
+        "config": {"workload": f"{solver_desc}, {args.iters} iters/step, {n}^3 volume, {n}^2 detector, "
+                               f"{na} angles, cone DSO=2n DOD=n pixel 1.5, matched {args.projector.capitalize()} "
+                               f"({config_name})",
                    "parallelism": f"{args.shard}-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "inputs larger than L2 (volume 512 MiB, projections 360 MiB)"},
         "ax_gvox_s": ax_gvox,

@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -94,6 +95,14 @@ struct Geometry {
     DevBuf host_x, host_y;  // device staging for host-pointer entry points
     DevBuf red;         // reduction scratch (partials + results)
     double* pinned = nullptr;  // host-side reduction results
+    // solver workspaces, kept across solves on this handle (cudaMalloc/cudaFree per solve
+    // cost several ms and synchronise); slots are handed out in call order and only grow
+    std::vector<std::unique_ptr<DevBuf>> ws_pool;
+    size_t ws_next = 0;
+    DevBuf& ws_take() {
+        if (ws_next == ws_pool.size()) ws_pool.emplace_back(new DevBuf());
+        return *ws_pool[ws_next++];
+    }
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 
     size_t domain() const { return size_t(nx) * ny * (slab ? nzl : nz); }

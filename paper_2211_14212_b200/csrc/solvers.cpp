@@ -34,15 +34,23 @@ constexpr double breakdown_factor() {  // krylov.hpp:14-17
 }
 constexpr double kIncreaseSlack = 1e-12;  // solve_log.hpp:80
 
+// the handle whose workspace pool the current solve draws from (solve_device sets it)
+thread_local Geometry* t_pool = nullptr;
+DevBuf& pooled() {
+    if (!t_pool) fail(CTK_E_PARAMETER, "solver workspace requested outside a solve");
+    return t_pool->ws_take();
+}
+
 template <class T>
 struct Vec {
-    DevBuf buf;
+    DevBuf* buf = nullptr;
     size_t n = 0;
     T* p = nullptr;
     void alloc(size_t nn) {
         n = nn;
-        buf.ensure(sizeof(T) * std::max<size_t>(nn, 1));
-        p = buf.as<T>();
+        if (!buf) buf = &pooled();
+        buf->ensure(sizeof(T) * std::max<size_t>(nn, 1));
+        p = buf->as<T>();
     }
 };
 
@@ -79,16 +87,17 @@ struct Dev {
     // ---- one-slice halos of z-slab sharding (gradient.hpp:19-21 and its transpose) ----
     // Every rank's chosen slice is gathered by a sum-allreduce of a zeroed [nranks][nx*ny]
     // buffer in which each rank fills only its own row: one nonzero term per entry, exact.
-    DevBuf halo;
+    DevBuf* halo = nullptr;
     bool last_slab() const { return g.comm->cb.rank == g.comm->cb.nranks - 1; }
     const T* gather_slices(const T* slice) {
         const size_t S = size_t(g.nx) * g.ny, R = size_t(g.comm->cb.nranks);
-        halo.ensure(sizeof(T) * S * R);
-        fill<T>(S * R, T(0), halo.as<T>(), s);
-        CTK_CUDA(cudaMemcpyAsync(halo.as<T>() + size_t(g.comm->cb.rank) * S, slice, sizeof(T) * S,
+        if (!halo) halo = &pooled();
+        halo->ensure(sizeof(T) * S * R);
+        fill<T>(S * R, T(0), halo->as<T>(), s);
+        CTK_CUDA(cudaMemcpyAsync(halo->as<T>() + size_t(g.comm->cb.rank) * S, slice, sizeof(T) * S,
                                  cudaMemcpyDeviceToDevice, s));
-        comm_allreduce(g.comm, halo.p, S * R, sizeof(T) == 8 ? 1 : 0, s);
-        return halo.as<T>();
+        comm_allreduce(g.comm, halo->p, S * R, sizeof(T) == 8 ? 1 : 0, s);
+        return halo->as<T>();
     }
     // the next rank's first slice of x (null when unsharded or on the last slab)
     const T* slice_above(const T* x) {
@@ -421,7 +430,7 @@ void hybrid_lsqr(Dev<T>& d, const T* b, const ctk_hybrid_strategy& strat, const 
     if (strat.kind < 0 || strat.kind > 2) fail(CTK_E_PARAMETER, "unknown lambda strategy");
     Monitor<T> mon(d, b, o, log, "hybrid_lsqr");
     const int cap = o.max_iters + 2;
-    DevBuf Ub, Vb, coefb, scratchb;
+    DevBuf &Ub = pooled(), &Vb = pooled(), &coefb = pooled(), &scratchb = pooled();
     Ub.ensure(sizeof(T) * nr * size_t(cap));
     Vb.ensure(sizeof(T) * nd * size_t(cap));
     coefb.ensure(sizeof(double) * size_t(cap));
@@ -441,7 +450,7 @@ void hybrid_lsqr(Dev<T>& d, const T* b, const ctk_hybrid_strategy& strat, const 
     int nu_ = 1, nv_ = 1;
     std::vector<double> alphas{alpha1}, betas;
     Vec<T> ynum;
-    DevBuf dy;
+    DevBuf& dy = pooled();
     dy.ensure(sizeof(double) * size_t(cap));
     int k = 0;
     while (k < o.max_iters) {
@@ -643,7 +652,7 @@ void abba_gmres(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve
     const size_t n = ab ? nr : nd;  // Arnoldi space
     Monitor<T> mon(d, b, o, log, ab ? "ab_gmres" : "ba_gmres");
     const int cap = o.max_iters + 1;
-    DevBuf Wb, dyb;
+    DevBuf &Wb = pooled(), &dyb = pooled();
     Wb.ensure(sizeof(T) * n * size_t(cap));
     dyb.ensure(sizeof(double) * size_t(cap));
     T* W = Wb.as<T>();
@@ -748,7 +757,7 @@ void flsqr_tv(Dev<T>& d, const T* b, const ctk_hybrid_strategy& strat, const ctk
     Monitor<T> mon(d, b, o, log, "flsqr_tv");
     log->n_warnings = 0;
     const int cap = o.max_iters + 2;
-    DevBuf Ub, Vb, Zb, coefb;
+    DevBuf &Ub = pooled(), &Vb = pooled(), &Zb = pooled(), &coefb = pooled();
     Ub.ensure(sizeof(T) * nr * size_t(cap));
     Vb.ensure(sizeof(T) * nd * size_t(cap));
     Zb.ensure(sizeof(T) * nd * size_t(cap));
@@ -892,6 +901,10 @@ void solve_device(Geometry& g, int solver, int variant, const T* d_b, double lam
     if (variant != CTK_BP_MATCHED && variant != CTK_BP_VOXEL_DRIVEN) fail(CTK_E_PARAMETER, "unknown backprojector variant");
     const int need = solver == 4 ? std::max(1, outer) * std::max(1, inner) : (o ? o->max_iters : 0);
     validate_opts(o, log, need);
+    struct PoolScope {  // hand out this handle's workspace slots from the start
+        explicit PoolScope(Geometry& gg) { gg.ws_next = 0; t_pool = &gg; }
+        ~PoolScope() { t_pool = nullptr; }
+    } pool_scope(g);
     Dev<T> d(g, variant);
     switch (solver) {
         case 0: cgls<T>(d, d_b, *o, d_x, log); break;
