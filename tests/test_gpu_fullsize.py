@@ -1,0 +1,96 @@
+"""Size-independent properties at BASELINE.json's full C3 size (512^3 volume, 512^2
+detector, 360 views; the oracle cannot run there): adjointness of the matched f32 pair,
+linearity, the slab partition, A^T b restriction, and bitwise rerun determinism of a solve.
+Also the C2 Siddon pair at its full size (256^3, 180 views)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctk():
+    import paper_2211_14212_b200 as m
+
+    m.load()
+    return m
+
+
+@pytest.fixture(scope="module")
+def c3(ctk):
+    import torch
+
+    g = ctk.bench_geometry(512, 360)
+    pair = ctk.projector_pair(g)
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.rand(pair.domain_size, device="cuda", generator=gen)
+    y = torch.rand(pair.range_size, device="cuda", generator=gen)
+    return g, pair, x, y
+
+
+def _dot(a, b):
+    return float((a.double() * b.double()).sum())
+
+
+def test_c3_matched_adjoint(ctk, c3):
+    g, pair, x, y = c3
+    ax = pair.apply_forward(x)
+    aty = pair.apply_back(y)
+    lhs, rhs = _dot(ax, y), _dot(x, aty)
+    assert abs(lhs - rhs) <= 2e-6 * abs(lhs)  # same f32 positions and weights both ways
+
+
+def test_c3_linearity_and_determinism(ctk, c3):
+    import torch
+
+    g, pair, x, y = c3
+    x2 = torch.flip(x, [0]).contiguous()
+    a1, a2 = pair.apply_forward(x), pair.apply_forward(x2)
+    a12 = pair.apply_forward(x + x2)
+    rel = float((a12.double() - a1.double() - a2.double()).norm() / a12.double().norm())
+    assert rel < 1e-6
+    assert torch.equal(pair.apply_forward(x), a1)  # bitwise rerun
+    b1 = pair.apply_back(y)
+    assert torch.equal(pair.apply_back(y), b1)
+
+
+def test_c3_slab_partition(ctk, c3):
+    import torch
+
+    from paper_2211_14212_b200.comm import shard_slabs
+
+    g, pair, x, y = c3
+    n = 512 * 512
+    full_ax = pair.apply_forward(x)
+    full_bt = pair.apply_back(y)
+    acc = torch.zeros_like(full_ax, dtype=torch.float64)
+    for r in range(4):
+        z0, cnt = shard_slabs(512, 4, r)
+        p = ctk.projector_pair(g, slab=(z0, cnt))
+        acc += p.apply_forward(x[z0 * n:(z0 + cnt) * n].contiguous()).double()
+        assert torch.equal(p.apply_back(y), full_bt[z0 * n:(z0 + cnt) * n])
+    assert float((acc - full_ax.double()).norm() / full_ax.double().norm()) < 2e-6
+
+
+def test_c3_lsmr_rerun_bitwise(ctk, c3):
+    g, pair, x, y = c3
+    b = pair.apply_forward(ctk.shepp_logan_3d(512))
+    opts = ctk.SolverOptions(max_iters=3, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
+    r1 = ctk.lsmr(pair, b, 30.0, opts)
+    r2 = ctk.lsmr(pair, b, 30.0, opts)
+    assert r1.log.explicit_residual == r2.log.explicit_residual
+    assert r1.log.implicit_residual == r2.log.implicit_residual
+    expl = r1.log.explicit_residual
+    assert expl[0] > expl[1] > expl[2]  # LSMR's residual decreases on consistent data
+
+
+def test_c2_siddon_adjoint(ctk):
+    import torch
+
+    g = ctk.bench_geometry(256, 180)
+    pair = ctk.projector_pair(g, projector=ctk.ProjectorKind.siddon)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.rand(pair.domain_size, device="cuda", generator=gen)
+    y = torch.rand(pair.range_size, device="cuda", generator=gen)
+    lhs, rhs = _dot(pair.apply_forward(x), y), _dot(x, pair.apply_back(y))
+    assert abs(lhs - rhs) <= 2e-6 * abs(lhs)
