@@ -124,9 +124,17 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
 
-    float acc[BP_KB];
+    // BP_KB accumulators as packed pairs: phase 2 adds wh * Z with FFMA2 (per element the
+    // scalar fma)
+    float2 acc2[BP_KB / 2];
 #pragma unroll
-    for (int m = 0; m < BP_KB; ++m) acc[m] = 0.f;
+    for (int m = 0; m < BP_KB / 2; ++m) acc2[m] = make_float2(0.f, 0.f);
+    auto add_entry = [&](float wh, int e) {
+        const float2 w2 = make_float2(wh, wh);
+#pragma unroll
+        for (int m = 0; m < BP_KB / 2; ++m)
+            acc2[m] = __ffma2_rn(w2, make_float2(Z[(2 * m) * BP_PB + e], Z[(2 * m + 1) * BP_PB + e]), acc2[m]);
+    };
 
     // candidate detector-column range of every view for this tile (projection of the
     // tile's row segment in the plane), computed once, in parallel
@@ -380,8 +388,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         const int e = lst[q] >> 1;
                         const float th = eth[e];
                         const float wh = (lst[q] & 1) ? th : 1.f - th;
-#pragma unroll
-                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_PB + e], acc[m]);
+                        add_entry(wh, e);
                     }
                 } else {
                     // overflow (very fine detector sampling): scan every slot of the batch in order
@@ -397,8 +404,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         if (ih == p) wh = 1.f - th;
                         else if (ih + 1 == p && th != 0.f) wh = th;
                         else continue;
-#pragma unroll
-                        for (int m = 0; m < BP_KB; ++m) acc[m] = fmaf(wh, Z[m * BP_PB + e], acc[m]);
+                        add_entry(wh, e);
                     }
                 }
             }
@@ -412,8 +418,9 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
             if (k >= g.nz) break;
             const size_t o = CLASS ? size_t(p) + size_t(g.nx) * (size_t(s) + size_t(g.ny) * k)
                                    : size_t(s) + size_t(g.nx) * (size_t(p) + size_t(g.ny) * k);
-            if (CLASS == 0) x[o] = acc[m];
-            else x[o] += acc[m];
+            const float am = (m & 1) ? acc2[m >> 1].y : acc2[m >> 1].x;
+            if (CLASS == 0) x[o] = am;
+            else x[o] += am;
         }
     }
 }
