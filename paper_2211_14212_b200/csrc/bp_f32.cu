@@ -177,6 +177,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     }
     __syncthreads();
     const int total = pref[g.na];
+    int a_run = 0;  // this thread's slot view, advanced monotonically across batches
 
     for (int b0 = 0; b0 < total; b0 += BP_PB) {
         {
@@ -184,14 +185,9 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
             cnt[t] = 0;
             int a = -1, iu = 0;
             const int gidx = b0 + t;
-            if (gidx < total) {  // the view of this slot: last a with pref[a] <= gidx
-                int lo = 0, hi = g.na - 1;
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (pref[mid] <= gidx) lo = mid;
-                    else hi = mid - 1;
-                }
-                a = lo;
+            if (gidx < total) {  // the view of this slot: pref[a] <= gidx < pref[a + 1]
+                while (pref[a_run + 1] <= gidx) ++a_run;  // monotone over batches: ~1 step
+                a = a_run;
                 iu = urange[a].x + (gidx - pref[a]);
             }
             slotcol[t] = a >= 0 ? a * g.nu + iu : -1;
@@ -377,11 +373,14 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                     int lst[BP_SL];
 #pragma unroll
                     for (int q = 0; q < BP_SL; ++q) lst[q] = q < n ? lists[t * BP_SL + q] : 0x7fffffff;
+                    // insertion sort of the n registered entries (n is small: 2-6 typically)
 #pragma unroll
-                    for (int i = 1; i < BP_SL; ++i)
+                    for (int i = 1; i < BP_SL; ++i) {
+                        if (i >= n) break;
 #pragma unroll
-                        for (int j = BP_SL - 1; j >= i; --j)
+                        for (int j = i; j > 0; --j)
                             if (lst[j - 1] > lst[j]) { const int tmp = lst[j]; lst[j] = lst[j - 1]; lst[j - 1] = tmp; }
+                    }
 #pragma unroll
                     for (int q = 0; q < BP_SL; ++q) {
                         if (q >= n) break;
