@@ -67,23 +67,11 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 //           the columns registered in its row, sorted by column -> deterministic order.
 // Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
 // their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
-// measured at 512^3 / 360 views: without view batching 4 CTAs/SM (64 regs) was best (89 ms;
-// prefetch at 3 CTAs/SM 111 ms, at 4 CTAs/SM 92 ms); with batching and 12-entry row lists
-// (60 KB of shared memory) 3 CTAs/SM: 82.4 ms
+// measured at 512^3 / 360 views: without view batching 4 CTAs/SM (64 regs) was best; with
+// batching, 12-entry row lists (60 KB of shared memory) and 3 CTAs/SM: 82.4 ms (8-entry lists
+// at 3 or 4 CTAs/SM overflow into the slow scan: 82-95 ms)
 #ifndef CTK_BP_MINB
 #define CTK_BP_MINB 3
-#endif
-#ifndef CTK_BP_PREFETCH
-#define CTK_BP_PREFETCH 0
-#endif
-#ifndef CTK_BP_U2
-#define CTK_BP_U2 1  // two row groups per iteration (87 ms vs 89 ms)
-#endif
-#ifndef CTK_BP_PAIR
-#define CTK_BP_PAIR 1  // packed f32x2 row positions (87.3 -> 86.3 ms)
-#endif
-#ifndef CTK_BP_UCLAMP
-#define CTK_BP_UCLAMP 1
 #endif
 #ifndef CTK_BP_SL
 #define CTK_BP_SL 12  // row list capacity: a batch can register entries of two views in a row
@@ -260,24 +248,13 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 A = ak + w0;
                                 B = bk + w1;
                                 cur = kk;
-#if CTK_BP_UCLAMP
                                 // one unsigned clamp: kk < -BP_ZG wraps high and lands in the top guard rows
                                 float* zp = zc - BP_ZG * BP_PB + min(unsigned(kk + BP_ZG), unsigned(BP_KB + 2 * BP_ZG - 2)) * BP_PB;
-#else
-                                float* zp = zc + min(max(kk, -BP_ZG), BP_KB + BP_ZG - 2) * BP_PB;
-#endif
                                 zp[0] = A;
                                 zp[BP_PB] = B;
                             };
-                            auto step = [&](float vd, float yv) {
-                                const float fz = fmaf(vd, gs, czf);
-                                const float tt = split_t(fz);
-                                const float tz = split_frac(fz, tt);
-                                step_w(tt, tz, 1.f - tz, yv);
-                            };
-#if CTK_BP_PAIR
                             // the row positions of a 4-row group in packed f32x2 arithmetic
-                            // (FFMA2 / FADD2): per lane the same operations as step()
+                            // (FFMA2 / FADD2): per lane fz = fmaf(vd, gs, cz), the floor and the fraction
                             const float2 gs2 = make_float2(gs, gs), cz2 = make_float2(czf, czf);
                             const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
                             const float2 m1 = make_float2(-1.f, -1.f), one2 = make_float2(1.f, 1.f);
@@ -289,7 +266,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 step_w(tt.x, tz.x, omt.x, ya);
                                 step_w(tt.y, tz.y, omt.y, yb);
                             };
-#endif
                             // whole 4-row groups; only the first and last are masked to [v0, v1]
                             const float4* vd4 = reinterpret_cast<const float4*>(vdtab);
                             const int q0 = v0 >> 2, q1 = v1 >> 2;
@@ -302,29 +278,10 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                     y4.z = (b + 2 >= v0 && b + 2 <= v1) ? y4.z : 0.f;
                                     y4.w = (b + 3 >= v0 && b + 3 <= v1) ? y4.w : 0.f;
                                 }
-#if CTK_BP_PAIR
                                 step2(make_float2(d4.x, d4.y), y4.x, y4.y);
                                 step2(make_float2(d4.z, d4.w), y4.z, y4.w);
-#else
-                                step(d4.x, y4.x);
-                                step(d4.y, y4.y);
-                                step(d4.z, y4.z);
-                                step(d4.w, y4.w);
-#endif
                             };
-                            // software pipelined: the next group's load is in flight while the
-                            // current group is marched
-#if CTK_BP_PREFETCH
-                            const float4 yfirst = __ldg(pc4 + q0 * qs);
-                            float4 ynext = q1 > q0 ? __ldg(pc4 + (q0 + 1) * qs) : yfirst;
-                            group(q0, yfirst, true);
-                            for (int q = q0 + 1; q < q1; ++q) {
-                                const float4 y4 = ynext;
-                                ynext = __ldg(pc4 + (q + 1) * qs);
-                                group(q, y4, false);
-                            }
-                            if (q1 > q0) group(q1, ynext, true);
-#elif CTK_BP_U2
+                            // two row groups per iteration: two 16-byte loads in flight
                             group(q0, __ldg(pc4 + q0 * qs), true);
                             int q = q0 + 1;
                             for (; q + 1 < q1; q += 2) {  // two loads in flight per iteration
@@ -334,11 +291,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             }
                             if (q < q1) group(q, __ldg(pc4 + q * qs), false);
                             if (q1 > q0) group(q1, __ldg(pc4 + q1 * qs), true);
-#else
-                            group(q0, __ldg(pc4 + q0 * qs), true);
-                            for (int q = q0 + 1; q < q1; ++q) group(q, __ldg(pc4 + q * qs), false);
-                            if (q1 > q0) group(q1, __ldg(pc4 + q1 * qs), true);
-#endif
                             zero_rows(cur + 2, BP_KB);
                         } else {
                             // no rows, or degenerate geometry (stencil point not in front of the source)
