@@ -76,7 +76,10 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 #ifndef CTK_BP_SL
 #define CTK_BP_SL 12  // row list capacity: a batch can register entries of two views in a row
 #endif
-constexpr int BP_PB = 256, BP_KB = 32, BP_SL = CTK_BP_SL;
+#ifndef CTK_BP_KB
+#define CTK_BP_KB 32
+#endif
+constexpr int BP_PB = 256, BP_KB = CTK_BP_KB, BP_SL = CTK_BP_SL;
 constexpr int BP_ZG = 2;  // guard rows of Z on each side: out-of-band entries land there, unread
 
 template <int CLASS>
