@@ -173,37 +173,42 @@ __global__ void __launch_bounds__(128) k_atb_matched_exact(KGeom g, int nparts, 
     const double xc = (i - 0.5 * (g.nx - 1)) * h, yc = (j - 0.5 * (g.ny - 1)) * h, zc = (k - 0.5 * (g.nz - 1)) * h;
     const int vidx[3] = {i, j, k};
     const size_t frame = size_t(g.nu) * g.nv;
-    const double cu = 0.5 * (g.nu - 1), cvv = 0.5 * (g.nv - 1), eps = 1e-6;
+    const double cu = 0.5 * (g.nu - 1), cvv = 0.5 * (g.nv - 1);
     double out = 0;
     for (int t = 0; t < nparts; ++t) {
         double part = 0;
         for (int a = t; a < g.na; a += nparts) {
             const double2 cs = g.ctst[a];
-            double umin = DBL_MAX, umax = -DBL_MAX, vmin = DBL_MAX, vmax = -DBL_MAX;
+            // candidate window in f32: only a superset of the touching rays is needed (each
+            // candidate is decided by the exact plan_walk test); 1e-2-pixel slack
+            float umin = FLT_MAX, umax = -FLT_MAX, vmin = FLT_MAX, vmax = -FLT_MAX;
             bool all = false;
+            const float ctf = float(cs.x), stf = float(cs.y), hf = float(h);
+            const float zlo = float(zc - h), zhi = float(zc + h);
             for (int q = 0; q < 4; ++q) {  // the cube's 4 (x, y) corners, each with z = zc -+ h
-                const double x = xc + ((q & 1) ? h : -h), y = yc + ((q & 2) ? h : -h);
-                double u, tz;
+                const float x = float(xc) + ((q & 1) ? hf : -hf), y = float(yc) + ((q & 2) ? hf : -hf);
+                float u, tz;
                 if (g.mode == CTK_CONE3D) {
-                    const double depth = g.dso - (x * cs.x + y * cs.y);
-                    if (!(depth > 1e-9 * g.dso)) { all = true; break; }
-                    tz = (g.dso + g.dod) / depth;
-                    u = (-x * cs.y + y * cs.x) * tz;
+                    const float depth = float(g.dso) - (x * ctf + y * stf);
+                    if (!(depth > 1e-6f * float(g.dso))) { all = true; break; }
+                    tz = float(g.dso + g.dod) * __frcp_rn(depth);
+                    u = (-x * stf + y * ctf) * tz;
                 } else {
-                    tz = 1.0;
-                    u = -x * cs.y + y * cs.x;
+                    tz = 1.f;
+                    u = -x * stf + y * ctf;
                 }
-                umin = fmin(umin, u); umax = fmax(umax, u);
-                vmin = fmin(vmin, fmin((zc - h) * tz, (zc + h) * tz));
-                vmax = fmax(vmax, fmax((zc - h) * tz, (zc + h) * tz));
+                umin = fminf(umin, u); umax = fmaxf(umax, u);
+                vmin = fminf(vmin, fminf(zlo * tz, zhi * tz));
+                vmax = fmaxf(vmax, fmaxf(zlo * tz, zhi * tz));
             }
             int iu0 = 0, iu1 = g.nu - 1, iv0 = 0, iv1 = g.nv - 1;
             if (!all) {
-                iu0 = max(iu0, int(ceil(fmax(umin / g.du + cu - eps, -1e9))));
-                iu1 = min(iu1, int(floor(fmin(umax / g.du + cu + eps, 1e9))));
+                const float idu = float(1.0 / g.du), epsf = 1e-2f;
+                iu0 = max(iu0, int(ceilf(fmaxf(fmaf(umin, idu, float(cu) - epsf), -1e9f))));
+                iu1 = min(iu1, int(floorf(fminf(fmaf(umax, idu, float(cu) + epsf), 1e9f))));
                 if (g.nv > 1) {
-                    iv0 = max(iv0, int(ceil(fmax(vmin / g.du + cvv - eps, -1e9))));
-                    iv1 = min(iv1, int(floor(fmin(vmax / g.du + cvv + eps, 1e9))));
+                    iv0 = max(iv0, int(ceilf(fmaxf(fmaf(vmin, idu, float(cvv) - epsf), -1e9f))));
+                    iv1 = min(iv1, int(floorf(fminf(fmaf(vmax, idu, float(cvv) + epsf), 1e9f))));
                 }
             }
             const double* fa = pt + size_t(a) * frame;

@@ -138,40 +138,44 @@ __global__ void k_siddon_rayinv(KGeom g, double* __restrict__ inv) {
 
 // Detector window of the box [lo3, lo3 + h]^3 for one view: the pixel centres inside the
 // bounding box of the 8 corner projections (a ray meets the box iff its detector point lies
-// in the box's projection; the 1e-6-pixel slack absorbs rounding).  For a cone the four
-// (x, y) corners share one depth each: u = w D / depth, v = z D / depth -- four divisions.
-// false: the box is not strictly in front of the source (every pixel is a candidate).
+// in the box's projection).  Only a superset of the hit pixels is needed -- every candidate
+// is decided by the exact fp64 slab test -- so the window is computed in f32 with a
+// 1e-2-pixel slack (f32 error at |u| <= 2^12 pixels is < 1e-3).  For a cone the four (x, y)
+// corners share one depth each: u = w D / depth, v = z D / depth.  false: the box is not
+// strictly in front of the source (every pixel is a candidate).
 __device__ __forceinline__ bool s_window(const KGeom& g, double ct, double st, const double lo3[3], double h,
                                          int& iu0, int& iu1, int& iv0, int& iv1) {
-    double umin = DBL_MAX, umax = -DBL_MAX, vmin = DBL_MAX, vmax = -DBL_MAX;
-    const double z0 = lo3[2], z1 = lo3[2] + h;
+    float umin = FLT_MAX, umax = -FLT_MAX, vmin = FLT_MAX, vmax = -FLT_MAX;
+    const float ctf = float(ct), stf = float(st), hf = float(h);
+    const float z0 = float(lo3[2]), z1 = float(lo3[2] + h);
+    const float dso = float(g.dso), D = float(g.dso + g.dod);
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-        const double x = lo3[0] + ((q & 1) ? h : 0.0), y = lo3[1] + ((q & 2) ? h : 0.0);
-        const double w = -x * st + y * ct;
+        const float x = float(lo3[0]) + ((q & 1) ? hf : 0.f), y = float(lo3[1]) + ((q & 2) ? hf : 0.f);
+        const float w = -x * stf + y * ctf;
         if (g.mode == CTK_CONE3D) {
-            const double depth = g.dso - (x * ct + y * st);
-            if (!(depth > 1e-9 * g.dso)) return false;
-            const double t = (g.dso + g.dod) / depth;
-            umin = fmin(umin, w * t);
-            umax = fmax(umax, w * t);
-            vmin = fmin(vmin, fmin(z0 * t, z1 * t));
-            vmax = fmax(vmax, fmax(z0 * t, z1 * t));
+            const float depth = dso - (x * ctf + y * stf);
+            if (!(depth > 1e-6f * dso)) return false;
+            const float t = D * __frcp_rn(depth);
+            umin = fminf(umin, w * t);
+            umax = fmaxf(umax, w * t);
+            vmin = fminf(vmin, fminf(z0 * t, z1 * t));
+            vmax = fmaxf(vmax, fmaxf(z0 * t, z1 * t));
         } else {
-            umin = fmin(umin, w);
-            umax = fmax(umax, w);
+            umin = fminf(umin, w);
+            umax = fmaxf(umax, w);
             vmin = z0;
             vmax = z1;
         }
     }
-    const double cu = 0.5 * (g.nu - 1), cv = 0.5 * (g.nv - 1), eps = 1e-6;
-    iu0 = max(0, int(ceil(fmax(umin / g.du + cu - eps, -1e9))));
-    iu1 = min(g.nu - 1, int(floor(fmin(umax / g.du + cu + eps, 1e9))));
+    const float idu = float(1.0 / g.du), cu = 0.5f * float(g.nu - 1), cv = 0.5f * float(g.nv - 1), eps = 1e-2f;
+    iu0 = max(0, int(ceilf(fmaxf(fmaf(umin, idu, cu - eps), -1e9f))));
+    iu1 = min(g.nu - 1, int(floorf(fminf(fmaf(umax, idu, cu + eps), 1e9f))));
     iv0 = 0;
     iv1 = g.nv - 1;
     if (g.nv > 1) {
-        iv0 = max(0, int(ceil(fmax(vmin / g.du + cv - eps, -1e9))));
-        iv1 = min(g.nv - 1, int(floor(fmin(vmax / g.du + cv + eps, 1e9))));
+        iv0 = max(0, int(ceilf(fmaxf(fmaf(vmin, idu, cv - eps), -1e9f))));
+        iv1 = min(g.nv - 1, int(floorf(fminf(fmaf(vmax, idu, cv + eps), 1e9f))));
     }
     return true;
 }
