@@ -35,7 +35,7 @@ namespace {
 #define CTK_FWD_PAIR 1  // packed f32x2 (FFMA2/FADD2) slice pairs: 63.4 vs 64.8 ms unchunked, 48.6 vs 50.4 ms chunked
 #endif
 #ifndef CTK_FWD_CHUNKS
-#define CTK_FWD_CHUNKS 2  // slice chunks per ray for L2 locality (env CTK_FWD_CHUNKS overrides): 64.8 -> 50.4 ms at 512^3
+#define CTK_FWD_CHUNKS 2  // minimum slice chunks per ray (fwd_chunks); 64.8 -> 50.4 ms at 512^3 vs unchunked
 #endif
 #ifndef CTK_FWD_UNROLL
 #define CTK_FWD_UNROLL 2  // measured: 2 (48 regs, 5 CTAs/SM) beats 1, 3, 4, 8 at 256^3 and 512^3
@@ -74,16 +74,16 @@ __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict
 }
 
 // MODE 0: y = A x.   MODE 1: per-block partial of sum (A x - b)^2 (y never stored).
-// nch > 1 (MODE 0 only): slice chunking for L2 locality -- blockIdx.z = band * nch + chunk,
-// each block sums the slices of its chunk and writes y[chunk] (a partial projection set),
-// reduced in chunk order afterwards (deterministic).
+// nch > 1 (MODE 0 only): slice chunking for L2 locality -- one launch per chunk of the
+// slices, in chunk order; chunk 0 writes y and later chunks add their partial sums to it
+// (deterministic: the launches are ordered on the stream).
 template <int MODE, class Off>
 __global__ void __launch_bounds__(ZW_BR * ZW_BC)
 k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
                const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
-               double* __restrict__ partials, int nch) {
+               double* __restrict__ partials, int nch, int chunk) {
     __shared__ float outs[ZW_BR][ZW_BC + 1];
-    const int band = blockIdx.z / nch, chunk = blockIdx.z - band * nch;
+    const int band = blockIdx.z;
     const int iv = band * ZW_BR + threadIdx.x;
     const int a = vorder[blockIdx.y];
     const int iu = blockIdx.x * ZW_BC + threadIdx.y;
@@ -221,8 +221,10 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
         const int t = threadIdx.x + ZW_BR * threadIdx.y;
         const int r = t / ZW_BC, cc = t % ZW_BC;
         const int ivw = band * ZW_BR + r, iuw = blockIdx.x * ZW_BC + cc;
-        if (ivw < g.nv && iuw < g.nu)
-            y[(size_t(chunk) * g.na + a) * g.nu * g.nv + size_t(ivw) * g.nu + iuw] = outs[r][cc];
+        if (ivw < g.nv && iuw < g.nu) {
+            float* yo = y + size_t(a) * g.nu * g.nv + size_t(ivw) * g.nu + iuw;
+            *yo = chunk == 0 ? outs[r][cc] : *yo + outs[r][cc];
+        }
     }
     if (MODE != 0) {
         double rr = 0.0;
@@ -246,18 +248,7 @@ void relayout_zfast(Geometry& g, const float* x, DevBuf& wx, DevBuf& wy, cudaStr
     after_launch("k_relayout_zfast");
 }
 
-dim3 fwd_grid(const Geometry& g, int nch = 1) {
-    return dim3((g.nu + ZW_BC - 1) / ZW_BC, g.na, unsigned((g.nv + ZW_BR - 1) / ZW_BR * nch));
-}
-
-// y = sum over chunks of the partial projection sets, in chunk order
-__global__ void k_sum_chunks(size_t n, int nch, const float* __restrict__ part, float* __restrict__ y) {
-    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
-        float acc = part[i];
-        for (int c = 1; c < nch; ++c) acc += part[size_t(c) * n + i];
-        y[i] = acc;
-    }
-}
+dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + ZW_BC - 1) / ZW_BC, g.na, (g.nv + ZW_BR - 1) / ZW_BR); }
 
 bool wide_offsets(const Geometry& g) {
     const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz_local() + 2);
@@ -265,24 +256,31 @@ bool wide_offsets(const Geometry& g) {
 }
 
 template <int MODE>
-void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s, int nch = 1) {
+void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s, int nch = 1,
+               int chunk = 0) {
     const KGeom k = g.kgeom();
     const int* vo = g.d_vorder.as<int>();
     const float *a0 = g.vx.as<float>(), *a1 = g.vy.as<float>();
     const dim3 blk(ZW_BR, ZW_BC);
     if (wide_offsets(g))
-        k_ax_zfast_f32<MODE, long long><<<fwd_grid(g, nch), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch);
+        k_ax_zfast_f32<MODE, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk);
     else
-        k_ax_zfast_f32<MODE, int><<<fwd_grid(g, nch), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch);
+        k_ax_zfast_f32<MODE, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk);
     after_launch(MODE == 0 ? "k_ax_zfast_f32" : "k_ax_zfast_f32_residual");
 }
 
-int fwd_chunks() {
-    static const int n = [] {
+// Slice chunks per ray: enough that the slab a (row band, chunk) pass touches -- about
+// 200 B per (slice, in-plane row) for a 32-row band -- stays near 26 MB, i.e. L2-resident
+// across all views; at least 2 (measured: 2 at 256^3 and 512^3, 8 at 1024^3: 3.06 s with 2
+// chunks vs 1.70 s with 8).  CTK_FWD_CHUNKS overrides.
+int fwd_chunks(const Geometry& g) {
+    static const int forced = [] {
         const char* e = std::getenv("CTK_FWD_CHUNKS");
-        return e ? std::max(1, std::atoi(e)) : CTK_FWD_CHUNKS;
+        return e ? std::max(1, std::atoi(e)) : 0;
     }();
-    return n;
+    if (forced) return forced;
+    const double slab = double(std::max(g.nx, g.ny)) * (std::max(g.nx, g.ny) + 2) * 200.0;
+    return std::max(CTK_FWD_CHUNKS, std::min(16, int(std::lround(slab / 26e6))));
 }
 
 double* residual_partials(Geometry& g, size_t& nblk) {
@@ -296,14 +294,10 @@ double* residual_partials(Geometry& g, size_t& nblk) {
 
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
     relayout_zfast(g, x, g.vx, g.vy, s);
-    const int nch = fwd_chunks();
+    const int nch = fwd_chunks(g);
     if (nch > 1) {
-        g.proj_t.ensure(size_t(nch) * g.range() * sizeof(float));
         CTK_CUDA(cudaEventRecord(g.ev0, s));
-        launch_ax<0>(g, x, g.proj_t.as<float>(), nullptr, nullptr, s, nch);
-        const size_t n = g.range();
-        k_sum_chunks<<<unsigned(std::min<size_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(n, nch, g.proj_t.as<float>(), y);
-        after_launch("k_sum_chunks");
+        for (int c = 0; c < nch; ++c) launch_ax<0>(g, x, y, nullptr, nullptr, s, nch, c);
         CTK_CUDA(cudaEventRecord(g.ev1, s));
         return;
     }
@@ -313,7 +307,7 @@ void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
 }
 
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
-    if (fwd_chunks() > 1) {  // chunked: A x into a scratch projection set, then the fused difference norm
+    if (fwd_chunks(g) > 1) {  // chunked: A x into a scratch projection set, then the fused difference norm
         g.host_y.ensure(g.range() * sizeof(float));
         ax_f32(g, x, g.host_y.as<float>(), s);
         RedWork w = red_work(&g);
