@@ -101,7 +101,9 @@ void solve_host(ctkb::Geometry& g, int solver, int variant, const T* hb, double 
                 int outer, int inner, int warm, const ctk_solver_opts* o, T* hx, ctk_solve_log* log) {
     if (!hb || !hx) ctkb::fail(CTK_E_PARAMETER, "null host buffer");
     const size_t nd = g.domain(), nr = g.range();
-    ctkb::DevBuf db, dx;
+    // the handle's staging buffers (kept between calls, like the solver workspaces)
+    ctkb::DevBuf& db = g.host_y;
+    ctkb::DevBuf& dx = g.host_x;
     db.ensure(sizeof(T) * nr);
     dx.ensure(sizeof(T) * nd);
     CTK_CUDA(cudaMemcpyAsync(db.p, hb, sizeof(T) * nr, cudaMemcpyHostToDevice, g.stream));

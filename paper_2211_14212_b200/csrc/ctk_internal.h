@@ -93,6 +93,7 @@ struct Geometry {
     DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
     DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers
     DevBuf host_x, host_y;  // device staging for host-pointer entry points
+    DevBuf ax_scratch;      // A x of the chunked explicit residual
     DevBuf red;         // reduction scratch (partials + results)
     double* pinned = nullptr;  // host-side reduction results
     // solver workspaces, kept across solves on this handle (cudaMalloc/cudaFree per solve

@@ -308,10 +308,10 @@ void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
 
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
     if (fwd_chunks(g) > 1) {  // chunked: A x into a scratch projection set, then the fused difference norm
-        g.host_y.ensure(g.range() * sizeof(float));
-        ax_f32(g, x, g.host_y.as<float>(), s);
+        g.ax_scratch.ensure(g.range() * sizeof(float));
+        ax_f32(g, x, g.ax_scratch.as<float>(), s);
         RedWork w = red_work(&g);
-        reduce_diff_nrm2sq<float>(g.range(), g.host_y.as<float>(), b, d_out, w, s);
+        reduce_diff_nrm2sq<float>(g.range(), g.ax_scratch.as<float>(), b, d_out, w, s);
         return;
     }
     relayout_zfast(g, x, g.vx, g.vy, s);
