@@ -88,6 +88,8 @@ struct Geometry {
     DevBuf d_rayinv;  // per ray: 1/d of make_ray, for the exact gathers (built on first use)
     bool rayinv_ready = false;
     DevBuf d_walk;    // per ray: the plan_walk parameters of the exact f64 path (built on first use)
+    DevBuf d_vscale;  // per view: parallel-beam scale of the voxel-driven f64 path (built on first use)
+    bool vscale_ready = false;
     bool walk_ready = false;
     // workspaces (grown lazily)
     DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
@@ -118,7 +120,7 @@ struct Geometry {
 // exact f64 path (kernels_f64.cu, compiled with --fmad=false)
 void launch_ax_exact_f64(const Geometry& g, const double* x, double* y, cudaStream_t s);
 void launch_atb_matched_exact_f64(Geometry& g, const double* y, double* x, cudaStream_t s);
-void launch_atb_voxel_f64(const Geometry& g, const double* y, double* x, cudaStream_t s);
+void launch_atb_voxel_f64(Geometry& g, const double* y, double* x, cudaStream_t s);
 
 // f32 performance path (kernels_f32.cu)
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s);

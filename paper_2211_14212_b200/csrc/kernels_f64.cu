@@ -348,21 +348,22 @@ void launch_atb_matched_exact_f64(Geometry& g, const double* y, double* x, cudaS
     after_launch("k_atb_matched_exact");
 }
 
-void launch_atb_voxel_f64(const Geometry& g, const double* y, double* x, cudaStream_t s) {
-    // per-view parallel-beam scale h / max(|cos|, |sin|) (projector.hpp:216-222), host libm
-    std::vector<double> sc(size_t(g.na), 0.0);
-    if (g.mode != CTK_CONE3D)
-        for (int a = 0; a < g.na; ++a) {
-            const double act = std::abs(g.ct[size_t(a)]), ast = std::abs(g.st[size_t(a)]);
-            sc[size_t(a)] = g.h / ((act < ast) ? ast : act);
-        }
-    DevBuf d_sc;
-    d_sc.ensure(sizeof(double) * sc.size());
-    CTK_CUDA(cudaMemcpyAsync(d_sc.p, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice, s));
+void launch_atb_voxel_f64(Geometry& g, const double* y, double* x, cudaStream_t s) {
+    if (!g.vscale_ready) {
+        // per-view parallel-beam scale h / max(|cos|, |sin|) (projector.hpp:216-222), host libm
+        std::vector<double> sc(size_t(g.na), 0.0);
+        if (g.mode != CTK_CONE3D)
+            for (int a = 0; a < g.na; ++a) {
+                const double act = std::abs(g.ct[size_t(a)]), ast = std::abs(g.st[size_t(a)]);
+                sc[size_t(a)] = g.h / ((act < ast) ? ast : act);
+            }
+        g.d_vscale.ensure(sizeof(double) * sc.size());
+        CTK_CUDA(cudaMemcpy(g.d_vscale.p, sc.data(), sizeof(double) * sc.size(), cudaMemcpyHostToDevice));
+        g.vscale_ready = true;
+    }
     const size_t n = g.domain();
-    k_atb_voxel_exact<<<unsigned((n + 127) / 128), 128, 0, s>>>(g.kgeom(), d_sc.as<double>(), y, x);
+    k_atb_voxel_exact<<<unsigned((n + 127) / 128), 128, 0, s>>>(g.kgeom(), g.d_vscale.as<double>(), y, x);
     after_launch("k_atb_voxel_exact");
-    CTK_CUDA(cudaStreamSynchronize(s));  // d_sc is released at scope exit
 }
 
 }  // namespace ctkb
