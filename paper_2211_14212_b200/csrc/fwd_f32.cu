@@ -250,9 +250,15 @@ void relayout_zfast(Geometry& g, const float* x, DevBuf& wx, DevBuf& wy, cudaStr
 
 dim3 fwd_grid(const Geometry& g) { return dim3((g.nu + ZW_BC - 1) / ZW_BC, g.na, (g.nv + ZW_BR - 1) / ZW_BR); }
 
+// 64-bit tap offsets once a padded layout exceeds 2^31 elements (volumes beyond ~1290^3);
+// CTK_FWD_WIDE=1 forces them (tests exercise that instantiation on small volumes)
 bool wide_offsets(const Geometry& g) {
+    static const bool forced = [] {
+        const char* e = std::getenv("CTK_FWD_WIDE");
+        return e && e[0] == '1';
+    }();
     const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz_local() + 2);
-    return mx >= 2147483000.0;
+    return forced || mx >= 2147483000.0;
 }
 
 template <int MODE>

@@ -94,3 +94,22 @@ def test_c2_siddon_adjoint(ctk):
     y = torch.rand(pair.range_size, device="cuda", generator=gen)
     lhs, rhs = _dot(pair.apply_forward(x), y), _dot(x, pair.apply_back(y))
     assert abs(lhs - rhs) <= 2e-6 * abs(lhs)
+
+
+def test_wide_offset_instantiation_matches(tmp_path):
+    """The 64-bit-offset forward (volumes beyond ~1290^3) forced on a small problem must give
+    the same projections as the 32-bit one."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys, numpy as np, torch; sys.path.insert(0, %r); import paper_2211_14212_b200 as ctk; "
+            "g = ctk.bench_geometry(64, 30); p = ctk.projector_pair(g); x = ctk.shepp_logan_3d(64); "
+            "y = p.apply_forward(x); np.save(sys.argv[1], y.cpu().numpy())") % root
+    outs = []
+    for wide in ("0", "1"):
+        f = str(tmp_path / f"y{wide}.npy")
+        subprocess.run([sys.executable, "-c", code, f], check=True, env={**os.environ, "CTK_FWD_WIDE": wide})
+        outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
