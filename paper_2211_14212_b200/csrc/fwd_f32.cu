@@ -7,12 +7,14 @@
 // a warp = 32 consecutive detector ROWS of one column has one in-plane index ih per slice
 // and consecutive z indices: each tap load of the warp is one contiguous z run (1-2 lines).
 //
-// Grid order = L2 reuse.  The volume (512 MiB at 512^3) does not fit the 126 MB L2, and
-// every view crosses all of it.  Blocks are dispatched with the detector-row band
-// SLOWEST: at any time the resident blocks cover every view of one band of rows, whose
-// rays stay in one z-slab of the volume, so each slab comes from HBM about once per Ax
-// instead of once per view.  Views are visited class by class (x-dominant first) so only
-// one of the two layout copies is hot at a time.
+// L2 reuse.  The volume (512 MiB at 512^3) does not fit the 126 MB L2 and every view
+// crosses all of it.  Each ray's slices are split into chunks, one launch per chunk (in
+// order, accumulating into y); inside a launch blocks are dispatched with the detector-row
+// band SLOWEST and views class by class (x-dominant first), so the resident blocks cover
+// every view of one (band, chunk), whose samples stay in one ~26 MB slab of one layout copy:
+// that slab comes from HBM about once per launch instead of once per view.
+//
+// Samples are taken two slices at a time in packed f32x2 arithmetic (FFMA2 / FADD2.RM).
 #include <climits>
 #include <cstdlib>
 
