@@ -93,6 +93,7 @@ struct Geometry {
     bool walk_ready = false;
     // workspaces (grown lazily)
     DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
+    DevBuf dx64, dy64;  // z-fast f64 copies for the exact forward: X[i][j][k], Y[j][i][k]
     DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers
     DevBuf host_x, host_y;  // device staging for host-pointer entry points
     DevBuf ax_scratch;      // A x of the chunked explicit residual
@@ -118,7 +119,7 @@ struct Geometry {
 
 // ---- kernels (launch wrappers) ---------------------------------------------------------
 // exact f64 path (kernels_f64.cu, compiled with --fmad=false)
-void launch_ax_exact_f64(const Geometry& g, const double* x, double* y, cudaStream_t s);
+void launch_ax_exact_f64(Geometry& g, const double* x, double* y, cudaStream_t s);
 void launch_atb_matched_exact_f64(Geometry& g, const double* y, double* x, cudaStream_t s);
 void launch_atb_voxel_f64(Geometry& g, const double* y, double* x, cudaStream_t s);
 

@@ -78,14 +78,29 @@ __device__ __forceinline__ void clip_axis(double f0, double fd, double lo, doubl
     s1 = min(s1, int(ceil(hi_s)) + 1);
 }
 
-__global__ void k_ax_exact(KGeom g, const double* __restrict__ vol, double* __restrict__ proj) {
-    const int iu = blockIdx.x * blockDim.x + threadIdx.x;
-    const int iv = blockIdx.y * blockDim.y + threadIdx.y;
+// forward_project (projector.hpp:134-162): thread per ray, make_walk + the slice loop
+// operation for operation; lanes along detector ROWS and z-fastest copies of the volume, so
+// a warp's taps are consecutive in memory: x-dominant rays read X[i][j][k] (slice i, b = y,
+// c = z), y-dominant rays Y[j][i][k] (slice j, b = z, c = x), z-dominant rays the original
+// x[k][j][i].  Only the strides change -- the taps, weights, skips and summation order are
+// make_walk's, so the result is bit-identical to the reference.
+__global__ void k_ax_exact_zfast(KGeom g, const double* __restrict__ vol, const double* __restrict__ vx,
+                                 const double* __restrict__ vy, double* __restrict__ proj) {
+    const int iv = blockIdx.x * blockDim.x + threadIdx.x;
+    const int iu = blockIdx.y * blockDim.y + threadIdx.y;
     const int a = blockIdx.z;
     if (iu >= g.nu || iv >= g.nv) return;
     const double2 cs = g.ctst[a];
     Walk w;
     make_walk(g, cs.x, cs.y, iu, iv, w);
+    const double* src = vol;
+    if (w.axis == 0) {
+        src = vx;
+        w.sa = size_t(g.ny) * g.nz; w.sb = size_t(g.nz); w.sc = 1;
+    } else if (w.axis == 1) {
+        src = vy;
+        w.sa = size_t(g.nx) * g.nz; w.sb = 1; w.sc = size_t(g.nz);
+    }
     int s0 = 0, s1 = w.n_slices - 1;
     clip_axis(w.fb0, w.fb_d, -1.0, double(w.nb), s0, s1);
     clip_axis(w.fc0, w.fc_d, -1.0, double(w.nc), s0, s1);
@@ -103,11 +118,31 @@ __global__ void k_ax_exact(KGeom g, const double* __restrict__ vol, double* __re
         for (int q = 0; q < 4; ++q) {
             const int jb = ib + (q & 1), jc = ic + (q >> 1);
             if (jb < 0 || jb >= w.nb || jc < 0 || jc >= w.nc || wq[q] == 0.0) continue;
-            sample += wq[q] * __ldg(vol + base + w.sb * size_t(jb) + w.sc * size_t(jc));
+            sample += wq[q] * __ldg(src + base + w.sb * size_t(jb) + w.sc * size_t(jc));
         }
         acc += sample;
     }
     proj[size_t(a) * g.nu * g.nv + size_t(iu) + size_t(g.nu) * iv] = w.step * acc;
+}
+
+// x[k][j][i] -> X[i][j][k] and Y[j][i][k] (32 x 32 (i, k) tile transposes per j)
+__global__ void k_relayout_f64(int nx, int ny, int nz, const double* __restrict__ x, double* __restrict__ X,
+                               double* __restrict__ Y) {
+    __shared__ double tile[32][33];
+    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + threadIdx.x, k = k0 + r;
+        tile[r][threadIdx.x] = (i < nx && k < nz) ? x[size_t(i) + size_t(nx) * (j + size_t(ny) * k)] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, k = k0 + threadIdx.x;
+        if (i < nx && k < nz) {
+            const double v = tile[threadIdx.x][r];
+            X[(size_t(i) * ny + j) * nz + k] = v;
+            Y[(size_t(j) * nx + i) * nz + k] = v;
+        }
+    }
 }
 
 // Projection of a point onto continuous detector coordinates (fu, fv); false when the
@@ -321,11 +356,19 @@ __global__ void k_atb_voxel_exact(KGeom g, const double* __restrict__ scale_par,
 
 }  // namespace
 
-void launch_ax_exact_f64(const Geometry& g, const double* x, double* y, cudaStream_t s) {
+void launch_ax_exact_f64(Geometry& g, const double* x, double* y, cudaStream_t s) {
+    const size_t nvox = g.domain();
+    g.dx64.ensure(nvox * sizeof(double));
+    g.dy64.ensure(nvox * sizeof(double));
+    {
+        dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.nz + 31) / 32, g.ny);
+        k_relayout_f64<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x, g.dx64.as<double>(), g.dy64.as<double>());
+        after_launch("k_relayout_f64");
+    }
     dim3 blk(32, 4);
-    dim3 grd((g.nu + 31) / 32, (g.nv + 3) / 4, g.na);
-    k_ax_exact<<<grd, blk, 0, s>>>(g.kgeom(), x, y);
-    after_launch("k_ax_exact");
+    dim3 grd((g.nv + 31) / 32, (g.nu + 3) / 4, g.na);
+    k_ax_exact_zfast<<<grd, blk, 0, s>>>(g.kgeom(), x, g.dx64.as<double>(), g.dy64.as<double>(), y);
+    after_launch("k_ax_exact_zfast");
 }
 
 void launch_atb_matched_exact_f64(Geometry& g, const double* y, double* x, cudaStream_t s) {
