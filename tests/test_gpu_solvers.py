@@ -236,3 +236,56 @@ def test_blas1_deterministic(ctk):
     assert outs[0] == outs[1] == outs[2]
     want = float((x.double() * y.double()).sum())
     assert abs(outs[0] - want) <= 1e-12 * abs(want) * 100 + 1e-9
+
+
+@pytest.mark.parametrize("strategy", ["dp", "fixed"])
+def test_hybrid_lsqr_dp_fixed_parity(ctk, reference, problem, strategy):
+    g, gt, b = problem
+    k = 8
+    sid = {"fixed": 0, "dp": 1}[strategy]
+    want = reference.solve(g, b, "hybrid_lsqr", k, strategy=sid, lam=0.5, noise_level=0.01, tol=0.0, stop_inc=False)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float64)
+    st = ctk.HybridStrategy.fixed(0.5) if strategy == "fixed" else ctk.HybridStrategy.dp(0.01)
+    res = ctk.hybrid_lsqr(pair, b, st, _opts(ctk, k))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+    assert np.allclose(res.log.lambda_, want["lambda"], rtol=1e-3, atol=1e-12)
+
+
+@pytest.mark.parametrize("solver", ["sirt", "ab_gmres", "ba_gmres", "cgls"])
+def test_unmatched_pair_solver_parity(ctk, reference, problem, solver):
+    """The voxel-driven (unmatched) backprojector through the newer solvers (f64)."""
+    g, gt, b = problem
+    k = 6
+    want = reference.solve(g, b, solver, k, variant=1, tol=0.0, stop_inc=False)
+    pair = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant.voxel_driven, dtype=np.float64)
+    res = getattr(ctk, solver)(pair, b, _opts(ctk, k))
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+
+
+def test_cgls_tv_warm_start_parity(ctk, reference, problem):
+    g, gt, b = problem
+    outer, inner, lam = 2, 3, 0.5
+    want = reference.solve(g, b, "cgls_tv", 1, lam=lam, outer=outer, inner=inner, warm=True, tol=0.0, stop_inc=False)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float64)
+    res = ctk.cgls_tv(pair, b, lam, outer, inner, _opts(ctk, 1), warm_start=True)
+    assert rel_l2(res.x, want["x"]) < TOL
+    _check_hist(res, want)
+
+
+def test_siddon_lsqr_matches_restated(ctk, restated):
+    """Siddon has no reference implementation: the device LSQR on the Siddon pair against the
+    numpy LSQR recurrence on the (pinned) C restatement of the same operators."""
+    from geoms import cone_bench
+    from oracle.oracle import lsqr as lsqr_np
+
+    g = cone_bench(24, 20)
+    gt = restated.shepp_logan_3d(24, np.float64)
+    b = restated.siddon_forward(g, gt)
+    want = lsqr_np(lambda v: restated.siddon_forward(g, v), lambda v: restated.siddon_back(g, v), b, 8, tol=0.0,
+                   stop_inc=False)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float64, projector=ctk.ProjectorKind.siddon)
+    res = ctk.lsqr(pair, b, _opts(ctk, 8))
+    assert rel_l2(res.x, want["x"]) < 1e-9
+    assert np.allclose(res.log.explicit_residual, want["explicit"], rtol=1e-9)
