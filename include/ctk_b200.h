@@ -119,9 +119,25 @@ int ctk_axpy_f64(size_t n, double alpha, const double* d_x, double* d_y, void* s
 int ctk_scal_f32(size_t n, double alpha, float* d_x, void* stream);
 int ctk_scal_f64(size_t n, double alpha, double* d_x, void* stream);
 
-/* ---- synthetic input: make_phantom(shepp_logan_3d) (phantom.hpp:74-145) on device -- */
-int ctk_shepp_logan_3d_f32(int n, float* d_out, void* stream);
+/* ---- synthetic input: make_phantom (phantom.hpp:118-145) rasterised on the device -----
+ * kind follows PhantomKind (phantom.hpp:13): 0 shepp_logan_3d (n^3), 1 shepp_logan_2d
+ * (n*n*1), 2 piecewise_blocks (n*n*1).  Bit-identical to the reference's make_phantom<T>. */
+#define CTK_PHANTOM_SHEPP_LOGAN_3D 0
+#define CTK_PHANTOM_SHEPP_LOGAN_2D 1
+#define CTK_PHANTOM_PIECEWISE_BLOCKS 2
+int ctk_make_phantom_f32(int kind, int n, float* d_out, void* stream);
+int ctk_make_phantom_f64(int kind, int n, double* d_out, void* stream);
+int ctk_shepp_logan_3d_f32(int n, float* d_out, void* stream); /* = make_phantom(0, n) */
 int ctk_shepp_logan_3d_f64(int n, double* d_out, void* stream);
+
+/* ---- count-domain noise, add_noise (noise.hpp:26-47) on HOST buffers ----------------
+ * One mt19937_64 stream walked in detector-index order (a Poisson then a Gaussian draw
+ * per sample, libstdc++ distributions): sequential by definition, so it stays on the
+ * host and is bit-identical to the reference built with the
+ * same C++ standard library.  in/out may alias.  Errors: PARAMETER (i0 <= 0, sigma < 0),
+ * DEGENERATE (a negative line integral, checked before any output is written). */
+int ctk_add_noise_f32(size_t n, const float* h_in, double i0, double sigma, uint64_t seed, float* h_out);
+int ctk_add_noise_f64(size_t n, const double* h_in, double i0, double sigma, uint64_t seed, double* h_out);
 
 /* ---- solvers (solvers.hpp:13-231, hybrid.hpp:76-116, tv.hpp:45-110) ---------------- */
 /* SolverOptions, solve_log.hpp:42-57 */

@@ -78,22 +78,29 @@ ctk::ConeGeometry to_geom(const ref_geom* d) {
 }
 
 int g_err_iter = 0;
+std::string g_err_msg;
 
 template <class F>
 int guarded(F&& f) {
+    g_err_msg.clear();
     try {
         f();
         return 0;
-    } catch (const ctk::DimensionError&) {
+    } catch (const ctk::DimensionError& e) {
+        g_err_msg = e.what();
         return 1;
-    } catch (const ctk::GeometryError&) {
+    } catch (const ctk::GeometryError& e) {
+        g_err_msg = e.what();
         return 2;
-    } catch (const ctk::ParameterError&) {
+    } catch (const ctk::ParameterError& e) {
+        g_err_msg = e.what();
         return 3;
-    } catch (const ctk::DegenerateInputError&) {
+    } catch (const ctk::DegenerateInputError& e) {
+        g_err_msg = e.what();
         return 4;
     } catch (const ctk::NumericalError& e) {
         g_err_iter = e.iteration;
+        g_err_msg = e.what();
         return 5;
     } catch (...) {
         return 9;
@@ -374,3 +381,110 @@ int ref_write_pgm16(const char* path, int w, int h, const float* values, double 
     return guarded([&] { ctk::write_pgm16(path, w, h, values, wmin, wmax); });
 }
 }  // extern "C"
+
+// ---- pipeline, config, metrics (src/config.cpp, src/pipeline.cpp compiled from where
+//      they lie; include/ctkrylov/{config,pipeline,metrics,noise}.hpp) ----------------------
+#ifdef CTK_REF_WITH_EIGEN
+#include <fstream>
+#include <sstream>
+
+#include "ctkrylov/config.hpp"
+#include "ctkrylov/metrics.hpp"
+#include "ctkrylov/pipeline.hpp"
+
+extern "C" {
+int ref_last_error_message(char* buf, size_t cap) {
+    if (cap) {
+        std::strncpy(buf, g_err_msg.c_str(), cap - 1);
+        buf[cap - 1] = 0;
+    }
+    return int(g_err_msg.size());
+}
+
+int ref_add_noise_f32(const ref_geom* d, const float* clean, double i0, double sigma, std::uint64_t seed,
+                      float* out) {
+    return guarded([&] {
+        ctk::ProjectionSet<float> p(std::vector<double>(d->angles, d->angles + d->na), d->nu, d->nv);
+        std::memcpy(p.data.data(), clean, p.data.size() * sizeof(float));
+        auto r = ctk::add_noise(p, ctk::NoiseModel{i0, sigma, seed});
+        std::memcpy(out, r.data.data(), r.data.size() * sizeof(float));
+    });
+}
+
+// cmd: 0 simulate, 1 reconstruct, 2 compare; cfg_text is a key = value config
+int ref_run_pipeline(int cmd, const char* cfg_text) {
+    return guarded([&] {
+        std::istringstream in(cfg_text);
+        ctk::RunConfig cfg = ctk::parse_config(in);
+        if (cmd == 0) ctk::run_simulate(cfg);
+        else if (cmd == 1) ctk::run_reconstruct(cfg);
+        else ctk::run_compare(cfg);
+    });
+}
+
+// parse_config(cfg_text) then write_config to out_path (resolve != 0: resolve_geometry first)
+int ref_config_write(const char* cfg_text, int resolve, const char* out_path) {
+    return guarded([&] {
+        std::istringstream in(cfg_text);
+        ctk::RunConfig cfg = ctk::parse_config(in);
+        if (resolve) ctk::resolve_geometry(cfg);
+        std::ofstream f(out_path);
+        ctk::write_config(f, cfg);
+    });
+}
+
+// resolve_geometry(cfg): geometry out (angles into a caller buffer of >= n_angles)
+int ref_resolve_geometry(const char* cfg_text, ref_geom* out, double* angles) {
+    return guarded([&] {
+        std::istringstream in(cfg_text);
+        ctk::RunConfig cfg = ctk::parse_config(in);
+        const ctk::ConeGeometry g = ctk::resolve_geometry(cfg);
+        out->mode = int(g.mode);
+        out->dso = g.source_to_origin;
+        out->dod = g.origin_to_detector;
+        out->du = g.detector_pixel_size;
+        out->nu = g.nu;
+        out->nv = g.nv;
+        out->nx = g.vol.nx;
+        out->ny = g.vol.ny;
+        out->nz = g.vol.nz;
+        out->h = g.vol.spacing;
+        out->na = int(g.angles.size());
+        std::memcpy(angles, g.angles.data(), g.angles.size() * sizeof(double));
+    });
+}
+
+// write_csv of a log given its four columns (metrics.hpp:80-91)
+int ref_write_csv(const char* path, const double* impl, int n_impl, const double* expl, int n_expl,
+                  const double* err, int n_err, const double* lam, int n_lam) {
+    return guarded([&] {
+        ctk::ConvergenceLog log;
+        log.implicit_residual.assign(impl, impl + n_impl);
+        log.explicit_residual.assign(expl, expl + n_expl);
+        log.relative_error.assign(err, err + n_err);
+        log.lambda.assign(lam, lam + n_lam);
+        std::ofstream f(path);
+        ctk::write_csv(f, log);
+    });
+}
+
+// detect_semiconvergence / residual_divergence (metrics.hpp:40-75)
+int ref_semiconvergence(const double* err, int n, int* min_index, double* rebound) {
+    return guarded([&] {
+        ctk::ConvergenceLog log;
+        log.relative_error.assign(err, err + n);
+        const auto s = ctk::detect_semiconvergence(log);
+        *min_index = s.min_index;
+        *rebound = s.rebound_ratio;
+    });
+}
+int ref_residual_divergence(const double* impl, int n_impl, const double* expl, int n_expl, double* out) {
+    return guarded([&] {
+        ctk::ConvergenceLog log;
+        log.implicit_residual.assign(impl, impl + n_impl);
+        log.explicit_residual.assign(expl, expl + n_expl);
+        *out = ctk::residual_divergence(log);
+    });
+}
+}  // extern "C"
+#endif

@@ -15,9 +15,11 @@ from .api import (  # noqa: F401
     GeometryError,
     HybridStrategy,
     LambdaStrategy,
+    NoiseModel,
     NumericalError,
     OperatorPair,
     ParameterError,
+    PhantomKind,
     Projector,
     ProjectorKind,
     SolveResult,
@@ -39,6 +41,10 @@ from .api import (  # noqa: F401
     launch_count,
     lsmr,
     lsqr,
+    make_phantom,
+    add_noise,
+    noise_rng_id,
+    phantom_kind_from_string,
     projector_pair,
     shepp_logan_3d,
     sirt,

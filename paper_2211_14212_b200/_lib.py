@@ -132,6 +132,10 @@ def load():
         "ctk_scal_f64": (i, [sz, d, vp, vp]),
         "ctk_shepp_logan_3d_f32": (i, [i, vp, vp]),
         "ctk_shepp_logan_3d_f64": (i, [i, vp, vp]),
+        "ctk_make_phantom_f32": (i, [i, i, vp, vp]),
+        "ctk_make_phantom_f64": (i, [i, i, vp, vp]),
+        "ctk_add_noise_f32": (i, [sz, vp, d, d, C.c_uint64, vp]),
+        "ctk_add_noise_f64": (i, [sz, vp, d, d, C.c_uint64, vp]),
         "ctk_solve_dev_f32": (i, [vp, i, i, vp, d, C.POINTER(HybridStrategyC), i, i, i, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)]),
         "ctk_solve_dev_f64": (i, [vp, i, i, vp, d, C.POINTER(HybridStrategyC), i, i, i, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)]),
         "ctk_shard_angles": (i, [i, i, i, C.POINTER(i), C.POINTER(i)]),

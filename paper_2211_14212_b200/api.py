@@ -18,6 +18,8 @@ error classes                          types.hpp:14-31
 ``cgls`` ``lsqr`` ``lsmr``             solvers.hpp:13-231
 ``HybridStrategy`` / ``hybrid_lsqr``   hybrid.hpp:15-33, 76-116
 ``cgls_tv``                            tv.hpp:45-110
+``PhantomKind`` / ``make_phantom``     phantom.hpp:13, 118-152
+``NoiseModel`` / ``add_noise``         noise.hpp:10-47
 =====================================  ==================================================
 
 Every computation runs in libctk_b200.so (sm_100a kernels + C++ solvers) through the
@@ -107,6 +109,21 @@ class BackprojectVariant(IntEnum):
 class ProjectorKind(IntEnum):
     joseph = 0
     siddon = 1
+
+
+class PhantomKind(IntEnum):
+    """phantom.hpp:13."""
+    shepp_logan_3d = 0
+    shepp_logan_2d = 1
+    piecewise_blocks = 2
+
+
+def phantom_kind_from_string(s: str) -> PhantomKind:
+    """phantom.hpp:147-152."""
+    try:
+        return PhantomKind[s]
+    except KeyError:
+        raise ParameterError("unknown phantom kind: " + s) from None
 
 
 class StopReason(IntEnum):
@@ -591,15 +608,57 @@ def cgls_tv(pair: OperatorPair, b, lambda_: float, outer_iters: int, inner_iters
     return _solve("cgls_tv", pair, b, opts, lam=lambda_, outer=outer_iters, inner=inner_iters, warm=warm_start)
 
 
-# ---- synthetic input (phantom.hpp:74-145), generated on the device ---------------------------
-def shepp_logan_3d(n: int, dtype="float32", device="cuda"):
+# ---- synthetic input (phantom.hpp:118-145), generated on the device ---------------------------
+def make_phantom(kind: PhantomKind, n: int, dtype="float32", device="cuda"):
+    """make_phantom<T>(kind, n): shepp_logan_3d is n^3, the other two n*n*1 (x fastest).
+    Bit-identical to the reference's rasteriser."""
     import torch
 
-    t = torch.empty(n * n * n, dtype=getattr(torch, dtype), device=device)
-    lib = L.load()
+    kind = PhantomKind(kind)
+    nz = n if kind == PhantomKind.shepp_logan_3d else 1
+    t = torch.empty(max(n, 0) * max(n, 0) * nz, dtype=getattr(torch, dtype), device=device)
     suf = "f32" if dtype == "float32" else "f64"
-    _check(getattr(lib, f"ctk_shepp_logan_3d_{suf}")(n, C.c_void_p(t.data_ptr()), _torch_stream()))
+    _check(getattr(L.load(), f"ctk_make_phantom_{suf}")(int(kind), n, C.c_void_p(t.data_ptr()), _torch_stream()))
     return t
+
+
+def shepp_logan_3d(n: int, dtype="float32", device="cuda"):
+    return make_phantom(PhantomKind.shepp_logan_3d, n, dtype, device)
+
+
+# ---- measurement noise (noise.hpp:10-47) -------------------------------------------------------
+@dataclass
+class NoiseModel:
+    """noise.hpp:12-22: air counts I0, electronic sigma (counts), RNG seed."""
+    i0: float = 1e5
+    sigma: float = 0.5
+    seed: int = 0
+
+    def validate(self):
+        if not (self.i0 > 0.0):
+            raise ParameterError("noise model: I0 must be positive")
+        if self.sigma < 0.0:
+            raise ParameterError("noise model: sigma must be nonnegative")
+
+
+def noise_rng_id() -> str:
+    """noise.hpp:24-27 (recorded in run metadata)."""
+    return "mt19937_64+std::poisson/normal,sequential"
+
+
+def add_noise(proj, model: NoiseModel):
+    """add_noise<T> (noise.hpp:29-47) on a host array of line integrals -> a new array of
+    the same dtype.  The single sequential mt19937_64 stream runs in libctk_b200.so on the
+    host (the stream order is the definition; see csrc/noise.cpp)."""
+    model.validate()
+    a = np.asarray(proj)
+    dt = np.float64 if a.dtype == np.float64 else np.float32
+    src = np.ascontiguousarray(a, dtype=dt).reshape(-1)
+    out = np.empty_like(src)
+    fn = getattr(L.load(), "ctk_add_noise_" + ("f64" if dt == np.float64 else "f32"))
+    _check(fn(src.size, src.ctypes.data_as(C.c_void_p), float(model.i0), float(model.sigma),
+              int(model.seed) & 0xFFFFFFFFFFFFFFFF, out.ctypes.data_as(C.c_void_p)))
+    return out
 
 
 def launch_count() -> int:

@@ -269,17 +269,28 @@ int ctk_scal_f64(size_t n, double a, double* x, void* s) {
     return guard([&] { ctkb::scal<double>(n, a, x, static_cast<cudaStream_t>(s)); });
 }
 
-int ctk_shepp_logan_3d_f32(int n, float* out, void* s) {
+int ctk_make_phantom_f32(int kind, int n, float* out, void* s) {
     return guard([&] {
+        if (kind < 0 || kind > 2) ctkb::fail(CTK_E_PARAMETER, "unknown phantom kind");
         if (n < 8) ctkb::fail(CTK_E_PARAMETER, "phantom size must be at least 8");
-        ctkb::launch_shepp_logan_f32(n, out, static_cast<cudaStream_t>(s));
+        ctkb::launch_phantom_f32(kind, n, out, static_cast<cudaStream_t>(s));
     });
 }
-int ctk_shepp_logan_3d_f64(int n, double* out, void* s) {
+int ctk_make_phantom_f64(int kind, int n, double* out, void* s) {
     return guard([&] {
+        if (kind < 0 || kind > 2) ctkb::fail(CTK_E_PARAMETER, "unknown phantom kind");
         if (n < 8) ctkb::fail(CTK_E_PARAMETER, "phantom size must be at least 8");
-        ctkb::launch_shepp_logan_f64(n, out, static_cast<cudaStream_t>(s));
+        ctkb::launch_phantom_f64(kind, n, out, static_cast<cudaStream_t>(s));
     });
+}
+int ctk_shepp_logan_3d_f32(int n, float* out, void* s) { return ctk_make_phantom_f32(0, n, out, s); }
+int ctk_shepp_logan_3d_f64(int n, double* out, void* s) { return ctk_make_phantom_f64(0, n, out, s); }
+
+int ctk_add_noise_f32(size_t n, const float* in, double i0, double sigma, uint64_t seed, float* out) {
+    return guard([&] { ctkb::add_noise<float>(n, in, i0, sigma, seed, out); });
+}
+int ctk_add_noise_f64(size_t n, const double* in, double i0, double sigma, uint64_t seed, double* out) {
+    return guard([&] { ctkb::add_noise<double>(n, in, i0, sigma, seed, out); });
 }
 
 #define CTK_SOLVE_HOST(NAME, T, SOLVER)                                                                       \

@@ -142,8 +142,10 @@ template <class T>
 void siddon_atb(Geometry& g, const T* y, T* x, cudaStream_t s);
 
 // phantom (stencils.cu)
-void launch_shepp_logan_f32(int n, float* out, cudaStream_t s);
-void launch_shepp_logan_f64(int n, double* out, cudaStream_t s);
+template <class T>
+void add_noise(size_t n, const T* in, double i0, double sigma, uint64_t seed, T* out);  // noise.cpp, host
+void launch_phantom_f32(int kind, int n, float* out, cudaStream_t s);  // kind: PhantomKind order
+void launch_phantom_f64(int kind, int n, double* out, cudaStream_t s);
 
 // ---- BLAS-1 (blas1.cu): deterministic fp64 reductions ----------------------------------
 constexpr int kRedBlocks = 592;   // 4 x 148 SMs; fixed => fixed summation order

@@ -81,7 +81,10 @@ __global__ void k_tv_weights(int nx, int ny, int nz, const T* __restrict__ x, do
     }
 }
 
-// Shepp-Logan 3D: ten ellipsoids (phantom.hpp:77-89), cell-centre sampling (:93-112).
+// Synthetic ground truth, make_phantom (phantom.hpp:118-145).  Ellipsoid tables
+// (phantom.hpp:57-89; columns cx cy cz ax ay az phi intensity), `contains` (:31-39),
+// rasterised on cell centres (:93-112): a grid point sums the intensity of every ellipsoid that contains it, in table
+// order, in fp64 with the reference's operation order, then converts to T.
 __constant__ double c_sl3d[10][8] = {
     {0.0, 0.0, 0.0, 0.69, 0.92, 0.81, 0.0, 2.0},
     {0.0, -0.0184, 0.0, 0.6624, 0.874, 0.78, 0.0, -0.8},
@@ -94,19 +97,31 @@ __constant__ double c_sl3d[10][8] = {
     {0.0, -0.605, 0.0, 0.023, 0.023, 0.02, 0.0, 0.1},
     {0.06, -0.605, 0.0, 0.023, 0.046, 0.02, 0.0, 0.1},
 };
+__constant__ double c_sl2d[10][8] = {
+    {0.0, 0.0, 0.0, 0.69, 0.92, 1.0, 0.0, 2.0},
+    {0.0, -0.0184, 0.0, 0.6624, 0.874, 1.0, 0.0, -0.98},
+    {0.22, 0.0, 0.0, 0.11, 0.31, 1.0, -18.0, -0.02},
+    {-0.22, 0.0, 0.0, 0.16, 0.41, 1.0, 18.0, -0.02},
+    {0.0, 0.35, 0.0, 0.21, 0.25, 1.0, 0.0, 0.01},
+    {0.0, 0.1, 0.0, 0.046, 0.046, 1.0, 0.0, 0.01},
+    {0.0, -0.1, 0.0, 0.046, 0.046, 1.0, 0.0, 0.01},
+    {-0.08, -0.605, 0.0, 0.046, 0.023, 1.0, 0.0, 0.01},
+    {0.0, -0.605, 0.0, 0.023, 0.023, 1.0, 0.0, 0.01},
+    {0.06, -0.605, 0.0, 0.023, 0.046, 1.0, 0.0, 0.01},
+};
 
-template <class T>
-__global__ void k_shepp_logan(int n, const double2* __restrict__ rot, T* __restrict__ out) {
-    const size_t nn = size_t(n) * n * n;
+template <class T, bool FLAT>
+__global__ void k_ellipsoids(int n, int nz, const double2* __restrict__ rot, T* __restrict__ out) {
+    const size_t nn = size_t(n) * n * nz;
     for (size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x; id < nn; id += size_t(gridDim.x) * blockDim.x) {
         int i, j, k;
         unpack(id, n, n, i, j, k);
-        const double z = n == 1 ? 0.0 : double(2 * k + 1 - n) / n;
+        const double z = nz == 1 ? 0.0 : double(2 * k + 1 - nz) / nz;
         const double y = double(2 * j + 1 - n) / n;
         const double x = double(2 * i + 1 - n) / n;
         double v = 0.0;
         for (int e = 0; e < 10; ++e) {
-            const double* p = c_sl3d[e];
+            const double* p = FLAT ? c_sl2d[e] : c_sl3d[e];
             const double c = rot[e].x, s = rot[e].y;
             const double dx = x - p[0], dy = y - p[1], dz = z - p[2];
             const double xr = __dadd_rn(__dmul_rn(c, dx), __dmul_rn(s, dy));
@@ -118,9 +133,32 @@ __global__ void k_shepp_logan(int n, const double2* __restrict__ rot, T* __restr
     }
 }
 
+// piecewise_blocks (phantom.hpp:133-142): two nested axis-aligned squares, one slice.
 template <class T>
-void shepp_logan(int n, T* out, cudaStream_t s) {
-    // rotation cos/sin from the host libm, like the reference (phantom.hpp:16-17)
+__global__ void k_blocks(int n, T* __restrict__ out) {
+    const size_t nn = size_t(n) * n;
+    const int lo1 = n / 4, hi1 = (3 * n) / 4, lo2 = (3 * n) / 8, hi2 = (5 * n) / 8;
+    for (size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x; id < nn; id += size_t(gridDim.x) * blockDim.x) {
+        const int i = int(id % size_t(n)), j = int(id / size_t(n));
+        T v = 0;
+        if (i >= lo1 && i < hi1 && j >= lo1 && j < hi1) v += T(0.5);
+        if (i >= lo2 && i < hi2 && j >= lo2 && j < hi2) v += T(0.5);
+        out[id] = v;
+    }
+}
+
+template <class T>
+void make_phantom(int kind, int n, T* out, cudaStream_t s) {
+    const int nz = kind == 0 ? n : 1;
+    const size_t nn = size_t(n) * n * nz;
+    const size_t blocks = std::min<size_t>((nn + 255) / 256, size_t(148) * 32);
+    if (kind == 2) {
+        k_blocks<T><<<unsigned(blocks), 256, 0, s>>>(n, out);
+        after_launch("k_blocks");
+        return;
+    }
+    // rotation cos/sin from the host libm, like the reference (phantom.hpp:33); both
+    // tables share the same angles
     double2 rot[10];
     const double pi = 3.14159265358979323846;
     const double ang[10] = {0.0, 0.0, -18.0, 18.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -131,19 +169,18 @@ void shepp_logan(int n, T* out, cudaStream_t s) {
     DevBuf d_rot;
     d_rot.ensure(sizeof(rot));
     CTK_CUDA(cudaMemcpyAsync(d_rot.p, rot, sizeof(rot), cudaMemcpyHostToDevice, s));
-    const size_t nn = size_t(n) * n * n;
-    const size_t blocks = std::min<size_t>((nn + 255) / 256, size_t(148) * 32);
-    k_shepp_logan<T><<<unsigned(blocks), 256, 0, s>>>(n, d_rot.as<double2>(), out);
-    after_launch("k_shepp_logan");
-    CTK_CUDA(cudaStreamSynchronize(s));
+    if (kind == 0) k_ellipsoids<T, false><<<unsigned(blocks), 256, 0, s>>>(n, nz, d_rot.as<double2>(), out);
+    else k_ellipsoids<T, true><<<unsigned(blocks), 256, 0, s>>>(n, nz, d_rot.as<double2>(), out);
+    after_launch("k_ellipsoids");
+    CTK_CUDA(cudaStreamSynchronize(s));  // d_rot is freed on return
 }
 
 size_t grid_for(size_t n) { return std::min<size_t>((n + 255) / 256, size_t(148) * 16); }
 
 }  // namespace
 
-void launch_shepp_logan_f32(int n, float* out, cudaStream_t s) { shepp_logan<float>(n, out, s); }
-void launch_shepp_logan_f64(int n, double* out, cudaStream_t s) { shepp_logan<double>(n, out, s); }
+void launch_phantom_f32(int kind, int n, float* out, cudaStream_t s) { make_phantom<float>(kind, n, out, s); }
+void launch_phantom_f64(int kind, int n, double* out, cudaStream_t s) { make_phantom<double>(kind, n, out, s); }
 
 template <class T>
 void gradient_scaled(int nx, int ny, int nz, const T* x, const T* scale, double lam, T* gx, T* gy, T* gz, cudaStream_t s,

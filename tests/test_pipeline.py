@@ -1,0 +1,418 @@
+"""Pipeline, config, noise and metrics around the hot path against
+the reference's own src/config.cpp, src/pipeline.cpp, noise.hpp and metrics.hpp, compiled
+unmodified into oracle/_ref/libctkref.so.
+
+CPU tests: config parse/serialise byte-identical, the same errors and messages, geometry
+resolution, the noise stream bit-identical (a host function of libctk_b200.so), the
+convergence-log metrics and CSV byte-identical, CLI exit codes.
+GPU tests: run_simulate in double precision writes byte-identical files; run_reconstruct
+and run_compare agree with the reference's runs (recon within 1e-4, histories within 1e-4,
+metadata identical apart from the wall-clock line).
+"""
+import ctypes as C
+import os
+import shutil
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Geom, Reference
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+needs_ref = pytest.mark.skipif(not (Reference.available() and hasattr(Reference().lib, "ref_run_pipeline")),
+                               reason="oracle/_ref (with the Eigen shim) not built")
+
+
+@pytest.fixture(scope="module")
+def ref():
+    lib = Reference().lib
+    lib.ref_run_pipeline.argtypes = [C.c_int, C.c_char_p]
+    lib.ref_config_write.argtypes = [C.c_char_p, C.c_int, C.c_char_p]
+    lib.ref_last_error_message.argtypes = [C.c_char_p, C.c_size_t]
+    return lib
+
+
+def _ref_msg(ref):
+    buf = C.create_string_buffer(512)
+    ref.ref_last_error_message(buf, 512)
+    return buf.value.decode()
+
+
+def _fp(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+CFG_FULL = """# every key, some odd spellings
+phantom = shepp_logan_3d
+size = 24
+geometry = cone3d   # trailing comment
+n_angles = 17
+angle_start_deg = 12.5
+angle_range_deg = 200
+detector_pixels_u = 30
+detector_pixels_v = 0
+detector_pixel_size = 1.25
+source_to_origin = 0
+origin_to_detector = 3.0e1
+spacing = 1
+i0 = 2e4
+sigma = 0.25
+seed = 12345678901
+solver = hybrid_lsqr
+solvers = lsqr, cgls ,, lsmr,
+lambda = 0.1
+strategy = gcv
+noise_level = 0.01
+outer_iters = 3
+inner_iters = 7
+warm_start = yes
+backprojector = voxel_driven
+max_iters = 9
+residual_tolerance = 1e-9
+stop_on_residual_increase = off
+reorth = 0
+precision = single
+projections = /tmp/p.proj
+ground_truth = gt.vol
+output_dir = out dir
+window_min = -0.5
+window_max = 1.5
+threads = 3
+"""
+
+
+@needs_ref
+@pytest.mark.parametrize("text", [CFG_FULL, "", "size=8\n\n  # only a comment\r\nseed = -1\n", "lambda = .5e-3\nseed=+7"])
+@pytest.mark.parametrize("resolve", [0, 1])
+def test_config_serialisation_byte_identical(ref, tmp_path, text, resolve):
+    from paper_2211_14212_b200 import config, pipeline
+
+    theirs = str(tmp_path / "theirs.cfg")
+    rc = ref.ref_config_write(text.encode(), resolve, theirs.encode())
+    cfg = config.parse_config(text)
+    if rc:
+        with pytest.raises(Exception):
+            pipeline.resolve_geometry(cfg)
+        return
+    if resolve:
+        pipeline.resolve_geometry(cfg)
+    assert config.write_config(cfg) == open(theirs).read()
+    # parse(serialize(c)) == c (config.hpp:78) -- except, in the reference too, a seed >= 2^63
+    # (e.g. "seed = -1"): it is written as an unsigned value that std::stoll then rejects
+    if cfg.seed < 2**63:
+        assert config.parse_config(config.write_config(cfg)) == cfg
+    else:
+        assert ref.ref_config_write(open(theirs).read().encode(), 0, theirs.encode()) == 3
+        with pytest.raises(config.ParameterError):
+            config.parse_config(config.write_config(cfg))
+
+
+@needs_ref
+@pytest.mark.parametrize("text", [
+    "bogus = 1", "size = 12x", "size = ", "seed = 1.5", "lambda = abc", "lambda = 1e999", "warm_start = maybe",
+    "just a line", "size = 4", "precision = half", "geometry = fan", "phantom = cube", "strategy = lcurve",
+    "backprojector = cone", "sigma = -1", "i0 = 0", "lambda = -1", "threads = -2", "max_iters = 0",
+    "n_angles = 0", "residual_tolerance = -1e-3", "lambda = nan", "geometry = cone3d\nsource_to_origin = 5",
+])
+def test_config_errors_match(ref, tmp_path, text):
+    from paper_2211_14212_b200 import ParameterError, GeometryError, config, pipeline
+
+    rc = ref.ref_config_write(text.encode(), 1, str(tmp_path / "x.cfg").encode())
+    want = _ref_msg(ref)
+    codes = {2: GeometryError, 3: ParameterError}
+    if rc == 0:  # accepted by the reference (e.g. lambda = nan passes the >= 0 check)
+        cfg = config.parse_config(text)
+        pipeline.resolve_geometry(cfg)
+        return
+    with pytest.raises(codes[rc]) as e:
+        cfg = config.parse_config(text)
+        pipeline.resolve_geometry(cfg)
+    assert str(e.value) == want
+
+
+@needs_ref
+@pytest.mark.parametrize("text", ["", "geometry = parallel3d\nsize = 20\nn_angles = 33\nangle_range_deg = 180",
+                                  "geometry = cone3d\nphantom = shepp_logan_3d\nsize = 16\nangle_start_deg = 90\n"
+                                  "detector_pixel_size = 2\nsource_to_origin = 100"])
+def test_resolve_geometry_matches(ref, text):
+    from paper_2211_14212_b200 import config, pipeline
+
+    g = pipeline.resolve_geometry(config.parse_config(text))
+    angles = np.zeros(4096)
+    ref.ref_resolve_geometry.argtypes = [C.c_char_p, C.c_void_p, C.POINTER(C.c_double)]
+    rg = Geom(0, 0, 0, 0, 0, 0, 0, 0, 0, 0).cstruct()
+    assert ref.ref_resolve_geometry(text.encode(), C.byref(rg), _fp(angles, C.c_double)) == 0
+    assert (int(g.mode), g.source_to_origin, g.origin_to_detector, g.detector_pixel_size, g.nu, g.nv) == \
+        (rg.mode, rg.dso, rg.dod, rg.du, rg.nu, rg.nv)
+    assert (g.vol.nx, g.vol.ny, g.vol.nz, g.vol.spacing) == (rg.nx, rg.ny, rg.nz, rg.h)
+    assert list(g.angles) == list(angles[:rg.na])
+
+
+@needs_ref
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("i0,sigma,seed", [(1e5, 0.5, 0), (50.0, 2.0, 99), (1e3, 0.0, 2**63 + 5)])
+def test_noise_stream_bit_identical(ref, dtype, i0, sigma, seed):
+    """add_noise (noise.hpp:29-47): counts spanning the Poisson sampler's small-mean and
+    rejection branches; libctk_b200.so's host stream vs the reference's."""
+    import paper_2211_14212_b200 as ctk
+
+    g = Geom(2, 0.0, 10.0, 1.0, 9, 7, 4, 4, 1, 1.0, np.array([0.0, 1.0, 2.0, 3.0, 4.0]))
+    rng = np.random.default_rng(5)
+    clean = (rng.random(g.range_size) * 9.0).astype(dtype)
+    clean[::7] = 0.0
+    ours = ctk.add_noise(clean, ctk.NoiseModel(i0, sigma, seed))
+    theirs = np.zeros_like(clean)
+    suf, ct = ("f32", C.c_float) if dtype == np.float32 else ("f64", C.c_double)
+    gs = g.cstruct()
+    assert getattr(ref, f"ref_add_noise_{suf}")(C.byref(gs), _fp(clean, ct), C.c_double(i0), C.c_double(sigma),
+                                                C.c_uint64(seed), _fp(theirs, ct)) == 0
+    assert ours.dtype == dtype and np.array_equal(ours, theirs)
+
+
+def test_noise_errors():
+    import paper_2211_14212_b200 as ctk
+
+    with pytest.raises(ctk.ParameterError, match="I0 must be positive"):
+        ctk.add_noise(np.zeros(3), ctk.NoiseModel(0.0))
+    with pytest.raises(ctk.ParameterError, match="sigma must be nonnegative"):
+        ctk.add_noise(np.zeros(3), ctk.NoiseModel(1e5, -1.0))
+    with pytest.raises(ctk.DegenerateInputError, match="negative line integral"):
+        ctk.add_noise(np.array([0.5, -1e-9, 0.1], np.float32), ctk.NoiseModel())
+    assert ctk.noise_rng_id() == "mt19937_64+std::poisson/normal,sequential"
+
+
+def _log(ctk, imp, exp, err, lam):
+    return ctk.ConvergenceLog(list(imp), list(exp), list(err), list(lam), "lsqr", "double", True)
+
+
+@needs_ref
+def test_metrics_helpers_match(ref, tmp_path):
+    import paper_2211_14212_b200 as ctk
+    from paper_2211_14212_b200 import metrics
+
+    rng = np.random.default_rng(2)
+    imp, exp = rng.random(7), rng.random(7)
+    imp[2] = 0.0
+    err = np.array([0.9, 0.5, 0.3, 0.3, 0.35, 0.4, 0.31])
+    lam = rng.random(4) * 1e-7
+    for cols in ((imp, exp, err, lam), (imp, exp, err[:0], lam[:0]), (imp[:0], exp, err[:3], lam)):
+        log = _log(ctk, *cols)
+        ours, theirs = str(tmp_path / "o.csv"), str(tmp_path / "t.csv")
+        metrics.write_csv(ours, log)
+        args = []
+        for c in cols:
+            c = np.ascontiguousarray(c, dtype=np.float64)
+            args += [_fp(c, C.c_double), len(c)]
+        assert ref.ref_write_csv(theirs.encode(), *args) == 0
+        assert open(ours).read() == open(theirs).read()
+    mi, rb = C.c_int(), C.c_double()
+    assert ref.ref_semiconvergence(_fp(err, C.c_double), len(err), C.byref(mi), C.byref(rb)) == 0
+    s = metrics.detect_semiconvergence(_log(ctk, [], [], err, []))
+    assert (s.min_index, s.rebound_ratio) == (mi.value, rb.value)
+    with pytest.raises(ctk.ParameterError):
+        metrics.detect_semiconvergence(_log(ctk, [], [], err[:2], []))
+    out = C.c_double()
+    assert ref.ref_residual_divergence(_fp(imp, C.c_double), 7, _fp(exp, C.c_double), 7, C.byref(out)) == 0
+    assert metrics.residual_divergence(_log(ctk, imp, exp, [], [])) == out.value
+    with pytest.raises(ctk.ParameterError):
+        metrics.residual_divergence(_log(ctk, imp[:3], exp, [], []))
+
+
+def _cli(*args, cwd=None):
+    return subprocess.run([sys.executable, "-m", "paper_2211_14212_b200", *args], cwd=cwd or ROOT,
+                          capture_output=True, text=True, env={**os.environ, "PYTHONPATH": ROOT})
+
+
+def test_cli_exit_codes(tmp_path):
+    assert _cli().returncode == 2  # a subcommand is required
+    r = _cli("simulate", "--set", "bogus=1", "--output", str(tmp_path))
+    assert r.returncode == 2 and "error: config: unknown key 'bogus'" in r.stderr
+    r = _cli("reconstruct", "--output", str(tmp_path))
+    assert r.returncode == 2 and "needs a projections file" in r.stderr
+    r = _cli("compare", "--set", "solvers=lsqr", "x.proj", "--output", str(tmp_path))
+    assert r.returncode == 2 and "at least two solvers" in r.stderr
+    r = _cli("reconstruct", str(tmp_path / "missing.proj"), "--output", str(tmp_path))
+    assert r.returncode == 2 and "missing header" in r.stderr
+    assert _cli("simulate", "--set", "size").returncode == 2
+    cfg = tmp_path / "c.cfg"
+    cfg.write_text("size = 4\n")
+    r = _cli("simulate", "--config", str(cfg))
+    assert r.returncode == 2 and "size must be at least 8" in r.stderr
+
+
+# ---------------------------------------------------------------------------------------- GPU
+def _files(d):
+    out = {}
+    for name in sorted(os.listdir(d)):
+        with open(os.path.join(d, name), "rb") as f:
+            out[name] = f.read()
+    return out
+
+
+def _run_both(ref, cmd, text, tmp_path, ours_fn, ref_text=None):
+    """Run the reference then ours into the same output directory (so paths recorded in
+    metadata agree); return (reference files, our files).  ref_text: the reference's config
+    when it differs (single-precision runs are checked against the reference's double run)."""
+    d = str(tmp_path / "run")
+    os.makedirs(d, exist_ok=True)
+    full = text + f"\noutput_dir = {d}\n"
+    rc = ref.ref_run_pipeline(cmd, ((ref_text or text) + f"\noutput_dir = {d}\n").encode())
+    assert rc == 0, _ref_msg(ref)
+    theirs = _files(d)
+    shutil.rmtree(d)
+    from paper_2211_14212_b200 import config
+
+    ours_fn(config.parse_config(full))
+    return theirs, _files(d)
+
+
+SIM_CASES = [
+    "precision = double",  # defaults: shepp_logan_2d 64^2, parallel2d, 60 views
+    "precision = double\nphantom = shepp_logan_3d\ngeometry = cone3d\nsize = 20\nn_angles = 24\nseed = 3",
+    "precision = double\nphantom = piecewise_blocks\ngeometry = parallel3d\nsize = 16\nn_angles = 10\n"
+    "angle_range_deg = 180\ni0 = 300\nsigma = 1.5",
+]
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("text", SIM_CASES)
+def test_simulate_double_byte_identical(ref, tmp_path, text):
+    from paper_2211_14212_b200 import pipeline
+
+    theirs, ours = _run_both(ref, 0, text, tmp_path, pipeline.run_simulate)
+    assert sorted(theirs) == sorted(ours) == sorted(
+        ["phantom.vol", "phantom.vol.hdr", "projections_clean.proj", "projections_clean.proj.hdr",
+         "projections_noisy.proj", "projections_noisy.proj.hdr", "simulate_meta.cfg"])
+    for k in theirs:
+        assert ours[k] == theirs[k], k
+
+
+@needs_ref
+@pytest.mark.gpu
+def test_simulate_single_close(ref, tmp_path):
+    from paper_2211_14212_b200 import pipeline
+
+    text = "precision = single\nphantom = shepp_logan_3d\ngeometry = cone3d\nsize = 20\nn_angles = 24"
+    theirs, ours = _run_both(ref, 0, text, tmp_path, pipeline.run_simulate)
+    for k in ("phantom.vol", "phantom.vol.hdr", "projections_clean.proj.hdr", "simulate_meta.cfg"):
+        assert ours[k] == theirs[k], k
+    a = np.frombuffer(theirs["projections_clean.proj"], "<f4")
+    b = np.frombuffer(ours["projections_clean.proj"], "<f4")
+    assert np.linalg.norm(a - b) / np.linalg.norm(a) < 1e-5
+
+
+def _csv(blob):
+    lines = blob.decode().strip().split("\n")
+    rows = [[float(c) if c else np.nan for c in ln.split(",")] for ln in lines[1:]]
+    return lines[0], np.array(rows)
+
+
+def _meta(blob):
+    return [ln for ln in blob.decode().split("\n") if not ln.startswith("# wall_seconds")]
+
+
+def _close(a, b, tol):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    assert a.shape == b.shape
+    m = ~np.isnan(a)
+    assert np.array_equal(m, ~np.isnan(b))
+    assert np.all(np.abs(a[m] - b[m]) <= tol * np.maximum(np.abs(a[m]), 1e-300)), np.max(np.abs(a[m] - b[m]))
+
+
+# Noisy parallel2d data is ill-conditioned: in the reference itself a 1e-13 relative change
+# of b moves the LSQR iterate by ~1e3 x that at k = 5, ~3e5 x at k = 8 (LSMR(0.5) ~1e5 x at
+# k = 8; CGLS-TV ~1 x), so the iteration counts below keep rounding-level differences
+# (fp64 reduction order; f32 arithmetic) below the tolerances.
+RECON_CASES = [
+    ("precision = double\nsolver = lsqr\nmax_iters = 6", 1e-6),
+    ("precision = double\nsolver = cgls_tv\nlambda = 0.05\nouter_iters = 2\ninner_iters = 5\nwindow_min = 0\n"
+     "window_max = 1", 1e-6),
+    ("precision = double\nsolver = hybrid_lsqr\nstrategy = gcv\nmax_iters = 10\nbackprojector = voxel_driven", 1e-6),
+    ("precision = single\nsolver = lsmr\nlambda = 0.5\nmax_iters = 3", 1e-4),
+]
+
+
+@needs_ref
+@pytest.mark.gpu
+@pytest.mark.parametrize("text,tol", RECON_CASES)
+def test_reconstruct_matches_reference(ref, tmp_path, text, tol):
+    from paper_2211_14212_b200 import pipeline
+
+    sim = str(tmp_path / "sim")
+    os.makedirs(sim)
+    assert ref.ref_run_pipeline(0, f"precision = double\noutput_dir = {sim}\n".encode()) == 0
+    base = f"{text}\nprojections = {sim}/projections_noisy.proj\nground_truth = {sim}/phantom.vol"
+    # the parity gate for f32 is the reference's T=double run (the reference's own single
+    # precision accumulates in float on purpose, types.hpp:136-137)
+    ref_base = base.replace("precision = single", "precision = double")
+    theirs, ours = _run_both(ref, 1, base, tmp_path, pipeline.run_reconstruct, ref_base)
+    assert sorted(theirs) == sorted(ours)
+    a = np.frombuffer(theirs["recon.vol"], "<f4")
+    b = np.frombuffer(ours["recon.vol"], "<f4")
+    assert np.linalg.norm(a - b) / np.linalg.norm(a) < max(tol, 1e-6) * 10
+    assert ours["recon.vol.hdr"] == theirs["recon.vol.hdr"]
+    h1, c1 = _csv(theirs["convergence.csv"])
+    h2, c2 = _csv(ours["convergence.csv"])
+    assert h1 == h2
+    _close(c2, c1, tol)
+    assert _meta(ours["reconstruct_meta.cfg"]) == \
+        [ln.replace("precision = double", "precision = single") if ref_base != base else ln
+         for ln in _meta(theirs["reconstruct_meta.cfg"])]
+    for pgm in ("slice_transversal.pgm", "slice_sagittal.pgm"):
+        n_hdr = theirs[pgm].index(b"65535\n") + 6
+        assert ours[pgm][:n_hdr] == theirs[pgm][:n_hdr]
+        pa = np.frombuffer(theirs[pgm][n_hdr:], ">u2").astype(int)
+        pb = np.frombuffer(ours[pgm][n_hdr:], ">u2").astype(int)
+        assert np.max(np.abs(pa - pb)) <= (1 if tol < 1e-5 else 64)
+
+
+@needs_ref
+@pytest.mark.gpu
+def test_compare_matches_reference(ref, tmp_path):
+    from paper_2211_14212_b200 import pipeline
+
+    sim = str(tmp_path / "sim")
+    os.makedirs(sim)
+    assert ref.ref_run_pipeline(0, f"precision = double\nsize = 32\nn_angles = 30\noutput_dir = {sim}\n".encode()) == 0
+    text = (f"precision = double\nsize = 32\nn_angles = 30\nsolvers = cgls, lsmr, hybrid_lsqr, sirt\nlambda = 0.25\n"
+            f"strategy = gcv\nmax_iters = 6\nprojections = {sim}/projections_noisy.proj\n"
+            f"ground_truth = {sim}/phantom.vol")
+    theirs, ours = _run_both(ref, 2, text, tmp_path, pipeline.run_compare)
+    assert sorted(theirs) == sorted(ours)
+    for name in ("cgls.csv", "lsmr.csv", "hybrid_lsqr.csv", "sirt.csv", "compare_wide.csv"):
+        h1, c1 = _csv(theirs[name])
+        h2, c2 = _csv(ours[name])
+        assert h1 == h2, name
+        _close(c2, c1, 1e-6)
+    assert _meta(ours["compare_meta.cfg"]) == _meta(theirs["compare_meta.cfg"])
+    s1 = [ln.split("  ") for ln in theirs["summary.txt"].decode().strip().split("\n")]
+    s2 = [ln.split("  ") for ln in ours["summary.txt"].decode().strip().split("\n")]
+    assert s1[0] == s2[0]
+    for r1, r2 in zip(s1[1:], s2[1:]):
+        assert r1[:3] == r2[:3] and r1[4] == r2[4]  # label, iterations, stop reason, min-error iteration
+        _close([float(r2[3]), float(r2[5]), float(r2[6])], [float(r1[3]), float(r1[5]), float(r1[6])], 1e-5)
+
+
+@needs_ref
+@pytest.mark.gpu
+def test_metrics_relative_residual_and_error(ref):
+    import torch
+
+    import paper_2211_14212_b200 as ctk
+    from paper_2211_14212_b200 import metrics
+
+    g = ctk.bench_geometry(16, 12)
+    x = ctk.shepp_logan_3d(16, "float64").cpu().numpy()
+    pair = ctk.projector_pair(g, dtype=np.float64)
+    b = pair.apply_forward(x) * 1.01
+    want = np.linalg.norm(pair.apply_forward(x) - b) / np.linalg.norm(b)
+    assert abs(metrics.relative_residual(pair, x, b) - want) <= 1e-12 * want
+    xt = torch.from_numpy(x).cuda()
+    assert abs(metrics.relative_error(xt * 1.1, xt) - 0.1) < 1e-12
+    with pytest.raises(ctk.DimensionError):
+        metrics.relative_error(xt[:10], xt)
+    with pytest.raises(ctk.DegenerateInputError):
+        metrics.relative_residual(pair, x, np.zeros_like(b))
