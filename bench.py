@@ -314,12 +314,15 @@ def main():
     b_host.copy_(b.cpu())
     b_np = b_host.numpy()
     e2e_steps = max(1, min(args.steps, 2))
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(e2e_steps):
-        r = solve(b_np)  # H2D b, solve, D2H x inside the call
-    barrier()
-    e2e_s = maxed(time.perf_counter() - t0)
+    with Clocks(local) as clk_e2e:
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            r = solve(b_np)  # H2D b, solve, D2H x inside the call
+        barrier()
+        t1 = time.perf_counter()
+    clk_e2e.window(t0, t1)
+    e2e_s = maxed(t1 - t0)
     e2e_value = args.iters * e2e_steps / e2e_s
 
     hbm_peak, sm_mhz, peak_src = peaks()
@@ -366,7 +369,8 @@ def main():
         "roofline_gather": {"kernel": dom, "achieved": samples / (t_dom / 1e3) / 1e9, "peak": gather_peak,
                             "unit": "G samples/s", "frac": samples / (t_dom / 1e3) / 1e9 / gather_peak,
                             "note": "binding on-chip ceiling: 16 B/sample at 128 B/clk/SM x 148 SMs (SURVEY.md 8(d))"},
-        "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": 4 * nproj, "d2h_bytes_per_step": 4 * nvox},
+        "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": 4 * nproj, "d2h_bytes_per_step": 4 * nvox,
+                "clocks": clk_e2e.summary()},
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "wall_s_timed": wall,
