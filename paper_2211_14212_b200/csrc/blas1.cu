@@ -36,12 +36,26 @@ __device__ __forceinline__ Chunk my_chunk(size_t n) {
     return {b, min(n, b + per)};
 }
 
+// Four independent partial sums per thread (elements i, i+B, i+2B, i+3B of the block's
+// chunk): four loads per operand in flight instead of one -- with 4 resident blocks of 256
+// threads per SM a single load each keeps only ~8 KB in flight, well short of what HBM
+// latency x bandwidth needs.  The combination order is fixed, so results stay
+// run-to-run bitwise identical.
 template <class T, class F>
 __device__ __forceinline__ double chunk_reduce(size_t n, F f) {
     const Chunk c = my_chunk(n);
-    double acc = 0.0;
-    for (size_t i = c.b + threadIdx.x; i < c.e; i += blockDim.x) acc += f(i);
-    return block_sum(acc);
+    const size_t B = blockDim.x;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    size_t i = c.b + threadIdx.x;
+    for (; i + 3 * B < c.e; i += 4 * B) {
+        const double v0 = f(i), v1 = f(i + B), v2 = f(i + 2 * B), v3 = f(i + 3 * B);
+        a0 += v0;
+        a1 += v1;
+        a2 += v2;
+        a3 += v3;
+    }
+    for (; i < c.e; i += B) a0 += f(i);
+    return block_sum((a0 + a1) + (a2 + a3));
 }
 
 template <class T>
@@ -184,17 +198,51 @@ void run_map(size_t n, F f, cudaStream_t s, const char* what) {
     after_launch(what);
 }
 
-// block_dot: coef[i] = <basis_i, w>, partials[i][blk] then a fixed-order finish per i
+// block_dot: coef[q] = <basis_q, w>, partials[q][blk] then a fixed-order finish per q.
+// Basis vectors in groups of BD_G: w is read once per group (not once per vector) and each
+// thread has 1 + BD_G independent loads in flight per element.
+constexpr int BD_G = 8;
 template <class T>
 __global__ void k_block_dot(size_t n, int m, const T* __restrict__ basis, size_t ld, const T* __restrict__ w,
                             double* __restrict__ part) {
     const Chunk c = my_chunk(n);
-    for (int q = 0; q < m; ++q) {
-        const T* bq = basis + size_t(q) * ld;
-        double acc = 0.0;
-        for (size_t i = c.b + threadIdx.x; i < c.e; i += blockDim.x) acc += double(bq[i]) * double(w[i]);
-        acc = block_sum(acc);
-        if (threadIdx.x == 0) part[size_t(q) * gridDim.x + blockIdx.x] = acc;
+    for (int q0 = 0; q0 < m; q0 += BD_G) {
+        const int g = min(BD_G, m - q0);
+        const T* bq = basis + size_t(q0) * ld;
+        double acc[BD_G];
+#pragma unroll
+        for (int j = 0; j < BD_G; ++j) acc[j] = 0.0;
+        // a partial group loads its last vector in the unused slots (unpredicated loads, so
+        // all of them issue before the first FMA; the extra sums are discarded); two
+        // elements per iteration -> 2 * (1 + BD_G) loads in flight
+        size_t off[BD_G];
+#pragma unroll
+        for (int j = 0; j < BD_G; ++j) off[j] = size_t(min(j, g - 1)) * ld;
+        const size_t B = blockDim.x;
+        size_t i = c.b + threadIdx.x;
+        for (; i + B < c.e; i += 2 * B) {
+            const double w0 = double(__ldg(w + i)), w1 = double(__ldg(w + i + B));
+            T b0[BD_G], b1[BD_G];
+#pragma unroll
+            for (int j = 0; j < BD_G; ++j) {
+                b0[j] = __ldg(bq + off[j] + i);
+                b1[j] = __ldg(bq + off[j] + i + B);
+            }
+#pragma unroll
+            for (int j = 0; j < BD_G; ++j) acc[j] += double(b0[j]) * w0 + double(b1[j]) * w1;
+        }
+        if (i < c.e) {
+            const double w0 = double(__ldg(w + i));
+#pragma unroll
+            for (int j = 0; j < BD_G; ++j) acc[j] += double(__ldg(bq + off[j] + i)) * w0;
+        }
+#pragma unroll
+        for (int j = 0; j < BD_G; ++j) {
+            if (j < g) {  // uniform across the block
+                const double v = block_sum(acc[j]);
+                if (threadIdx.x == 0) part[size_t(q0 + j) * gridDim.x + blockIdx.x] = v;
+            }
+        }
     }
 }
 
@@ -208,12 +256,27 @@ __global__ void k_finish_many(const double* __restrict__ part, int nblk, double*
     if (threadIdx.x == 0) out[blockIdx.x] = v;
 }
 
+// w += alpha * sum_q coef[q] basis_q, accumulated in T in q order (as the sequence of
+// per-vector axpys it replaces); the scaled coefficients are staged in shared memory and the
+// basis loads of a group of BD_G vectors are issued together.
+constexpr int BA_MAXM = 1024;
 template <class T>
 __global__ void k_block_axpy(size_t n, int m, double alpha, const double* __restrict__ coef, const T* __restrict__ basis,
                              size_t ld, T* __restrict__ w) {
+    __shared__ T cs[BA_MAXM];
+    for (int q = threadIdx.x; q < m; q += blockDim.x) cs[q] = T(alpha * coef[q]);
+    __syncthreads();
     for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
         T acc = w[i];
-        for (int q = 0; q < m; ++q) acc += T(alpha * coef[q]) * basis[size_t(q) * ld + i];
+        int q0 = 0;
+        for (; q0 + BD_G <= m; q0 += BD_G) {  // full groups: all loads issue before the FMAs
+            T bv[BD_G];
+#pragma unroll
+            for (int j = 0; j < BD_G; ++j) bv[j] = __ldg(basis + size_t(q0 + j) * ld + i);
+#pragma unroll
+            for (int j = 0; j < BD_G; ++j) acc += cs[q0 + j] * bv[j];
+        }
+        for (; q0 < m; ++q0) acc += cs[q0] * basis[size_t(q0) * ld + i];
         w[i] = acc;
     }
 }
@@ -311,8 +374,13 @@ template <class T>
 void block_axpy(size_t n, int m, double alpha, const double* d_coef, const T* basis, size_t ld, T* w, cudaStream_t s) {
     if (m <= 0) return;
     const size_t blocks = std::min<size_t>((n + 255) / 256, size_t(148) * 16);
-    k_block_axpy<T><<<unsigned(blocks), 256, 0, s>>>(n, m, alpha, d_coef, basis, ld, w);
-    after_launch("k_block_axpy");
+    // more than BA_MAXM vectors: consecutive launches over consecutive vector ranges keep
+    // the per-element q order
+    for (int q0 = 0; q0 < m; q0 += BA_MAXM) {
+        k_block_axpy<T><<<unsigned(blocks), 256, 0, s>>>(n, std::min(BA_MAXM, m - q0), alpha, d_coef + q0,
+                                                         basis + size_t(q0) * ld, ld, w);
+        after_launch("k_block_axpy");
+    }
 }
 
 #define CTK_INST(T)                                                                                        \
