@@ -3,6 +3,8 @@
 // the step-scaled projections in 4-row groups pg[a][iv/4][iu][iv%4], the voxel-driven one
 // from the projections transposed to pt[a][iu][iv] -- so no float atomics are used and
 // every voxel sums its contributions in a fixed order.
+#include <cstdlib>
+
 #include "f32_common.cuh"
 
 namespace ctkb {
@@ -67,24 +69,35 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 //           the columns registered in its row, sorted by column -> deterministic order.
 // Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
 // their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
-// measured at 512^3 / 360 views: without view batching 4 CTAs/SM (64 regs) was best; with
-// batching, 12-entry row lists (60 KB of shared memory) and 3 CTAs/SM: 82.4 ms (8-entry lists
-// at 3 or 4 CTAs/SM overflow into the slow scan: 82-95 ms)
-#ifndef CTK_BP_MINB
-#define CTK_BP_MINB 3
-#endif
-#ifndef CTK_BP_SL
-#define CTK_BP_SL 12  // row list capacity: a batch can register entries of two views in a row
-#endif
+// Tile size PB (rows = threads per CTA) is a template parameter with its own row-list
+// capacity SL and occupancy (measured, matched A^T b f32):
+//   PB = 128, SL = 10, 6 CTAs/SM: 256^3/180 4.70 ms, 512^3/360 67.8 ms, 512^3/720 137 ms
+//   PB = 256, SL = 12, 3 CTAs/SM: 256^3/180 5.32 ms, 512^3/360 72.8 ms, 512^3/720 147 ms,
+//                                 1024^3/1600 2569 ms (PB = 128: 3034 ms -- per-CTA setup over
+//                                 1600 views and twice the tiles)
+// so the launcher takes PB = 128 up to 768 rows per plane and PB = 256 beyond.  Smaller
+// lists (SL = 8 at PB = 128) overflow into the slow scan: 74.5 ms.  Without view batching
+// 4 CTAs/SM (64 regs) was best.
+template <int PB>
+struct PlaneCfg;
+template <>
+struct PlaneCfg<128> {
+    static constexpr int SL = 10, MINB = 6;
+};
+template <>
+struct PlaneCfg<256> {
+    static constexpr int SL = 12, MINB = 3;
+};
 #ifndef CTK_BP_KB
 #define CTK_BP_KB 32
 #endif
-constexpr int BP_PB = 256, BP_KB = CTK_BP_KB, BP_SL = CTK_BP_SL;
+constexpr int BP_KB = CTK_BP_KB;
 constexpr int BP_ZG = 2;  // guard rows of Z on each side: out-of-band entries land there, unread
 
-template <int CLASS>
-__global__ void __launch_bounds__(BP_PB, CTK_BP_MINB)
+template <int CLASS, int PB>
+__global__ void __launch_bounds__(PB, PlaneCfg<PB>::MINB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles) {
+    constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
     extern __shared__ __align__(16) float sm[];
     float* Z = sm + BP_ZG * BP_PB;                              // [-BP_ZG, BP_KB+BP_ZG) x [BP_PB]
     int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG) * BP_PB);  // [BP_PB][BP_SL]
@@ -540,8 +553,9 @@ void group_proj(Geometry& g, const float* y, cudaStream_t s) {
     after_launch("k_proj_group4");
 }
 
-template <int CLASS>
-void launch_plane(Geometry& g, float* x, cudaStream_t s) {
+template <int CLASS, int PB>
+void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
+    constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
     const int nh = CLASS ? g.nx : g.ny;
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
@@ -552,12 +566,24 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     static size_t configured = 0;
     if (smem > configured) {
-        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         configured = smem;
     }
     dim3 grd(unsigned(planes), unsigned(ptiles * kbands));
-    k_atb_plane_f32<CLASS><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
+    k_atb_plane_f32<CLASS, PB><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
     after_launch("k_atb_plane_f32");
+}
+
+template <int CLASS>
+void launch_plane(Geometry& g, float* x, cudaStream_t s) {
+    const int nh = CLASS ? g.nx : g.ny;
+    static const int forced = [] {
+        const char* e = std::getenv("CTK_BP_TILE");  // A/B timing: 128 or 256
+        return e ? std::atoi(e) : 0;
+    }();
+    const int pb = forced == 128 || forced == 256 ? forced : (nh <= 768 ? 128 : 256);
+    if (pb == 128) launch_plane_pb<CLASS, 128>(g, x, s);
+    else launch_plane_pb<CLASS, 256>(g, x, s);
 }
 
 template <int KZ>
