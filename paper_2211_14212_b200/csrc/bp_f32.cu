@@ -71,22 +71,28 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 // their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
 // Tile size PB (rows = threads per CTA) is a template parameter with its own row-list
 // capacity SL and occupancy (measured, matched A^T b f32):
-//   PB = 128, SL = 10, 6 CTAs/SM: 256^3/180 4.70 ms, 512^3/360 67.8 ms, 512^3/720 137 ms
-//   PB = 256, SL = 12, 3 CTAs/SM: 256^3/180 5.32 ms, 512^3/360 72.8 ms, 512^3/720 147 ms,
-//                                 1024^3/1600 2569 ms (PB = 128: 3034 ms -- per-CTA setup over
-//                                 1600 views and twice the tiles)
+//   PB = 128, 6 CTAs/SM: 256^3/180 4.61 ms, 512^3/360 66.9 ms (SL = 9/10/11/12: 71.2/67.7/66.9/69.0)
+//   PB = 256, 3 CTAs/SM: 256^3/180 5.32 ms, 512^3/360 72.8 ms, 512^3/720 147 ms,
+//                        1024^3/1600 2518 ms at SL = 11 (SL = 10/12/14: 2563/2565/3275;
+//                        PB = 128: 3034 ms -- per-CTA setup over 1600 views, twice the tiles)
 // so the launcher takes PB = 128 up to 768 rows per plane and PB = 256 beyond.  Smaller
 // lists (SL = 8 at PB = 128) overflow into the slow scan: 74.5 ms.  Without view batching
 // 4 CTAs/SM (64 regs) was best.
+#ifndef CTK_BP_SL128
+#define CTK_BP_SL128 11
+#endif
+#ifndef CTK_BP_SL256
+#define CTK_BP_SL256 11
+#endif
 template <int PB>
 struct PlaneCfg;
 template <>
 struct PlaneCfg<128> {
-    static constexpr int SL = 10, MINB = 6;
+    static constexpr int SL = CTK_BP_SL128, MINB = 6;
 };
 template <>
 struct PlaneCfg<256> {
-    static constexpr int SL = 12, MINB = 3;
+    static constexpr int SL = CTK_BP_SL256, MINB = 3;
 };
 #ifndef CTK_BP_KB
 #define CTK_BP_KB 32
