@@ -49,6 +49,17 @@ def cone_adjoint():
     return Geom(CONE3D, 30.0, 12.0, 1.5, 18, 18, 12, 12, 12, 1.0, equidistant_angles(9))
 
 
+def cone_multitile():
+    # rows per plane (140, 300) span several 128-row tiles of the f32 plane backprojector with
+    # ragged ends; 40 slices = a full and a ragged 32-slice band
+    return Geom(CONE3D, 400.0, 200.0, 2.5, 200, 32, 300, 140, 40, 1.0, equidistant_angles(24))
+
+
+def cone_wide():
+    # 800 rows per plane in the y-dominant pass: the 256-row tiles of the plane backprojector
+    return Geom(CONE3D, 900.0, 300.0, 4.0, 300, 8, 800, 24, 8, 1.0, equidistant_angles(20))
+
+
 ALL = {
     "parallel2d": parallel2d,
     "parallel3d": parallel3d,
@@ -56,4 +67,6 @@ ALL = {
     "cone_ragged": cone_ragged,
     "cone_steep": cone_steep,
     "cone_adjoint": cone_adjoint,
+    "cone_multitile": cone_multitile,
+    "cone_wide": cone_wide,
 }

@@ -113,3 +113,28 @@ def test_wide_offset_instantiation_matches(tmp_path):
         subprocess.run([sys.executable, "-c", code, f], check=True, env={**os.environ, "CTK_FWD_WIDE": wide})
         outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.skipif(not __import__("oracle.oracle", fromlist=["Reference"]).Reference.available(),
+                    reason="oracle/_ref not built")
+def test_c3_parity_on_view_subset(ctk):
+    """The north-star bar at the full C3 size: the reference T=double Ax and matched A^T b
+    (oracle/_ref, all host threads) on 16 of the 360 views of the 512^3 / 512^2 acquisition,
+    Shepp-Logan phantom input; f32 Ax and A^T b within 1e-5 relative L2."""
+    from geoms import to_ctk
+    from oracle.oracle import CONE3D, Geom, Reference, equidistant_angles
+
+    n = 512
+    ang = np.array(equidistant_angles(360))[np.linspace(0, 359, 16).astype(int)]
+    g = Geom(CONE3D, 2.0 * n, 1.0 * n, 1.5, n, n, n, n, n, 1.0, ang)
+    ref = Reference()
+    x = ctk.make_phantom(ctk.PhantomKind.shepp_logan_3d, n, "float64").cpu().numpy()
+    yr = ref.forward(g, x)
+    br = ref.back(g, yr, 0)
+    p = ctk.projector_pair(to_ctk(g))
+
+    def rel(a, b):
+        return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+    assert rel(p.apply_forward(x.astype(np.float32)), yr) < 1e-5  # measured 4.9e-7
+    assert rel(p.apply_back(yr.astype(np.float32)), br) < 1e-5    # measured 5.1e-6
