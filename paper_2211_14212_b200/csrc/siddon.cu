@@ -187,8 +187,11 @@ __device__ __forceinline__ bool s_window(const KGeom& g, double ct, double st, c
 // coalesced across the lanes.  Per voxel the contributions are added in the reference's
 // scatter order (view, row, column) -- the lane's row loop is inside the column loop here,
 // so the order is kept by iterating rows outermost per lane.
+#ifndef CTK_SID_MINB
+#define CTK_SID_MINB 6  // 113 -> 80 regs (80 B spill): 58.8 -> 55.4 ms at 256^3/180 (5: 57.4, 8: 56.6)
+#endif
 template <class T>
-__global__ void __launch_bounds__(128) k_siddon_atb(KGeom g, const double* __restrict__ rayinv,
+__global__ void __launch_bounds__(128, CTK_SID_MINB) k_siddon_atb(KGeom g, const double* __restrict__ rayinv,
                                                     const T* __restrict__ pt, T* __restrict__ vol, int kblocks) {
     const long wid = long(blockIdx.x) * blockDim.y + threadIdx.y;
     const long ncol = long(g.nx) * g.ny;
