@@ -62,6 +62,20 @@ def peaks():
         return 6650.0, 1965.0, "fallback"
 
 
+def traffic_bytes(kernel, n, na):
+    """DRAM bytes per operation of the dominant kernel from the committed ncu capture (same
+    workload only), else None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic_ax_512_360.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if t.get("kernel") == kernel and t.get("n") == n and t.get("angles") == na:
+        return t["dram_bytes_per_op"]  # bytes per operation (compare "algorithmic_bytes")
+    return None
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
 
@@ -364,8 +378,12 @@ def main():
         "atb_gvox_s": bt_gvox,
         "kernels_ms": {"k_ax_f32": t_ax, "k_atb_matched_f32": t_bt, "ax_call": statistics.median(ax_call_ms[1:])},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
-                     "note": f"algorithmic bytes 4*(N_vox+N_proj) per launch; peak {peak_src}"},
+                     "frac": achieved / hbm_peak, "traffic": traffic_bytes(dom, n, my_angles) if my_slices == n else None, "algorithmic_bytes": alg_bytes,
+                     "note": f"algorithmic bytes 4*(N_vox+N_proj) per launch; peak {peak_src}; traffic = measured "
+                             "DRAM bytes of the same operation (both slice-chunk launches) from the committed ncu "
+                             "capture, profiles/r01/traffic_ax_512_360.json, when the workload matches; the volume "
+                             "slab of each detector-row band is re-read from DRAM by design (L2 residency per band; "
+                             "154 GB/s, the kernel is bound on chip)"},
         "roofline_gather": {"kernel": dom, "achieved": samples / (t_dom / 1e3) / 1e9, "peak": gather_peak,
                             "unit": "G samples/s", "frac": samples / (t_dom / 1e3) / 1e9 / gather_peak,
                             "note": "binding on-chip ceiling: 16 B/sample at 128 B/clk/SM x 148 SMs (SURVEY.md 8(d))"},
