@@ -163,10 +163,14 @@ def cpu_reference_rate(n, na, budget_s, dtype_f32=True):
         t2 = time.perf_counter()
         return S, t1 - t0, t2 - t1
 
-    S, tax, tbt = run(1)  # calibration (also warms caches / threads)
-    per_angle = (tax + tbt)
-    S = max(1, min(na, int(budget_s / max(per_angle, 1e-6))))
-    S, tax, tbt = run(S)
+    # The reference parallelises Ax and A^T b over angles (projector.hpp:148-150, 172-201), so
+    # a sample of fewer angles than threads would leave cores idle: calibrate on one angle
+    # per thread, then grow the sample in whole multiples of the thread count.
+    S0 = min(na, cores)
+    S, tax, tbt = run(S0)  # calibration (also warms caches / threads)
+    reps = max(1, int(budget_s / max(tax + tbt, 1e-6)))
+    if reps > 1 and S0 < na:
+        S, tax, tbt = run(min(na, S0 * reps))
     t_iter = (na / S) * (2.0 * tax + tbt)
     samples_ax = S * n * n * n  # rays*slices for S angles (Gray-voxel normaliser)
     return {
