@@ -7,8 +7,9 @@ slab -- bit-identical, since a voxel's contributions are summed in the same orde
 
 Solver side: two processes on the one GPU, each owning one slab, with the product's
 collectives over gloo (host-staged; no kernel waits on another rank), must reproduce the
-unsharded solve: LSQR (A x partials sum-reduced, domain dots summed in rank order) and
-CGLS-TV (plus the one-slice halos of the gradient stencils)."""
+unsharded solve for every solver (A x partials sum-reduced, domain dots and the domain-basis
+CGS2 coefficients summed in rank order; CGLS-TV / flsqr_tv also the one-slice halos of the
+gradient stencils)."""
 import os
 import socket
 import sys
@@ -93,11 +94,19 @@ def _problem():
     return g, gt.astype(np.float32), b
 
 
+SOLVERS = ["cgls", "lsqr", "lsmr", "sirt", "hybrid_lsqr", "ab_gmres", "ba_gmres", "cgls_tv", "flsqr_tv"]
+
+
 def _solve(ctk, pair, b, which):
-    opts = ctk.SolverOptions(max_iters=6, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
-    if which == "lsqr":
-        return ctk.lsqr(pair, b, opts)
-    return ctk.cgls_tv(pair, b, 0.5, 2, 3, opts)
+    opts = ctk.SolverOptions(max_iters=4 if which == "flsqr_tv" else 6, stop_on_explicit_residual_increase=False,
+                             residual_tolerance=0.0)
+    if which == "lsmr":
+        return ctk.lsmr(pair, b, 5.0, opts)
+    if which in ("hybrid_lsqr", "flsqr_tv"):
+        return getattr(ctk, which)(pair, b, ctk.HybridStrategy.gcv(), opts)
+    if which == "cgls_tv":
+        return ctk.cgls_tv(pair, b, 0.5, 2, 3, opts)
+    return getattr(ctk, which)(pair, b, opts)
 
 
 def _worker(rank, world, port, outdir):
@@ -114,7 +123,7 @@ def _worker(rank, world, port, outdir):
     z0, cnt = shard_slabs(g.nz, world, rank)
     comm = TorchComm(rank, world, device="cuda")
     out = {}
-    for which in ("lsqr", "cgls_tv"):
+    for which in SOLVERS:
         pair = ctk.projector_pair(_to_ctk(g), slab=(z0, cnt))
         pair.projector.attach_comm(comm)
         r = _solve(ctk, pair, b, which)
@@ -135,12 +144,12 @@ def test_slab_sharded_solvers_two_ranks(ctk, tmp_path):
     g, gt, b = _problem()
     n = g.nx * g.ny
     ranks = [np.load(tmp_path / f"rank{r}.npz") for r in range(world)]
-    for which in ("lsqr", "cgls_tv"):
+    for which in SOLVERS:
         ref = _solve(ctk, ctk.projector_pair(to_ctk(g)), b, which)
         x = np.concatenate([r[which + "_x"] for r in ranks])
         assert x.size == n * g.nz
-        assert rel_l2(x, ref.x) < 1e-5, which
+        assert rel_l2(x, ref.x) < 1e-4, which
         for r in ranks:  # every rank logs the same (global) residual history
-            assert np.allclose(r[which + "_expl"], ref.log.explicit_residual, rtol=1e-5)
-            assert np.allclose(r[which + "_impl"], ref.log.implicit_residual, rtol=1e-5)
+            assert np.allclose(r[which + "_expl"], ref.log.explicit_residual, rtol=1e-4), which
+            assert np.allclose(r[which + "_impl"], ref.log.implicit_residual, rtol=1e-4), which
         assert np.array_equal(ranks[0][which + "_expl"], ranks[1][which + "_expl"])
