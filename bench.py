@@ -402,7 +402,11 @@ def main():
         try:
             cb = cpu_reference_rate(n, na, args.cpu_budget)
             line["cpu_baseline"] = {"value": cb["iters_per_s"], "unit": "iters/s", "cores": cb["cores"],
-                                    "kind": cb["kind"], "sample": cb["sample"], "ax_gvox_s": cb["ax_gvox_s"],
+                                    "kind": cb["kind"],
+                                    "sample": cb["sample"] + ("; the reference has no Siddon projector, so its Joseph "
+                                                              "path (same rays and sizes) stands in"
+                                                              if args.projector == "siddon" else ""),
+                                    "ax_gvox_s": cb["ax_gvox_s"],
                                     "atb_gvox_s": cb["atb_gvox_s"]}
         except Exception as e:  # reported, never fatal to the GPU number
             line["cpu_baseline"] = {"value": None, "unit": "iters/s", "cores": os.cpu_count(), "kind": "reference",
