@@ -221,6 +221,42 @@ __global__ void __launch_bounds__(128, CTK_SID_MINB) k_siddon_atb(KGeom g, const
         const double sx = g.dso * cs.x, sy = g.dso * cs.y;  // cone: every ray starts at the source
         const T* fa = pt + size_t(a) * frame;
         const double* ra = rayinv + 3 * size_t(a) * frame;
+        if (cone) {
+            // every ray of the view starts at the source: the plane offsets (plane - o) are
+            // per (voxel, view), the same subtractions the general path does per candidate
+            const double o3[3] = {sx, sy, 0.0};
+            double dlo[3], dhi[3];
+            bool flat[3];
+#pragma unroll
+            for (int ax = 0; ax < 3; ++ax) {
+                dlo[ax] = plo[ax] - o3[ax];
+                dhi[ax] = phi[ax] - o3[ax];
+                flat[ax] = s_slab(o3[ax], n3[ax], h) == idx3[ax];  // a ray with d_ax == 0 stays in o's slab
+            }
+            for (int iv = iv0; iv <= iv1; ++iv)
+                for (int iu = iu0; iu <= iu1; ++iu) {
+                    const size_t q = size_t(iu) * g.nv + iv;  // [a][iu][iv]
+                    const T value = __ldg(fa + q);
+                    if (value == T(0)) continue;
+                    const double inv[3] = {__ldg(ra + 3 * q), __ldg(ra + 3 * q + 1), __ldg(ra + 3 * q + 2)};
+                    double lo = -DBL_MAX, hi = DBL_MAX;
+                    bool miss = false;
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) {
+                        if (inv[ax] == 0.0) {
+                            miss |= !flat[ax];
+                            continue;
+                        }
+                        const double a0 = dlo[ax] * inv[ax];
+                        const double a1 = dhi[ax] * inv[ax];
+                        lo = fmax(lo, fmin(a0, a1));
+                        hi = fmin(hi, fmax(a0, a1));
+                    }
+                    if (miss || !(hi > lo)) continue;
+                    acc += T(hi - lo) * value;
+                }
+            continue;
+        }
         for (int iv = iv0; iv <= iv1; ++iv)
             for (int iu = iu0; iu <= iu1; ++iu) {
                 const size_t q = size_t(iu) * g.nv + iv;  // [a][iu][iv]
