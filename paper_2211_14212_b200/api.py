@@ -300,10 +300,25 @@ class Projector:
             return "f64"
         raise ParameterError(f"unsupported dtype {dtype}; use float32 or float64")
 
+    @staticmethod
+    def _check_buffers(a, b):
+        """Both operands CUDA tensors or both host arrays, one dtype, contiguous: the native
+        entry points read and write them as flat arrays."""
+        dev = _is_torch_cuda(a)
+        if dev != _is_torch_cuda(b):
+            raise ParameterError("input and output must both be CUDA tensors or both host arrays")
+        if a.dtype != b.dtype:
+            raise ParameterError(f"input and output dtypes differ ({a.dtype} vs {b.dtype})")
+        for v in (a, b):
+            if not (v.is_contiguous() if dev else (isinstance(v, np.ndarray) and v.flags.c_contiguous
+                                                   and v.dtype.isnative)):
+                raise ParameterError("operator buffers must be contiguous (native byte order)")
+
     def forward(self, x, y, stream=None):
         """y <- A x (overwrites y).  numpy -> host entry point; CUDA tensors -> device."""
         if _numel(x) != self.domain_size or _numel(y) != self.range_size:
             raise DimensionError("operator domain size mismatch")
+        self._check_buffers(x, y)
         t = self._suffix(x.dtype)
         if _is_torch_cuda(x):
             _check(getattr(self.lib, f"ctk_ax_{t}")(self.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
@@ -314,6 +329,7 @@ class Projector:
     def back(self, y, x, variant=BackprojectVariant.matched, stream=None):
         if _numel(y) != self.range_size or _numel(x) != self.domain_size:
             raise DimensionError("operator range size mismatch")
+        self._check_buffers(y, x)
         t = self._suffix(y.dtype)
         if _is_torch_cuda(y):
             _check(getattr(self.lib, f"ctk_atb_{t}")(self.handle, int(variant), C.c_void_p(y.data_ptr()),
@@ -336,6 +352,18 @@ def _empty_like(a, n):
 
         return torch.empty(n, dtype=a.dtype, device=a.device)
     return np.empty(n, dtype=a.dtype)
+
+
+def _contiguous(a):
+    """apply_forward/apply_back take any array-like (the reference's spans are contiguous):
+    CUDA tensors are made contiguous on the device, everything else becomes a contiguous
+    host array in native byte order."""
+    if _is_torch_cuda(a):
+        return a if a.is_contiguous() else a.contiguous()
+    a = np.asarray(a)
+    if not a.dtype.isnative:
+        a = a.astype(a.dtype.newbyteorder("="))
+    return np.ascontiguousarray(a)
 
 
 def _host(a, dtype=None):
@@ -365,12 +393,14 @@ class OperatorPair:
             raise DimensionError("operator range size mismatch")
 
     def apply_forward(self, x):
+        x = _contiguous(x)
         self.check_domain(x.size if isinstance(x, np.ndarray) else x.numel())
         y = _empty_like(x, self.range_size)
         self.forward(x, y)
         return y
 
     def apply_back(self, y):
+        y = _contiguous(y)
         self.check_range(y.size if isinstance(y, np.ndarray) else y.numel())
         x = _empty_like(y, self.domain_size)
         self.back(y, x)
@@ -500,6 +530,8 @@ def _solve(name, pair: OperatorPair, b, opts: SolverOptions, lam=0.0, strategy=N
     proj = pair.projector
     lib = proj.lib
     dev = _is_torch_cuda(b)
+    if dev and not b.is_contiguous():
+        b = b.contiguous()
     t = Projector._suffix(b.dtype)
     ndt = np.float32 if t == "f32" else np.float64
     cap = outer * inner if name == "cgls_tv" else opts.max_iters
