@@ -280,7 +280,7 @@ void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* pa
 // Slice chunks per ray: enough that the slab a (row band, chunk) pass touches -- about
 // 200 B per (slice, in-plane row) for a 32-row band -- stays near 26 MB, i.e. L2-resident
 // across all views; at least 2 (measured: 2 at 256^3 and 512^3, 8 at 1024^3: 3.06 s with 2
-// chunks vs 1.70 s with 8).  CTK_FWD_CHUNKS overrides.
+// chunks vs 1.70 s with 8).  CTK_FWD_CHUNKS (environment) overrides.
 int fwd_chunks(const Geometry& g) {
     static const int forced = [] {
         const char* e = std::getenv("CTK_FWD_CHUNKS");
@@ -288,7 +288,11 @@ int fwd_chunks(const Geometry& g) {
     }();
     if (forced) return forced;
     const double slab = double(std::max(g.nx, g.ny)) * (std::max(g.nx, g.ny) + 2) * 200.0;
-    return std::max(CTK_FWD_CHUNKS, std::min(16, int(std::lround(slab / 26e6))));
+    const int base = std::max(CTK_FWD_CHUNKS, std::min(16, int(std::lround(slab / 26e6))));
+    // fewer views per handle (an angle-sharded rank) -> fewer reuses of each slab: halve it
+    // (512^3: 45/90/180 views 7.43/13.57/25.33 -> 7.03/13.02/24.88 ms with 4 chunks, 360 views
+    // unchanged; at 256^3 the minimum of 2 stays best at every view count)
+    return (g.na < 300 && slab > 26e6) ? std::min(16, 2 * base) : base;
 }
 
 double* residual_partials(Geometry& g, size_t& nblk) {
