@@ -4,6 +4,7 @@
 // from the projections transposed to pt[a][iu][iv] -- so no float atomics are used and
 // every voxel sums its contributions in a fixed order.
 #include <cstdlib>
+#include <mutex>
 
 #include "f32_common.cuh"
 
@@ -570,11 +571,15 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
                                          ((size_t(g.nv) + 3) & ~size_t(3))) +
                         sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
-    static size_t configured = 0;
-    if (smem > configured) {
-        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-        configured = smem;
-    }
+    // opt in once to the largest size this launcher accepts (occupancy follows the size of
+    // each launch, not the opt-in); call_once keeps concurrent handles on other threads safe
+    static std::once_flag opted[64];  // function attributes are per device
+    int dev = 0;
+    CTK_CUDA(cudaGetDevice(&dev));
+    std::call_once(opted[dev & 63], [] {
+        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      200 * 1024));
+    });
     dim3 grd(unsigned(planes), unsigned(ptiles * kbands));
     k_atb_plane_f32<CLASS, PB><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
     after_launch("k_atb_plane_f32");
