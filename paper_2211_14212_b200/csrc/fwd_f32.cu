@@ -83,9 +83,9 @@ template <int MODE, class Off>
 __global__ void __launch_bounds__(ZW_BR * ZW_BC)
 k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
                const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
-               double* __restrict__ partials, int nch, int chunk) {
+               double* __restrict__ partials, int nch, int chunk, int band0) {
     __shared__ float outs[ZW_BR][ZW_BC + 1];
-    const int band = blockIdx.z;
+    const int band = blockIdx.z + band0;
     const int iv = band * ZW_BR + threadIdx.x;
     const int a = vorder[blockIdx.y];
     const int iu = blockIdx.x * ZW_BC + threadIdx.y;
@@ -265,15 +265,18 @@ bool wide_offsets(const Geometry& g) {
 
 template <int MODE>
 void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* partials, cudaStream_t s, int nch = 1,
-               int chunk = 0) {
+               int chunk = 0, int band0 = 0, int band1 = -1) {
     const KGeom k = g.kgeom();
     const int* vo = g.d_vorder.as<int>();
     const float *a0 = g.vx.as<float>(), *a1 = g.vy.as<float>();
     const dim3 blk(ZW_BR, ZW_BC);
+    dim3 grd = fwd_grid(g);
+    if (band1 >= 0) grd.z = unsigned(band1 - band0);
+    if (grd.z == 0) return;
     if (wide_offsets(g))
-        k_ax_zfast_f32<MODE, long long><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk);
+        k_ax_zfast_f32<MODE, long long><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
     else
-        k_ax_zfast_f32<MODE, int><<<fwd_grid(g), blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk);
+        k_ax_zfast_f32<MODE, int><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
     after_launch(MODE == 0 ? "k_ax_zfast_f32" : "k_ax_zfast_f32_residual");
 }
 
@@ -295,6 +298,38 @@ int fwd_chunks(const Geometry& g) {
     return (g.na < 300 && slab > 26e6) ? std::min(16, 2 * base) : base;
 }
 
+// Detector-row bands whose rays can reach this handle's slices.  A cone ray through row
+// coordinate v meets height z at depth d (from the source) where z = v d / (DSO + DOD), and
+// the volume spans depths DSO -+ R (R: in-plane half-diagonal), so a z-slab is seen only by
+// the rows between its edges' images at the nearest and farthest depth (parallel beams:
+// v = z).  With a thin slab most bands see nothing: they are not launched (their rows are
+// zeroed instead).  Whole-volume handles keep every band.
+void slab_bands(const Geometry& g, int& b0, int& b1) {
+    const int nb = (g.nv + ZW_BR - 1) / ZW_BR;
+    b0 = 0;
+    b1 = nb;
+    if (!g.slab || g.nv == 1) return;
+    const double h = g.h, cz = 0.5 * (g.nz - 1);
+    const double zlo = (g.z0 - 2.0 - cz) * h, zhi = (g.z0 + g.nz_local() + 1.0 - cz) * h;  // taps + margin
+    double vlo = zlo, vhi = zhi;
+    if (g.mode == CTK_CONE3D) {
+        const double R = 0.5 * h * std::sqrt(double(g.nx) * g.nx + double(g.ny) * g.ny) + 2.0 * h;
+        if (!(g.dso - R > 0.0)) return;
+        const double D = g.dso + g.dod, dn = g.dso - R, df = g.dso + R;
+        vlo = std::min(zlo * D / dn, zlo * D / df);
+        vhi = std::max(zhi * D / dn, zhi * D / df);
+    }
+    const double cv = 0.5 * (g.nv - 1);
+    const int r0 = std::max(0, int(std::floor(vlo / g.du + cv)) - 2);
+    const int r1 = std::min(g.nv, int(std::ceil(vhi / g.du + cv)) + 3);
+    if (r1 <= r0) {
+        b1 = b0;
+        return;
+    }
+    b0 = r0 / ZW_BR;
+    b1 = std::min(nb, (r1 + ZW_BR - 1) / ZW_BR);
+}
+
 double* residual_partials(Geometry& g, size_t& nblk) {
     const dim3 grd = fwd_grid(g);
     nblk = size_t(grd.x) * grd.y * grd.z;
@@ -307,14 +342,12 @@ double* residual_partials(Geometry& g, size_t& nblk) {
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
     relayout_zfast(g, x, g.vx, g.vy, s);
     const int nch = fwd_chunks(g);
-    if (nch > 1) {
-        CTK_CUDA(cudaEventRecord(g.ev0, s));
-        for (int c = 0; c < nch; ++c) launch_ax<0>(g, x, y, nullptr, nullptr, s, nch, c);
-        CTK_CUDA(cudaEventRecord(g.ev1, s));
-        return;
-    }
+    int b0, b1;
+    slab_bands(g, b0, b1);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    launch_ax<0>(g, x, y, nullptr, nullptr, s);
+    if (b0 > 0 || b1 < int((g.nv + ZW_BR - 1) / ZW_BR))
+        CTK_CUDA(cudaMemsetAsync(y, 0, g.range() * sizeof(float), s));  // rows no launched band writes
+    for (int c = 0; c < nch; ++c) launch_ax<0>(g, x, y, nullptr, nullptr, s, nch, c, b0, b1);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
 }
 
