@@ -27,6 +27,13 @@ __global__ void k_finish_max(const double* __restrict__ p, int n, double* __rest
     if (threadIdx.x == 0) *out = v;
 }
 
+template <class T>
+struct Pair2 {
+    T a, b;
+};
+template <class T>
+__device__ __forceinline__ Pair2<T> make_pair2(T a, T b) { return {a, b}; }
+
 struct Chunk {
     size_t b, e;
 };
@@ -36,25 +43,46 @@ __device__ __forceinline__ Chunk my_chunk(size_t n) {
     return {b, min(n, b + per)};
 }
 
-// Four independent partial sums per thread (elements i, i+B, i+2B, i+3B of the block's
-// chunk): four loads per operand in flight instead of one -- with 4 resident blocks of 256
-// threads per SM a single load each keeps only ~8 KB in flight, well short of what HBM
-// latency x bandwidth needs.  The combination order is fixed, so results stay
-// run-to-run bitwise identical.
+// Four independent partial sums per thread over eight elements per iteration (i, i+B, ...,
+// i+7B of the block's chunk): eight loads per operand in flight instead of one -- with 4
+// resident blocks of 256 threads per SM a single load each keeps only ~8 KB in flight, well
+// short of what HBM latency x bandwidth needs.  The combination order is fixed, so results
+// stay run-to-run bitwise identical.
 template <class T, class F>
 __device__ __forceinline__ double chunk_reduce(size_t n, F f) {
     const Chunk c = my_chunk(n);
     const size_t B = blockDim.x;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     size_t i = c.b + threadIdx.x;
-    for (; i + 3 * B < c.e; i += 4 * B) {
+    for (; i + 7 * B < c.e; i += 8 * B) {  // eight elements' loads in flight
         const double v0 = f(i), v1 = f(i + B), v2 = f(i + 2 * B), v3 = f(i + 3 * B);
-        a0 += v0;
-        a1 += v1;
-        a2 += v2;
-        a3 += v3;
+        const double v4 = f(i + 4 * B), v5 = f(i + 5 * B), v6 = f(i + 6 * B), v7 = f(i + 7 * B);
+        a0 += v0 + v4;
+        a1 += v1 + v5;
+        a2 += v2 + v6;
+        a3 += v3 + v7;
     }
     for (; i < c.e; i += B) a0 += f(i);
+    return block_sum((a0 + a1) + (a2 + a3));
+}
+
+// The same with a store per element: ld(i) reads element i's operands, st(i, v) writes it
+// and returns its contribution.  All four elements' loads are issued before any store (the
+// operations are elementwise, so this reorders nothing that could alias).
+template <class T, class LD, class ST>
+__device__ __forceinline__ double chunk_reduce_st(size_t n, LD ld, ST st) {
+    const Chunk c = my_chunk(n);
+    const size_t B = blockDim.x;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    size_t i = c.b + threadIdx.x;
+    for (; i + 3 * B < c.e; i += 4 * B) {
+        const auto v0 = ld(i), v1 = ld(i + B), v2 = ld(i + 2 * B), v3 = ld(i + 3 * B);
+        a0 += st(i, v0);
+        a1 += st(i + B, v1);
+        a2 += st(i + 2 * B, v2);
+        a3 += st(i + 3 * B, v3);
+    }
+    for (; i < c.e; i += B) a0 += st(i, ld(i));
     return block_sum((a0 + a1) + (a2 + a3));
 }
 
@@ -75,11 +103,13 @@ __global__ void k_diff_nrm2sq(size_t n, const T* __restrict__ a, const T* __rest
 
 template <class T>
 __global__ void k_axpy_nrm2sq(size_t n, T alpha, const T* __restrict__ x, T* __restrict__ y, double* __restrict__ part) {
-    const double r = chunk_reduce<T>(n, [&](size_t i) {
-        const T v = y[i] + alpha * x[i];
-        y[i] = v;
-        return double(v) * double(v);
-    });
+    const double r = chunk_reduce_st<T>(
+        n, [&](size_t i) { return make_pair2(x[i], y[i]); },
+        [&](size_t i, Pair2<T> p) {
+            const T v = p.b + alpha * p.a;
+            y[i] = v;
+            return double(v) * double(v);
+        });
     if (threadIdx.x == 0) part[blockIdx.x] = r;
 }
 
@@ -87,11 +117,13 @@ __global__ void k_axpy_nrm2sq(size_t n, T alpha, const T* __restrict__ x, T* __r
 template <class T>
 __global__ void k_sub_nrm2sq(size_t n, const T* __restrict__ b, const T* __restrict__ ax, T* __restrict__ r,
                              double* __restrict__ part) {
-    const double v = chunk_reduce<T>(n, [&](size_t i) {
-        const T d = b[i] - ax[i];
-        r[i] = d;
-        return double(d) * double(d);
-    });
+    const double v = chunk_reduce_st<T>(
+        n, [&](size_t i) { return make_pair2(b[i], ax[i]); },
+        [&](size_t i, Pair2<T> p) {
+            const T d = p.a - p.b;
+            r[i] = d;
+            return double(d) * double(d);
+        });
     if (threadIdx.x == 0) part[blockIdx.x] = v;
 }
 
@@ -104,37 +136,70 @@ __global__ void k_absmax(size_t n, const T* __restrict__ x, double* __restrict__
     if (threadIdx.x == 0) part[blockIdx.x] = m;
 }
 
+// Elementwise maps: F::load(i) reads element i's operands, F::store(i, v) writes its
+// results.  Four grid-stride elements per iteration with all loads issued before the stores
+// (four loads per operand in flight; elementwise, so nothing that can alias is reordered).
 template <class T, class F>
 __global__ void k_map(size_t n, F f) {
-    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) f(i);
+    const size_t S = size_t(gridDim.x) * blockDim.x;
+    size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; i + 3 * S < n; i += 4 * S) {
+        const auto v0 = f.load(i), v1 = f.load(i + S), v2 = f.load(i + 2 * S), v3 = f.load(i + 3 * S);
+        f.store(i, v0);
+        f.store(i + S, v1);
+        f.store(i + 2 * S, v2);
+        f.store(i + 3 * S, v3);
+    }
+    for (; i < n; i += S) f.store(i, f.load(i));
 }
 
 template <class T>
-struct AxpyF {
+struct V1 {
+    T a;
+};
+template <class T>
+struct V2 {
+    T a, b;
+};
+template <class T>
+struct V3 {
+    T a, b, c;
+};
+template <class T>
+struct V4 {
+    T a, b, c, d;
+};
+
+template <class T>
+struct AxpyF {  // y += a x
     T a;
     const T* x;
     T* y;
-    __device__ void operator()(size_t i) const { y[i] += a * x[i]; }
+    __device__ V2<T> load(size_t i) const { return {x[i], y[i]}; }
+    __device__ void store(size_t i, V2<T> v) const { y[i] = v.b + a * v.a; }
 };
 template <class T>
-struct XpbyF {
+struct XpbyF {  // y = x + b y
     const T* x;
     T b;
     T* y;
-    __device__ void operator()(size_t i) const { y[i] = x[i] + b * y[i]; }
+    __device__ V2<T> load(size_t i) const { return {x[i], y[i]}; }
+    __device__ void store(size_t i, V2<T> v) const { y[i] = v.a + b * v.b; }
 };
 template <class T>
 struct ScalF {
     T a;
     T* x;
-    __device__ void operator()(size_t i) const { x[i] *= a; }
+    __device__ V1<T> load(size_t i) const { return {x[i]}; }
+    __device__ void store(size_t i, V1<T> v) const { x[i] = v.a * a; }
 };
 template <class T>
 struct ScaleCopyF {
     T a;
     const T* x;
     T* y;
-    __device__ void operator()(size_t i) const { y[i] = a * x[i]; }
+    __device__ V1<T> load(size_t i) const { return {x[i]}; }
+    __device__ void store(size_t i, V1<T> v) const { y[i] = a * v.a; }
 };
 template <class T>
 struct LsqrF {
@@ -142,10 +207,10 @@ struct LsqrF {
     T* x;
     T* w;
     const T* v;
-    __device__ void operator()(size_t i) const {
-        const T wi = w[i];
-        x[i] += c1 * wi;
-        w[i] = v[i] - c2 * wi;
+    __device__ V3<T> load(size_t i) const { return {x[i], w[i], v[i]}; }
+    __device__ void store(size_t i, V3<T> e) const {
+        x[i] = e.a + c1 * e.b;
+        w[i] = e.c - c2 * e.b;
     }
 };
 template <class T>
@@ -155,39 +220,43 @@ struct LsmrF {
     T* h;
     T* hbar;
     const T* v;
-    __device__ void operator()(size_t i) const {
-        const T hi = h[i];
-        const T hb = hi - c1 * hbar[i];
+    __device__ V4<T> load(size_t i) const { return {h[i], hbar[i], x[i], v[i]}; }
+    __device__ void store(size_t i, V4<T> e) const {
+        const T hb = e.a - c1 * e.b;
         hbar[i] = hb;
-        x[i] += c2 * hb;
-        h[i] = v[i] - c3 * hi;
+        x[i] = e.c + c2 * hb;
+        h[i] = e.d - c3 * e.a;
     }
 };
 template <class T>
 struct InvFloorF {  // x = 1 / max(x, floor)   (solvers.hpp:257-263)
     T floor;
     T* x;
-    __device__ void operator()(size_t i) const { x[i] = T(1) / (x[i] > floor ? x[i] : floor); }
+    __device__ V1<T> load(size_t i) const { return {x[i]}; }
+    __device__ void store(size_t i, V1<T> v) const { x[i] = T(1) / (v.a > floor ? v.a : floor); }
 };
 template <class T>
 struct MulF {  // out = a .* b
     const T* a;
     const T* b;
     T* out;
-    __device__ void operator()(size_t i) const { out[i] = a[i] * b[i]; }
+    __device__ V2<T> load(size_t i) const { return {a[i], b[i]}; }
+    __device__ void store(size_t i, V2<T> v) const { out[i] = v.a * v.b; }
 };
 template <class T>
 struct AddMulF {  // x += a .* b
     const T* a;
     const T* b;
     T* x;
-    __device__ void operator()(size_t i) const { x[i] += a[i] * b[i]; }
+    __device__ V3<T> load(size_t i) const { return {a[i], b[i], x[i]}; }
+    __device__ void store(size_t i, V3<T> v) const { x[i] = v.c + v.a * v.b; }
 };
 template <class T>
 struct FillF {
     T v;
     T* x;
-    __device__ void operator()(size_t i) const { x[i] = v; }
+    __device__ V1<T> load(size_t) const { return {v}; }
+    __device__ void store(size_t i, V1<T> e) const { x[i] = e.a; }
 };
 
 template <class T, class F>
@@ -202,6 +271,31 @@ void run_map(size_t n, F f, cudaStream_t s, const char* what) {
 // Basis vectors in groups of BD_G: w is read once per group (not once per vector) and each
 // thread has 1 + BD_G independent loads in flight per element.
 constexpr int BD_G = 8;
+// One group of G basis vectors over the block's chunk: two elements per iteration, all
+// 2 * (1 + G) loads issued before the FMAs.
+template <int G, class T>
+__device__ __forceinline__ void block_dot_group(const Chunk& c, const T* __restrict__ bq, size_t ld,
+                                                const T* __restrict__ w, double* acc) {
+    const size_t B = blockDim.x;
+    size_t i = c.b + threadIdx.x;
+    for (; i + B < c.e; i += 2 * B) {
+        const double w0 = double(__ldg(w + i)), w1 = double(__ldg(w + i + B));
+        T b0[G], b1[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            b0[j] = __ldg(bq + size_t(j) * ld + i);
+            b1[j] = __ldg(bq + size_t(j) * ld + i + B);
+        }
+#pragma unroll
+        for (int j = 0; j < G; ++j) acc[j] += double(b0[j]) * w0 + double(b1[j]) * w1;
+    }
+    if (i < c.e) {
+        const double w0 = double(__ldg(w + i));
+#pragma unroll
+        for (int j = 0; j < G; ++j) acc[j] += double(__ldg(bq + size_t(j) * ld + i)) * w0;
+    }
+}
+
 template <class T>
 __global__ void k_block_dot(size_t n, int m, const T* __restrict__ basis, size_t ld, const T* __restrict__ w,
                             double* __restrict__ part) {
@@ -212,29 +306,15 @@ __global__ void k_block_dot(size_t n, int m, const T* __restrict__ basis, size_t
         double acc[BD_G];
 #pragma unroll
         for (int j = 0; j < BD_G; ++j) acc[j] = 0.0;
-        // a partial group loads its last vector in the unused slots (unpredicated loads, so
-        // all of them issue before the first FMA; the extra sums are discarded); two
-        // elements per iteration -> 2 * (1 + BD_G) loads in flight
-        size_t off[BD_G];
-#pragma unroll
-        for (int j = 0; j < BD_G; ++j) off[j] = size_t(min(j, g - 1)) * ld;
-        const size_t B = blockDim.x;
-        size_t i = c.b + threadIdx.x;
-        for (; i + B < c.e; i += 2 * B) {
-            const double w0 = double(__ldg(w + i)), w1 = double(__ldg(w + i + B));
-            T b0[BD_G], b1[BD_G];
-#pragma unroll
-            for (int j = 0; j < BD_G; ++j) {
-                b0[j] = __ldg(bq + off[j] + i);
-                b1[j] = __ldg(bq + off[j] + i + B);
-            }
-#pragma unroll
-            for (int j = 0; j < BD_G; ++j) acc[j] += double(b0[j]) * w0 + double(b1[j]) * w1;
-        }
-        if (i < c.e) {
-            const double w0 = double(__ldg(w + i));
-#pragma unroll
-            for (int j = 0; j < BD_G; ++j) acc[j] += double(__ldg(bq + off[j] + i)) * w0;
+        switch (g) {  // a group of exactly g vectors: no idle or duplicated loads
+            case 1: block_dot_group<1>(c, bq, ld, w, acc); break;
+            case 2: block_dot_group<2>(c, bq, ld, w, acc); break;
+            case 3: block_dot_group<3>(c, bq, ld, w, acc); break;
+            case 4: block_dot_group<4>(c, bq, ld, w, acc); break;
+            case 5: block_dot_group<5>(c, bq, ld, w, acc); break;
+            case 6: block_dot_group<6>(c, bq, ld, w, acc); break;
+            case 7: block_dot_group<7>(c, bq, ld, w, acc); break;
+            default: block_dot_group<BD_G>(c, bq, ld, w, acc); break;
         }
 #pragma unroll
         for (int j = 0; j < BD_G; ++j) {
