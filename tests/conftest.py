@@ -12,6 +12,22 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
     config.addinivalue_line("markers", "slow: larger parity cases")
+    _ensure_built()
+
+
+def _ensure_built():
+    """A checkout without the in-tree build (the .so files are not in git) builds the product
+    library and the C oracle first (nvcc cross-compiles; no GPU needed).  oracle/_ref needs
+    /root/reference and is built by __graft_entry__.build() where that exists."""
+    import subprocess
+
+    lib = os.path.join(ROOT, "paper_2211_14212_b200", "lib", "libctk_b200.so")
+    orc = os.path.join(ROOT, "oracle", "libctk_oracle.so")
+    if not os.path.exists(lib):
+        subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "paper_2211_14212_b200", "csrc")], check=True)
+    if not os.path.exists(orc):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), os.path.join(ROOT, "oracle", "libctk_oracle.so")],
+                       check=True)
 
 
 @pytest.fixture(scope="session")
