@@ -130,6 +130,20 @@ int ctk_make_phantom_f64(int kind, int n, double* d_out, void* stream);
 int ctk_shepp_logan_3d_f32(int n, float* d_out, void* stream); /* = make_phantom(0, n) */
 int ctk_shepp_logan_3d_f64(int n, double* d_out, void* stream);
 
+/* ---- forward-difference gradient and its adjoint (gradient.hpp:9-54), IRN TV weights
+ * (tv.hpp:17-43), on device pointers of an nx*ny*nz volume (x fastest).  The gradient and
+ * its adjoint are bit-identical to the reference's loops; the weights agree to an ulp (the
+ * device pow).  ctk_tv_weights takes eps (tv_epsilon: 1e-4 max|x|, > 0); the reference's
+ * all-ones case for eps == 0 is the caller's.  ctk_gradient_adjoint overwrites out. */
+int ctk_gradient_f32(int nx, int ny, int nz, const float* d_x, float* d_dx, float* d_dy, float* d_dz, void* stream);
+int ctk_gradient_f64(int nx, int ny, int nz, const double* d_x, double* d_dx, double* d_dy, double* d_dz, void* stream);
+int ctk_gradient_adjoint_f32(int nx, int ny, int nz, const float* d_dx, const float* d_dy, const float* d_dz,
+                             float* d_out, void* stream);
+int ctk_gradient_adjoint_f64(int nx, int ny, int nz, const double* d_dx, const double* d_dy, const double* d_dz,
+                             double* d_out, void* stream);
+int ctk_tv_weights_f32(int nx, int ny, int nz, const float* d_x, double eps, float* d_w, void* stream);
+int ctk_tv_weights_f64(int nx, int ny, int nz, const double* d_x, double eps, double* d_w, void* stream);
+
 /* ---- count-domain noise, add_noise (noise.hpp:26-47) on HOST buffers ----------------
  * One mt19937_64 stream walked in detector-index order (a Poisson then a Gaussian draw
  * per sample, libstdc++ distributions): sequential by definition, so it stays on the

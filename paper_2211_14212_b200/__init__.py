@@ -41,6 +41,12 @@ from .api import (  # noqa: F401
     launch_count,
     lsmr,
     lsqr,
+    gradient,
+    gradient_adjoint,
+    tv_epsilon,
+    tv_weights,
+    augment_tikhonov,
+    stack_weighted_gradient,
     make_phantom,
     add_noise,
     noise_rng_id,

@@ -135,6 +135,12 @@ def load():
         "ctk_make_phantom_f32": (i, [i, i, vp, vp]),
         "ctk_make_phantom_f64": (i, [i, i, vp, vp]),
         "ctk_add_noise_f32": (i, [sz, vp, d, d, C.c_uint64, vp]),
+        "ctk_gradient_f32": (i, [i, i, i, vp, vp, vp, vp, vp]),
+        "ctk_gradient_f64": (i, [i, i, i, vp, vp, vp, vp, vp]),
+        "ctk_gradient_adjoint_f32": (i, [i, i, i, vp, vp, vp, vp, vp]),
+        "ctk_gradient_adjoint_f64": (i, [i, i, i, vp, vp, vp, vp, vp]),
+        "ctk_tv_weights_f32": (i, [i, i, i, vp, d, vp, vp]),
+        "ctk_tv_weights_f64": (i, [i, i, i, vp, d, vp, vp]),
         "ctk_add_noise_f64": (i, [sz, vp, d, d, C.c_uint64, vp]),
         "ctk_solve_dev_f32": (i, [vp, i, i, vp, d, C.POINTER(HybridStrategyC), i, i, i, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)]),
         "ctk_solve_dev_f64": (i, [vp, i, i, vp, d, C.POINTER(HybridStrategyC), i, i, i, C.POINTER(SolverOpts), vp, C.POINTER(SolveLog)]),

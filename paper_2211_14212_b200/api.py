@@ -20,6 +20,10 @@ error classes                          types.hpp:14-31
 ``cgls_tv``                            tv.hpp:45-110
 ``PhantomKind`` / ``make_phantom``     phantom.hpp:13, 118-152
 ``NoiseModel`` / ``add_noise``         noise.hpp:10-47
+``gradient`` / ``gradient_adjoint``    gradient.hpp:9-54
+``tv_epsilon`` / ``tv_weights``        tv.hpp:17-43
+``augment_tikhonov``                   operators.hpp:118-139
+``stack_weighted_gradient``            operators.hpp:141-186
 =====================================  ==================================================
 
 Every computation runs in libctk_b200.so (sm_100a kernels + C++ solvers) through the
@@ -638,6 +642,154 @@ def cgls_tv(pair: OperatorPair, b, lambda_: float, outer_iters: int, inner_iters
             warm_start: bool = False) -> SolveResult:
     """tv.hpp:45-110."""
     return _solve("cgls_tv", pair, b, opts, lam=lambda_, outer=outer_iters, inner=inner_iters, warm=warm_start)
+
+
+# ---- gradient, TV weights and operator compositions (gradient.hpp, tv.hpp:17-43,
+#      operators.hpp:118-186) on the device ----------------------------------------------------
+def _as_device(a, dtype=None):
+    """(CUDA tensor, was_host) -- host arrays are copied to the device once."""
+    import torch
+
+    if _is_torch_cuda(a):
+        t = a.reshape(-1)
+        return (t.to(dtype) if dtype is not None and t.dtype != dtype else t).contiguous(), False
+    h = np.ascontiguousarray(np.asarray(a)).reshape(-1)
+    t = torch.from_numpy(h).cuda()
+    return (t.to(dtype) if dtype is not None and t.dtype != dtype else t), True
+
+
+def _like_input(t, was_host):
+    return t.cpu().numpy() if was_host else t
+
+
+def _vol_suffix(t):
+    return Projector._suffix(t.dtype)
+
+
+def gradient(vol, shape: VolumeShape):
+    """gradient.hpp:9-30: forward differences (dx, dy, dz), zero on the far boundary."""
+    import torch
+
+    if shape.nx <= 0 or shape.ny <= 0 or shape.nz <= 0:
+        raise DimensionError("volume dimensions must be positive")
+    x, host = _as_device(vol)
+    if x.numel() != shape.size():
+        raise DimensionError("volume data length does not match nx*ny*nz")
+    g = [torch.empty_like(x) for _ in range(3)]
+    _check(getattr(L.load(), f"ctk_gradient_{_vol_suffix(x)}")(
+        shape.nx, shape.ny, shape.nz, C.c_void_p(x.data_ptr()), *[C.c_void_p(v.data_ptr()) for v in g],
+        _torch_stream()))
+    return tuple(_like_input(v, host) for v in g)
+
+
+def gradient_adjoint(dx, dy, dz, shape: VolumeShape):
+    """gradient.hpp:32-54: the exact transpose of gradient()."""
+    import torch
+
+    comps = [_as_device(v) for v in (dx, dy, dz)]
+    host = comps[0][1]
+    g = [c[0] for c in comps]
+    if any(v.numel() != shape.size() for v in g):
+        raise DimensionError("gradient component lengths do not match volume shape")
+    if len({v.dtype for v in g}) != 1:
+        raise ParameterError("gradient components must share one dtype")
+    out = torch.empty_like(g[0])
+    _check(getattr(L.load(), f"ctk_gradient_adjoint_{_vol_suffix(out)}")(
+        shape.nx, shape.ny, shape.nz, *[C.c_void_p(v.data_ptr()) for v in g], C.c_void_p(out.data_ptr()),
+        _torch_stream()))
+    return _like_input(out, host)
+
+
+def tv_epsilon(x) -> float:
+    """tv.hpp:17-24: 1e-4 * max|x|."""
+    t, _ = _as_device(x)
+    return 1e-4 * float(t.abs().max().double()) if t.numel() else 0.0
+
+
+def tv_weights(x, shape: VolumeShape):
+    """tv.hpp:26-43: w_i = (|Dx|_i^2 + eps^2)^(-1/4); all ones for an identically zero image."""
+    import torch
+
+    t, host = _as_device(x)
+    if t.numel() != shape.size():
+        raise DimensionError("volume data length does not match nx*ny*nz")
+    eps = tv_epsilon(t)
+    if eps == 0.0:
+        return _like_input(torch.ones_like(t), host)
+    w = torch.empty_like(t)
+    _check(getattr(L.load(), f"ctk_tv_weights_{_vol_suffix(t)}")(shape.nx, shape.ny, shape.nz, C.c_void_p(t.data_ptr()),
+                                                                eps, C.c_void_p(w.data_ptr()), _torch_stream()))
+    return _like_input(w, host)
+
+
+def _device_blas(name, t):
+    return getattr(L.load(), f"ctk_{name}_{_vol_suffix(t)}")
+
+
+def augment_tikhonov(pair: OperatorPair, lambda_: float) -> OperatorPair:
+    """operators.hpp:118-139: forward x -> [A x; lambda x], back [y1; y2] -> B y1 + lambda y2."""
+    if lambda_ < 0.0:
+        raise ParameterError("tikhonov lambda must be nonnegative")
+    nr, nd = pair.range_size, pair.domain_size
+
+    def fwd(x, y):
+        xd, host = _as_device(x)
+        yd = _as_device(y)[0] if not host else __import__("torch").empty(nr + nd, dtype=xd.dtype, device="cuda")
+        pair.forward(xd, yd[:nr])
+        yd[nr:].copy_(xd)  # then y2 = T(lambda) * x in place
+        _check(_device_blas("scal", xd)(nd, float(lambda_), C.c_void_p(yd[nr:].data_ptr()), _torch_stream()))
+        if host:
+            np.copyto(np.asarray(y).reshape(-1), yd.cpu().numpy())
+
+    def bck(y, x):
+        yd, host = _as_device(y)
+        xd = _as_device(x)[0] if not host else __import__("torch").empty(nd, dtype=yd.dtype, device="cuda")
+        pair.back(yd[:nr], xd)
+        _check(_device_blas("axpy", yd)(nd, float(lambda_), C.c_void_p(yd[nr:].data_ptr()), C.c_void_p(xd.data_ptr()),
+                                        _torch_stream()))
+        if host:
+            np.copyto(np.asarray(x).reshape(-1), xd.cpu().numpy())
+
+    return OperatorPair(nd, nr + nd, pair.matched, pair.domain_shape, fwd, bck, pair.dtype, None, pair.variant)
+
+
+def stack_weighted_gradient(pair: OperatorPair, lambda_: float, weights) -> OperatorPair:
+    """operators.hpp:141-186: [A; lambda diag(w) D] -- range = measurements then the three
+    weighted gradient components."""
+    import torch
+
+    nr, nd = pair.range_size, pair.domain_size
+    w0, _ = _as_device(weights)
+    if w0.numel() != nd:
+        raise DimensionError("weight vector must have one entry per voxel")
+    shape = pair.domain_shape
+
+    def scaled(t):  # lambda * w in the operand's dtype (the reference forms lam * w[i] in T)
+        w = w0.to(t.dtype)
+        return w * torch.tensor(lambda_, dtype=t.dtype, device=w.device)
+
+    def fwd(x, y):
+        xd, host = _as_device(x)
+        yd = _as_device(y)[0] if not host else torch.empty(nr + 3 * nd, dtype=xd.dtype, device="cuda")
+        pair.forward(xd, yd[:nr])
+        dx, dy, dz = gradient(xd, shape)
+        s = scaled(xd)
+        for q, comp in enumerate((dx, dy, dz)):
+            yd[nr + q * nd: nr + (q + 1) * nd] = s * comp
+        if host:
+            np.copyto(np.asarray(y).reshape(-1), yd.cpu().numpy())
+
+    def bck(y, x):
+        yd, host = _as_device(y)
+        xd = _as_device(x)[0] if not host else torch.empty(nd, dtype=yd.dtype, device="cuda")
+        pair.back(yd[:nr], xd)
+        s = scaled(yd)
+        g = [s * yd[nr + q * nd: nr + (q + 1) * nd] for q in range(3)]
+        xd += gradient_adjoint(*g, shape)
+        if host:
+            np.copyto(np.asarray(x).reshape(-1), xd.cpu().numpy())
+
+    return OperatorPair(nd, nr + 3 * nd, pair.matched, shape, fwd, bck, pair.dtype, None, pair.variant)
 
 
 # ---- synthetic input (phantom.hpp:118-145), generated on the device ---------------------------

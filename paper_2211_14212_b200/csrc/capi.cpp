@@ -132,6 +132,10 @@ void dot_dev(size_t n, const T* x, const T* y, double* out, void* stream) {
 
 }  // namespace
 
+static void check_vol(int nx, int ny, int nz) {
+    if (nx <= 0 || ny <= 0 || nz <= 0) ctkb::fail(CTK_E_DIMENSION, "volume dimensions must be positive");
+}
+
 extern "C" {
 
 int ctk_last_error(char* buf, size_t len) {
@@ -285,6 +289,32 @@ int ctk_make_phantom_f64(int kind, int n, double* out, void* s) {
 }
 int ctk_shepp_logan_3d_f32(int n, float* out, void* s) { return ctk_make_phantom_f32(0, n, out, s); }
 int ctk_shepp_logan_3d_f64(int n, double* out, void* s) { return ctk_make_phantom_f64(0, n, out, s); }
+
+#define CTK_STENCIL_API(T, SUF)                                                                                  \
+    int ctk_gradient_##SUF(int nx, int ny, int nz, const T* x, T* dx, T* dy, T* dz, void* s) {                \
+        return guard([&] {                                                                                   \
+            check_vol(nx, ny, nz);                                                                        \
+            ctkb::gradient_scaled<T>(nx, ny, nz, x, nullptr, 1.0, dx, dy, dz, static_cast<cudaStream_t>(s)); \
+        });                                                                                                  \
+    }                                                                                                        \
+    int ctk_gradient_adjoint_##SUF(int nx, int ny, int nz, const T* dx, const T* dy, const T* dz, T* out,    \
+                                   void* s) {                                                                \
+        return guard([&] {                                                                                   \
+            check_vol(nx, ny, nz);                                                                        \
+            const cudaStream_t st = static_cast<cudaStream_t>(s);                                            \
+            CTK_CUDA(cudaMemsetAsync(out, 0, sizeof(T) * size_t(nx) * ny * nz, st));                         \
+            ctkb::gradient_adjoint_scaled_add<T>(nx, ny, nz, dx, dy, dz, nullptr, 1.0, out, st);            \
+        });                                                                                                  \
+    }                                                                                                        \
+    int ctk_tv_weights_##SUF(int nx, int ny, int nz, const T* x, double eps, T* w, void* s) {                 \
+        return guard([&] {                                                                                   \
+            check_vol(nx, ny, nz);                                                                        \
+            ctkb::tv_weights<T>(nx, ny, nz, x, eps, w, static_cast<cudaStream_t>(s));                       \
+        });                                                                                                  \
+    }
+CTK_STENCIL_API(float, f32)
+CTK_STENCIL_API(double, f64)
+#undef CTK_STENCIL_API
 
 int ctk_add_noise_f32(size_t n, const float* in, double i0, double sigma, uint64_t seed, float* out) {
     return guard([&] { ctkb::add_noise<float>(n, in, i0, sigma, seed, out); });
