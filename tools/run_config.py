@@ -11,7 +11,10 @@ import paper_2211_14212_b200 as ctk
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", choices=["C4", "C5"], required=True)
 ap.add_argument("--n", type=int, default=0); ap.add_argument("--angles", type=int, default=0)
-ap.add_argument("--iters", type=int, default=50); ap.add_argument("--tv-lam", type=float, default=0.5)
+ap.add_argument("--iters", type=int, default=50)
+# C5 TV weight from the 128^3 proxy sweep (tools/tv_lambda_sweep.py: 0.1); the cost per
+# iteration does not depend on it (the 1024^3 run in DESIGN.md used 0.5)
+ap.add_argument("--tv-lam", type=float, default=0.1)
 a = ap.parse_args()
 n = a.n or (512 if a.config == "C4" else 1024)
 na = a.angles or (720 if a.config == "C4" else 1600)
