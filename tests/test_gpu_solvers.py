@@ -289,3 +289,48 @@ def test_siddon_lsqr_matches_restated(ctk, restated):
     res = ctk.lsqr(pair, b, _opts(ctk, 8))
     assert rel_l2(res.x, want["x"]) < 1e-9
     assert np.allclose(res.log.explicit_residual, want["explicit"], rtol=1e-9)
+
+
+@pytest.mark.parametrize("solver", ["cgls", "lsqr", "lsmr", "sirt", "hybrid_lsqr", "ab_gmres", "ba_gmres", "cgls_tv"])
+@pytest.mark.parametrize("bad", ["inf", "nan", "zero"])
+def test_error_behaviour_matches_reference(ctk, problem, reference, solver, bad):
+    """Non-finite or zero measurements: the same error class (and, for a NumericalError, the
+    same iteration) as the reference's solver (IterationMonitor::record's finite check,
+    solve_log.hpp:116-117; the zero-b guards)."""
+    from oracle.oracle import RefError
+
+    g, gt, b = problem
+    b = b.copy()
+    if bad == "zero":
+        b[:] = 0.0
+    else:
+        b[b.size // 3] = np.inf if bad == "inf" else np.nan
+    codes = {1: ctk.DimensionError, 2: ctk.GeometryError, 3: ctk.ParameterError, 4: ctk.DegenerateInputError,
+             5: ctk.NumericalError}
+    try:
+        reference.solve(g, b, solver, 5, lam=1.0, strategy=2 if solver == "hybrid_lsqr" else 0, outer=2, inner=3,
+                        tol=0.0, stop_inc=False)
+        want = None
+    except RefError as e:
+        want = e
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float64)
+    opts = _opts(ctk, 5)
+    if solver == "lsmr":
+        def run():
+            return ctk.lsmr(pair, b, 1.0, opts)
+    elif solver == "hybrid_lsqr":
+        def run():
+            return ctk.hybrid_lsqr(pair, b, ctk.HybridStrategy.gcv(), opts)
+    elif solver == "cgls_tv":
+        def run():
+            return ctk.cgls_tv(pair, b, 1.0, 2, 3, opts)
+    else:
+        def run():
+            return getattr(ctk, solver)(pair, b, opts)
+    if want is None:
+        run()
+        return
+    with pytest.raises(codes[want.code]) as e:
+        run()
+    if want.code == 5:
+        assert e.value.iteration == want.iteration
