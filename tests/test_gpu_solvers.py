@@ -154,15 +154,28 @@ def test_voxel_driven_lsqr_parity(ctk, reference, problem):
     _check_hist(res, want)
 
 
-def test_stopping_rules_match(ctk, reference):
-    """Default options (tolerance 1e-6, residual-increase stop) on a noisy unmatched run."""
+@pytest.mark.parametrize("solver", ["cgls", "lsqr", "lsmr", "sirt", "hybrid_lsqr", "ab_gmres", "ba_gmres", "cgls_tv"])
+@pytest.mark.parametrize("variant,tol", [(1, 1e-6), (0, 0.05)])
+def test_stopping_rules_match(ctk, reference, solver, variant, tol):
+    """The reference's stopping rules (solve_log.hpp:129-137): on a noisy unmatched run the
+    explicit-residual-increase stop, on a matched run a residual tolerance -- same stop
+    reason at the same iteration."""
     g = parallel2d(32, 30)
     rng = np.random.default_rng(3)
     x = rng.random(g.domain_size)
-    b = reference.forward(g, x) + 0.05 * rng.standard_normal(g.range_size)
-    want = reference.solve(g, b, "lsqr", 60, variant=1)
-    pair = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant.voxel_driven, dtype=np.float64)
-    res = ctk.lsqr(pair, b, ctk.SolverOptions(max_iters=60))
+    b = reference.forward(g, x) + (0.05 if variant == 1 else 0.01) * rng.standard_normal(g.range_size)
+    want = reference.solve(g, b, solver, 60, variant=variant, lam=0.5, strategy=2 if solver == "hybrid_lsqr" else 0,
+                           outer=3, inner=20, tol=tol)
+    pair = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant(variant), dtype=np.float64)
+    opts = ctk.SolverOptions(max_iters=60, residual_tolerance=tol)
+    if solver == "lsmr":
+        res = ctk.lsmr(pair, b, 0.5, opts)
+    elif solver == "hybrid_lsqr":
+        res = ctk.hybrid_lsqr(pair, b, ctk.HybridStrategy.gcv(), opts)
+    elif solver == "cgls_tv":
+        res = ctk.cgls_tv(pair, b, 0.5, 3, 20, opts)
+    else:
+        res = getattr(ctk, solver)(pair, b, opts)
     assert res.stop_reason.name == want["stop_reason"]
     assert res.iterations_run == want["iterations_run"]
 
