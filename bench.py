@@ -145,6 +145,16 @@ def cpu_reference_rate(n, na, budget_s, dtype_f32=True):
 
     kind = "reference" if Reference.available() else "port"
     cores = os.cpu_count() or 1
+    # the reference's matched A^T b keeps one partial volume per thread (projector.hpp:172-201):
+    # cap the threads so those stay within ~40 % of the free host memory
+    try:
+        import psutil
+
+        free = psutil.virtual_memory().available
+        per = (4 if dtype_f32 else 8) * float(n) ** 3
+        cores = max(1, min(cores, int(0.4 * free / per) - 1))
+    except Exception:
+        pass
     orc = Reference() if kind == "reference" else None
     if orc is not None:
         orc.set_threads(cores)
