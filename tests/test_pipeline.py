@@ -416,3 +416,25 @@ def test_metrics_relative_residual_and_error(ref):
         metrics.relative_error(xt[:10], xt)
     with pytest.raises(ctk.DegenerateInputError):
         metrics.relative_residual(pair, x, np.zeros_like(b))
+
+
+@pytest.mark.gpu
+def test_cli_end_to_end(tmp_path):
+    """simulate -> reconstruct -> compare through the command line, as the reference's
+    ctkrylov executable is used; exit code 0 and the reference's output files."""
+    sim, rec, cmp_ = (str(tmp_path / d) for d in ("sim", "rec", "cmp"))
+    r = _cli("simulate", "--output", sim, "--set", "size=32", "--set", "n_angles=24", "--seed", "5")
+    assert r.returncode == 0, r.stderr
+    assert sorted(os.listdir(sim)) == ["phantom.vol", "phantom.vol.hdr", "projections_clean.proj",
+                                       "projections_clean.proj.hdr", "projections_noisy.proj",
+                                       "projections_noisy.proj.hdr", "simulate_meta.cfg"]
+    proj = os.path.join(sim, "projections_noisy.proj")
+    r = _cli("reconstruct", proj, "--config", os.path.join(sim, "simulate_meta.cfg"), "--output", rec,
+             "--precision", "single", "--set", "max_iters=5")
+    assert r.returncode == 0, r.stderr
+    assert {"recon.vol", "recon.vol.hdr", "slice_transversal.pgm", "slice_sagittal.pgm", "convergence.csv",
+            "reconstruct_meta.cfg"} <= set(os.listdir(rec))
+    r = _cli("compare", proj, "--config", os.path.join(sim, "simulate_meta.cfg"), "--output", cmp_,
+             "--set", "solvers=cgls,lsqr", "--set", "max_iters=4")
+    assert r.returncode == 0, r.stderr
+    assert {"cgls.csv", "lsqr.csv", "compare_wide.csv", "summary.txt", "compare_meta.cfg"} <= set(os.listdir(cmp_))
