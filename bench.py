@@ -316,22 +316,34 @@ def main():
 
     # ---- the solve: W warmup steps, K timed steps (device-resident b and x).  The clock
     # sampler starts before the warmup so its start-up never overlaps the timed region.
-    with Clocks(local) as clk:
-        for _ in range(args.warmup):
-            solve(b)
-        barrier()
-        launches0 = ctk.launch_count()
-        t0 = time.perf_counter()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record()
-        for _ in range(args.steps):
-            res = solve(b)
-        s1.record()
-        barrier()
-        t1 = time.perf_counter()
-        wall = t1 - t0
-        launches = ctk.launch_count() - launches0
-    clk.window(t0, t1)
+    # A window that saw a hardware or thermal slowdown is re-measured once (timing rules).
+    remeasured = False
+    for attempt in range(2):
+        with Clocks(local) as clk:
+            for _ in range(args.warmup if attempt == 0 else 1):
+                solve(b)
+            barrier()
+            launches0 = ctk.launch_count()
+            t0 = time.perf_counter()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(args.steps):
+                res = solve(b)
+            s1.record()
+            barrier()
+            t1 = time.perf_counter()
+            wall = t1 - t0
+            launches = ctk.launch_count() - launches0
+        clk.window(t0, t1)
+        throttled = bool(set(clk.summary().get("reasons", [])) &
+                         {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"})
+        if dist is not None:  # every rank takes the same decision
+            flag = torch.tensor([1.0 if throttled else 0.0], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            throttled = bool(flag.item())
+        if not throttled or attempt == 1:
+            break
+        remeasured = True
     dev_ms = maxed(s0.elapsed_time(s1))
     iters_total = sum([args.iters]) * args.steps
     ms_per_step = dev_ms / args.steps
@@ -409,7 +421,7 @@ def main():
         "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": 4 * nproj, "d2h_bytes_per_step": 4 * nvox,
                 "clocks": clk_e2e.summary()},
         "gpu_launches": launches,
-        "clocks": clk.summary(),
+        "clocks": dict(clk.summary(), remeasured=remeasured),
         "wall_s_timed": wall,
         "final_explicit_residual": res.log.explicit_residual[-1],
     }
