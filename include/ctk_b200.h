@@ -256,6 +256,10 @@ int ctk_comm_create(const ctk_comm_callbacks* cb, ctk_comm** out);
 /* NCCL (dlopen'd libnccl.so.2): unique id is 128 bytes, exchanged by the caller. */
 int ctk_nccl_get_unique_id(void* out128);
 int ctk_comm_create_nccl(const void* id128, int nranks, int rank, ctk_comm** out);
+/* Adopt a communicator the caller already initialised (an ncclComm_t passed as void*, e.g.
+ * the one behind a torch.distributed NCCL process group).  The caller keeps ownership:
+ * ctk_comm_destroy does not destroy it, and it must outlive the ctk_comm. */
+int ctk_comm_adopt_nccl(void* nccl_comm, int nranks, int rank, ctk_comm** out);
 void ctk_comm_destroy(ctk_comm* c);
 /* Attach a communicator.  Angle sharding (no slab set): the handle's angles are this
  * rank's shard; A^T b partial volumes are sum-reduced and range-space dots are summed over

@@ -147,7 +147,10 @@ struct Call {
     ctk_solver_opts o{};
     const ctk::SolverOptions<T>* opts;
 
-    Call(const ctk::SolverOptions<T>& so, int cap, int outer_cap) : opts(&so) {
+    Call(const ctk::OperatorPair<T>& pair, const ctk::SolverOptions<T>& so, int cap, int outer_cap) : opts(&so) {
+        // IterationMonitor's constructor check (solve_log.hpp:92-94): a ground truth of the
+        // wrong length is a DimensionError before any work
+        if (so.ground_truth) pair.check_domain(so.ground_truth->size());
         impl.resize(size_t(cap));
         expl.resize(size_t(cap));
         err.resize(size_t(cap));
@@ -206,7 +209,7 @@ template <class T>
 ctk::SolveResult<T> cgls(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::cgls(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "cgls");
@@ -215,7 +218,7 @@ template <class T>
 ctk::SolveResult<T> lsqr(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::lsqr(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "lsqr");
@@ -225,7 +228,7 @@ template <class T>
 ctk::SolveResult<T> sirt(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::sirt(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "sirt");
@@ -235,7 +238,7 @@ template <class T>
 ctk::SolveResult<T> ab_gmres(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::ab_gmres(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "ab_gmres");
@@ -244,7 +247,7 @@ template <class T>
 ctk::SolveResult<T> ba_gmres(const B200Pair<T>& pair, std::span<const T> b, const ctk::SolverOptions<T>& opts) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::ba_gmres(pair.native->get(), pair.variant, b.data(), &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "ba_gmres");
@@ -255,7 +258,7 @@ ctk::SolveResult<T> lsmr(const B200Pair<T>& pair, std::span<const T> b, double l
     opts.validate();
     pair.check_range(b.size());
     if (lambda < 0.0) throw ctk::ParameterError("lsmr: lambda must be nonnegative");
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::lsmr(pair.native->get(), pair.variant, b.data(), lambda, &c.o, x.data(), &c.log));
     return c.result(std::move(x), pair, "lsmr");
@@ -266,7 +269,7 @@ ctk::SolveResult<T> hybrid_lsqr(const B200Pair<T>& pair, std::span<const T> b, c
                                 const ctk::SolverOptions<T>& opts) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     const ctk_hybrid_strategy cs{int(s.kind), s.lambda, s.noise_level};
     check(Ops<T>::hybrid(pair.native->get(), pair.variant, b.data(), &cs, &c.o, x.data(), &c.log));
@@ -278,7 +281,7 @@ ctk::SolveResult<T> flsqr_tv(const B200Pair<T>& pair, std::span<const T> b, cons
                              const ctk::SolverOptions<T>& opts) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, opts.max_iters, 1);
+    detail::Call<T> c(pair, opts, opts.max_iters, 1);
     std::vector<T> x(pair.domain_size);
     const ctk_hybrid_strategy cs{int(s.kind), s.lambda, s.noise_level};
     check(Ops<T>::flsqr_tv(pair.native->get(), pair.variant, b.data(), &cs, &c.o, x.data(), &c.log));
@@ -289,7 +292,7 @@ ctk::SolveResult<T> cgls_tv(const B200Pair<T>& pair, std::span<const T> b, doubl
                             int inner_iters, const ctk::SolverOptions<T>& opts, bool warm_start = false) {
     opts.validate();
     pair.check_range(b.size());
-    detail::Call<T> c(opts, std::max(1, outer_iters) * std::max(1, inner_iters), std::max(1, outer_iters));
+    detail::Call<T> c(pair, opts, std::max(1, outer_iters) * std::max(1, inner_iters), std::max(1, outer_iters));
     std::vector<T> x(pair.domain_size);
     check(Ops<T>::tv(pair.native->get(), pair.variant, b.data(), lambda, outer_iters, inner_iters, &c.o,
                      int(warm_start), x.data(), &c.log));

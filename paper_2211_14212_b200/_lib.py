@@ -149,6 +149,7 @@ def load():
         "ctk_comm_create": (i, [C.POINTER(CommCallbacks), C.POINTER(vp)]),
         "ctk_nccl_get_unique_id": (i, [vp]),
         "ctk_comm_create_nccl": (i, [vp, i, i, C.POINTER(vp)]),
+        "ctk_comm_adopt_nccl": (i, [vp, i, i, C.POINTER(vp)]),
         "ctk_comm_destroy": (None, [vp]),
         "ctk_launch_count": (C.c_uint64, []),
         "ctk_projected_gcv_lambda": (i, [pd, i, d, pd]),

@@ -104,19 +104,24 @@ class TorchComm:
 
         try:
             t = self._wrap(ptr, count, dtype)
-            if self.device != "cpu":
-                import torch
+            if self.device == "cpu":
+                dist.all_reduce(t, group=self.group)
+                return 0
+            import torch
 
-                # the library's kernels ran on `stream`: finish them before reducing
-                if stream:
-                    torch.cuda.ExternalStream(stream).synchronize()
-                else:
-                    torch.cuda.synchronize()
-            dist.all_reduce(t, group=self.group)
-            if self.device != "cpu" and dist.get_backend(self.group) != "nccl":
-                import torch
-
-                torch.cuda.synchronize()  # host-staged (gloo) result visible before the next kernel
+            # Run the collective on the library's stream: the kernels that produced the buffer
+            # and the ones that consume the result are queued there, so the reduction is
+            # ordered after the former and before the latter (NCCL enqueues on the current
+            # stream).  Host-staged backends (gloo) complete synchronously on the host, so the
+            # stream is drained first and the copy back is finished before returning.
+            ext = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+            if dist.get_backend(self.group) == "nccl":
+                with torch.cuda.stream(ext):
+                    dist.all_reduce(t, group=self.group)
+            else:
+                ext.synchronize()
+                dist.all_reduce(t, group=self.group)
+                torch.cuda.synchronize()
             return 0
         except Exception:  # surfaced by the library as CTK_E_CUDA
             return 1

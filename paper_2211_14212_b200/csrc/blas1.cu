@@ -363,6 +363,22 @@ __global__ void k_block_axpy(size_t n, int m, double alpha, const double* __rest
 
 }  // namespace
 
+// out[j] = sum_r g[r*m + j] with r ascending: the rank-ordered sum of an all-gathered
+// coefficient vector (every rank evaluates the same sequence -> bitwise equal results)
+__global__ void k_rank_sum(const double* __restrict__ g, int nranks, int m, double* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    double acc = 0.0;
+    for (int r = 0; r < nranks; ++r) acc += g[size_t(r) * m + j];
+    out[j] = acc;
+}
+
+void rank_sum(const double* gathered, int nranks, int m, double* d_out, cudaStream_t s) {
+    if (m <= 0) return;
+    k_rank_sum<<<(m + 127) / 128, 128, 0, s>>>(gathered, nranks, m, d_out);
+    after_launch("k_rank_sum");
+}
+
 void finish_sum(const double* partials, int n, double* d_out, cudaStream_t s) {
     k_finish_sum<<<1, 256, 0, s>>>(partials, n, d_out);
     after_launch("k_finish_sum");

@@ -13,6 +13,7 @@ namespace ctkb {
 Geometry* geometry_create(const ctk_geom_desc* d);
 void nccl_unique_id(void* out128);
 Comm* comm_create_nccl(const void* id128, int nranks, int rank);
+Comm* comm_adopt_nccl(void* nccl_comm, int nranks, int rank);
 void comm_destroy(Comm* c);
 template <class T>
 void solve_device(Geometry& g, int solver, int variant, const T* d_b, double lambda, const ctk_hybrid_strategy* st,
@@ -60,10 +61,14 @@ void check_variant(int v) {
     if (v != CTK_BP_MATCHED && v != CTK_BP_VOXEL_DRIVEN) ctkb::fail(CTK_E_PARAMETER, "unknown backprojector variant");
 }
 
+// With a communicator attached the public operators follow the solvers' rule (solvers.cpp
+// Dev::ax / Dev::atb): under angle sharding A x is local and every A^T b partial volume is
+// summed; under z-slab sharding A x = sum_r A x_r is summed and A^T b is local.
 template <class T>
 void ax_dev(ctkb::Geometry& g, const T* x, T* y, cudaStream_t s) {
     g.require_angles();
     ctkb::op_ax<T>(g, x, y, s);
+    if (g.comm && g.slab) ctkb::comm_allreduce(g.comm, y, g.range(), sizeof(T) == 8 ? 1 : 0, s);
 }
 
 template <class T>
@@ -71,7 +76,7 @@ void atb_dev(ctkb::Geometry& g, int variant, const T* y, T* x, cudaStream_t s) {
     g.require_angles();
     check_variant(variant);
     ctkb::op_atb<T>(g, variant, y, x, s);
-    if (g.comm) ctkb::comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
+    if (g.comm && !g.slab) ctkb::comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
 }
 
 template <class T>
@@ -224,11 +229,17 @@ int ctk_ax_residual_f32(ctk_geom* g, const float* x, const float* b, double* out
         if (gg.projector != CTK_PROJ_JOSEPH) ctkb::fail(CTK_E_UNSUPPORTED, "fused residual is Joseph-only");
         auto st = S(gg, s);
         auto w = ctkb::red_work(&gg);
-        ctkb::ax_residual_f32(gg, x, b, w.results, st);
+        if (gg.comm && gg.slab) {  // the partial projections must be summed before the difference
+            gg.ax_scratch.ensure(gg.range() * sizeof(float));
+            ax_dev<float>(gg, x, gg.ax_scratch.as<float>(), st);
+            ctkb::reduce_diff_nrm2sq<float>(gg.range(), gg.ax_scratch.as<float>(), b, w.results, w, st);
+        } else {
+            ctkb::ax_residual_f32(gg, x, b, w.results, st);
+        }
         CTK_CUDA(cudaMemcpyAsync(gg.pinned, w.results, sizeof(double), cudaMemcpyDeviceToHost, st));
         CTK_CUDA(cudaStreamSynchronize(st));
         double v = gg.pinned[0];
-        if (gg.comm) v = ctkb::comm_sum_scalar(gg.comm, v);
+        if (gg.comm && !gg.slab) v = ctkb::comm_sum_scalar(gg.comm, v);  // angle shards: range partials
         *out = v;
     });
 }
@@ -423,6 +434,9 @@ int ctk_comm_create(const ctk_comm_callbacks* cb, ctk_comm** out) {
     });
 }
 int ctk_nccl_get_unique_id(void* out128) { return guard([&] { ctkb::nccl_unique_id(out128); }); }
+int ctk_comm_adopt_nccl(void* nccl_comm, int nranks, int rank, ctk_comm** out) {
+    return guard([&] { *out = reinterpret_cast<ctk_comm*>(ctkb::comm_adopt_nccl(nccl_comm, nranks, rank)); });
+}
 int ctk_comm_create_nccl(const void* id, int nranks, int rank, ctk_comm** out) {
     return guard([&] { *out = reinterpret_cast<ctk_comm*>(ctkb::comm_create_nccl(id, nranks, rank)); });
 }

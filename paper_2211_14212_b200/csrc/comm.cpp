@@ -58,6 +58,7 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 struct NcclState {
     ncclComm_t comm = nullptr;
+    bool owned = true;  // false: adopted from the caller (ctk_comm_adopt_nccl), not destroyed here
     cudaStream_t stream = nullptr;
     double* d_scalars = nullptr;  // [nranks] gather target + [1] send
     double* h_scalars = nullptr;
@@ -106,6 +107,24 @@ double comm_sum_scalar(Comm* c, double v) {
     return s;
 }
 
+void comm_sum_vector(Comm* c, double* d_v, int m, cudaStream_t s) {
+    if (!c || c->cb.nranks <= 1 || m <= 0) return;
+    const size_t R = size_t(c->cb.nranks), M = size_t(m);
+    c->gather.ensure(sizeof(double) * R * M);
+    double* gb = c->gather.as<double>();
+    if (c->nccl_comm) {
+        auto* st = static_cast<NcclState*>(c->nccl_comm);
+        nccl_check(nccl().AllGather(d_v, gb, M, ncclFloat64, st->comm, s), "ncclAllGather");
+    } else {
+        // callback transport: a sum-allreduce of a zeroed [nranks][m] buffer in which each
+        // rank fills its own row -- one nonzero term per entry, so the gather is exact
+        CTK_CUDA(cudaMemsetAsync(gb, 0, sizeof(double) * R * M, s));
+        CTK_CUDA(cudaMemcpyAsync(gb + size_t(c->cb.rank) * M, d_v, sizeof(double) * M, cudaMemcpyDeviceToDevice, s));
+        comm_allreduce(c, gb, R * M, 1, s);
+    }
+    rank_sum(gb, int(R), m, d_v, s);
+}
+
 double comm_max_scalar(Comm* c, double v) {
     if (!c || c->cb.nranks <= 1) return v;
     double m = v;
@@ -143,11 +162,38 @@ Comm* comm_create_nccl(const void* id128, int nranks, int rank) {
     return c;
 }
 
+// Adopt a communicator the caller already initialised (e.g. torch.distributed's NCCL
+// process group); the caller keeps ownership and must outlive the ctk_comm.
+Comm* comm_adopt_nccl(void* nccl_comm, int nranks, int rank) {
+    if (!nccl_comm) fail(CTK_E_PARAMETER, "null ncclComm_t");
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(CTK_E_PARAMETER, "invalid rank / nranks");
+    (void)nccl();  // the NCCL entry points must resolve in this process
+    auto* st = new NcclState();
+    st->comm = static_cast<ncclComm_t>(nccl_comm);
+    st->owned = false;
+    try {
+        CTK_CUDA(cudaStreamCreateWithFlags(&st->stream, cudaStreamNonBlocking));
+        CTK_CUDA(cudaMalloc(&st->d_scalars, sizeof(double) * (size_t(nranks) + 1)));
+    } catch (...) {
+        if (st->stream) cudaStreamDestroy(st->stream);
+        delete st;
+        throw;
+    }
+    auto* c = new Comm();
+    c->cb.rank = rank;
+    c->cb.nranks = nranks;
+    c->cb.allreduce_sum = nccl_allreduce_cb;
+    c->cb.allgather_f64 = nullptr;
+    c->cb.user = st;
+    c->nccl_comm = st;
+    return c;
+}
+
 void comm_destroy(Comm* c) {
     if (!c) return;
     if (c->nccl_comm) {
         auto* st = static_cast<NcclState*>(c->nccl_comm);
-        if (st->comm) nccl().CommDestroy(st->comm);
+        if (st->comm && st->owned) nccl().CommDestroy(st->comm);
         if (st->d_scalars) cudaFree(st->d_scalars);
         if (st->stream) cudaStreamDestroy(st->stream);
         delete st;

@@ -215,10 +215,15 @@ void tv_weights(int nx, int ny, int nz, const T* x, double eps, T* w, cudaStream
 struct Comm {
     ctk_comm_callbacks cb{};
     void* nccl_comm = nullptr;  // when NCCL-backed
+    DevBuf gather;              // [nranks][m] staging of comm_sum_vector
 };
 void comm_allreduce(Comm* c, void* d_buf, size_t count, int dtype, cudaStream_t s);
 double comm_sum_scalar(Comm* c, double v);  // rank-ordered sum of per-rank partials
 double comm_max_scalar(Comm* c, double v);
+// d_v[0..m) <- rank-ordered sum over ranks of every rank's d_v, on stream s: one collective
+// for the whole vector (CGS2 coefficients), no host round trip
+void comm_sum_vector(Comm* c, double* d_v, int m, cudaStream_t s);
+void rank_sum(const double* gathered, int nranks, int m, double* d_out, cudaStream_t s);
 
 uint64_t launch_count();
 

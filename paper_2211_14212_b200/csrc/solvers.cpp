@@ -408,13 +408,7 @@ template <class T>
 void cgs2(Dev<T>& d, const T* basis, size_t ld, int m, T* wv, size_t n, bool range, double* d_coef, double* scratch) {
     for (int pass = 0; pass < 2; ++pass) {
         block_dot<T>(n, m, basis, ld, wv, d_coef, scratch, d.s);
-        if (d.sharded(range)) {
-            std::vector<double> c(static_cast<size_t>(m));
-            CTK_CUDA(cudaMemcpyAsync(c.data(), d_coef, sizeof(double) * m, cudaMemcpyDeviceToHost, d.s));
-            CTK_CUDA(cudaStreamSynchronize(d.s));
-            for (auto& v : c) v = comm_sum_scalar(d.g.comm, v);
-            CTK_CUDA(cudaMemcpyAsync(d_coef, c.data(), sizeof(double) * m, cudaMemcpyHostToDevice, d.s));
-        }
+        if (d.sharded(range)) comm_sum_vector(d.g.comm, d_coef, m, d.s);  // one gather per pass
         block_axpy<T>(n, m, -1.0, d_coef, basis, ld, wv, d.s);
     }
 }

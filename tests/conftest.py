@@ -37,13 +37,23 @@ def restated():
     return Restated()
 
 
+def _gpu_selected(config) -> bool:
+    expr = (config.getoption("markexpr") or "").replace(" ", "")
+    return "gpu" in expr and "notgpu" not in expr
+
+
 @pytest.fixture(scope="session")
-def reference():
-    """The unmodified reference compiled into oracle/_ref (skips when absent)."""
+def reference(pytestconfig):
+    """The unmodified reference compiled into oracle/_ref.  Under -m gpu its absence is a
+    FAILURE (a parity test must not pass vacuously on a checkout that lacks the prebuilt
+    .so); on the CPU suite it skips."""
     from oracle.oracle import Reference
 
     if not Reference.available():
-        pytest.skip("oracle/_ref/libctkref.so not built")
+        msg = "oracle/_ref/libctkref.so not built (run __graft_entry__.build() where /root/reference exists)"
+        if _gpu_selected(pytestconfig):
+            pytest.fail(msg)
+        pytest.skip(msg)
     r = Reference()
     r.set_threads(1)
     return r

@@ -153,3 +153,60 @@ def test_slab_sharded_solvers_two_ranks(ctk, tmp_path):
             assert np.allclose(r[which + "_expl"], ref.log.explicit_residual, rtol=1e-4), which
             assert np.allclose(r[which + "_impl"], ref.log.implicit_residual, rtol=1e-4), which
         assert np.array_equal(ranks[0][which + "_expl"], ranks[1][which + "_expl"])
+
+
+def _ops_worker(rank, world, port, outdir):
+    """The public operators of a slab handle with a communicator attached (unequal slab
+    heights): A x must be the reduced whole projection, A^T b the local restriction, and
+    the fused residual the reduced one."""
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_14212_b200 as ctk
+    from geoms import cone_bench as _cb, to_ctk as _to_ctk
+    from paper_2211_14212_b200.comm import TorchComm, shard_slabs
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    g = _to_ctk(_cb(25, 12))
+    n = g.vol.nx * g.vol.ny
+    z0, cnt = shard_slabs(g.vol.nz, world, rank)
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(n * g.vol.nz).astype(np.float32)
+    y = rng.standard_normal(g.nu * g.nv * len(g.angles)).astype(np.float32)
+    comm = TorchComm(rank, world, device="cuda")
+    p = ctk.projector_pair(g, slab=(z0, cnt))
+    p.projector.attach_comm(comm)
+    xs = torch.from_numpy(x[z0 * n:(z0 + cnt) * n].copy()).cuda()
+    ax = p.apply_forward(xs).cpu().numpy()
+    bt = p.apply_back(torch.from_numpy(y).cuda()).cpu().numpy()
+    r2 = p.projector.residual2(xs, torch.from_numpy(y).cuda())
+    np.savez(os.path.join(outdir, f"ops{rank}.npz"), z0=z0, cnt=cnt, ax=ax, bt=bt, r2=r2)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_slab_public_operators_with_comm_three_ranks(ctk, tmp_path):
+    import torch.multiprocessing as mp
+
+    world = 3
+    mp.spawn(_ops_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    g = to_ctk(cone_bench(25, 12))
+    n = g.vol.nx * g.vol.ny
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(n * g.vol.nz).astype(np.float32)
+    y = rng.standard_normal(g.nu * g.nv * len(g.angles)).astype(np.float32)
+    full = ctk.projector_pair(g)
+    ax_full = full.apply_forward(x)
+    bt_full = full.apply_back(y)
+    r2_full = float(np.sum((ax_full.astype(np.float64) - y) ** 2))
+    ranks = [np.load(tmp_path / f"ops{r}.npz") for r in range(world)]
+    assert sorted(int(r["cnt"]) for r in ranks) == [8, 8, 9]
+    for r in ranks:
+        assert rel_l2(r["ax"], ax_full) < 2e-6  # the reduced whole projection on every rank
+        z0, cnt = int(r["z0"]), int(r["cnt"])
+        assert np.array_equal(r["bt"], bt_full[z0 * n:(z0 + cnt) * n])  # local, not summed
+        assert abs(float(r["r2"]) - r2_full) <= 1e-5 * r2_full
+    assert np.array_equal(ranks[0]["ax"], ranks[1]["ax"]) and np.array_equal(ranks[1]["ax"], ranks[2]["ax"])
