@@ -35,15 +35,18 @@ __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __
 // groups (one 16-byte load per lane): with the columns of a row group contiguous, the warp's
 // load is one contiguous 512-byte run instead of 32 scattered 16-byte pieces.  Rows are
 // zero-padded to a multiple of 4.
+// row groups per view, rounded up to even so the plane kernel can march whole pairs of groups
+// (the padding groups are zero)
+__host__ __device__ __forceinline__ int pg_groups(int nv) { return (((nv + 3) >> 2) + 1) & ~1; }
 __device__ __forceinline__ size_t pg_index(const KGeom& g, int a, int iu, int iv) {
-    return ((size_t(a) * ((g.nv + 3) >> 2) + (iv >> 2)) * g.nu + iu) * 4 + (iv & 3);
+    return ((size_t(a) * pg_groups(g.nv) + (iv >> 2)) * g.nu + iu) * 4 + (iv & 3);
 }
 
 __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __restrict__ pg) {
     // block: 32 columns x 8 row groups; thread (u, q) writes one float4
     const int a = blockIdx.z;
     const int iu = blockIdx.x * 32 + threadIdx.x, q = blockIdx.y * 8 + threadIdx.y;
-    const int nq = (g.nv + 3) >> 2;
+    const int nq = pg_groups(g.nv);
     if (iu >= g.nu || q >= nq) return;
     const int c = a * g.nu + iu;
     const double2 cs = g.colstep[c];
@@ -99,7 +102,8 @@ struct PlaneCfg<256> {
 #define CTK_BP_KB 32
 #endif
 constexpr int BP_KB = CTK_BP_KB;
-constexpr int BP_ZG = 2;  // guard rows of Z on each side: out-of-band entries land there, unread
+constexpr int BP_ZG = 2;
+  // guard rows of Z on each side: out-of-band entries land there, unread
 
 template <int CLASS, int PB>
 __global__ void __launch_bounds__(PB, PlaneCfg<PB>::MINB)
@@ -110,8 +114,9 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG) * BP_PB);  // [BP_PB][BP_SL]
     int* cnt = lists + BP_PB * BP_SL;                           // [BP_PB]
     float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_PB]
-    float* vdtab = eth + BP_PB;                                 // [nv rounded up to 4], 16-byte aligned
-    int2* urange = reinterpret_cast<int2*>(vdtab + ((g.nv + 3) & ~3));  // [na]
+    const int nv4 = 4 * pg_groups(g.nv);
+    float* vrtab = eth + BP_PB;                                 // [nv4] iv - (nv-1)/2, 16-byte aligned
+    int2* urange = reinterpret_cast<int2*>(vrtab + nv4);        // [na]
     int* pref = reinterpret_cast<int*>(urange + g.na);          // [na + 1] candidate prefix sums
     int* slotcol = pref + g.na + 1;                             // [BP_PB] (view, column) of a slot
 
@@ -123,14 +128,16 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const int p0 = ptile * BP_PB, k0 = kband * BP_KB;
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
-    for (int q = t; q < 4 * ((g.nv + 3) >> 2); q += BP_PB) vdtab[q] = float(row_coord(g, q));
+    for (int q = t; q < nv4; q += BP_PB) vrtab[q] = row_vr(g, q);
+    const int sc = slice_centre(s);  // anchored positions (f32_common.cuh): block centre of plane s
+    const float kf = float(s - sc);
     const float czf = 0.5f * float(g.nzg - 1);  // global z centre; this handle's slices start at z0
     const int kg0 = k0 + g.z0;                   // global index of the band's first slice
     const float cvf = 0.5f * float(g.nv - 1);
     const float invdu = float(1.0 / g.du);
     const float fs = float(s);
     const double h = g.h;
-    const int nq = (g.nv + 3) >> 2;  // row groups of the grouped projection layout
+    const int nq = pg_groups(g.nv);  // row groups of the grouped projection layout
     // world coordinates of the plane and of the tile's row segment ends
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
@@ -207,10 +214,13 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                 const int c = a * g.nu + iu;
                 if (g.colaxis[c] == CLASS) {
                     const float4 cd = g.col[c];
-                    const float fh = fmaf(fs, cd.y, cd.x);
-                    const float fih = floorf(fh);
-                    const int ih = int(fih);
-                    const float th = fh - fih;
+                    const double4 c64 = g.col64[c];
+                    int ih, ihA;
+                    float th, thA;
+                    double G;
+                    slice_anchor(c64, sc, ihA, thA, G);  // fh exactly as the forward evaluates it
+                    split(fmaf(kf, cd.y, thA), ih, th);
+                    ih += ihA;
                     if (ih + 1 >= p0 && ih <= p0 + BP_PB - 1 && ih + 1 >= 0 && ih < nh) {
                         const float gs = fmaf(fs, cd.w, cd.z);
                         int v0 = 0, v1 = g.nv - 1;
@@ -234,6 +244,21 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
                         const size_t qs = size_t(g.nu);
                         float* zc = Z + t;
+                        // z of row iv at this plane (f32_common.cuh), the forward's expression:
+                        //   S = fmaf(vr, Whi, fc) (exact), T = fmaf(vr, Wlo, S),
+                        //   iz = izc + floor(T), tz = fmaf(vr, Wlo, S - floor(T))
+                        float Whi, Wr;
+                        z_split(g, G, Whi, Wr);
+                        const float Wlo = fmaf(kf, z_cross(g, c64), Wr), fc = cz_frac(g);
+                        const int koff = cz_int(g) - kSplitBias - kg0;  // kk = bits(T + M, rd) + koff
+                        float tf_unused;
+                        auto row_k = [&](int iv, float& tz) {  // band slice index of row iv's z floor
+                            const float vr = vrtab[iv];
+                            const float S = fmaf(vr, Whi, fc);
+                            const float tt = split_t(fmaf(vr, Wlo, S));
+                            tz = fmaf(vr, Wlo, fmaf(__fsub_rn(tt, kSplitM), -1.f, S));
+                            return __float_as_int(tt) + koff;
+                        };
                         auto zero_rows = [&](int lo, int hi) {  // Z rows [lo, hi) of this column
                             for (int m = max(lo, 0); m < min(hi, BP_KB); ++m) zc[m * BP_PB] = 0.f;
                         };
@@ -249,11 +274,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             // sparser columns zero the whole band first.
                             const float rg = invdu / gs;
                             if (rg >= 0.75f) {
-                                int kf, kfi;
-                                float tf;
-                                split(fmaf(vdtab[v0], gs, czf), kfi, tf);
-                                kf = kfi - kg0;
-                                zero_rows(0, kf);
+                                zero_rows(0, row_k(v0, tf_unused));
                             } else {
                                 zero_rows(0, BP_KB);
                             }
@@ -261,8 +282,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             float A = 0.f, B = 0.f;
                             // one row: tt = fz + 1.5*2^23 rounded down (its bits carry the slice
                             // index), tz = the z fraction, omt = 1 - tz
-                            auto step_w = [&](float tt, float tz, float omt, float yv) {
-                                const int kk = __float_as_int(tt) - (kSplitBias + kg0);
+                            auto step_w = [&](int kk, float tz, float omt, float yv) {
                                 const float w0 = omt * yv, w1 = tz * yv;
                                 const int adv = kk - cur;
                                 float ak = adv == 1 ? B : 0.f;  // two selects, no branch
@@ -277,23 +297,23 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 zp[BP_PB] = B;
                             };
                             // the row positions of a 4-row group in packed f32x2 arithmetic
-                            // (FFMA2 / FADD2): per lane fz = fmaf(vd, gs, cz), the floor and the fraction
-                            const float2 gs2 = make_float2(gs, gs), cz2 = make_float2(czf, czf);
+                            // (FFMA2 / FADD2), per lane the scalar sequence of row_k
+                            const float2 Whi2 = make_float2(Whi, Whi), Wlo2 = make_float2(Wlo, Wlo), fc2 = make_float2(fc, fc);
                             const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
                             const float2 m1 = make_float2(-1.f, -1.f), one2 = make_float2(1.f, 1.f);
-                            auto step2 = [&](float2 vd, float ya, float yb) {
-                                const float2 fz = __ffma2_rn(vd, gs2, cz2);
-                                const float2 tt = __fadd2_rd(fz, M2);
-                                const float2 tz = __ffma2_rn(__fadd2_rn(tt, nM2), m1, fz);
+                            auto step2 = [&](float2 vr, float ya, float yb) {
+                                const float2 S = __ffma2_rn(vr, Whi2, fc2);
+                                const float2 tt = __fadd2_rd(__ffma2_rn(vr, Wlo2, S), M2);
+                                const float2 tz = __ffma2_rn(vr, Wlo2, __ffma2_rn(__fadd2_rn(tt, nM2), m1, S));
                                 const float2 omt = __ffma2_rn(tz, m1, one2);
-                                step_w(tt.x, tz.x, omt.x, ya);
-                                step_w(tt.y, tz.y, omt.y, yb);
+                                step_w(__float_as_int(tt.x) + koff, tz.x, omt.x, ya);
+                                step_w(__float_as_int(tt.y) + koff, tz.y, omt.y, yb);
                             };
                             // whole 4-row groups; only the first and last are masked to [v0, v1]
-                            const float4* vd4 = reinterpret_cast<const float4*>(vdtab);
+                            const float4* vr4 = reinterpret_cast<const float4*>(vrtab);
                             const int q0 = v0 >> 2, q1 = v1 >> 2;
                             auto group = [&](int q, float4 y4, bool mask) {
-                                const float4 d4 = vd4[q];
+                                const float4 d4 = vr4[q];
                                 if (mask) {
                                     const int b = 4 * q;
                                     y4.x = (b >= v0 && b <= v1) ? y4.x : 0.f;
@@ -307,7 +327,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             // two row groups per iteration: two 16-byte loads in flight
                             group(q0, __ldg(pc4 + q0 * qs), true);
                             int q = q0 + 1;
-                            for (; q + 1 < q1; q += 2) {  // two loads in flight per iteration
+                            for (; q + 1 < q1; q += 2) {
                                 const float4 ya = __ldg(pc4 + q * qs), yb = __ldg(pc4 + (q + 1) * qs);
                                 group(q, ya, false);
                                 group(q + 1, yb, false);
@@ -320,10 +340,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             zero_rows(0, BP_KB);
                             for (int iv = v0; iv <= v1; ++iv) {
                                 const float yv = reinterpret_cast<const float*>(pc4 + (iv >> 2) * qs)[iv & 3];
-                                int iz;
                                 float tz;
-                                split(fmaf(vdtab[iv], gs, czf), iz, tz);
-                                const int kk = iz - kg0;
+                                const int kk = row_k(iv, tz);
                                 if (unsigned(kk) < unsigned(BP_KB)) zc[kk * BP_PB] = fmaf(1.f - tz, yv, zc[kk * BP_PB]);
                                 if (unsigned(kk + 1) < unsigned(BP_KB)) zc[(kk + 1) * BP_PB] = fmaf(tz, yv, zc[(kk + 1) * BP_PB]);
                             }
@@ -369,11 +387,12 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                     for (int e = 0; e < BP_PB; ++e) {
                         const int c = slotcol[e];
                         if (c < 0 || g.colaxis[c] != CLASS) continue;
-                        const float4 cd = g.col[c];
-                        const float fh = fmaf(fs, cd.y, cd.x);
-                        const float fih = floorf(fh);
-                        const int ih = int(fih);
-                        const float th = fh - fih;
+                        int ih, ihA;
+                        float th, thA;
+                        double G;
+                        slice_anchor(g.col64[c], sc, ihA, thA, G);
+                        split(fmaf(kf, g.col[c].y, thA), ih, th);
+                        ih += ihA;
                         float wh;
                         if (ih == p) wh = 1.f - th;
                         else if (ih + 1 == p && th != 0.f) wh = th;
@@ -553,7 +572,7 @@ void transpose_proj(Geometry& g, const float* y, cudaStream_t s) {
 }
 
 void group_proj(Geometry& g, const float* y, cudaStream_t s) {
-    const int nq = (g.nv + 3) >> 2;
+    const int nq = pg_groups(g.nv);
     g.proj_t.ensure(size_t(g.na) * g.nu * nq * 4 * sizeof(float));
     dim3 blk(32, 8), grd((g.nu + 31) / 32, (nq + 7) / 8, g.na);
     k_proj_group4<<<grd, blk, 0, s>>>(g.kgeom(), y, g.proj_t.as<float>());
@@ -568,7 +587,7 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz_local() + BP_KB - 1) / BP_KB;
     const size_t smem = sizeof(float) * (size_t(BP_PB) * (BP_KB + 2 * BP_ZG) + size_t(BP_PB) * BP_SL + 2 * BP_PB +
-                                         ((size_t(g.nv) + 3) & ~size_t(3))) +
+                                         4 * size_t(pg_groups(g.nv))) +
                         sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     // opt in once to the largest size this launcher accepts (occupancy follows the size of

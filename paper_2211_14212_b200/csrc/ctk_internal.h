@@ -55,6 +55,7 @@ struct KGeom {
     double dso, dod, du, h;
     const double2* ctst;          // per view (cos, sin), host libm values
     const float4* col;            // per (view, iu): fh0, fhd, g0, gd   (f32 separable model)
+    const double4* col64;         // the same in fp64 (anchors of the f32 positions, f32_common.cuh)
     const unsigned char* colaxis; // per (view, iu): 0 = x-dominant, 1 = y-dominant
     const double2* colstep;       // per (view, iu): (dx^2+dy^2, |d_A|) of the unnormalised ray
     const int4* vclass;           // per view: column hull [x.. y] of x-dominant, [z.. w] of y-dominant columns
@@ -82,7 +83,7 @@ struct Geometry {
     Comm* comm = nullptr;
 
     // device tables
-    DevBuf d_ctst, d_col, d_colaxis, d_colstep;
+    DevBuf d_ctst, d_col, d_col64, d_colaxis, d_colstep;
     DevBuf d_vorder;  // views grouped by ray class (x-dominant first) for L2 reuse in Ax
     DevBuf d_vclass;  // per view: hull of the columns of each ray class (matched A^T b batching)
     DevBuf d_rayinv;  // per ray: 1/d of make_ray, for the exact gathers (built on first use)

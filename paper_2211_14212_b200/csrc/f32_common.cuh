@@ -146,5 +146,61 @@ __device__ __forceinline__ void split(float f, int& i, float& frac) {
     frac = split_frac(f, t);
 }
 
+
+// ---- anchored f32 positions (both the forward and the matched transpose) ---------------
+// The reference evaluates the sample positions in fp64 even for T = float
+// (projector.hpp:97-103): fb = fb0 + s*fb_d, floor, fraction.  A plain f32 evaluation of
+// fh(s) = fh0 + s*fhd or fz = vd*G(s) + cz rounds at the magnitude of the coordinate (up to
+// n), i.e. ~ulp(512) = 6e-5 voxel at 512^3, which random-signed data expose as ~2e-5
+// relative error.  Here positions round at the magnitude of a small offset instead:
+//  * in-plane: slices are grouped in blocks of kSB anchored at the block centre sc
+//      fh(s) = ihA + fmaf(k, fhd, thA),  k = s - sc in [-kSB/2, kSB/2),
+//    with ihA + thA = fh0 + sc*fhd split exactly in fp64;
+//  * z: fz(s, iv) = cz + vr*W(s) with vr = iv - (nv-1)/2 and W(s) = du*G(s) (dz per row).
+//    W(sc) is split into Whi (12 significant bits) + Wr, so that S = fmaf(vr, Whi, fc) is
+//    EXACT in f32 (fc = cz - floor(cz) in {0, 1/2}), and the small rest
+//    vr*Wlo, Wlo = fmaf(k, Wd, Wr) (Wd = du*gd), is added to S's fraction:
+//      T = fmaf(vr, Wlo, S)          (rounded; only its floor is used)
+//      iz = floor(cz) + floor(T),  tz = fmaf(vr, Wlo, S - floor(T))   (S - floor(T) exact)
+//    tz can leave [0, 1) by a rounding (1e-7) where T sits on a voxel boundary; the
+//    bilinear weights then extrapolate by that amount, a continuous, negligible change.
+// The forward (lane = row, loop over s; S per block) and the transpose (thread = column,
+// loop over rows at a fixed plane s) evaluate these same expressions with the same
+// operands, so positions and weights stay bit-identical between A and A^T.  fp64 parts use
+// explicit intrinsics (no contraction differences between the two kernels).
+#ifndef CTK_APOS_SB
+#define CTK_APOS_SB 32
+#endif
+constexpr int kSB = CTK_APOS_SB;
+static_assert((kSB & (kSB - 1)) == 0, "slice blocks are a power of two");
+
+// floor / exact fraction of an fp64 value (|x| < 2^31): x + 1.5*2^52 rounded down carries
+// floor(x) in its low word; the fraction is exact in fp64 and rounded once to f32
+__device__ __forceinline__ void dsplit(double x, int& i, float& frac) {
+    constexpr double kM52 = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = __dadd_rd(x, kM52);
+    i = __double2loint(t);
+    frac = __double2float_rn(__dsub_rn(x, __dsub_rn(t, kM52)));
+}
+__device__ __forceinline__ int slice_centre(int s) { return (s & ~(kSB - 1)) + kSB / 2; }
+// fh anchor and G(sc) of a column at the block centre sc
+__device__ __forceinline__ void slice_anchor(const double4& c, int sc, int& ihA, float& thA, double& G) {
+    dsplit(__fma_rn(double(sc), c.y, c.x), ihA, thA);
+    G = __fma_rn(double(sc), c.w, c.z);
+}
+// W = du*G split into Whi (12 significant bits: vr*Whi is exact for |vr| < 2^12) + Wr
+__device__ __forceinline__ void z_split(const KGeom& g, double G, float& Whi, float& Wr) {
+    const double W = __dmul_rn(g.du, G);
+    Whi = __int_as_float(__float_as_int(__double2float_rn(W)) & int(0xFFFFF000u));
+    Wr = __double2float_rn(__dsub_rn(W, double(Whi)));
+}
+// Wd = du*gd: the change of W per slice
+__device__ __forceinline__ float z_cross(const KGeom& g, const double4& c) { return __double2float_rn(__dmul_rn(g.du, c.w)); }
+// row offset from the detector centre, exact in f32 (half-integers below 2^22)
+__device__ __forceinline__ float row_vr(const KGeom& g, int iv) { return float(iv) - 0.5f * float(g.nv - 1); }
+// cz = (nzg-1)/2 = izc + fc
+__device__ __forceinline__ int cz_int(const KGeom& g) { return (g.nzg - 1) >> 1; }
+__device__ __forceinline__ float cz_frac(const KGeom& g) { return ((g.nzg - 1) & 1) ? 0.5f : 0.f; }
+
 }  // namespace
 }  // namespace ctkb

@@ -1,8 +1,8 @@
 // Joseph forward projection Ax for T = float (projector.hpp:113-162) on sm_100a.
 //
 // Layouts in HBM (f32, z fastest, zero-padded so the four bilinear taps need no checks):
-//   wx[i][j+1][k+1]  one plane per x-slice, h = y   (x-dominant rays walk x)
-//   wy[j][i+1][k+1]  one plane per y-slice, h = x   (y-dominant rays walk y)
+//   wx[i][j+2][k+2]  one plane per x-slice, h = y   (x-dominant rays walk x)
+//   wy[j][i+2][k+2]  one plane per y-slice, h = x   (y-dominant rays walk y)
 // All rays of one detector column share fh(s) exactly (it depends on the column only), so
 // a warp = 32 consecutive detector ROWS of one column has one in-plane index ih per slice
 // and consecutive z indices: each tap load of the warp is one contiguous z run (1-2 lines).
@@ -27,34 +27,27 @@ namespace {
 // All rays of one detector column share fh(s) exactly (it depends on the column only), so a
 // warp of 32 consecutive detector ROWS of one column has a single in-plane index ih per
 // slice and consecutive z indices.  With the layouts stored z-fastest,
-//   wx[i][j+1][k+1]  (x-dominant rays: slice i, h = j)     wy[j][i+1][k+1]  (h = i)
+//   wx[i][j+2][k+2]  (x-dominant rays: slice i, h = j)     wy[j][i+2][k+2]  (h = i)
 // each of the 4 tap loads of a warp covers one contiguous z run (1-2 cache lines) instead
 // of two partial rows of a y/x-fastest plane.
 #ifndef CTK_FWD_BC
 #define CTK_FWD_BC 8
 #endif
-#ifndef CTK_FWD_PAIR
-#define CTK_FWD_PAIR 1  // packed f32x2 (FFMA2/FADD2) slice pairs: 63.4 vs 64.8 ms unchunked, 48.6 vs 50.4 ms chunked
-#endif
 #ifndef CTK_FWD_CHUNKS
 #define CTK_FWD_CHUNKS 2  // minimum slice chunks per ray (fwd_chunks); 64.8 -> 50.4 ms at 512^3 vs unchunked
 #endif
-#ifndef CTK_FWD_UNROLL
-#define CTK_FWD_UNROLL 2  // measured: 2 (48 regs, 5 CTAs/SM) beats 1, 3, 4, 8 at 256^3 and 512^3
-#endif
 constexpr int ZW_BR = 32, ZW_BC = CTK_FWD_BC;  // block: 32 detector rows (lanes) x ZW_BC columns
-constexpr int kFwdUnroll = CTK_FWD_UNROLL;
-#ifndef CTK_FWD_PAIR_UNROLL
-#define CTK_FWD_PAIR_UNROLL 1
-#endif
-constexpr int kFwdPairUnroll = CTK_FWD_PAIR_UNROLL;
+// zero guard planes on each side of the z-fast layouts (h and z): a tap index may step one
+// beyond the contributing range where anchored positions round across a voxel boundary
+constexpr int kPad = 2;
 
 __device__ __forceinline__ const float* opaque_ptr(const float* p) {
     asm("" : "+l"(p));
     return p;
 }
 
-// x[i + nx(j + ny k)] -> wx[i][j+1][k+1] and wy[j][i+1][k+1]: 32x32 (i, k) tile transposes
+// x[i + nx(j + ny k)] -> wx[i][j+kPad][k+kPad] and wy[j][i+kPad][k+kPad]: 32x32 (i, k) tile
+// transposes
 __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict__ x, float* __restrict__ wx,
                                  float* __restrict__ wy) {
     __shared__ float tile[32][33];
@@ -64,13 +57,13 @@ __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict
         tile[r][threadIdx.x] = (i < nx && k < nz) ? __ldg(x + size_t(i) + size_t(nx) * (j + size_t(ny) * k)) : 0.f;
     }
     __syncthreads();
-    const size_t pz = size_t(nz) + 2;
+    const size_t pz = size_t(nz) + 2 * kPad;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int i = i0 + r, k = k0 + threadIdx.x;
         if (i < nx && k < nz) {
             const float v = tile[threadIdx.x][r];
-            wx[(size_t(i) * (ny + 2) + (j + 1)) * pz + k + 1] = v;
-            wy[(size_t(j) * (nx + 2) + (i + 1)) * pz + k + 1] = v;
+            wx[(size_t(i) * (ny + 2 * kPad) + (j + kPad)) * pz + k + kPad] = v;
+            wy[(size_t(j) * (nx + 2 * kPad) + (i + kPad)) * pz + k + kPad] = v;
         }
     }
 }
@@ -104,25 +97,44 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             }
         } else {
             const float4 cd = g.col[c];
+            const double4 c64 = g.col64[c];
             const int A = g.colaxis[c];
             const int nh = A ? g.nx : g.ny;
             const int ns = A ? g.ny : g.nx;
-            const Off pz = g.nz + 2;
-            const Off plane = pz * Off(nh + 2);
-            const float* base = (A ? wy : wx) + pz + 1;  // tap (h, z) of slice s at base[s*plane + h*pz + z]
+            const Off pz = g.nz + 2 * kPad;
+            const Off plane = pz * Off(nh + 2 * kPad);
+            // tap (h, z) of slice s at base[s*plane + h*pz + (z - z0)]
+            const float* base = (A ? wy : wx) + kPad * pz + kPad;
             const float vd = float(v);
             const float czf = 0.5f * float(g.nzg - 1);  // global z centre; slab slices start at z0
             const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            // anchored positions (f32_common.cuh): per slice block the fp64 anchors, per lane
+            // the exact row term S
+            const float Wd = z_cross(g, c64), vr = row_vr(g, iv), fc = cz_frac(g);
+            const int izc = cz_int(g);
+            auto pos = [&](int s, int& ih, int& iz) {
+                const int sc = slice_centre(s);
+                int ihA, a, b;
+                float thA, Whi, Wr, t0, t1;
+                double G;
+                slice_anchor(c64, sc, ihA, thA, G);
+                z_split(g, G, Whi, Wr);
+                const float kf = float(s - sc);
+                split(fmaf(kf, cd.y, thA), a, t0);
+                split(fmaf(vr, fmaf(kf, Wd, Wr), fmaf(vr, Whi, fc)), b, t1);
+                ih = ihA + a;
+                iz = izc + b;
+            };
             // a sample contributes iff some tap is inside the volume: ih in [-1, nh-1] and
-            // iz in [-1, nz-1].  ih(s) and iz(s) are monotone in s (monotone roundings of
-            // affine functions), so the contributing slices form one interval; find it
-            // exactly with the kernel's own f32 arithmetic, starting from the fp64 estimate.
+            // iz in [-1, nz-1].  ih(s) and iz(s) are monotone in s up to the rounding of the
+            // anchored offsets, so the contributing slices form one interval; find its ends
+            // exactly with the kernel's own arithmetic, starting from the fp64 estimate.  (A
+            // slice inside the interval can sit one index beyond the volume when a position
+            // lies within rounding of a voxel boundary: the layouts carry two zero guard
+            // planes on each side, so its taps read zeros.)
             auto inside = [&](int s) {
-                const float fs = float(s);
                 int ih, iz;
-                float th, tz;
-                split(fmaf(fs, cd.y, cd.x), ih, th);
-                split(fmaf(vd, fmaf(fs, cd.w, cd.z), czf), iz, tz);
+                pos(s, ih, iz);
                 return unsigned(ih + 1) <= unh && unsigned(iz - g.z0 + 1) <= unz;
             };
             int s0 = 0, s1 = ns - 1;
@@ -141,41 +153,48 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             }
             float acc = 0.f;
             // Offsets are formed from the raw bit patterns of the split sums (ih + bias,
-            // iz + bias); the bias term is folded into the running slice offset, in unsigned
-            // (modular) arithmetic, so a sample costs one IMAD and no float->int conversion.
+            // iz + bias); the bias and the anchors are folded into the running slice offset,
+            // in unsigned (modular) arithmetic, so a sample costs one IMAD and no
+            // float->int conversion.
             using U = typename std::conditional<sizeof(Off) == 4, unsigned, unsigned long long>::type;
-            const U upz = U(pz), uplane = U(plane);
-            U sb = U(s0) * uplane - U(kSplitBias) * (upz + 1u) - U(unsigned(g.z0));
+            const U upz = U(pz), uplane = U(plane), uplane2 = uplane + uplane;
+            const U cbias = U(kSplitBias) * (upz + 1u) + U(unsigned(g.z0)) - U(unsigned(izc));
             // tap row ih+1; opaque so each tap row costs one IMAD.WIDE rather than a
             // sign-extended 64-bit add chain on (off + pz)
             const float* base1 = opaque_ptr(base + pz);
-            float fs = float(s0);
-#if CTK_FWD_PAIR
             // Two slices per iteration in packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a):
             // every lane of a pair performs exactly the scalar operation sequence, so the
             // positions, floors and weights are bit-identical to the matched backprojector's;
             // only the ray sum is split into even / odd slices.
-            {
-                const float2 fhd2 = make_float2(cd.y, cd.y), fh02 = make_float2(cd.x, cd.x);
-                const float2 gd2 = make_float2(cd.w, cd.w), g02 = make_float2(cd.z, cd.z);
-                const float2 vd2 = make_float2(vd, vd), cz2 = make_float2(czf, czf);
-                const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
-                const float2 m1 = make_float2(-1.f, -1.f), two = make_float2(2.f, 2.f);
-                float2 fs2 = make_float2(float(s0), float(s0 + 1));
-                float2 acc2 = make_float2(0.f, 0.f);
-                const U uplane2 = uplane + uplane;
-                int npairs = max(0, s1 - s0 + 1) >> 1;  // the chunk clip can leave s1 < s0 - 1
-#pragma unroll kFwdPairUnroll
-                for (; npairs > 0; --npairs) {
-                    const float2 fh = __ffma2_rn(fs2, fhd2, fh02);
-                    const float2 fz = __ffma2_rn(vd2, __ffma2_rn(fs2, gd2, g02), cz2);
-                    const float2 tht = __fadd2_rd(fh, M2), tzt = __fadd2_rd(fz, M2);
+            const float2 fhd2 = make_float2(cd.y, cd.y), Wd2 = make_float2(Wd, Wd), vr2 = make_float2(vr, vr);
+            const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
+            const float2 m1 = make_float2(-1.f, -1.f), two = make_float2(2.f, 2.f);
+            float2 acc2 = make_float2(0.f, 0.f);
+            for (int s = s0; s <= s1;) {  // slice blocks
+                const int sc = slice_centre(s);
+                const int se = min(s1, sc + kSB / 2 - 1);
+                int ihA;
+                float thA, Whi, Wr;
+                double G;
+                slice_anchor(c64, sc, ihA, thA, G);
+                z_split(g, G, Whi, Wr);
+                const float S = fmaf(vr, Whi, fc);  // exact
+                U sb = U(s) * uplane + U(unsigned(ihA)) * upz - cbias;
+                const float2 thA2 = make_float2(thA, thA), Wr2 = make_float2(Wr, Wr), S2 = make_float2(S, S);
+                float2 k2 = make_float2(float(s - sc), float(s - sc + 1));
+                const int cnt = se - s + 1;
+#pragma unroll 1
+                for (int np = cnt >> 1; np > 0; --np) {
+                    const float2 fh = __ffma2_rn(k2, fhd2, thA2);
+                    const float2 wlo = __ffma2_rn(k2, Wd2, Wr2);
+                    const float2 tht = __fadd2_rd(fh, M2);
+                    const float2 tzt = __fadd2_rd(__ffma2_rn(vr2, wlo, S2), M2);
                     const float2 th = __ffma2_rn(__fadd2_rn(tht, nM2), m1, fh);  // fh - floor(fh)
-                    const float2 tz = __ffma2_rn(__fadd2_rn(tzt, nM2), m1, fz);
+                    const float2 tz = __ffma2_rn(vr2, wlo, __ffma2_rn(__fadd2_rn(tzt, nM2), m1, S2));
                     const Off o0 = Off(U(unsigned(__float_as_int(tht.x))) * upz + (sb + U(unsigned(__float_as_int(tzt.x)))));
                     const Off o1 =
                         Off(U(unsigned(__float_as_int(tht.y))) * upz + (sb + uplane + U(unsigned(__float_as_int(tzt.y)))));
-                    fs2 = __fadd2_rn(fs2, two);
+                    k2 = __fadd2_rn(k2, two);
                     sb += uplane2;
                     const float* p0 = base + o0;
                     const float* q0 = base1 + o0;
@@ -187,22 +206,14 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                     const float2 a1 = __ffma2_rn(th, __ffma2_rn(v01, m1, v11), v01);
                     acc2 = __fadd2_rn(acc2, __ffma2_rn(tz, __ffma2_rn(a0, m1, a1), a0));
                 }
-                acc = acc2.x + acc2.y;
-                fs = fs2.x;
-            }
-            if (s1 >= s0 && ((s1 - s0 + 1) & 1)) {  // odd count: the last slice, scalar
-#else
-#pragma unroll kFwdUnroll
-            for (int n = s1 - s0; n >= 0; --n) {
-#endif
-                const float fh = fmaf(fs, cd.y, cd.x);
-                const float fz = fmaf(vd, fmaf(fs, cd.w, cd.z), czf);
-                const float tht = split_t(fh), tzt = split_t(fz);
-                const float th = split_frac(fh, tht), tz = split_frac(fz, tzt);
-                const Off off = Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt)))));
-                fs += 1.f;
-                sb += uplane;
-                {
+                if (cnt & 1) {  // odd count: the block's last slice, scalar
+                    const float kf = k2.x;
+                    const float fh = fmaf(kf, cd.y, thA);
+                    const float wlo = fmaf(kf, Wd, Wr);
+                    const float tht = split_t(fh), tzt = split_t(fmaf(vr, wlo, S));
+                    const float th = split_frac(fh, tht);
+                    const float tz = fmaf(vr, wlo, fmaf(__fsub_rn(tzt, kSplitM), -1.f, S));
+                    const Off off = Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt)))));
                     const float* p = base + off;
                     const float* q = base1 + off;
                     const float v00 = __ldg(p), v01 = __ldg(p + 1);  // (ih, iz), (ih, iz+1)
@@ -211,7 +222,9 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                     const float a1 = fmaf(th, v11 - v01, v01);
                     acc += fmaf(tz, a1 - a0, a0);
                 }
+                s = se + 1;
             }
+            acc += acc2.x + acc2.y;
             const float stp = ray_step(g, cs, v);
             out = stp * acc;
         }
@@ -241,8 +254,8 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
 }
 
 void relayout_zfast(Geometry& g, const float* x, DevBuf& wx, DevBuf& wy, cudaStream_t s) {
-    const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2) * (size_t(g.nz_local()) + 2);
-    const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2) * (size_t(g.nz_local()) + 2);
+    const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2 * kPad) * (size_t(g.nz_local()) + 2 * kPad);
+    const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2 * kPad) * (size_t(g.nz_local()) + 2 * kPad);
     if (wx.ensure(nwx * sizeof(float))) CTK_CUDA(cudaMemsetAsync(wx.p, 0, nwx * sizeof(float), s));
     if (wy.ensure(nwy * sizeof(float))) CTK_CUDA(cudaMemsetAsync(wy.p, 0, nwy * sizeof(float), s));
     dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.nz_local() + 31) / 32, g.ny);
@@ -259,7 +272,7 @@ bool wide_offsets(const Geometry& g) {
         const char* e = std::getenv("CTK_FWD_WIDE");
         return e && e[0] == '1';
     }();
-    const double mx = std::max(double(g.nx) * (g.ny + 2), double(g.ny) * (g.nx + 2)) * (g.nz_local() + 2);
+    const double mx = std::max(double(g.nx) * (g.ny + 2 * kPad), double(g.ny) * (g.nx + 2 * kPad)) * (g.nz_local() + 2 * kPad);
     return forced || mx >= 2147483000.0;
 }
 

@@ -52,6 +52,7 @@ KGeom Geometry::kgeom() const {
     k.h = h;
     k.ctst = d_ctst.as<double2>();
     k.col = d_col.as<float4>();
+    k.col64 = d_col64.as<double4>();
     k.colaxis = d_colaxis.as<unsigned char>();
     k.vclass = d_vclass.as<int4>();
     k.colstep = d_colstep.as<double2>();
@@ -146,6 +147,7 @@ Geometry* geometry_create(const ctk_geom_desc* d) {
         // per-(view, column) separable ray model, fp64 -> f32
         const size_t ncol = size_t(g->na) * g->nu;
         std::vector<float4> col(ncol);
+        std::vector<double4> col64(ncol);
         std::vector<unsigned char> cax(ncol);
         std::vector<double2> cst(ncol);
         const double h = g->h;
@@ -190,6 +192,7 @@ Geometry* geometry_create(const ctk_geom_desc* d) {
                 }
                 const size_t c = size_t(a) * g->nu + iu;
                 col[c] = make_float4(float(fh0), float(fhd), float(g0), float(gd));
+                col64[c] = make_double4(fh0, fhd, g0, gd);
                 cax[c] = (unsigned char)A;
                 cst[c] = make_double2(dx * dx + dy * dy, dA);
                 if (g->mode == CTK_CONE3D && vmax > dA) g->has_zrays = true;
@@ -223,6 +226,8 @@ Geometry* geometry_create(const ctk_geom_desc* d) {
         CTK_CUDA(cudaMemcpy(g->d_vorder.p, vorder.data(), sizeof(int) * vorder.size(), cudaMemcpyHostToDevice));
         g->d_ctst.ensure(sizeof(double2) * ctst.size());
         g->d_col.ensure(sizeof(float4) * col.size());
+        g->d_col64.ensure(sizeof(double4) * col64.size());
+        CTK_CUDA(cudaMemcpy(g->d_col64.p, col64.data(), sizeof(double4) * col64.size(), cudaMemcpyHostToDevice));
         g->d_colaxis.ensure(cax.size());
         g->d_colstep.ensure(sizeof(double2) * cst.size());
         CTK_CUDA(cudaMemcpy(g->d_ctst.p, ctst.data(), sizeof(double2) * ctst.size(), cudaMemcpyHostToDevice));

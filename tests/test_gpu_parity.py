@@ -68,45 +68,46 @@ def test_atb_voxel_f64_bit_exact(ctk, reference, name):
     assert np.array_equal(got, want), f"max |d| = {np.abs(got - want).max()}"
 
 
-def _large(g):
-    return max(g.nx, g.ny, g.nz) > 128
+# Random-signed data is the worst case for the f32 path: with cancelling terms the rounding
+# of the sample positions shows directly.  The f32 kernels anchor every position in fp64 and
+# round only small offsets in f32 (f32_common.cuh; the reference computes positions in fp64
+# even for T = float, projector.hpp:97-103), so every geometry -- including the 800-row
+# cone_wide and the multi-tile cone_multitile -- is held to half the north-star bar on
+# signed data (measured ~3e-7 at C3; the plain-f32 positions of round 1 gave 2.4e-5 here).
+TOL_SIGNED = 5e-6
 
 
-# Random-signed data is the worst case for the f32 path: with cancelling terms the error of
-# the f32 sample positions (~ulp of the coordinate extent) shows directly -- 2.4e-5 at the
-# 800-row cone_wide geometry, 2.1e-5 for A^T b at C3 with 4 views.  Physical data (the
-# phantom and its line integrals, nonnegative) stay far inside the bar: at C3, 4.9e-7 (Ax)
-# and 9.2e-6 / 5.1e-6 / 3.0e-6 (A^T b at 4 / 16 / 48 views; tests/test_gpu_fullsize.py,
-# tools/precision_probe.py).  The large test geometries therefore use physical data: a
-# nonnegative volume and its line integrals (tools/precision_wide.py).
 @pytest.mark.parametrize("name", sorted(ALL))
-def test_ax_f32_within_1e5(ctk, reference, name, restated):
+def test_ax_f32_within_1e5(ctk, reference, name):
     g = ALL[name]()
-    n = max(g.nx, g.ny, g.nz)
-    if _large(g):
-        x = np.abs(_rand(g.domain_size, 4)).astype(np.float32).astype(np.float64)
-    elif g.nz > 1:
-        ph = restated.shepp_logan_3d(n, np.float64)
-        x = ph.reshape(n, n, n)[: g.nz, : g.ny, : g.nx].astype(np.float32).astype(np.float64).ravel()
-    else:
-        x = _rand(g.domain_size, 4).astype(np.float32).astype(np.float64)
+    x = _rand(g.domain_size, 4).astype(np.float32).astype(np.float64)
     want = reference.forward(g, x)
     got = ctk.projector_pair(to_ctk(g)).apply_forward(x.astype(np.float32))
-    assert rel_l2(got, want) < TOL_F32
+    e = rel_l2(got, want)
+    assert e < TOL_SIGNED < TOL_F32, e
 
 
 @pytest.mark.parametrize("name", sorted(ALL))
 @pytest.mark.parametrize("variant", [0, 1])
 def test_atb_f32_within_1e5(ctk, reference, name, variant):
     g = ALL[name]()
-    if _large(g):  # line integrals of a nonnegative volume (cone_wide: 2.5e-6; |random| y: 9.8e-6)
-        y = reference.forward(g, np.abs(_rand(g.domain_size, 5)).astype(np.float32).astype(np.float64))
-    else:
-        y = _rand(g.range_size, 5)
-    y = y.astype(np.float32).astype(np.float64)
+    y = _rand(g.range_size, 5).astype(np.float32).astype(np.float64)
     want = reference.back(g, y, variant)
     got = ctk.projector_pair(to_ctk(g), ctk.BackprojectVariant(variant)).apply_back(y.astype(np.float32))
-    assert rel_l2(got, want) < TOL_F32
+    e = rel_l2(got, want)
+    assert e < TOL_SIGNED < TOL_F32, e
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+def test_ax_f32_phantom(ctk, reference, name, restated):
+    """Physical data (a Shepp-Logan volume, nonnegative) on every geometry."""
+    g = ALL[name]()
+    n = max(g.nx, g.ny, g.nz)
+    ph = restated.shepp_logan_3d(n, np.float64)
+    x = ph.reshape(n, n, n)[: g.nz, : g.ny, : g.nx].astype(np.float32).astype(np.float64).ravel()
+    want = reference.forward(g, x)
+    got = ctk.projector_pair(to_ctk(g)).apply_forward(x.astype(np.float32))
+    assert rel_l2(got, want) < TOL_SIGNED
 
 
 def test_c1_config_parity(ctk, reference, restated):
