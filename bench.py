@@ -35,6 +35,8 @@ GATHER_BYTES_PER_SAMPLE = 16  # 4 fp32 taps per bilinear sample
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--config", default=None, choices=["C1", "C2", "C3", "C4", "C5"],
+                   help="BASELINE.json config preset (default: C3, the headline metric's config)")
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -42,15 +44,30 @@ def parse():
     p.add_argument("--angles", type=int, default=360)
     p.add_argument("--iters", type=int, default=50)
     p.add_argument("--lam", type=float, default=30.0)
-    p.add_argument("--solver", default="lsmr", choices=["lsmr", "lsqr", "cgls"],
-                   help="lsmr (C3, the headline), lsqr (C2) or cgls (C1)")
+    p.add_argument("--solver", default="lsmr", choices=["lsmr", "lsqr", "cgls", "hybrid_lsqr", "cgls_tv"],
+                   help="lsmr (C3, the headline), lsqr (C2), cgls (C1), hybrid_lsqr GCV (C4), cgls_tv (C5)")
+    p.add_argument("--outer", type=int, default=4, help="cgls_tv outer (reweighting) cycles")
     p.add_argument("--projector", default="joseph", choices=["joseph", "siddon"],
                    help="joseph (C1, C3) or siddon (C2: exact-length projector and its transpose)")
     p.add_argument("--shard", default="angle", choices=["angle", "slab"],
                    help="multi-GPU partition (SURVEY.md 8(e)): angle blocks (C3/C4) or z-slabs (C5)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU work for the cpu_baseline sample")
-    return p.parse_args()
+    p.add_argument("--cpu-budget", type=float, default=20.0, help="unused (kept for old command lines)")
+    a = p.parse_args()
+    if a.config:
+        a.__dict__.update(CONFIGS[a.config])
+    return a
+
+
+# BASELINE.json configs; every preset is the named acquisition at its full size
+CONFIGS = {
+    "C1": dict(solver="cgls", n=64, angles=100, iters=20, projector="joseph", shard="angle"),
+    "C2": dict(solver="lsqr", n=256, angles=180, iters=50, projector="siddon", shard="angle"),
+    "C3": dict(solver="lsmr", n=512, angles=360, iters=50, lam=30.0, projector="joseph", shard="angle"),
+    "C4": dict(solver="hybrid_lsqr", n=512, angles=720, iters=50, projector="joseph", shard="angle"),
+    # C5: 4 outer x 15 inner; lambda from the coarse 128^3 proxy sweep (tools/tv_lambda_sweep.py)
+    "C5": dict(solver="cgls_tv", n=1024, angles=1600, iters=60, outer=4, lam=0.1, projector="joseph", shard="slab"),
+}
 
 
 def peaks():
@@ -134,14 +151,20 @@ class Clocks:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_reference_rate(n, na, budget_s, dtype_f32=True):
+def cpu_sample_angles(n, na, cores):
+    """The CPU sample: 64 evenly spaced angles up to 512^3 (16 at 1024^3, one
+    per host thread, where one angle is 8x the work), never fewer than the thread count."""
+    return min(na, max(cores, 64 if n <= 512 else 16))
+
+
+def cpu_reference_rate(n, na, reps=3, dtype_f32=True):
     """Reference CPU path (oracle/_ref) on the host cores: Ax + matched A^T b over an evenly
-    spaced subset of S angles, extrapolated linearly in angles (projector.hpp:150,187 are
-    independent per angle) to one Krylov iteration = 2 Ax + 1 A^T b (BLAS-1 excluded,
-    which favours the CPU)."""
+    spaced subset of S angles, best of `reps` runs after one warm-up, extrapolated linearly in
+    angles (projector.hpp:150,187 are independent per angle) to one Krylov iteration = 2 Ax +
+    1 A^T b (BLAS-1, CGS2 and the TV stencils excluded, which favours the CPU)."""
     import numpy as np
 
-    from oracle.oracle import REF_SO, Reference, Restated, bench_geometry
+    from oracle.oracle import Reference, Restated, bench_geometry
 
     kind = "reference" if Reference.available() else "port"
     cores = os.cpu_count() or 1
@@ -162,25 +185,20 @@ def cpu_reference_rate(n, na, budget_s, dtype_f32=True):
     g = bench_geometry(n, na)
     dt = np.float32 if dtype_f32 else np.float64
     x = rest.shepp_logan_3d(n, dt)
+    S = cpu_sample_angles(n, na, cores)
+    gs = g.subset(np.linspace(0, na, S, endpoint=False).astype(int))
 
-    def run(S):
-        idx = np.linspace(0, na, S, endpoint=False).astype(int)
-        gs = g.subset(idx)
+    def run():
         t0 = time.perf_counter()
         y = orc.forward(gs, x) if orc else rest.forward(gs, x)
         t1 = time.perf_counter()
         _ = orc.back(gs, y, 0) if orc else rest.back(gs, y)
         t2 = time.perf_counter()
-        return S, t1 - t0, t2 - t1
+        return t1 - t0, t2 - t1
 
-    # The reference parallelises Ax and A^T b over angles (projector.hpp:148-150, 172-201), so
-    # a sample of fewer angles than threads would leave cores idle: calibrate on one angle
-    # per thread, then grow the sample in whole multiples of the thread count.
-    S0 = min(na, cores)
-    S, tax, tbt = run(S0)  # calibration (also warms caches / threads)
-    reps = max(1, int(budget_s / max(tax + tbt, 1e-6)))
-    if reps > 1 and S0 < na:
-        S, tax, tbt = run(min(na, S0 * reps))
+    run()  # warm-up (threads, page faults)
+    best = min((run() for _ in range(max(1, reps))), key=lambda t: t[0] + t[1])
+    tax, tbt = best
     t_iter = (na / S) * (2.0 * tax + tbt)
     samples_ax = S * n * n * n  # rays*slices for S angles (Gray-voxel normaliser)
     return {
@@ -189,47 +207,64 @@ def cpu_reference_rate(n, na, budget_s, dtype_f32=True):
         "atb_gvox_s": 1e-9 * samples_ax / tbt,
         "kind": kind,
         "cores": cores,
-        "sample": f"Ax + matched A^T b on {S} of {na} angles ({'f32' if dtype_f32 else 'f64'}, reference headers "
-                  f"-O3 -fopenmp, {cores} threads), extrapolated x{na / S:.1f} to 2 Ax + 1 A^T b per iteration",
+        "sample": f"Ax + matched A^T b on {S} of {na} evenly spaced angles, best of {max(1, reps)} after a warm-up "
+                  f"({'f32' if dtype_f32 else 'f64'}, reference headers -O3 -fopenmp, {cores} threads), "
+                  f"extrapolated x{na / S:.1f} to 2 Ax + 1 A^T b per iteration",
         "seconds": tax + tbt,
     }
 
 
 def reference_arm(args, rank, world):
+    """The reference's own CPU implementation on this box's host cores, timed on the same
+    sample as bench's cpu_baseline: each timed step is one best-of-1 run of the Ax + A^T b
+    sample (one warm-up first); at most 3 timed steps so the run stays within minutes."""
     if rank != 0:
         return
-    budget = max(3.0, 150.0 / max(1, args.steps + args.warmup))
-    vals = []
-    last = None
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference_rate(args.n, args.angles, budget)
-        if i >= args.warmup:
-            vals.append(r["iters_per_s"])
+    steps = max(1, min(args.steps, 3))
+    vals, last = [], None
+    for i in range(steps):
+        r = cpu_reference_rate(args.n, args.angles, reps=1)
+        vals.append(r["iters_per_s"])
         last = r
-    v = statistics.mean(vals)
+    v = max(vals)
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": v,
         "unit": "iters/s",
         "n_gpus": args.gpus,
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": steps,
+        "warmup": 1,
         "ms_per_step": 1000.0 / v,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic Shepp-Logan 3D (phantom.hpp), b = A x",
-        "config": {"workload": f"LSMR lambda={args.lam}, {args.n}^3 volume, {args.n}^2 detector, {args.angles} angles, "
-                               f"matched Joseph (config 3); CPU sample extrapolated"},
+        "config": {"workload": workload_desc(args) + "; CPU sample extrapolated"},
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": last["cores"], "kind": last["kind"],
-                         "sample": last["sample"]},
+                         "sample": last["sample"] + f"; best of {steps} steps"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "ax_gvox_s": last["ax_gvox_s"],
         "atb_gvox_s": last["atb_gvox_s"],
     }
     print(json.dumps(line), flush=True)
+
+
+def config_name(args):
+    for k, c in CONFIGS.items():
+        if all(getattr(args, f) == v for f, v in c.items() if f != "shard"):
+            return f"BASELINE config {k[1]}"
+    return "custom"
+
+
+def workload_desc(args):
+    n, na = args.n, args.angles
+    sd = {"lsmr": f"LSMR lambda={args.lam}", "hybrid_lsqr": "hybrid LSQR (GCV, CGS2 reorthogonalisation)",
+          "cgls_tv": f"IRN-TV-CGLS {args.outer} outer x {args.iters // max(1, args.outer)} inner, lambda={args.lam}"
+          }.get(args.solver, args.solver.upper())
+    return (f"{sd}, {args.iters} iters/step, {n}^3 volume, {n}^2 detector, {na} angles, cone DSO=2n DOD=n pixel 1.5, "
+            f"matched {args.projector.capitalize()} ({config_name(args)})")
 
 
 def main():
@@ -260,6 +295,10 @@ def main():
     def solve(bb):
         if args.solver == "lsmr":
             return ctk.lsmr(pair, bb, args.lam, opts)
+        if args.solver == "hybrid_lsqr":
+            return ctk.hybrid_lsqr(pair, bb, ctk.HybridStrategy.gcv(), opts)
+        if args.solver == "cgls_tv":
+            return ctk.cgls_tv(pair, bb, args.lam, args.outer, args.iters // args.outer, opts)
         return getattr(ctk, args.solver)(pair, bb, opts)
     # synthetic inputs, resident in HBM: phantom rasterised on the device, b = A x
     x_true = ctk.shepp_logan_3d(n)
@@ -327,8 +366,10 @@ def main():
             t0 = time.perf_counter()
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record()
+            runs = []
             for _ in range(args.steps):
                 res = solve(b)
+                runs.append(res.iterations_run)
             s1.record()
             barrier()
             t1 = time.perf_counter()
@@ -345,7 +386,10 @@ def main():
             break
         remeasured = True
     dev_ms = maxed(s0.elapsed_time(s1))
-    iters_total = sum([args.iters]) * args.steps
+    # every timed solve must have run all its iterations (no early stop inflating the rate)
+    assert all(r == args.iters for r in runs), f"iterations_run {runs} != {args.iters}"
+    iters_total = sum(runs)
+    free_b, total_b = torch.cuda.mem_get_info()  # device-wide: sees the library's own cudaMalloc
     ms_per_step = dev_ms / args.steps
     value = iters_total / (dev_ms / 1000.0)
 
@@ -364,11 +408,9 @@ def main():
     clk_e2e.window(t0, t1)
     e2e_s = maxed(t1 - t0)
     e2e_value = args.iters * e2e_steps / e2e_s
+    assert r.iterations_run == args.iters
 
     hbm_peak, sm_mhz, peak_src = peaks()
-    solver_desc = f"LSMR lambda={args.lam}" if args.solver == "lsmr" else args.solver.upper()
-    config_name = {("lsmr", "joseph", 512, 360): "BASELINE config 3", ("lsqr", "siddon", 256, 180): "BASELINE config 2",
-                   ("cgls", "joseph", 64, 100): "BASELINE config 1"}.get((args.solver, args.projector, n, na), "custom")
     # this rank's share of the work: its angle block (angle) or its slab of slices (slab)
     my_angles = count if args.shard == "angle" else na
     my_slices = n if args.shard == "angle" else nzl
@@ -400,9 +442,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic: Shepp-Logan 3D rasterised on device (phantom.hpp), b = A x (GPU Ax)",
-        "config": {"workload": f"{solver_desc}, {args.iters} iters/step, {n}^3 volume, {n}^2 detector, "
-                               f"{na} angles, cone DSO=2n DOD=n pixel 1.5, matched {args.projector.capitalize()} "
-                               f"({config_name})",
+        "config": {"workload": workload_desc(args),
                    "parallelism": f"{args.shard}-sharded x{world}" if world > 1 else "single GPU",
                    "l2": l2_note},
         "ax_gvox_s": ax_gvox,
@@ -424,10 +464,11 @@ def main():
         "clocks": dict(clk.summary(), remeasured=remeasured),
         "wall_s_timed": wall,
         "final_explicit_residual": res.log.explicit_residual[-1],
+        "device_mem_used_gib": (total_b - free_b) / 2**30,
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cb = cpu_reference_rate(n, na, args.cpu_budget)
+            cb = cpu_reference_rate(n, na, reps=3)
             line["cpu_baseline"] = {"value": cb["iters_per_s"], "unit": "iters/s", "cores": cb["cores"],
                                     "kind": cb["kind"],
                                     "sample": cb["sample"] + ("; the reference has no Siddon projector, so its Joseph "

@@ -88,32 +88,59 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 #ifndef CTK_BP_SL256
 #define CTK_BP_SL256 11
 #endif
+// Phase 2 by row PAIRS (CTK_BP_PAIR=1): thread = (row pair, half of the z band).  A column
+// registered in rows ih and ih+1 with ih even feeds BOTH rows of one pair from a single read
+// of its Z column (one FFMA2 per slice on the packed (row 2r, row 2r+1) accumulators), so
+// the shared-memory reads of phase 2 drop from ~2 to ~1.5 per (column, row) registration.
+#ifndef CTK_BP_PAIR
+#define CTK_BP_PAIR 1
+#endif
+#ifndef CTK_BP_SL2
+#define CTK_BP_SL2 14
+#endif
+#ifndef CTK_BP_TIGHT
+#define CTK_BP_TIGHT 1
+#endif
 template <int PB>
 struct PlaneCfg;
 template <>
 struct PlaneCfg<128> {
-    static constexpr int SL = CTK_BP_SL128, MINB = 6;
+    static constexpr int SL = CTK_BP_PAIR ? CTK_BP_SL2 : CTK_BP_SL128, MINB = 6;
 };
 template <>
 struct PlaneCfg<256> {
-    static constexpr int SL = CTK_BP_SL256, MINB = 3;
+    static constexpr int SL = CTK_BP_PAIR ? CTK_BP_SL2 : CTK_BP_SL256, MINB = 3;
 };
 #ifndef CTK_BP_KB
 #define CTK_BP_KB 32
 #endif
 constexpr int BP_KB = CTK_BP_KB;
 constexpr int BP_ZG = 2;
+// Z column swizzle (CTK_BP_SWZ=1): slot e lives in column e + e/32 of a row of stride
+// PB + PB/32, so slots e and e+32 fall in different banks.  Phase-2 lanes (consecutive rows
+// or row pairs) read slots about one or two apart, which without it pairs lanes l and l+16
+// on one bank whenever the slots span more than 32; phase-1 lanes (32 consecutive slots)
+// stay conflict-free.
+#ifndef CTK_BP_SWZ
+#define CTK_BP_SWZ 1
+#endif
+template <int PB>
+__host__ __device__ constexpr int z_stride() { return PB + (CTK_BP_SWZ ? PB / 32 : 0); }
+__device__ __forceinline__ int z_col(int e) { return CTK_BP_SWZ ? e + (e >> 5) : e; }
   // guard rows of Z on each side: out-of-band entries land there, unread
 
 template <int CLASS, int PB>
 __global__ void __launch_bounds__(PB, PlaneCfg<PB>::MINB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles) {
     constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
+    constexpr int NL = CTK_BP_PAIR ? PB / 2 : PB;  // registration lists: per row pair / per row
     extern __shared__ __align__(16) float sm[];
-    float* Z = sm + BP_ZG * BP_PB;                              // [-BP_ZG, BP_KB+BP_ZG) x [BP_PB]
-    int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG) * BP_PB);  // [BP_PB][BP_SL]
-    int* cnt = lists + BP_PB * BP_SL;                           // [BP_PB]
-    float* eth = reinterpret_cast<float*>(cnt + BP_PB);         // [BP_PB]
+    constexpr int ZS = z_stride<PB>();                          // row stride of Z
+    float* Z = sm + BP_ZG * ZS;                                 // [-BP_ZG, BP_KB+BP_ZG) x [ZS]
+    int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG) * ZS);  // [NL][BP_SL]
+    int* cnt = lists + NL * BP_SL;                              // [NL]
+    float* eth = reinterpret_cast<float*>(cnt + NL);            // [BP_PB]
+    static_assert((NL * BP_SL) % 4 == 0 && NL % 4 == 0, "keeps vrtab 16-byte aligned");
     const int nv4 = 4 * pg_groups(g.nv);
     float* vrtab = eth + BP_PB;                                 // [nv4] iv - (nv-1)/2, 16-byte aligned
     int2* urange = reinterpret_cast<int2*>(vrtab + nv4);        // [na]
@@ -142,6 +169,23 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
 
+#if CTK_BP_PAIR
+    // thread = (row pair r: rows p0+2r, p0+2r+1; half kh of the z band): BP_KB/2 packed
+    // accumulators (row 2r, row 2r+1) per slice
+    const int r2 = t % (BP_PB / 2), kh = t / (BP_PB / 2);
+    const int kz0 = kh * (BP_KB / 2);
+    float2 acc2[BP_KB / 2];
+#pragma unroll
+    for (int m = 0; m < BP_KB / 2; ++m) acc2[m] = make_float2(0.f, 0.f);
+    auto add_entry2 = [&](float2 w2, int e) {
+        const int ze = z_col(e);
+#pragma unroll
+        for (int m = 0; m < BP_KB / 2; ++m) {
+            const float z = Z[(kz0 + m) * ZS + ze];
+            acc2[m] = __ffma2_rn(w2, make_float2(z, z), acc2[m]);
+        }
+    };
+#else
     // BP_KB accumulators as packed pairs: phase 2 adds wh * Z with FFMA2 (per element the
     // scalar fma)
     float2 acc2[BP_KB / 2];
@@ -149,10 +193,12 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     for (int m = 0; m < BP_KB / 2; ++m) acc2[m] = make_float2(0.f, 0.f);
     auto add_entry = [&](float wh, int e) {
         const float2 w2 = make_float2(wh, wh);
+        const int ze = z_col(e);
 #pragma unroll
         for (int m = 0; m < BP_KB / 2; ++m)
-            acc2[m] = __ffma2_rn(w2, make_float2(Z[(2 * m) * BP_PB + e], Z[(2 * m + 1) * BP_PB + e]), acc2[m]);
+            acc2[m] = __ffma2_rn(w2, make_float2(Z[(2 * m) * ZS + ze], Z[(2 * m + 1) * ZS + ze]), acc2[m]);
     };
+#endif
 
     // candidate detector-column range of every view for this tile (projection of the
     // tile's row segment in the plane), computed once, in parallel
@@ -200,7 +246,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     for (int b0 = 0; b0 < total; b0 += BP_PB) {
         {
             // ---- phase 1 ----
-            cnt[t] = 0;
+            if (t < NL) cnt[t] = 0;
             int a = -1, iu = 0;
             const int gidx = b0 + t;
             if (gidx < total) {  // the view of this slot: pref[a] <= gidx < pref[a + 1]
@@ -243,7 +289,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         // column iu of view a, row group q: pc4[q * nu] (grouped layout)
                         const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
                         const size_t qs = size_t(g.nu);
-                        float* zc = Z + t;
+                        float* zc = Z + z_col(t);
                         // z of row iv at this plane (f32_common.cuh), the forward's expression:
                         //   S = fmaf(vr, Whi, fc) (exact), T = fmaf(vr, Wlo, S),
                         //   iz = izc + floor(T), tz = fmaf(vr, Wlo, S - floor(T))
@@ -260,7 +306,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             return __float_as_int(tt) + koff;
                         };
                         auto zero_rows = [&](int lo, int hi) {  // Z rows [lo, hi) of this column
-                            for (int m = max(lo, 0); m < min(hi, BP_KB); ++m) zc[m * BP_PB] = 0.f;
+                            for (int m = max(lo, 0); m < min(hi, BP_KB); ++m) zc[m * ZS] = 0.f;
                         };
                         if (gs > 0.f && v0 <= v1) {
                             // fz increases with iv, so Z[k] is final once the march passes it:
@@ -273,6 +319,13 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             // only the rows before the first / after the last k need zeroing;
                             // sparser columns zero the whole band first.
                             const float rg = invdu / gs;
+#if CTK_BP_TIGHT
+                            // trim the estimated row range to the rows whose z stencil meets the
+                            // band (kk in [-1, BP_KB-1]), with the exact arithmetic of the march:
+                            // rows outside only reach the guard rows
+                            while (v0 < v1 && row_k(v0, tf_unused) < -1) ++v0;
+                            while (v1 > v0 && row_k(v1, tf_unused) > BP_KB - 1) --v1;
+#endif
                             if (rg >= 0.75f) {
                                 zero_rows(0, row_k(v0, tf_unused));
                             } else {
@@ -292,9 +345,9 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 B = bk + w1;
                                 cur = kk;
                                 // one unsigned clamp: kk < -BP_ZG wraps high and lands in the top guard rows
-                                float* zp = zc - BP_ZG * BP_PB + min(unsigned(kk + BP_ZG), unsigned(BP_KB + 2 * BP_ZG - 2)) * BP_PB;
+                                float* zp = zc - BP_ZG * ZS + min(unsigned(kk + BP_ZG), unsigned(BP_KB + 2 * BP_ZG - 2)) * ZS;
                                 zp[0] = A;
-                                zp[BP_PB] = B;
+                                zp[ZS] = B;
                             };
                             // the row positions of a 4-row group in packed f32x2 arithmetic
                             // (FFMA2 / FADD2), per lane the scalar sequence of row_k
@@ -342,11 +395,27 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 const float yv = reinterpret_cast<const float*>(pc4 + (iv >> 2) * qs)[iv & 3];
                                 float tz;
                                 const int kk = row_k(iv, tz);
-                                if (unsigned(kk) < unsigned(BP_KB)) zc[kk * BP_PB] = fmaf(1.f - tz, yv, zc[kk * BP_PB]);
-                                if (unsigned(kk + 1) < unsigned(BP_KB)) zc[(kk + 1) * BP_PB] = fmaf(tz, yv, zc[(kk + 1) * BP_PB]);
+                                if (unsigned(kk) < unsigned(BP_KB)) zc[kk * ZS] = fmaf(1.f - tz, yv, zc[kk * ZS]);
+                                if (unsigned(kk + 1) < unsigned(BP_KB)) zc[(kk + 1) * ZS] = fmaf(tz, yv, zc[(kk + 1) * ZS]);
                             }
                         }
                         eth[t] = th;
+#if CTK_BP_PAIR
+                        // rows rel (weight 1-th) and rel+1 (weight th), relative to p0 (even):
+                        // mode 0 = both rows of pair rel/2, 1 = row rel as the .y of its pair,
+                        // 2 = row rel+1 as the .x of its pair
+                        auto reg = [&](int pr, int mode) {
+                            const int sl = atomicAdd(&cnt[pr], 1);
+                            if (sl < BP_SL) lists[pr * BP_SL + sl] = (t << 2) | mode;
+                        };
+                        const int rel = ih - p0;
+                        if (!(rel & 1)) {
+                            reg(rel >> 1, 0);
+                        } else {
+                            if (rel >= 0) reg(rel >> 1, 1);
+                            if (rel + 1 <= BP_PB - 1 && th != 0.f) reg((rel + 1) >> 1, 2);
+                        }
+#else
                         if (ih >= p0) {
                             const int sl = atomicAdd(&cnt[ih - p0], 1);
                             if (sl < BP_SL) lists[(ih - p0) * BP_SL + sl] = (t << 1);
@@ -355,10 +424,59 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             const int sl = atomicAdd(&cnt[ih + 1 - p0], 1);
                             if (sl < BP_SL) lists[(ih + 1 - p0) * BP_SL + sl] = (t << 1) | 1;
                         }
+#endif
                     }
                 }
             }
             __syncthreads();
+#if CTK_BP_PAIR
+            // ---- phase 2: row pair r2 gathers its registered columns in column order ----
+            const int n = cnt[r2];
+            if (n > 0 && p0 + 2 * r2 < nh) {
+                if (n <= BP_SL) {
+                    int lst[BP_SL];
+#pragma unroll
+                    for (int q = 0; q < BP_SL; ++q) lst[q] = q < n ? lists[r2 * BP_SL + q] : 0x7fffffff;
+                    // insertion sort of the n registered entries (n is small: 3-6 typically)
+#pragma unroll
+                    for (int i = 1; i < BP_SL; ++i) {
+                        if (i >= n) break;
+#pragma unroll
+                        for (int j = i; j > 0; --j)
+                            if (lst[j - 1] > lst[j]) { const int tmp = lst[j]; lst[j] = lst[j - 1]; lst[j - 1] = tmp; }
+                    }
+#pragma unroll
+                    for (int q = 0; q < BP_SL; ++q) {
+                        if (q >= n) break;
+                        const int e = lst[q] >> 2, mode = lst[q] & 3;
+                        const float th = eth[e], omt = 1.f - th;
+                        const float2 w2 = mode == 0 ? make_float2(omt, th) : (mode == 1 ? make_float2(0.f, omt) : make_float2(th, 0.f));
+                        add_entry2(w2, e);
+                    }
+                } else {
+                    // overflow (very fine detector sampling): scan every slot of the batch in order
+                    const int pa = p0 + 2 * r2;
+                    for (int e = 0; e < BP_PB; ++e) {
+                        const int c = slotcol[e];
+                        if (c < 0 || g.colaxis[c] != CLASS) continue;
+                        int ih, ihA;
+                        float th, thA;
+                        double G;
+                        slice_anchor(g.col64[c], sc, ihA, thA, G);
+                        split(fmaf(kf, g.col[c].y, thA), ih, th);
+                        ih += ihA;
+                        if (ih + 1 < p0 || ih > p0 + BP_PB - 1 || ih + 1 < 0 || ih >= nh) continue;  // not registered
+                        const float omt = 1.f - th;
+                        float2 w2;
+                        if (ih == pa) w2 = make_float2(omt, th);
+                        else if (ih == pa + 1) w2 = make_float2(0.f, omt);
+                        else if (ih + 1 == pa && th != 0.f) w2 = make_float2(th, 0.f);
+                        else continue;
+                        add_entry2(w2, e);
+                    }
+                }
+            }
+#else
             // ---- phase 2: row p gathers its registered columns in column order ----
             const int n = cnt[t];
             if (n > 0 && p < nh) {
@@ -401,9 +519,27 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                     }
                 }
             }
+#endif
             __syncthreads();
         }
     }
+#if CTK_BP_PAIR
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+        const int pr = p0 + 2 * r2 + h2;
+        if (pr >= nh) break;
+#pragma unroll
+        for (int m = 0; m < BP_KB / 2; ++m) {
+            const int k = k0 + kz0 + m;
+            if (k >= g.nz) break;
+            const size_t o = CLASS ? size_t(pr) + size_t(g.nx) * (size_t(s) + size_t(g.ny) * k)
+                                   : size_t(s) + size_t(g.nx) * (size_t(pr) + size_t(g.ny) * k);
+            const float am = h2 ? acc2[m].y : acc2[m].x;
+            if (CLASS == 0) x[o] = am;
+            else x[o] += am;
+        }
+    }
+#else
     if (p < nh) {
 #pragma unroll
         for (int m = 0; m < BP_KB; ++m) {
@@ -416,6 +552,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
             else x[o] += am;
         }
     }
+#endif
 }
 
 __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x) {
@@ -473,7 +610,16 @@ __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, f
     x[id] += acc;
 }
 
-// ---- voxel-driven A^T b (projector.hpp:204-279), warp per column as above --------------
+// ---- voxel-driven A^T b (projector.hpp:204-279) -----------------------------------------
+// Warp = one voxel column (i, j), lanes along z (KZ slices per lane).  Views are taken 32 at
+// a time: lane L sets up view a0+L for the column in fp64 -- source offset, perspective
+// factor t, detector column fu split into (iu, tu) -- exactly the reference's expressions,
+// and the warp then walks the 32 views in order with the per-view values broadcast by
+// __shfl_sync (1/32 of the warp-uniform fp64 work per lane instead of all of it).  The row
+// position fv = t*z/du + cv is evaluated per sample in fp64 (B200 runs FP64 at half the FP32
+// rate) and split into (iv, tv) exactly, so positions round like the reference's double
+// positions rather than at ulp(nv) of an f32 coordinate; taps, weights and the per-view sum
+// are f32 and the views are summed in the reference's order.
 template <int KZ>
 __global__ void __launch_bounds__(128)
 k_atb_voxel_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, int kblocks) {
@@ -484,69 +630,92 @@ k_atb_voxel_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
     const int kb = int(wid / ncol) * 32 * KZ;
     const long col = wid % ncol;
     const int i = int(col % g.nx), j = int(col / g.nx);
+    const double xd = (i - 0.5 * (g.nx - 1)) * g.h, yd = (j - 0.5 * (g.ny - 1)) * g.h;
+    const double cu = 0.5 * (g.nu - 1), cv = 0.5 * (g.nv - 1);
+    const double invdu = 1.0 / g.du;
     const float h = float(g.h);
-    const float xf = float((i - 0.5 * (g.nx - 1)) * g.h), yf = float((j - 0.5 * (g.ny - 1)) * g.h);
-    const float cuf = 0.5f * float(g.nu - 1), cvf = 0.5f * float(g.nv - 1);
-    const float invdu = float(1.0 / g.du);
     const bool cone = g.mode == CTK_CONE3D;
+    const bool flat = g.nv == 1;
     float zk[KZ], acc[KZ];
+    double zq[KZ];  // z / du
 #pragma unroll
     for (int m = 0; m < KZ; ++m) {
         const int k = kb + lane + 32 * m;
-        zk[m] = float((k + g.z0 - 0.5 * (g.nzg - 1)) * g.h);
+        const double z = (k + g.z0 - 0.5 * (g.nzg - 1)) * g.h;
+        zk[m] = float(z);
+        zq[m] = z * invdu;
         acc[m] = 0.f;
     }
-    for (int a = 0; a < g.na; ++a) {
-        const double2 tr = g.ctst[a];
-        const float ct = float(tr.x), st = float(tr.y);
-        float fu, t = 1.f, rx = 0.f, ry = 0.f, scale_par = 0.f;
-        if (cone) {
-            const float sx = float(g.dso) * ct, sy = float(g.dso) * st;
-            rx = xf - sx;
-            ry = yf - sy;
-            const float depth = -(rx * ct + ry * st);
-            if (depth <= 0.f) continue;
-            t = float(g.dso + g.dod) / depth;
-            const float px = sx + t * rx, py = sy + t * ry;
-            fu = (-px * st + py * ct) * invdu + cuf;
-        } else {
-            fu = (-xf * st + yf * ct) * invdu + cuf;
-            scale_par = h / fmaxf(fabsf(ct), fabsf(st));
-        }
-        const float fiu = floorf(fu);
-        const int iu = int(fiu);
-        const float tu = fu - fiu;
-        if (iu < -1 || iu >= g.nu) continue;
-        const bool u0ok = iu >= 0, u1ok = iu + 1 < g.nu;
-        const float* c0 = pt + size_t(a * g.nu + iu) * g.nv;
-        const float* c1 = c0 + g.nv;
-        const float arxy = fmaxf(fabsf(rx), fabsf(ry));
-        const float rxy2 = rx * rx + ry * ry;
-#pragma unroll
-        for (int m = 0; m < KZ; ++m) {
-            const int k = kb + lane + 32 * m;
-            if (k >= g.nz) break;
-            const float z = zk[m];
-            const float fv = (g.nv == 1) ? 0.f : fmaf(t * z, invdu, cvf);
-            const float fiv = floorf(fv);
-            const int iv = int(fiv);
-            const float tv = fv - fiv;
-            const bool v0ok = iv >= 0 && iv < g.nv, v1ok = iv + 1 >= 0 && iv + 1 < g.nv;
-            const float p00 = (u0ok && v0ok) ? __ldg(c0 + iv) : 0.f;
-            const float p10 = (u1ok && v0ok) ? __ldg(c1 + iv) : 0.f;
-            const float p01 = (u0ok && v1ok) ? __ldg(c0 + iv + 1) : 0.f;
-            const float p11 = (u1ok && v1ok) ? __ldg(c1 + iv + 1) : 0.f;
-            const float s0 = fmaf(tu, p10 - p00, p00);
-            const float s1 = fmaf(tu, p11 - p01, p01);
-            const float sample = fmaf(tv, s1 - s0, s0);
-            float scale;
+    for (int a0 = 0; a0 < g.na; a0 += 32) {
+        // ---- lane L: view a0 + L of this column, fp64 ----
+        const int av = a0 + lane;
+        double tD = 1.0;
+        int iuL = 0;
+        float tuL = 0.f, arxy = 0.f, rxy2 = 0.f, spar = 0.f;
+        bool ok = false;
+        if (av < g.na) {
+            const double2 tr = g.ctst[av];
+            double fu;
+            ok = true;
             if (cone) {
-                const float dom = fmaxf(arxy, fabsf(z));
-                scale = h * sqrtf(rxy2 + z * z) / dom;
+                const double sx = g.dso * tr.x, sy = g.dso * tr.y;
+                const double rx = xd - sx, ry = yd - sy;
+                const double depth = -(rx * tr.x + ry * tr.y);
+                if (depth <= 0.0) ok = false;
+                tD = (g.dso + g.dod) / depth;
+                const double px = sx + tD * rx, py = sy + tD * ry;
+                fu = (-px * tr.y + py * tr.x) * invdu + cu;
+                arxy = float(fmax(fabs(rx), fabs(ry)));
+                rxy2 = float(rx * rx + ry * ry);
             } else {
-                scale = scale_par;
+                fu = (-xd * tr.y + yd * tr.x) * invdu + cu;
+                spar = float(g.h / fmax(fabs(tr.x), fabs(tr.y)));
             }
-            acc[m] = fmaf(scale, sample, acc[m]);
+            if (ok && fu > -2.0 && fu < double(g.nu)) {
+                dsplit(fu, iuL, tuL);
+                if (iuL < -1 || iuL >= g.nu) ok = false;
+            } else {
+                ok = false;
+            }
+        }
+        unsigned live = __ballot_sync(0xffffffffu, ok);
+        while (live) {  // views in ascending order
+            const int L = __ffs(live) - 1;
+            live &= live - 1;
+            const int a = a0 + L;
+            const double t = __shfl_sync(0xffffffffu, tD, L);
+            const int iu = __shfl_sync(0xffffffffu, iuL, L);
+            const float tu = __shfl_sync(0xffffffffu, tuL, L);
+            const float vax = __shfl_sync(0xffffffffu, arxy, L), vr2 = __shfl_sync(0xffffffffu, rxy2, L);
+            const float vsp = __shfl_sync(0xffffffffu, spar, L);
+            const bool u0ok = iu >= 0, u1ok = iu + 1 < g.nu;
+            const float* c0 = pt + size_t(a * g.nu + iu) * g.nv;
+            const float* c1 = c0 + g.nv;
+#pragma unroll
+            for (int m = 0; m < KZ; ++m) {
+                const int k = kb + lane + 32 * m;
+                if (k >= g.nz) break;
+                int iv = 0;
+                float tv = 0.f;
+                if (!flat)  // clamped far outside the detector so the split stays exact (taps then read nothing)
+                    dsplit(fmin(fmax(__fma_rn(cone ? t : 1.0, zq[m], cv), -4.0), g.nv + 4.0), iv, tv);
+                const bool v0ok = iv >= 0 && iv < g.nv, v1ok = iv + 1 >= 0 && iv + 1 < g.nv;
+                const float p00 = (u0ok && v0ok) ? __ldg(c0 + iv) : 0.f;
+                const float p10 = (u1ok && v0ok) ? __ldg(c1 + iv) : 0.f;
+                const float p01 = (u0ok && v1ok) ? __ldg(c0 + iv + 1) : 0.f;
+                const float p11 = (u1ok && v1ok) ? __ldg(c1 + iv + 1) : 0.f;
+                const float s0 = fmaf(tu, p10 - p00, p00);
+                const float s1 = fmaf(tu, p11 - p01, p01);
+                const float sample = fmaf(tv, s1 - s0, s0);
+                float scale;
+                if (cone) {
+                    const float z = zk[m];
+                    scale = h * sqrtf(fmaf(z, z, vr2)) / fmaxf(vax, fabsf(z));
+                } else {
+                    scale = vsp;
+                }
+                acc[m] = fmaf(scale, sample, acc[m]);
+            }
         }
     }
 #pragma unroll
@@ -586,7 +755,8 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz_local() + BP_KB - 1) / BP_KB;
-    const size_t smem = sizeof(float) * (size_t(BP_PB) * (BP_KB + 2 * BP_ZG) + size_t(BP_PB) * BP_SL + 2 * BP_PB +
+    constexpr int NL = CTK_BP_PAIR ? PB / 2 : PB;
+    const size_t smem = sizeof(float) * (size_t(z_stride<PB>()) * (BP_KB + 2 * BP_ZG) + size_t(NL) * BP_SL + NL + BP_PB +
                                          4 * size_t(pg_groups(g.nv))) +
                         sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");

@@ -179,7 +179,8 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                 slice_anchor(c64, sc, ihA, thA, G);
                 z_split(g, G, Whi, Wr);
                 const float S = fmaf(vr, Whi, fc);  // exact
-                U sb = U(s) * uplane + U(unsigned(ihA)) * upz - cbias;
+                // U(Off(ihA)): sign-extended, ihA < 0 at the volume edge (a 64-bit U must not zero-extend)
+                U sb = U(s) * uplane + U(Off(ihA)) * upz - cbias;
                 const float2 thA2 = make_float2(thA, thA), Wr2 = make_float2(Wr, Wr), S2 = make_float2(S, S);
                 float2 k2 = make_float2(float(s - sc), float(s - sc + 1));
                 const int cnt = se - s + 1;
