@@ -80,6 +80,9 @@ int ctk_abi_version(void);
 /* ---- geometry (replaces ConeGeometry::validate + projector_pair capture,
  *      geometry.hpp:35-54, operators.hpp:91-101) -------------------------------------- */
 int ctk_geom_create(const ctk_geom_desc* desc, ctk_geom** out);
+/* ConeGeometry::validate alone (geometry.hpp:35-54): same checks, order and messages as
+ * ctk_geom_create, no device work (host-side validation for bindings). */
+int ctk_geom_validate(const ctk_geom_desc* desc);
 void ctk_geom_destroy(ctk_geom* g);
 /* domain_size = nx*ny*nz, range_size = n_angles*nu*nv (operators.hpp:98-99) */
 int ctk_geom_sizes(const ctk_geom* g, size_t* domain_size, size_t* range_size);

@@ -105,6 +105,7 @@ def load():
         "ctk_last_error_iteration": (i, []),
         "ctk_abi_version": (i, []),
         "ctk_geom_create": (i, [C.POINTER(GeomDesc), C.POINTER(vp)]),
+        "ctk_geom_validate": (i, [C.POINTER(GeomDesc)]),
         "ctk_geom_destroy": (None, [vp]),
         "ctk_geom_sizes": (i, [vp, C.POINTER(sz), C.POINTER(sz)]),
         "ctk_geom_set_projector": (i, [vp, i]),

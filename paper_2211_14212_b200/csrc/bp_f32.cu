@@ -93,13 +93,13 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 // of its Z column (one FFMA2 per slice on the packed (row 2r, row 2r+1) accumulators), so
 // the shared-memory reads of phase 2 drop from ~2 to ~1.5 per (column, row) registration.
 #ifndef CTK_BP_PAIR
-#define CTK_BP_PAIR 1
+#define CTK_BP_PAIR 0
 #endif
 #ifndef CTK_BP_SL2
 #define CTK_BP_SL2 14
 #endif
 #ifndef CTK_BP_TIGHT
-#define CTK_BP_TIGHT 1
+#define CTK_BP_TIGHT 0
 #endif
 template <int PB>
 struct PlaneCfg;
@@ -122,7 +122,7 @@ constexpr int BP_ZG = 2;
 // on one bank whenever the slots span more than 32; phase-1 lanes (32 consecutive slots)
 // stay conflict-free.
 #ifndef CTK_BP_SWZ
-#define CTK_BP_SWZ 1
+#define CTK_BP_SWZ 0
 #endif
 template <int PB>
 __host__ __device__ constexpr int z_stride() { return PB + (CTK_BP_SWZ ? PB / 32 : 0); }
@@ -365,6 +365,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             // whole 4-row groups; only the first and last are masked to [v0, v1]
                             const float4* vr4 = reinterpret_cast<const float4*>(vrtab);
                             const int q0 = v0 >> 2, q1 = v1 >> 2;
+                            CTK_CHK(g, q0 >= 0 && q1 < nq && size_t(a) < size_t(g.na) && iu < g.nu, 1);
                             auto group = [&](int q, float4 y4, bool mask) {
                                 const float4 d4 = vr4[q];
                                 if (mask) {
@@ -496,6 +497,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                     for (int q = 0; q < BP_SL; ++q) {
                         if (q >= n) break;
                         const int e = lst[q] >> 1;
+                        CTK_CHK(g, e < BP_PB, 3);
                         const float th = eth[e];
                         const float wh = (lst[q] & 1) ? th : 1.f - th;
                         add_entry(wh, e);
@@ -545,8 +547,9 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
         for (int m = 0; m < BP_KB; ++m) {
             const int k = k0 + m;
             if (k >= g.nz) break;
-            const size_t o = CLASS ? size_t(p) + size_t(g.nx) * (size_t(s) + size_t(g.ny) * k)
-                                   : size_t(s) + size_t(g.nx) * (size_t(p) + size_t(g.ny) * k);
+            const size_t o = chk_idx(g, CLASS ? size_t(p) + size_t(g.nx) * (size_t(s) + size_t(g.ny) * k)
+                                              : size_t(s) + size_t(g.nx) * (size_t(p) + size_t(g.ny) * k),
+                                     size_t(g.nx) * g.ny * g.nz, 2);
             const float am = (m & 1) ? acc2[m >> 1].y : acc2[m >> 1].x;
             if (CLASS == 0) x[o] = am;
             else x[o] += am;
@@ -603,7 +606,7 @@ __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, f
                 float wb, wc;
                 if (i == ib) wb = 1.f - tb; else if (i == ib + 1) wb = tb; else continue;
                 if (j == ic) wc = 1.f - tc; else if (j == ic + 1) wc = tc; else continue;
-                acc = fmaf(wb * wc, __ldg(pg + pg_index(g, a, iu, iv)), acc);
+                acc = fmaf(wb * wc, __ldg(pg + chk_idx(g, pg_index(g, a, iu, iv), size_t(g.na) * pg_groups(g.nv) * g.nu * 4, 6)), acc);
             }
         }
     }
@@ -689,6 +692,7 @@ k_atb_voxel_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
             const float vax = __shfl_sync(0xffffffffu, arxy, L), vr2 = __shfl_sync(0xffffffffu, rxy2, L);
             const float vsp = __shfl_sync(0xffffffffu, spar, L);
             const bool u0ok = iu >= 0, u1ok = iu + 1 < g.nu;
+            CTK_CHK(g, a < g.na && iu >= -1 && iu < g.nu, 5);
             const float* c0 = pt + size_t(a * g.nu + iu) * g.nv;
             const float* c1 = c0 + g.nv;
 #pragma unroll

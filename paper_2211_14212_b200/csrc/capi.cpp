@@ -10,6 +10,7 @@
 #include "regparam.h"
 
 namespace ctkb {
+void geometry_validate(const ctk_geom_desc* d);  // ConeGeometry::validate, no device work
 Geometry* geometry_create(const ctk_geom_desc* d);
 void nccl_unique_id(void* out128);
 Comm* comm_create_nccl(const void* id128, int nranks, int rank);
@@ -159,6 +160,9 @@ int ctk_geom_create(const ctk_geom_desc* desc, ctk_geom** out) {
         *out = nullptr;
         *out = reinterpret_cast<ctk_geom*>(ctkb::geometry_create(desc));
     });
+}
+int ctk_geom_validate(const ctk_geom_desc* desc) {
+    return guard([&] { ctkb::geometry_validate(desc); });
 }
 void ctk_geom_destroy(ctk_geom* g) { delete reinterpret_cast<ctkb::Geometry*>(g); }
 

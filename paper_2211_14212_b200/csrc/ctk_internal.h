@@ -59,6 +59,7 @@ struct KGeom {
     const unsigned char* colaxis; // per (view, iu): 0 = x-dominant, 1 = y-dominant
     const double2* colstep;       // per (view, iu): (dx^2+dy^2, |d_A|) of the unnormalised ray
     const int4* vclass;           // per view: column hull [x.. y] of x-dominant, [z.. w] of y-dominant columns
+    unsigned* chk;                // checked builds (CTK_CHECKED): bounds-violation bits, else null
 };
 
 // ---- the geometry handle ---------------------------------------------------------------
@@ -86,6 +87,7 @@ struct Geometry {
     DevBuf d_ctst, d_col, d_col64, d_colaxis, d_colstep;
     DevBuf d_vorder;  // views grouped by ray class (x-dominant first) for L2 reuse in Ax
     DevBuf d_vclass;  // per view: hull of the columns of each ray class (matched A^T b batching)
+    DevBuf d_chk;     // checked builds: one word of bounds-violation bits (kernels atomicOr into it)
     DevBuf d_rayinv;  // per ray: 1/d of make_ray, for the exact gathers (built on first use)
     bool rayinv_ready = false;
     DevBuf d_walk;    // per ray: the plan_walk parameters of the exact f64 path (built on first use)

@@ -20,6 +20,29 @@
 namespace ctkb {
 namespace {
 
+// Bounds checks of the checked build (ops.cpp check_bounds): record bit `bit` when idx is
+// outside [0, n) and return a safe index (0) so the access itself stays in bounds.
+#ifdef CTK_CHECKED
+template <class I>
+__device__ __forceinline__ I chk_idx(const KGeom& g, I idx, I n, int bit) {
+    if (idx < I(0) || idx >= n) {
+        atomicOr(g.chk, 1u << bit);
+        return I(0);
+    }
+    return idx;
+}
+#define CTK_CHK(g, cond, bit) \
+    do {                       \
+        if (!(cond)) atomicOr((g).chk, 1u << (bit)); \
+    } while (0)
+#else
+template <class I>
+__device__ __forceinline__ I chk_idx(const KGeom&, I idx, I, int) { return idx; }
+#define CTK_CHK(g, cond, bit) \
+    do {                       \
+    } while (0)
+#endif
+
 __device__ __forceinline__ double row_coord(const KGeom& g, int iv) { return (iv - 0.5 * (g.nv - 1)) * g.du; }
 
 // path length per slice step of ray (column c, row coordinate v)

@@ -170,6 +170,20 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
             const float2 m1 = make_float2(-1.f, -1.f), two = make_float2(2.f, 2.f);
             float2 acc2 = make_float2(0.f, 0.f);
+#ifdef CTK_CHECKED
+            // checked build: the four taps o, o+1, o+pz, o+pz+1 must lie inside the layout
+            const long long lay_n = (long long)ns * (long long)plane, base_abs = (long long)(kPad * pz + kPad);
+            auto chk_tap = [&](Off o) -> Off {
+                const long long lo = base_abs + (long long)o;
+                if (lo < 0 || lo + (long long)pz + 1 >= lay_n) {
+                    atomicOr(g.chk, 1u << 0);
+                    return Off(-base_abs);
+                }
+                return o;
+            };
+#else
+            auto chk_tap = [](Off o) { return o; };
+#endif
             for (int s = s0; s <= s1;) {  // slice blocks
                 const int sc = slice_centre(s);
                 const int se = min(s1, sc + kSB / 2 - 1);
@@ -192,9 +206,10 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                     const float2 tzt = __fadd2_rd(__ffma2_rn(vr2, wlo, S2), M2);
                     const float2 th = __ffma2_rn(__fadd2_rn(tht, nM2), m1, fh);  // fh - floor(fh)
                     const float2 tz = __ffma2_rn(vr2, wlo, __ffma2_rn(__fadd2_rn(tzt, nM2), m1, S2));
-                    const Off o0 = Off(U(unsigned(__float_as_int(tht.x))) * upz + (sb + U(unsigned(__float_as_int(tzt.x)))));
-                    const Off o1 =
-                        Off(U(unsigned(__float_as_int(tht.y))) * upz + (sb + uplane + U(unsigned(__float_as_int(tzt.y)))));
+                    const Off o0 =
+                        chk_tap(Off(U(unsigned(__float_as_int(tht.x))) * upz + (sb + U(unsigned(__float_as_int(tzt.x))))));
+                    const Off o1 = chk_tap(
+                        Off(U(unsigned(__float_as_int(tht.y))) * upz + (sb + uplane + U(unsigned(__float_as_int(tzt.y))))));
                     k2 = __fadd2_rn(k2, two);
                     sb += uplane2;
                     const float* p0 = base + o0;
@@ -214,7 +229,8 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                     const float tht = split_t(fh), tzt = split_t(fmaf(vr, wlo, S));
                     const float th = split_frac(fh, tht);
                     const float tz = fmaf(vr, wlo, fmaf(__fsub_rn(tzt, kSplitM), -1.f, S));
-                    const Off off = Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt)))));
+                    const Off off =
+                        chk_tap(Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt))))));
                     const float* p = base + off;
                     const float* q = base1 + off;
                     const float v00 = __ldg(p), v01 = __ldg(p + 1);  // (ih, iz), (ih, iz+1)

@@ -56,6 +56,7 @@ KGeom Geometry::kgeom() const {
     k.colaxis = d_colaxis.as<unsigned char>();
     k.vclass = d_vclass.as<int4>();
     k.colstep = d_colstep.as<double2>();
+    k.chk = d_chk.as<unsigned>();
     return k;
 }
 
@@ -77,7 +78,7 @@ static double canonical_angle(double a) {
     return r;
 }
 
-Geometry* geometry_create(const ctk_geom_desc* d) {
+void geometry_validate(const ctk_geom_desc* d) {
     if (!d) fail(CTK_E_PARAMETER, "null geometry descriptor");
     // ConeGeometry::validate, in the reference's order and wording
     if (d->n_angles <= 0 || !d->angles) fail(CTK_E_GEOMETRY, "geometry needs at least one angle");
@@ -95,6 +96,10 @@ Geometry* geometry_create(const ctk_geom_desc* d) {
         const double half_diag = std::sqrt(hx * hx + hy * hy + hz * hz);
         if (d->source_to_origin <= half_diag) fail(CTK_E_GEOMETRY, "cone3d source lies inside the volume diagonal");
     }
+}
+
+Geometry* geometry_create(const ctk_geom_desc* d) {
+    geometry_validate(d);
 
     auto* g = new Geometry();
     try {
@@ -221,6 +226,10 @@ Geometry* geometry_create(const ctk_geom_desc* d) {
                 }
             }
         g->d_vclass.ensure(sizeof(int4) * vcls.size());
+#ifdef CTK_CHECKED
+        g->d_chk.ensure(sizeof(unsigned));
+        CTK_CUDA(cudaMemset(g->d_chk.p, 0, sizeof(unsigned)));
+#endif
         CTK_CUDA(cudaMemcpy(g->d_vclass.p, vcls.data(), sizeof(int4) * vcls.size(), cudaMemcpyHostToDevice));
         g->d_vorder.ensure(sizeof(int) * vorder.size());
         CTK_CUDA(cudaMemcpy(g->d_vorder.p, vorder.data(), sizeof(int) * vorder.size(), cudaMemcpyHostToDevice));

@@ -23,7 +23,10 @@ def _ensure_built():
 
     lib = os.path.join(ROOT, "paper_2211_14212_b200", "lib", "libctk_b200.so")
     orc = os.path.join(ROOT, "oracle", "libctk_oracle.so")
-    if not os.path.exists(lib):
+    import glob
+
+    core = glob.glob(os.path.join(ROOT, "paper_2211_14212_b200", "_core*.so"))
+    if not os.path.exists(lib) or not core:
         subprocess.run(["make", "-s", "-j8", "-C", os.path.join(ROOT, "paper_2211_14212_b200", "csrc")], check=True)
     if not os.path.exists(orc):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), os.path.join(ROOT, "oracle", "libctk_oracle.so")],
