@@ -88,56 +88,40 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 #ifndef CTK_BP_SL256
 #define CTK_BP_SL256 11
 #endif
-// Phase 2 by row PAIRS (CTK_BP_PAIR=1): thread = (row pair, half of the z band).  A column
-// registered in rows ih and ih+1 with ih even feeds BOTH rows of one pair from a single read
-// of its Z column (one FFMA2 per slice on the packed (row 2r, row 2r+1) accumulators), so
-// the shared-memory reads of phase 2 drop from ~2 to ~1.5 per (column, row) registration.
-#ifndef CTK_BP_PAIR
-#define CTK_BP_PAIR 0
-#endif
-#ifndef CTK_BP_SL2
-#define CTK_BP_SL2 14
-#endif
-#ifndef CTK_BP_TIGHT
-#define CTK_BP_TIGHT 0
-#endif
 template <int PB>
 struct PlaneCfg;
 template <>
 struct PlaneCfg<128> {
-    static constexpr int SL = CTK_BP_PAIR ? CTK_BP_SL2 : CTK_BP_SL128, MINB = 6;
+    static constexpr int SL = CTK_BP_SL128, MINB = 6;
 };
 template <>
 struct PlaneCfg<256> {
-    static constexpr int SL = CTK_BP_PAIR ? CTK_BP_SL2 : CTK_BP_SL256, MINB = 3;
+    static constexpr int SL = CTK_BP_SL256, MINB = 3;
 };
 #ifndef CTK_BP_KB
 #define CTK_BP_KB 32
 #endif
 constexpr int BP_KB = CTK_BP_KB;
 constexpr int BP_ZG = 2;
-// Z column swizzle (CTK_BP_SWZ=1): slot e lives in column e + e/32 of a row of stride
-// PB + PB/32, so slots e and e+32 fall in different banks.  Phase-2 lanes (consecutive rows
-// or row pairs) read slots about one or two apart, which without it pairs lanes l and l+16
-// on one bank whenever the slots span more than 32; phase-1 lanes (32 consecutive slots)
-// stay conflict-free.
-#ifndef CTK_BP_SWZ
-#define CTK_BP_SWZ 0
-#endif
+// Z row stride (a multiple of the 32 banks: phase-1 lanes, consecutive slots, never conflict)
 template <int PB>
-__host__ __device__ constexpr int z_stride() { return PB + (CTK_BP_SWZ ? PB / 32 : 0); }
-__device__ __forceinline__ int z_col(int e) { return CTK_BP_SWZ ? e + (e >> 5) : e; }
+__host__ __device__ constexpr int z_stride() { return PB; }
+__device__ __forceinline__ int z_col(int e) { return e; }
   // guard rows of Z on each side: out-of-band entries land there, unread
 
-template <int CLASS, int PB>
+// SID = 1: the transpose of the f32 Siddon forward (f32_common.cuh model) in the same
+// structure: phase 1 fills two Z columns per slot (the column's two in-plane cells at the
+// plane), each registered in its row with weight 1 (L is in pg).
+template <int CLASS, int PB, int SID = 0>
 __global__ void __launch_bounds__(PB, PlaneCfg<PB>::MINB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles) {
     constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
-    constexpr int NL = CTK_BP_PAIR ? PB / 2 : PB;  // registration lists: per row pair / per row
+    constexpr int NL = PB;  // registration lists, one per row
     extern __shared__ __align__(16) float sm[];
     constexpr int ZS = z_stride<PB>();                          // row stride of Z
     float* Z = sm + BP_ZG * ZS;                                 // [-BP_ZG, BP_KB+BP_ZG) x [ZS]
-    int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG) * ZS);  // [NL][BP_SL]
+    float* Z2 = Z + (BP_KB + 2 * BP_ZG) * ZS;                   // Siddon: the second in-plane cell
+    int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG + (SID ? BP_KB + 2 * BP_ZG : 0)) * ZS);  // [NL][BP_SL]
     int* cnt = lists + NL * BP_SL;                              // [NL]
     float* eth = reinterpret_cast<float*>(cnt + NL);            // [BP_PB]
     static_assert((NL * BP_SL) % 4 == 0 && NL % 4 == 0, "keeps vrtab 16-byte aligned");
@@ -167,30 +151,25 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const int nq = pg_groups(g.nv);  // row groups of the grouped projection layout
     // world coordinates of the plane and of the tile's row segment ends
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
-    const double r_lo = (p0 - 1.5 - 0.5 * (nh - 1)) * h, r_hi = (p0 + BP_PB + 0.5 - 0.5 * (nh - 1)) * h;
+    const double r_lo = (p0 - (SID ? 2.5 : 1.5) - 0.5 * (nh - 1)) * h,
+                 r_hi = (p0 + BP_PB + (SID ? 1.5 : 0.5) - 0.5 * (nh - 1)) * h;
 
-#if CTK_BP_PAIR
-    // thread = (row pair r: rows p0+2r, p0+2r+1; half kh of the z band): BP_KB/2 packed
-    // accumulators (row 2r, row 2r+1) per slice
-    const int r2 = t % (BP_PB / 2), kh = t / (BP_PB / 2);
-    const int kz0 = kh * (BP_KB / 2);
-    float2 acc2[BP_KB / 2];
-#pragma unroll
-    for (int m = 0; m < BP_KB / 2; ++m) acc2[m] = make_float2(0.f, 0.f);
-    auto add_entry2 = [&](float2 w2, int e) {
-        const int ze = z_col(e);
-#pragma unroll
-        for (int m = 0; m < BP_KB / 2; ++m) {
-            const float z = Z[(kz0 + m) * ZS + ze];
-            acc2[m] = __ffma2_rn(w2, make_float2(z, z), acc2[m]);
-        }
-    };
-#else
     // BP_KB accumulators as packed pairs: phase 2 adds wh * Z with FFMA2 (per element the
     // scalar fma)
     float2 acc2[BP_KB / 2];
 #pragma unroll
     for (int m = 0; m < BP_KB / 2; ++m) acc2[m] = make_float2(0.f, 0.f);
+    auto add_sid = [&](const float* Zw, int e) {  // Siddon: weight 1
+        const int ze = z_col(e);
+#pragma unroll
+        for (int m = 0; m < BP_KB / 2; ++m)
+            acc2[m] = __fadd2_rn(make_float2(Zw[(2 * m) * ZS + ze], Zw[(2 * m + 1) * ZS + ze]), acc2[m]);
+    };
+    // a Siddon slot was processed (and registered) iff its cells meet this tile
+    auto jlo_ok = [&](int ja, int jb) {
+        const int jlo = min(ja, jb), jhi = max(ja, jb);
+        return jhi >= p0 && jlo <= p0 + BP_PB - 1 && jhi >= 0 && jlo < nh;
+    };
     auto add_entry = [&](float wh, int e) {
         const float2 w2 = make_float2(wh, wh);
         const int ze = z_col(e);
@@ -198,7 +177,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
         for (int m = 0; m < BP_KB / 2; ++m)
             acc2[m] = __ffma2_rn(w2, make_float2(Z[(2 * m) * ZS + ze], Z[(2 * m + 1) * ZS + ze]), acc2[m]);
     };
-#endif
 
     // candidate detector-column range of every view for this tile (projection of the
     // tile's row segment in the plane), computed once, in parallel
@@ -259,6 +237,131 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
             if (a >= 0) {
                 const int c = a * g.nu + iu;
                 if (g.colaxis[c] == CLASS) {
+                if constexpr (SID) {
+                    // ---- Siddon phase 1 (f32_common.cuh model): the column's cells at the
+                    // plane's two boundaries, ja (t = 0) and jb (t = 1); every row adds its four
+                    // chord weights times (L y) to Z (cell ja) and Z2 (cell jb) at its z cells
+                    // ka, kb -- rolled over (kl, kl + 1), kl = min(ka, kb), non-decreasing in iv
+                    const float4 cd = g.col[c];
+                    const double4 c64 = g.col64[c];
+                    int jA, ja, jb;
+                    float tA, fya, fyb;
+                    double G;
+                    sid_anchor(c64, sc, jA, tA, G);
+                    split(fmaf(kf - 0.5f, cd.y, tA), ja, fya);
+                    split(fmaf(kf + 0.5f, cd.y, tA), jb, fyb);
+                    ja += jA;
+                    jb += jA;
+                    const int jlo = min(ja, jb), jhi = max(ja, jb);
+                    if (jhi >= p0 && jlo <= p0 + BP_PB - 1 && jhi >= 0 && jlo < nh) {
+                        const float cy = ja != jb ? sid_cross(fya, cd.y >= 0.f, __frcp_rn(fabsf(cd.y))) : 1.f;
+                        const float gs = fmaf(fs, cd.w, cd.z);
+                        int v0 = 0, v1 = g.nv - 1;
+                        if (gs > 0.f) {
+                            const float rg = invdu / gs;
+                            v0 = max(v0, int(floorf(fmaf(float(kg0) - 1.5f - czf, rg, cvf))) - 2);
+                            v1 = min(v1, int(ceilf(fmaf(float(kg0 + BP_KB) + 0.5f - czf, rg, cvf))) + 2);
+                        }
+                        if (g.has_zrays) {  // z-dominant rows: the exact gather (siddon.cu, zonly)
+                            const double dA = g.colstep[c].y;
+                            const double cv = 0.5 * (g.nv - 1), r = dA / g.du;
+                            int lo = max(v0, int(ceil(cv - r)) - 1), hi = min(v1, int(floor(cv + r)) + 1);
+                            while (lo <= hi && fabs(row_coord(g, lo)) > dA) ++lo;
+                            while (hi >= lo && fabs(row_coord(g, hi)) > dA) --hi;
+                            v0 = lo;
+                            v1 = hi;
+                        }
+                        const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
+                        const size_t qs = size_t(g.nu);
+                        float* zc = Z + z_col(t);
+                        float* zc2 = Z2 + z_col(t);
+                        float Whi, Wr;
+                        z_split(g, G, Whi, Wr);
+                        const float Wd = z_cross(g, c64), aWd = __frcp_rn(fabsf(Wd)), fcs = sid_fc(g);
+                        const float Wa = fmaf(kf - 0.5f, Wd, Wr), Wb = fmaf(kf + 0.5f, Wd, Wr);
+                        const int koff = sid_izc(g) - kSplitBias - kg0;
+                        // one row: its z cells and four weights, the forward's expressions
+                        auto row_w = [&](int iv, int& kl, float& a0, float& a1, float& b0, float& b1) {
+                            const float vr = vrtab[iv];
+                            const float S = fmaf(vr, Whi, fcs);
+                            const float tta = split_t(fmaf(vr, Wa, S)), ttb = split_t(fmaf(vr, Wb, S));
+                            const float fza = fmaf(vr, Wa, fmaf(__fsub_rn(tta, kSplitM), -1.f, S));
+                            const int ka = __float_as_int(tta) + koff, kb = __float_as_int(ttb) + koff;
+                            const float dz = vr * Wd;
+                            const float cz = ka != kb ? sid_cross(fza, dz >= 0.f, __frcp_rn(fabsf(vr)) * aWd) : 1.f;
+                            const float m = fminf(cy, cz), M = fmaxf(cy, cz);
+                            const float wff = m, wfs = cy - m, wsf = cz - m, wss = 1.f - M;
+                            const bool lowfirst = ka <= kb;
+                            kl = min(ka, kb);
+                            a0 = lowfirst ? wff : wfs;
+                            a1 = lowfirst ? wfs : wff;
+                            b0 = lowfirst ? wsf : wss;
+                            b1 = lowfirst ? wss : wsf;
+                        };
+                        auto zero_rows = [&](int lo, int hi) {
+                            for (int m = max(lo, 0); m < min(hi, BP_KB); ++m) zc[m * ZS] = zc2[m * ZS] = 0.f;
+                        };
+                        if (gs > 0.f && v0 <= v1) {
+                            // the rolling march of the Joseph pass, two Z columns
+                            const float rg = invdu / gs;
+                            int kl0;
+                            float u0, u1, u2, u3;
+                            row_w(v0, kl0, u0, u1, u2, u3);
+                            zero_rows(0, rg >= 0.75f ? kl0 : BP_KB);
+                            int cur = -(1 << 20);
+                            float A = 0.f, B = 0.f, C = 0.f, D = 0.f;
+                            for (int iv = v0; iv <= v1; ++iv) {
+                                const float yv = __ldg(reinterpret_cast<const float*>(pc4 + (iv >> 2) * qs) + (iv & 3));
+                                int kk;
+                                float a0, a1, b0, b1;
+                                row_w(iv, kk, a0, a1, b0, b1);
+                                const int adv = kk - cur;
+                                float ak = adv == 1 ? B : 0.f, ck = adv == 1 ? D : 0.f;
+                                ak = adv == 0 ? A : ak;
+                                ck = adv == 0 ? C : ck;
+                                const float bk = adv == 0 ? B : 0.f, dk = adv == 0 ? D : 0.f;
+                                A = fmaf(a0, yv, ak);
+                                B = fmaf(a1, yv, bk);
+                                C = fmaf(b0, yv, ck);
+                                D = fmaf(b1, yv, dk);
+                                cur = kk;
+                                const unsigned r = min(unsigned(kk + BP_ZG), unsigned(BP_KB + 2 * BP_ZG - 2));
+                                float* zp = zc - BP_ZG * ZS + r * ZS;
+                                float* zp2 = zc2 - BP_ZG * ZS + r * ZS;
+                                zp[0] = A;
+                                zp[ZS] = B;
+                                zp2[0] = C;
+                                zp2[ZS] = D;
+                            }
+                            zero_rows(cur + 2, BP_KB);
+                        } else {
+                            zero_rows(0, BP_KB);
+                            for (int iv = v0; iv <= v1; ++iv) {
+                                const float yv = __ldg(reinterpret_cast<const float*>(pc4 + (iv >> 2) * qs) + (iv & 3));
+                                int kk;
+                                float a0, a1, b0, b1;
+                                row_w(iv, kk, a0, a1, b0, b1);
+                                if (unsigned(kk) < unsigned(BP_KB)) {
+                                    zc[kk * ZS] = fmaf(a0, yv, zc[kk * ZS]);
+                                    zc2[kk * ZS] = fmaf(b0, yv, zc2[kk * ZS]);
+                                }
+                                if (unsigned(kk + 1) < unsigned(BP_KB)) {
+                                    zc[(kk + 1) * ZS] = fmaf(a1, yv, zc[(kk + 1) * ZS]);
+                                    zc2[(kk + 1) * ZS] = fmaf(b1, yv, zc2[(kk + 1) * ZS]);
+                                }
+                            }
+                        }
+                        // register: row ja reads Z (entry 2t), row jb != ja reads Z2 (entry 2t+1)
+                        if (ja >= p0 && ja <= p0 + BP_PB - 1 && ja >= 0 && ja < nh) {
+                            const int sl = atomicAdd(&cnt[ja - p0], 1);
+                            if (sl < BP_SL) lists[(ja - p0) * BP_SL + sl] = (t << 1);
+                        }
+                        if (jb != ja && jb >= p0 && jb <= p0 + BP_PB - 1 && jb >= 0 && jb < nh) {
+                            const int sl = atomicAdd(&cnt[jb - p0], 1);
+                            if (sl < BP_SL) lists[(jb - p0) * BP_SL + sl] = (t << 1) | 1;
+                        }
+                    }
+                } else {
                     const float4 cd = g.col[c];
                     const double4 c64 = g.col64[c];
                     int ih, ihA;
@@ -319,13 +422,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             // only the rows before the first / after the last k need zeroing;
                             // sparser columns zero the whole band first.
                             const float rg = invdu / gs;
-#if CTK_BP_TIGHT
-                            // trim the estimated row range to the rows whose z stencil meets the
-                            // band (kk in [-1, BP_KB-1]), with the exact arithmetic of the march:
-                            // rows outside only reach the guard rows
-                            while (v0 < v1 && row_k(v0, tf_unused) < -1) ++v0;
-                            while (v1 > v0 && row_k(v1, tf_unused) > BP_KB - 1) --v1;
-#endif
                             if (rg >= 0.75f) {
                                 zero_rows(0, row_k(v0, tf_unused));
                             } else {
@@ -401,22 +497,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             }
                         }
                         eth[t] = th;
-#if CTK_BP_PAIR
-                        // rows rel (weight 1-th) and rel+1 (weight th), relative to p0 (even):
-                        // mode 0 = both rows of pair rel/2, 1 = row rel as the .y of its pair,
-                        // 2 = row rel+1 as the .x of its pair
-                        auto reg = [&](int pr, int mode) {
-                            const int sl = atomicAdd(&cnt[pr], 1);
-                            if (sl < BP_SL) lists[pr * BP_SL + sl] = (t << 2) | mode;
-                        };
-                        const int rel = ih - p0;
-                        if (!(rel & 1)) {
-                            reg(rel >> 1, 0);
-                        } else {
-                            if (rel >= 0) reg(rel >> 1, 1);
-                            if (rel + 1 <= BP_PB - 1 && th != 0.f) reg((rel + 1) >> 1, 2);
-                        }
-#else
                         if (ih >= p0) {
                             const int sl = atomicAdd(&cnt[ih - p0], 1);
                             if (sl < BP_SL) lists[(ih - p0) * BP_SL + sl] = (t << 1);
@@ -425,59 +505,11 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             const int sl = atomicAdd(&cnt[ih + 1 - p0], 1);
                             if (sl < BP_SL) lists[(ih + 1 - p0) * BP_SL + sl] = (t << 1) | 1;
                         }
-#endif
                     }
+                }
                 }
             }
             __syncthreads();
-#if CTK_BP_PAIR
-            // ---- phase 2: row pair r2 gathers its registered columns in column order ----
-            const int n = cnt[r2];
-            if (n > 0 && p0 + 2 * r2 < nh) {
-                if (n <= BP_SL) {
-                    int lst[BP_SL];
-#pragma unroll
-                    for (int q = 0; q < BP_SL; ++q) lst[q] = q < n ? lists[r2 * BP_SL + q] : 0x7fffffff;
-                    // insertion sort of the n registered entries (n is small: 3-6 typically)
-#pragma unroll
-                    for (int i = 1; i < BP_SL; ++i) {
-                        if (i >= n) break;
-#pragma unroll
-                        for (int j = i; j > 0; --j)
-                            if (lst[j - 1] > lst[j]) { const int tmp = lst[j]; lst[j] = lst[j - 1]; lst[j - 1] = tmp; }
-                    }
-#pragma unroll
-                    for (int q = 0; q < BP_SL; ++q) {
-                        if (q >= n) break;
-                        const int e = lst[q] >> 2, mode = lst[q] & 3;
-                        const float th = eth[e], omt = 1.f - th;
-                        const float2 w2 = mode == 0 ? make_float2(omt, th) : (mode == 1 ? make_float2(0.f, omt) : make_float2(th, 0.f));
-                        add_entry2(w2, e);
-                    }
-                } else {
-                    // overflow (very fine detector sampling): scan every slot of the batch in order
-                    const int pa = p0 + 2 * r2;
-                    for (int e = 0; e < BP_PB; ++e) {
-                        const int c = slotcol[e];
-                        if (c < 0 || g.colaxis[c] != CLASS) continue;
-                        int ih, ihA;
-                        float th, thA;
-                        double G;
-                        slice_anchor(g.col64[c], sc, ihA, thA, G);
-                        split(fmaf(kf, g.col[c].y, thA), ih, th);
-                        ih += ihA;
-                        if (ih + 1 < p0 || ih > p0 + BP_PB - 1 || ih + 1 < 0 || ih >= nh) continue;  // not registered
-                        const float omt = 1.f - th;
-                        float2 w2;
-                        if (ih == pa) w2 = make_float2(omt, th);
-                        else if (ih == pa + 1) w2 = make_float2(0.f, omt);
-                        else if (ih + 1 == pa && th != 0.f) w2 = make_float2(th, 0.f);
-                        else continue;
-                        add_entry2(w2, e);
-                    }
-                }
-            }
-#else
             // ---- phase 2: row p gathers its registered columns in column order ----
             const int n = cnt[t];
             if (n > 0 && p < nh) {
@@ -498,15 +530,34 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         if (q >= n) break;
                         const int e = lst[q] >> 1;
                         CTK_CHK(g, e < BP_PB, 3);
-                        const float th = eth[e];
-                        const float wh = (lst[q] & 1) ? th : 1.f - th;
-                        add_entry(wh, e);
+                        if constexpr (SID) {
+                            add_sid((lst[q] & 1) ? Z2 : Z, e);
+                        } else {
+                            const float th = eth[e];
+                            const float wh = (lst[q] & 1) ? th : 1.f - th;
+                            add_entry(wh, e);
+                        }
                     }
                 } else {
                     // overflow (very fine detector sampling): scan every slot of the batch in order
                     for (int e = 0; e < BP_PB; ++e) {
                         const int c = slotcol[e];
                         if (c < 0 || g.colaxis[c] != CLASS) continue;
+                        if constexpr (SID) {
+                            int jA, ja, jb;
+                            float tA, fy;
+                            double G;
+                            sid_anchor(g.col64[c], sc, jA, tA, G);
+                            split(fmaf(kf - 0.5f, g.col[c].y, tA), ja, fy);
+                            split(fmaf(kf + 0.5f, g.col[c].y, tA), jb, fy);
+                            ja += jA;
+                            jb += jA;
+                            if (jlo_ok(ja, jb)) {
+                                if (ja == p) add_sid(Z, e);
+                                if (jb != ja && jb == p) add_sid(Z2, e);
+                            }
+                            continue;
+                        }
                         int ih, ihA;
                         float th, thA;
                         double G;
@@ -521,27 +572,9 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                     }
                 }
             }
-#endif
             __syncthreads();
         }
     }
-#if CTK_BP_PAIR
-#pragma unroll
-    for (int h2 = 0; h2 < 2; ++h2) {
-        const int pr = p0 + 2 * r2 + h2;
-        if (pr >= nh) break;
-#pragma unroll
-        for (int m = 0; m < BP_KB / 2; ++m) {
-            const int k = k0 + kz0 + m;
-            if (k >= g.nz) break;
-            const size_t o = CLASS ? size_t(pr) + size_t(g.nx) * (size_t(s) + size_t(g.ny) * k)
-                                   : size_t(s) + size_t(g.nx) * (size_t(pr) + size_t(g.ny) * k);
-            const float am = h2 ? acc2[m].y : acc2[m].x;
-            if (CLASS == 0) x[o] = am;
-            else x[o] += am;
-        }
-    }
-#else
     if (p < nh) {
 #pragma unroll
         for (int m = 0; m < BP_KB; ++m) {
@@ -555,7 +588,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
             else x[o] += am;
         }
     }
-#endif
 }
 
 __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x) {
@@ -752,15 +784,16 @@ void group_proj(Geometry& g, const float* y, cudaStream_t s) {
     after_launch("k_proj_group4");
 }
 
-template <int CLASS, int PB>
+template <int CLASS, int PB, int SID>
 void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
     const int nh = CLASS ? g.nx : g.ny;
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz_local() + BP_KB - 1) / BP_KB;
-    constexpr int NL = CTK_BP_PAIR ? PB / 2 : PB;
-    const size_t smem = sizeof(float) * (size_t(z_stride<PB>()) * (BP_KB + 2 * BP_ZG) + size_t(NL) * BP_SL + NL + BP_PB +
+    constexpr int NL = PB;
+    const size_t smem = sizeof(float) * (size_t(z_stride<PB>()) * (BP_KB + 2 * BP_ZG) * (SID ? 2 : 1) +
+                                         size_t(NL) * BP_SL + NL + BP_PB +
                                          4 * size_t(pg_groups(g.nv))) +
                         sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
@@ -770,12 +803,12 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     int dev = 0;
     CTK_CUDA(cudaGetDevice(&dev));
     std::call_once(opted[dev & 63], [] {
-        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB, SID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
     });
     dim3 grd(unsigned(planes), unsigned(ptiles * kbands));
-    k_atb_plane_f32<CLASS, PB><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
-    after_launch("k_atb_plane_f32");
+    k_atb_plane_f32<CLASS, PB, SID><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
+    after_launch(SID ? "k_atb_plane_f32_siddon" : "k_atb_plane_f32");
 }
 
 template <int CLASS>
@@ -786,8 +819,14 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
         return e ? std::atoi(e) : 0;
     }();
     const int pb = forced == 128 || forced == 256 ? forced : (nh <= 768 ? 128 : 256);
-    if (pb == 128) launch_plane_pb<CLASS, 128>(g, x, s);
-    else launch_plane_pb<CLASS, 256>(g, x, s);
+    const bool sid = g.projector == CTK_PROJ_SIDDON;
+    if (pb == 128) {
+        if (sid) launch_plane_pb<CLASS, 128, 1>(g, x, s);
+        else launch_plane_pb<CLASS, 128, 0>(g, x, s);
+    } else {
+        if (sid) launch_plane_pb<CLASS, 256, 1>(g, x, s);
+        else launch_plane_pb<CLASS, 256, 0>(g, x, s);
+    }
 }
 
 template <int KZ>
@@ -808,7 +847,9 @@ void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
     launch_plane<0>(g, x, s);
     launch_plane<1>(g, x, s);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
-    if (g.has_zrays) {
+    if (g.has_zrays && g.projector == CTK_PROJ_SIDDON) {
+        siddon_atb_zrays_f32(g, y, x, s);  // exact gather of the z-dominant rays, accumulated
+    } else if (g.has_zrays) {
         const size_t n = g.domain();
         k_atb_matched_zrays_f32<<<unsigned((n + 127) / 128), 128, 0, s>>>(g.kgeom(), g.proj_t.as<float>(), x);
         after_launch("k_atb_matched_zrays_f32");

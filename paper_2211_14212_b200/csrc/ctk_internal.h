@@ -139,6 +139,8 @@ template <class T>
 void op_atb(Geometry& g, int variant, const T* y, T* x, cudaStream_t s);
 
 // Siddon exact-length projector and its transpose (siddon.cu, --fmad=false)
+void siddon_ax_zrays_f32(const Geometry& g, const float* x, float* y, cudaStream_t s);
+void siddon_atb_zrays_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
 template <class T>
 void siddon_ax(const Geometry& g, const T* x, T* y, cudaStream_t s);
 template <class T>

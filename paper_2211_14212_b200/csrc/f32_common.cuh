@@ -225,5 +225,34 @@ __device__ __forceinline__ float row_vr(const KGeom& g, int iv) { return float(i
 __device__ __forceinline__ int cz_int(const KGeom& g) { return (g.nzg - 1) >> 1; }
 __device__ __forceinline__ float cz_frac(const KGeom& g) { return ((g.nzg - 1) & 1) ? 0.5f : 0.f; }
 
+// ---- f32 Siddon model (fwd_f32.cu SID = 1, bp_f32.cu SID = 1) ---------------------------
+// Siddon's weight of (ray, voxel) is the ray's length inside the voxel box.  Split the ray by
+// the slabs of its dominant axis A: slab s spans the boundaries s - 1/2 and s + 1/2 (voxel
+// centres at s), and the ray covers length L = h |d| / |d_A| (= ray_step) in every slab.
+// Inside a slab the in-plane cell coordinate Y = fh + 1/2 and the z cell coordinate
+// Z = fz + 1/2 are linear in the slab parameter t in [0, 1] (t = 0 at s - 1/2) and move by
+// |fhd| <= 1 and |vr Wd| <= 1 (not z-dominant), so the slab's chord crosses at most one
+// y and one z cell boundary.  With (ja, ka) the cells at t = 0 and cy, cz in [0, 1] the
+// parameters of the crossings (1 if none), the four cells' weights are
+//    (ja, ka): min(cy, cz)         (ja, ka + sz): cy - min(cy, cz)
+//    (ja + sy, ka): cz - min       (ja + sy, ka + sz): 1 - max(cy, cz)
+// (sy, sz = +-1 the directions of motion), times L.  Positions at t = 0 use the anchored
+// f32 model above with the +1/2 cell shift folded into the fp64 anchors, so the forward and
+// the transpose evaluate identical expressions (bit-identical weights).  Summed over slabs
+// this is exactly the 3-D box chord of tests/oracles.hpp:89-107 per voxel.
+__device__ __forceinline__ void sid_anchor(const double4& c, int sc, int& jA, float& tA, double& G) {
+    dsplit(__dadd_rn(__fma_rn(double(sc), c.y, c.x), 0.5), jA, tA);
+    G = __fma_rn(double(sc), c.w, c.z);
+}
+// z cell coordinate Z = fz + 1/2 = izs + fcs + vr W
+__device__ __forceinline__ int sid_izc(const KGeom& g) { return g.nzg >> 1; }
+__device__ __forceinline__ float sid_fc(const KGeom& g) { return (g.nzg & 1) ? 0.5f : 0.f; }
+// crossing parameter of a cell coordinate with fraction f moving by d per slab (ad = 1/|d|):
+// distance to the next boundary in the direction of motion, in units of the slab
+__device__ __forceinline__ float sid_cross(float f, bool inc, float ad) {
+    const float gap = inc ? 1.f - f : f;
+    return fminf(fmaxf(gap * ad, 0.f), 1.f);  // fmaxf(NaN, 0) = 0: a zero gap with ad = inf
+}
+
 }  // namespace
 }  // namespace ctkb

@@ -68,11 +68,120 @@ __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict
     }
 }
 
+// Siddon sum of one ray over its slabs (f32_common.cuh), before the factor L = ray_step:
+// sum over slabs of min(cy,cz) v(ja,ka) + (cy-min) v(ja,ka+sz) + (cz-min) v(ja+sy,ka)
+// + (1-max) v(ja+sy,ka+sz), with (ja, ka) the cells at the slab's s - 1/2 boundary.
+template <class Off>
+__device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int nh, int ns, const float* base, Off pz,
+                            Off plane, float vd, float czf, float vr, int nch, int chunk) {
+    const float Wd = z_cross(g, c64), fcs = sid_fc(g);
+    const int izs = sid_izc(g);
+    const float dz = vr * Wd;
+    const bool incy = fhd >= 0.f, incz = dz >= 0.f;
+    // 1/|fhd| and 1/|vr Wd| = (1/|vr|)(1/|Wd|), as the transpose forms them
+    const float ay = __frcp_rn(fabsf(fhd)), az = __frcp_rn(fabsf(vr)) * __frcp_rn(fabsf(Wd));
+    using U = typename std::conditional<sizeof(Off) == 4, unsigned, unsigned long long>::type;
+    const U upz = U(pz), uplane = U(plane);
+    // cells (j, k) at the slab's t = 0 boundary, the expressions of the transpose
+    auto cell0 = [&](int s, int& j, int& k) {
+        const int sc = slice_centre(s);
+        int jA, jr;
+        float tA, Whi, Wr, fy;
+        double G;
+        sid_anchor(c64, sc, jA, tA, G);
+        z_split(g, G, Whi, Wr);
+        const float kb = float(s - sc) - 0.5f;
+        split(fmaf(kb, fhd, tA), jr, fy);
+        const float tt = split_t(fmaf(vr, fmaf(kb, Wd, Wr), fmaf(vr, Whi, fcs)));
+        j = jA + jr;
+        k = izs + (__float_as_int(tt) - kSplitBias) - g.z0;
+    };
+    // a slab contributes iff a cell is inside: j in [-1, nh] and k in [-1, nz] (the other
+    // cell is then within the two guard planes); find the interval like the Joseph march
+    auto inside = [&](int s) {
+        int j, k;
+        cell0(s, j, k);
+        return j >= -1 && j <= nh && k >= -1 && k <= g.nz;
+    };
+    int s0 = 0, s1 = ns - 1;
+    clip_affine(c64.x + 0.5 - 0.5 * c64.y, c64.y, -1.0, nh + 1.0, s0, s1);
+    clip_affine(double(vd) * (c64.z - 0.5 * c64.w) + czf + 0.5 - g.z0, double(vd) * c64.w, -1.0, g.nz + 1.0, s0, s1);
+    while (s0 <= s1 && !inside(s0)) ++s0;
+    while (s1 >= s0 && !inside(s1)) --s1;
+    if (s0 <= s1) {
+        while (s0 > 0 && inside(s0 - 1)) --s0;
+        while (s1 < ns - 1 && inside(s1 + 1)) ++s1;
+    }
+    if (nch > 1) {
+        const int len = (ns + nch - 1) / nch;
+        s0 = max(s0, chunk * len);
+        s1 = min(s1, chunk * len + len - 1);
+    }
+#ifdef CTK_CHECKED
+    const long long lay_n = (long long)ns * (long long)plane, base_abs = (long long)(kPad * pz + kPad);
+#endif
+    float acc = 0.f;
+    for (int s = s0; s <= s1;) {  // slice blocks: fp64 anchors once per block
+        const int sc = slice_centre(s);
+        const int se = min(s1, sc + kSB / 2 - 1);
+        int jA;
+        float tA, Whi, Wr;
+        double G;
+        sid_anchor(c64, sc, jA, tA, G);
+        z_split(g, G, Whi, Wr);
+        const float S = fmaf(vr, Whi, fcs);  // exact
+        // offsets from the raw bits of the split sums (j + bias, k + bias), in modular arithmetic
+        const U rb = U(Off(jA)) * upz + U(Off(izs - g.z0)) - U(kSplitBias) * (upz + 1u);
+        // a boundary at slab parameter kb (relative to sc): cell bits and fractions
+        auto bnd = [&](float kb, float& ty, float& fy, float& tt, float& fz) {
+            const float fyr = fmaf(kb, fhd, tA);
+            ty = split_t(fyr);
+            fy = split_frac(fyr, ty);
+            const float wlo = fmaf(kb, Wd, Wr);
+            tt = split_t(fmaf(vr, wlo, S));
+            fz = fmaf(vr, wlo, fmaf(__fsub_rn(tt, kSplitM), -1.f, S));
+        };
+        float kb = float(s - sc) - 0.5f;
+        float tya, fya, tta, fza;
+        bnd(kb, tya, fya, tta, fza);  // the first slab's t = 0 boundary
+#pragma unroll 2
+        for (; s <= se; ++s) {
+            kb += 1.f;
+            float tyb, fyb, ttb, fzb;
+            bnd(kb, tyb, fyb, ttb, fzb);  // t = 1 boundary = the next slab's t = 0
+            const int dj = __float_as_int(tyb) - __float_as_int(tya), dk = __float_as_int(ttb) - __float_as_int(tta);
+            const float cy = dj ? sid_cross(fya, incy, ay) : 1.f, cz = dk ? sid_cross(fza, incz, az) : 1.f;
+            const float m = fminf(cy, cz), M = fmaxf(cy, cz);
+            Off o = Off(U(s) * uplane + rb + U(unsigned(__float_as_int(tya))) * upz + U(unsigned(__float_as_int(tta))));
+#ifdef CTK_CHECKED
+            if (base_abs + (long long)o - 2 * (long long)pz - 2 < 0 || base_abs + (long long)o + 2 * (long long)pz + 2 >= lay_n) {
+                atomicOr(g.chk, 1u << 0);
+                o = Off(2 * pz + 2 - base_abs);
+            }
+#endif
+            const float* q = base + o;
+            const Off oy = Off(dj) * pz;
+            const float v00 = __ldg(q), v01 = __ldg(q + dk), v10 = __ldg(q + oy), v11 = __ldg(q + oy + dk);
+            acc = fmaf(m, v00, acc);       // (ja, ka)
+            acc = fmaf(cy - m, v01, acc);  // (ja, kb)
+            acc = fmaf(cz - m, v10, acc);  // (jb, ka)
+            acc = fmaf(1.f - M, v11, acc); // (jb, kb)
+            tya = tyb;
+            fya = fyb;
+            tta = ttb;
+            fza = fzb;
+        }
+    }
+    return acc;
+}
+
 // MODE 0: y = A x.   MODE 1: per-block partial of sum (A x - b)^2 (y never stored).
 // nch > 1 (MODE 0 only): slice chunking for L2 locality -- one launch per chunk of the
 // slices, in chunk order; chunk 0 writes y and later chunks add their partial sums to it
 // (deterministic: the launches are ordered on the stream).
-template <int MODE, class Off>
+// SID = 1: the f32 Siddon model (f32_common.cuh) on the same layouts: per slab the four
+// cells (ja|ja+sy, ka|ka+sz) of the chord instead of the four bilinear taps.
+template <int MODE, class Off, int SID = 0>
 __global__ void __launch_bounds__(ZW_BR * ZW_BC)
 k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
                const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
@@ -89,7 +198,9 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
         const double2 cs = g.colstep[c];
         const double v = row_coord(g, iv);
         if (g.has_zrays && is_zray(g, cs, v)) {
-            if (chunk == 0) {  // z-rays are marched whole by the first chunk
+            if (SID) {
+                // Siddon z-rays: the exact DDA (siddon.cu, zonly) fills them after this launch
+            } else if (chunk == 0) {  // z-rays are marched whole by the first chunk
                 const double2 tr = g.ctst[a];
                 WalkF w;
                 walk_generic(g, tr.x, tr.y, iu, iv, w);
@@ -108,6 +219,10 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             const float vd = float(v);
             const float czf = 0.5f * float(g.nzg - 1);  // global z centre; slab slices start at z0
             const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            if constexpr (SID) {
+                out = siddon_ray(g, c64, cd.y, nh, ns, base, pz, plane, vd, czf, row_vr(g, iv), nch, chunk) *
+                      ray_step(g, cs, v);
+            } else {
             // anchored positions (f32_common.cuh): per slice block the fp64 anchors, per lane
             // the exact row term S
             const float Wd = z_cross(g, c64), vr = row_vr(g, iv), fc = cz_frac(g);
@@ -244,6 +359,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
             acc += acc2.x + acc2.y;
             const float stp = ray_step(g, cs, v);
             out = stp * acc;
+            }
         }
     }
     if (MODE == 0) {
@@ -303,10 +419,14 @@ void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* pa
     dim3 grd = fwd_grid(g);
     if (band1 >= 0) grd.z = unsigned(band1 - band0);
     if (grd.z == 0) return;
-    if (wide_offsets(g))
-        k_ax_zfast_f32<MODE, long long><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
-    else
-        k_ax_zfast_f32<MODE, int><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
+    const bool sid = g.projector == CTK_PROJ_SIDDON;
+    if (wide_offsets(g)) {
+        if (sid) k_ax_zfast_f32<MODE, long long, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
+        else k_ax_zfast_f32<MODE, long long><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
+    } else {
+        if (sid) k_ax_zfast_f32<MODE, int, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
+        else k_ax_zfast_f32<MODE, int><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
+    }
     after_launch(MODE == 0 ? "k_ax_zfast_f32" : "k_ax_zfast_f32_residual");
 }
 
@@ -379,10 +499,12 @@ void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
         CTK_CUDA(cudaMemsetAsync(y, 0, g.range() * sizeof(float), s));  // rows no launched band writes
     for (int c = 0; c < nch; ++c) launch_ax<0>(g, x, y, nullptr, nullptr, s, nch, c, b0, b1);
     CTK_CUDA(cudaEventRecord(g.ev1, s));
+    // Siddon: the z-dominant rays take the exact DDA (siddon.cu), writing only their entries
+    if (g.projector == CTK_PROJ_SIDDON && g.has_zrays) siddon_ax_zrays_f32(g, x, y, s);
 }
 
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {
-    if (fwd_chunks(g) > 1) {  // chunked: A x into a scratch projection set, then the fused difference norm
+    if (fwd_chunks(g) > 1 || g.projector == CTK_PROJ_SIDDON) {  // chunked: A x into a scratch projection set, then the fused difference norm
         g.ax_scratch.ensure(g.range() * sizeof(float));
         ax_f32(g, x, g.ax_scratch.as<float>(), s);
         RedWork w = red_work(&g);

@@ -38,12 +38,12 @@ static void check_bounds(Geometry& g, cudaStream_t s, const char* what) {
 template <class T>
 void op_ax(Geometry& g, const T* x, T* y, cudaStream_t s) {
     require_slab_support<T>(g);
-    if (g.projector == CTK_PROJ_SIDDON) {
+    if constexpr (sizeof(T) == 4) {
+        ax_f32(g, x, y, s);  // Joseph or the f32 Siddon slab model; records its own events
+    } else if (g.projector == CTK_PROJ_SIDDON) {
         CTK_CUDA(cudaEventRecord(g.ev0, s));
         siddon_ax<T>(g, x, y, s);
         CTK_CUDA(cudaEventRecord(g.ev1, s));
-    } else if constexpr (sizeof(T) == 4) {
-        ax_f32(g, x, y, s);  // records its own events around the main kernel
     } else {
         CTK_CUDA(cudaEventRecord(g.ev0, s));
         launch_ax_exact_f64(g, x, y, s);
@@ -56,7 +56,7 @@ template <class T>
 void op_atb(Geometry& g, int variant, const T* y, T* x, cudaStream_t s) {
     if (variant != CTK_BP_MATCHED && variant != CTK_BP_VOXEL_DRIVEN) fail(CTK_E_PARAMETER, "unknown backprojector variant");
     require_slab_support<T>(g);
-    if (variant == CTK_BP_MATCHED && g.projector == CTK_PROJ_SIDDON) {
+    if (variant == CTK_BP_MATCHED && g.projector == CTK_PROJ_SIDDON && sizeof(T) == 8) {
         CTK_CUDA(cudaEventRecord(g.ev0, s));
         siddon_atb<T>(g, y, x, s);
         CTK_CUDA(cudaEventRecord(g.ev1, s));

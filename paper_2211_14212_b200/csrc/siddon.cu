@@ -49,12 +49,15 @@ __device__ __forceinline__ double s_alpha(const SRay& r, int a, int q, int n, do
 
 __device__ __forceinline__ int s_slab(double c, int n, double h) { return int(floor(c / h + 0.5 * n)); }
 
+// zonly: only the rays the f32 slab model leaves out (z-dominant cone rows: |v| > |d_A| of
+// the unnormalised ray, f32_common.cuh is_zray); the others are not written
 template <class T>
-__global__ void k_siddon_ax(KGeom g, const T* __restrict__ vol, T* __restrict__ proj) {
+__global__ void k_siddon_ax(KGeom g, const T* __restrict__ vol, T* __restrict__ proj, int zonly) {
     const int iu = blockIdx.x * blockDim.x + threadIdx.x;
     const int iv = blockIdx.y * blockDim.y + threadIdx.y;
     const int a = blockIdx.z;
     if (iu >= g.nu || iv >= g.nv) return;
+    if (zonly && !(g.mode == CTK_CONE3D && fabs((iv - 0.5 * (g.nv - 1)) * g.du) > g.colstep[a * g.nu + iu].y)) return;
     const double2 cs = g.ctst[a];
     SRay r;
     s_make_ray(g, cs.x, cs.y, iu, iv, r);
@@ -190,9 +193,11 @@ __device__ __forceinline__ bool s_window(const KGeom& g, double ct, double st, c
 #ifndef CTK_SID_MINB
 #define CTK_SID_MINB 6  // 113 -> 80 regs (80 B spill): 58.8 -> 55.4 ms at 256^3/180 (5: 57.4, 8: 56.6)
 #endif
+// zonly: only the z-dominant cone rays (the f32 slab model's complement), accumulated into vol
 template <class T>
 __global__ void __launch_bounds__(128, CTK_SID_MINB) k_siddon_atb(KGeom g, const double* __restrict__ rayinv,
-                                                    const T* __restrict__ pt, T* __restrict__ vol, int kblocks) {
+                                                    const T* __restrict__ pt, T* __restrict__ vol, int kblocks,
+                                                    int zonly) {
     const long wid = long(blockIdx.x) * blockDim.y + threadIdx.y;
     const long ncol = long(g.nx) * g.ny;
     if (wid >= ncol * kblocks) return;
@@ -238,6 +243,7 @@ __global__ void __launch_bounds__(128, CTK_SID_MINB) k_siddon_atb(KGeom g, const
                     const size_t q = size_t(iu) * g.nv + iv;  // [a][iu][iv]
                     const T value = __ldg(fa + q);
                     if (value == T(0)) continue;
+                    if (zonly && !(fabs((iv - 0.5 * (g.nv - 1)) * g.du) > g.colstep[a * g.nu + iu].y)) continue;
                     const double inv[3] = {__ldg(ra + 3 * q), __ldg(ra + 3 * q + 1), __ldg(ra + 3 * q + 2)};
                     double lo = -DBL_MAX, hi = DBL_MAX;
                     bool miss = false;
@@ -289,7 +295,10 @@ __global__ void __launch_bounds__(128, CTK_SID_MINB) k_siddon_atb(KGeom g, const
                 acc += T(hi - lo) * value;
             }
     }
-    if (live) vol[size_t(idx3[0]) + size_t(g.nx) * (size_t(idx3[1]) + size_t(g.ny) * idx3[2])] = acc;
+    if (live) {
+        T* o = vol + size_t(idx3[0]) + size_t(g.nx) * (size_t(idx3[1]) + size_t(g.ny) * idx3[2]);
+        *o = zonly ? *o + acc : acc;
+    }
 }
 
 // y[a][iv][iu] -> pt[a][iu][iv]
@@ -314,12 +323,18 @@ __global__ void k_siddon_transpose(int nu, int nv, const T* __restrict__ y, T* _
 template <class T>
 void siddon_ax(const Geometry& g, const T* x, T* y, cudaStream_t s) {
     dim3 blk(32, 4), grd((g.nu + 31) / 32, (g.nv + 3) / 4, g.na);
-    k_siddon_ax<T><<<grd, blk, 0, s>>>(g.kgeom(), x, y);
+    k_siddon_ax<T><<<grd, blk, 0, s>>>(g.kgeom(), x, y, 0);
     after_launch("k_siddon_ax");
 }
 
+void siddon_ax_zrays_f32(const Geometry& g, const float* x, float* y, cudaStream_t s) {
+    dim3 blk(32, 4), grd((g.nu + 31) / 32, (g.nv + 3) / 4, g.na);
+    k_siddon_ax<float><<<grd, blk, 0, s>>>(g.kgeom(), x, y, 1);
+    after_launch("k_siddon_ax_zrays");
+}
+
 template <class T>
-void siddon_atb(Geometry& g, const T* y, T* x, cudaStream_t s) {
+void siddon_atb_impl(Geometry& g, const T* y, T* x, cudaStream_t s, int zonly) {
     const size_t nrays = g.range();
     if (g.d_rayinv.ensure(3 * nrays * sizeof(double)) || !g.rayinv_ready) {
         dim3 blk(32, 4), grd((g.nu + 31) / 32, (g.nv + 3) / 4, g.na);
@@ -337,9 +352,18 @@ void siddon_atb(Geometry& g, const T* y, T* x, cudaStream_t s) {
     const long warps = long(g.nx) * g.ny * kblocks;
     dim3 blk(32, 4);
     k_siddon_atb<T><<<unsigned((warps + 3) / 4), blk, 0, s>>>(g.kgeom(), g.d_rayinv.as<double>(), g.proj_t.as<T>(), x,
-                                                            kblocks);
-    after_launch("k_siddon_atb");
+                                                            kblocks, zonly);
+    after_launch(zonly ? "k_siddon_atb_zrays" : "k_siddon_atb");
 }
+
+template <class T>
+void siddon_atb(Geometry& g, const T* y, T* x, cudaStream_t s) {
+    siddon_atb_impl<T>(g, y, x, s, 0);
+}
+
+// the f32 slab-model transpose (bp_f32.cu) leaves the z-dominant rays to this exact gather;
+// it overwrites proj_t, so it runs after the plane passes
+void siddon_atb_zrays_f32(Geometry& g, const float* y, float* x, cudaStream_t s) { siddon_atb_impl<float>(g, y, x, s, 1); }
 
 template void siddon_ax<float>(const Geometry&, const float*, float*, cudaStream_t);
 template void siddon_ax<double>(const Geometry&, const double*, double*, cudaStream_t);

@@ -2,8 +2,9 @@
 
 No reference implementation exists, so the checker is the C restatement
 (oracle/ctk_oracle.c), itself pinned by the reference's ray-box chord KAT
-(tests/test_oracle.py::test_siddon_*).  Both precisions are held BIT-EXACT to the
-restatement; the transpose passes the adjoint test; LSQR on the Siddon pair matches the
+(tests/test_oracle.py::test_siddon_*).  f64 is held BIT-EXACT to the restatement; f32 (the
+slab-model kernels that share the Joseph layouts) within 5e-6 of it on signed data; the
+transposes pass the adjoint test; LSQR on the Siddon pair matches the
 numpy solver restatement (pinned against the reference solvers) at config-2 shape."""
 import math
 
@@ -29,7 +30,7 @@ def _pair(ctk, g, dtype):
 
 
 @pytest.mark.parametrize("name", sorted(ALL))
-@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("dtype", [np.float64])
 def test_siddon_bit_exact_vs_restatement(ctk, restated, name, dtype):
     g = ALL[name]()
     rng = np.random.default_rng(3)
@@ -39,6 +40,21 @@ def test_siddon_bit_exact_vs_restatement(ctk, restated, name, dtype):
     pair = _pair(ctk, g, dtype)
     assert np.array_equal(pair.apply_forward(x), restated.siddon_forward(g, x))
     assert np.array_equal(pair.apply_back(y), restated.siddon_back(g, y))
+
+
+@pytest.mark.parametrize("name", sorted(ALL))
+def test_siddon_f32_slab_model_within_1e5(ctk, restated, name):
+    """The f32 Siddon pair (slab decomposition along the dominant axis with anchored f32
+    cell positions, f32_common.cuh; z-dominant rays by the exact DDA / gather) against the
+    f64 restatement, random-signed data (the cancelling inputs LSQR feeds A^T b)."""
+    g = ALL[name]()
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal(g.domain_size)
+    y = rng.standard_normal(g.range_size)
+    pair = _pair(ctk, g, np.float32)
+    ef = rel_l2(pair.apply_forward(x.astype(np.float32)), restated.siddon_forward(g, x))
+    eb = rel_l2(pair.apply_back(y.astype(np.float32)), restated.siddon_back(g, y))
+    assert ef < 5e-6 and eb < 5e-6, (ef, eb)
 
 
 def test_siddon_f32_within_1e5_of_f64(ctk, restated):
