@@ -127,7 +127,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     static_assert((NL * BP_SL) % 4 == 0 && NL % 4 == 0, "keeps vrtab 16-byte aligned");
     const int nv4 = 4 * pg_groups(g.nv);
     float* vrtab = eth + BP_PB;                                 // [nv4] iv - (nv-1)/2, 16-byte aligned
-    int2* urange = reinterpret_cast<int2*>(vrtab + nv4);        // [na]
+    float* ivrtab = vrtab + (SID ? nv4 : 0);                    // Siddon: [nv4] 1/|iv - (nv-1)/2|
+    int2* urange = reinterpret_cast<int2*>(vrtab + (SID ? 2 : 1) * nv4);  // [na]
     int* pref = reinterpret_cast<int*>(urange + g.na);          // [na + 1] candidate prefix sums
     int* slotcol = pref + g.na + 1;                             // [BP_PB] (view, column) of a slot
 
@@ -139,7 +140,10 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const int p0 = ptile * BP_PB, k0 = kband * BP_KB;
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
-    for (int q = t; q < nv4; q += BP_PB) vrtab[q] = row_vr(g, q);
+    for (int q = t; q < nv4; q += BP_PB) {
+        vrtab[q] = row_vr(g, q);
+        if (SID) ivrtab[q] = __frcp_rn(fabsf(row_vr(g, q)));
+    }
     const int sc = slice_centre(s);  // anchored positions (f32_common.cuh): block centre of plane s
     const float kf = float(s - sc);
     const float czf = 0.5f * float(g.nzg - 1);  // global z centre; this handle's slices start at z0
@@ -238,23 +242,23 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                 const int c = a * g.nu + iu;
                 if (g.colaxis[c] == CLASS) {
                 if constexpr (SID) {
-                    // ---- Siddon phase 1 (f32_common.cuh model): the column's cells at the
-                    // plane's two boundaries, ja (t = 0) and jb (t = 1); every row adds its four
-                    // chord weights times (L y) to Z (cell ja) and Z2 (cell jb) at its z cells
-                    // ka, kb -- rolled over (kl, kl + 1), kl = min(ka, kb), non-decreasing in iv
+                    // ---- Siddon phase 1 (f32_common.cuh model): the column's cell ja at the
+                    // plane's t = 0 boundary and jb = ja +- 1 when the chord crosses a y boundary
+                    // (cy < 1); every row adds its four chord weights times (L y) to Z (cell ja)
+                    // and Z2 (cell jb) at its z cells ka, kb -- rolled over (kl, kl + 1),
+                    // kl = min(ka, kb) non-decreasing in iv
                     const float4 cd = g.col[c];
                     const double4 c64 = g.col64[c];
-                    int jA, ja, jb;
-                    float tA, fya, fyb;
+                    int jA, ja;
+                    float tA, fya;
                     double G;
                     sid_anchor(c64, sc, jA, tA, G);
                     split(fmaf(kf - 0.5f, cd.y, tA), ja, fya);
-                    split(fmaf(kf + 0.5f, cd.y, tA), jb, fyb);
                     ja += jA;
-                    jb += jA;
-                    const int jlo = min(ja, jb), jhi = max(ja, jb);
-                    if (jhi >= p0 && jlo <= p0 + BP_PB - 1 && jhi >= 0 && jlo < nh) {
-                        const float cy = ja != jb ? sid_cross(fya, cd.y >= 0.f, __frcp_rn(fabsf(cd.y))) : 1.f;
+                    const bool incy = cd.y >= 0.f;
+                    const float cy = sid_cross(fya, incy, __frcp_rn(fabsf(cd.y)));
+                    const int jb = cy < 1.f ? (incy ? ja + 1 : ja - 1) : ja;
+                    if (jlo_ok(ja, jb)) {
                         const float gs = fmaf(fs, cd.w, cd.z);
                         int v0 = 0, v1 = g.nv - 1;
                         if (gs > 0.f) {
@@ -278,21 +282,22 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         float Whi, Wr;
                         z_split(g, G, Whi, Wr);
                         const float Wd = z_cross(g, c64), aWd = __frcp_rn(fabsf(Wd)), fcs = sid_fc(g);
-                        const float Wa = fmaf(kf - 0.5f, Wd, Wr), Wb = fmaf(kf + 0.5f, Wd, Wr);
+                        const float Wa = fmaf(kf - 0.5f, Wd, Wr);
                         const int koff = sid_izc(g) - kSplitBias - kg0;
                         // one row: its z cells and four weights, the forward's expressions
+                        // (1/|vr| from the shared table = __frcp_rn(|vr|))
                         auto row_w = [&](int iv, int& kl, float& a0, float& a1, float& b0, float& b1) {
                             const float vr = vrtab[iv];
                             const float S = fmaf(vr, Whi, fcs);
-                            const float tta = split_t(fmaf(vr, Wa, S)), ttb = split_t(fmaf(vr, Wb, S));
+                            const float tta = split_t(fmaf(vr, Wa, S));
                             const float fza = fmaf(vr, Wa, fmaf(__fsub_rn(tta, kSplitM), -1.f, S));
-                            const int ka = __float_as_int(tta) + koff, kb = __float_as_int(ttb) + koff;
-                            const float dz = vr * Wd;
-                            const float cz = ka != kb ? sid_cross(fza, dz >= 0.f, __frcp_rn(fabsf(vr)) * aWd) : 1.f;
+                            const int ka = __float_as_int(tta) + koff;
+                            const bool incz = vr * Wd >= 0.f;
+                            const float cz = sid_cross(fza, incz, ivrtab[iv] * aWd);
                             const float m = fminf(cy, cz), M = fmaxf(cy, cz);
                             const float wff = m, wfs = cy - m, wsf = cz - m, wss = 1.f - M;
-                            const bool lowfirst = ka <= kb;
-                            kl = min(ka, kb);
+                            const bool lowfirst = incz || !(cz < 1.f);  // ka <= kb
+                            kl = lowfirst ? ka : ka - 1;
                             a0 = lowfirst ? wff : wfs;
                             a1 = lowfirst ? wfs : wff;
                             b0 = lowfirst ? wsf : wss;
@@ -302,16 +307,18 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             for (int m = max(lo, 0); m < min(hi, BP_KB); ++m) zc[m * ZS] = zc2[m * ZS] = 0.f;
                         };
                         if (gs > 0.f && v0 <= v1) {
-                            // the rolling march of the Joseph pass, two Z columns
+                            // the rolling march of the Joseph pass over whole 4-row groups (rows
+                            // outside [v0, v1] masked to zero), two Z columns
                             const float rg = invdu / gs;
+                            const int q0 = v0 >> 2, q1 = v1 >> 2;
+                            CTK_CHK(g, q0 >= 0 && q1 < nq, 1);
                             int kl0;
                             float u0, u1, u2, u3;
-                            row_w(v0, kl0, u0, u1, u2, u3);
+                            row_w(4 * q0, kl0, u0, u1, u2, u3);
                             zero_rows(0, rg >= 0.75f ? kl0 : BP_KB);
                             int cur = -(1 << 20);
                             float A = 0.f, B = 0.f, C = 0.f, D = 0.f;
-                            for (int iv = v0; iv <= v1; ++iv) {
-                                const float yv = __ldg(reinterpret_cast<const float*>(pc4 + (iv >> 2) * qs) + (iv & 3));
+                            auto rowstep = [&](int iv, float yv) {
                                 int kk;
                                 float a0, a1, b0, b1;
                                 row_w(iv, kk, a0, a1, b0, b1);
@@ -332,7 +339,23 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 zp[ZS] = B;
                                 zp2[0] = C;
                                 zp2[ZS] = D;
-                            }
+                            };
+                            auto group = [&](int q, float4 y4, bool mask) {
+                                const int b = 4 * q;
+                                if (mask) {
+                                    y4.x = (b >= v0 && b <= v1) ? y4.x : 0.f;
+                                    y4.y = (b + 1 >= v0 && b + 1 <= v1) ? y4.y : 0.f;
+                                    y4.z = (b + 2 >= v0 && b + 2 <= v1) ? y4.z : 0.f;
+                                    y4.w = (b + 3 >= v0 && b + 3 <= v1) ? y4.w : 0.f;
+                                }
+                                rowstep(b, y4.x);
+                                rowstep(b + 1, y4.y);
+                                rowstep(b + 2, y4.z);
+                                rowstep(b + 3, y4.w);
+                            };
+                            group(q0, __ldg(pc4 + q0 * qs), true);
+                            for (int q = q0 + 1; q < q1; ++q) group(q, __ldg(pc4 + q * qs), false);
+                            if (q1 > q0) group(q1, __ldg(pc4 + q1 * qs), true);
                             zero_rows(cur + 2, BP_KB);
                         } else {
                             zero_rows(0, BP_KB);
@@ -544,14 +567,15 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         const int c = slotcol[e];
                         if (c < 0 || g.colaxis[c] != CLASS) continue;
                         if constexpr (SID) {
-                            int jA, ja, jb;
+                            int jA, ja;
                             float tA, fy;
                             double G;
+                            const float fhd = g.col[c].y;
                             sid_anchor(g.col64[c], sc, jA, tA, G);
-                            split(fmaf(kf - 0.5f, g.col[c].y, tA), ja, fy);
-                            split(fmaf(kf + 0.5f, g.col[c].y, tA), jb, fy);
+                            split(fmaf(kf - 0.5f, fhd, tA), ja, fy);
                             ja += jA;
-                            jb += jA;
+                            const float cy = sid_cross(fy, fhd >= 0.f, __frcp_rn(fabsf(fhd)));
+                            const int jb = cy < 1.f ? (fhd >= 0.f ? ja + 1 : ja - 1) : ja;
                             if (jlo_ok(ja, jb)) {
                                 if (ja == p) add_sid(Z, e);
                                 if (jb != ja && jb == p) add_sid(Z2, e);
@@ -794,7 +818,7 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     constexpr int NL = PB;
     const size_t smem = sizeof(float) * (size_t(z_stride<PB>()) * (BP_KB + 2 * BP_ZG) * (SID ? 2 : 1) +
                                          size_t(NL) * BP_SL + NL + BP_PB +
-                                         4 * size_t(pg_groups(g.nv))) +
+                                         4 * size_t(pg_groups(g.nv)) * (SID ? 2 : 1)) +
                         sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     // opt in once to the largest size this launcher accepts (occupancy follows the size of

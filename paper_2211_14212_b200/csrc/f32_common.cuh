@@ -233,7 +233,8 @@ __device__ __forceinline__ float cz_frac(const KGeom& g) { return ((g.nzg - 1) &
 // Z = fz + 1/2 are linear in the slab parameter t in [0, 1] (t = 0 at s - 1/2) and move by
 // |fhd| <= 1 and |vr Wd| <= 1 (not z-dominant), so the slab's chord crosses at most one
 // y and one z cell boundary.  With (ja, ka) the cells at t = 0 and cy, cz in [0, 1] the
-// parameters of the crossings (1 if none), the four cells' weights are
+// parameters of the crossings (the distance to the next boundary in the direction of
+// motion over the distance moved, clamped: 1 = no crossing), the four cells' weights are
 //    (ja, ka): min(cy, cz)         (ja, ka + sz): cy - min(cy, cz)
 //    (ja + sy, ka): cz - min       (ja + sy, ka + sz): 1 - max(cy, cz)
 // (sy, sz = +-1 the directions of motion), times L.  Positions at t = 0 use the anchored

@@ -80,6 +80,7 @@ __device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int n
     const bool incy = fhd >= 0.f, incz = dz >= 0.f;
     // 1/|fhd| and 1/|vr Wd| = (1/|vr|)(1/|Wd|), as the transpose forms them
     const float ay = __frcp_rn(fabsf(fhd)), az = __frcp_rn(fabsf(vr)) * __frcp_rn(fabsf(Wd));
+    const Off dy = incy ? pz : -pz, dz1 = incz ? 1 : -1;
     using U = typename std::conditional<sizeof(Off) == 4, unsigned, unsigned long long>::type;
     const U upz = U(pz), uplane = U(plane);
     // cells (j, k) at the slab's t = 0 boundary, the expressions of the transpose
@@ -132,44 +133,32 @@ __device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int n
         const float S = fmaf(vr, Whi, fcs);  // exact
         // offsets from the raw bits of the split sums (j + bias, k + bias), in modular arithmetic
         const U rb = U(Off(jA)) * upz + U(Off(izs - g.z0)) - U(kSplitBias) * (upz + 1u);
-        // a boundary at slab parameter kb (relative to sc): cell bits and fractions
-        auto bnd = [&](float kb, float& ty, float& fy, float& tt, float& fz) {
-            const float fyr = fmaf(kb, fhd, tA);
-            ty = split_t(fyr);
-            fy = split_frac(fyr, ty);
-            const float wlo = fmaf(kb, Wd, Wr);
-            tt = split_t(fmaf(vr, wlo, S));
-            fz = fmaf(vr, wlo, fmaf(__fsub_rn(tt, kSplitM), -1.f, S));
-        };
-        float kb = float(s - sc) - 0.5f;
-        float tya, fya, tta, fza;
-        bnd(kb, tya, fya, tta, fza);  // the first slab's t = 0 boundary
+        float kb = float(s - sc) - 0.5f;  // the slab's t = 0 boundary, relative to sc
 #pragma unroll 2
-        for (; s <= se; ++s) {
-            kb += 1.f;
-            float tyb, fyb, ttb, fzb;
-            bnd(kb, tyb, fyb, ttb, fzb);  // t = 1 boundary = the next slab's t = 0
-            const int dj = __float_as_int(tyb) - __float_as_int(tya), dk = __float_as_int(ttb) - __float_as_int(tta);
-            const float cy = dj ? sid_cross(fya, incy, ay) : 1.f, cz = dk ? sid_cross(fza, incz, az) : 1.f;
+        for (; s <= se; ++s, kb += 1.f) {
+            const float fyr = fmaf(kb, fhd, tA);
+            const float ty = split_t(fyr);
+            const float fy = split_frac(fyr, ty);
+            const float wlo = fmaf(kb, Wd, Wr);
+            const float tt = split_t(fmaf(vr, wlo, S));
+            const float fz = fmaf(vr, wlo, fmaf(__fsub_rn(tt, kSplitM), -1.f, S));
+            const float cy = sid_cross(fy, incy, ay), cz = sid_cross(fz, incz, az);
             const float m = fminf(cy, cz), M = fmaxf(cy, cz);
-            Off o = Off(U(s) * uplane + rb + U(unsigned(__float_as_int(tya))) * upz + U(unsigned(__float_as_int(tta))));
+            Off o = Off(U(s) * uplane + rb + U(unsigned(__float_as_int(ty))) * upz + U(unsigned(__float_as_int(tt))));
 #ifdef CTK_CHECKED
-            if (base_abs + (long long)o - 2 * (long long)pz - 2 < 0 || base_abs + (long long)o + 2 * (long long)pz + 2 >= lay_n) {
+            if (base_abs + (long long)o - (long long)pz - 1 < 0 || base_abs + (long long)o + (long long)pz + 1 >= lay_n) {
                 atomicOr(g.chk, 1u << 0);
-                o = Off(2 * pz + 2 - base_abs);
+                o = Off(pz + 1 - base_abs);
             }
 #endif
+            // second cells: one step in the direction of motion when the boundary is crossed
             const float* q = base + o;
-            const Off oy = Off(dj) * pz;
-            const float v00 = __ldg(q), v01 = __ldg(q + dk), v10 = __ldg(q + oy), v11 = __ldg(q + oy + dk);
-            acc = fmaf(m, v00, acc);       // (ja, ka)
-            acc = fmaf(cy - m, v01, acc);  // (ja, kb)
-            acc = fmaf(cz - m, v10, acc);  // (jb, ka)
-            acc = fmaf(1.f - M, v11, acc); // (jb, kb)
-            tya = tyb;
-            fya = fyb;
-            tta = ttb;
-            fza = fzb;
+            const Off oy = cy < 1.f ? dy : Off(0), oz = cz < 1.f ? dz1 : Off(0);
+            const float v00 = __ldg(q), v01 = __ldg(q + oz), v10 = __ldg(q + oy), v11 = __ldg(q + oy + oz);
+            acc = fmaf(m, v00, acc);        // (ja, ka)
+            acc = fmaf(cy - m, v01, acc);   // (ja, kb)
+            acc = fmaf(cz - m, v10, acc);   // (jb, ka)
+            acc = fmaf(1.f - M, v11, acc);  // (jb, kb)
         }
     }
     return acc;
