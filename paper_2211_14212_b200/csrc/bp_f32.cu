@@ -256,7 +256,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                     split(fmaf(kf - 0.5f, cd.y, tA), ja, fya);
                     ja += jA;
                     const bool incy = cd.y >= 0.f;
-                    const float cy = sid_cross(fya, incy, __frcp_rn(fabsf(cd.y)));
+                    const float cy = sid_cross(fya, sid_coef(incy, __frcp_rn(fabsf(cd.y))));
                     const int jb = cy < 1.f ? (incy ? ja + 1 : ja - 1) : ja;
                     if (jlo_ok(ja, jb)) {
                         const float gs = fmaf(fs, cd.w, cd.z);
@@ -293,7 +293,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             const float fza = fmaf(vr, Wa, fmaf(__fsub_rn(tta, kSplitM), -1.f, S));
                             const int ka = __float_as_int(tta) + koff;
                             const bool incz = vr * Wd >= 0.f;
-                            const float cz = sid_cross(fza, incz, ivrtab[iv] * aWd);
+                            const float cz = sid_cross(fza, sid_coef(incz, ivrtab[iv] * aWd));
                             const float m = fminf(cy, cz), M = fmaxf(cy, cz);
                             const float wff = m, wfs = cy - m, wsf = cz - m, wss = 1.f - M;
                             const bool lowfirst = incz || !(cz < 1.f);  // ka <= kb
@@ -574,7 +574,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             sid_anchor(g.col64[c], sc, jA, tA, G);
                             split(fmaf(kf - 0.5f, fhd, tA), ja, fy);
                             ja += jA;
-                            const float cy = sid_cross(fy, fhd >= 0.f, __frcp_rn(fabsf(fhd)));
+                            const float cy = sid_cross(fy, sid_coef(fhd >= 0.f, __frcp_rn(fabsf(fhd))));
                             const int jb = cy < 1.f ? (fhd >= 0.f ? ja + 1 : ja - 1) : ja;
                             if (jlo_ok(ja, jb)) {
                                 if (ja == p) add_sid(Z, e);

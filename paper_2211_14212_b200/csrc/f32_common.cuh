@@ -248,12 +248,15 @@ __device__ __forceinline__ void sid_anchor(const double4& c, int sc, int& jA, fl
 // z cell coordinate Z = fz + 1/2 = izs + fcs + vr W
 __device__ __forceinline__ int sid_izc(const KGeom& g) { return g.nzg >> 1; }
 __device__ __forceinline__ float sid_fc(const KGeom& g) { return (g.nzg & 1) ? 0.5f : 0.f; }
-// crossing parameter of a cell coordinate with fraction f moving by d per slab (ad = 1/|d|):
-// distance to the next boundary in the direction of motion, in units of the slab
-__device__ __forceinline__ float sid_cross(float f, bool inc, float ad) {
-    const float gap = inc ? 1.f - f : f;
-    return fminf(fmaxf(gap * ad, 0.f), 1.f);  // fmaxf(NaN, 0) = 0: a zero gap with ad = inf
+// crossing parameter of a cell coordinate with fraction f moving by d per slab: the distance
+// to the next boundary in the direction of motion over |d|, clamped to [0, 1] -- one
+// saturated FMA, c = sat(f * A + B) with (A, B) = (-1/|d|, 1/|d|) moving up, (1/|d|, 0) down;
+// 1/|d| is capped at 1e30 (d = 0: never crosses)
+__device__ __forceinline__ float2 sid_coef(bool inc, float ad) {
+    ad = fminf(ad, 1e30f);
+    return inc ? make_float2(-ad, ad) : make_float2(ad, 0.f);
 }
+__device__ __forceinline__ float sid_cross(float f, float2 ab) { return __saturatef(fmaf(f, ab.x, ab.y)); }
 
 }  // namespace
 }  // namespace ctkb
