@@ -249,11 +249,23 @@ int ctk_shard_angles(int n_angles, int nranks, int rank, int* first, int* count)
 /* Collectives as callbacks (NCCL below, or any transport e.g. torch.distributed).
  * allreduce_sum: in-place sum of `count` elements (dtype 0=f32, 1=f64) of a DEVICE buffer
  * on `stream`; allgather_f64: gathers one host double per rank into out[nranks]. */
+/* One point-to-point transfer of an exchange: send or receive `count` elements of a DEVICE
+ * buffer to / from rank `peer`. */
+typedef struct {
+    int peer;
+    int is_send;
+    void* d_buf;
+    size_t count;
+} ctk_p2p_op;
 typedef struct {
     int rank, nranks;
     int (*allreduce_sum)(void* d_buf, size_t count, int dtype, void* stream, void* user);
     int (*allgather_f64)(double value, double* h_out, void* user);
     void* user;
+    /* exchange (optional; needed by the band-sharded range, ctk_geom_shard_range): run all
+     * n_ops transfers (dtype 0=f32, 1=f64), ordered on `stream` after the kernels queued
+     * before and before the ones queued after; NULL in older callers. */
+    int (*exchange)(const ctk_p2p_op* ops, int n_ops, int dtype, void* stream, void* user);
 } ctk_comm_callbacks;
 int ctk_comm_create(const ctk_comm_callbacks* cb, ctk_comm** out);
 /* NCCL (dlopen'd libnccl.so.2): unique id is 128 bytes, exchanged by the caller. */
@@ -278,6 +290,19 @@ int ctk_shard_slabs(int nz, int nranks, int rank, int* z0, int* count);
  * geometry, angles and detector stay global); nz_local = 0 restores the whole volume.
  * Implemented for the f32 Joseph operators (others return CTK_E_UNSUPPORTED at apply). */
 int ctk_geom_set_slab(ctk_geom* g, int z0, int nz_local);
+/* Band-sharded range (needs a slab and an attached communicator whose ranks hold the slabs
+ * of ctk_shard_slabs in rank order): range vectors then hold only the detector rows
+ * [w0, w0 + nw) of every view -- the rows this slab's rays reach plus the rows this rank
+ * owns, [o0, o0 + no); rows held but not owned are kept at zero.  A x partials are summed by
+ * the rows' owners (point-to-point, rank order) and A^T b fetches the reached rows it does
+ * not own from their owners; per-rank memory O(N_vox / G + band).  Collective: every rank
+ * calls it.  ctk_geom_sizes then reports the local range size n_angles * nw * nu. */
+int ctk_geom_shard_range(ctk_geom* g);
+int ctk_geom_range_rows(const ctk_geom* g, int* w0, int* nw, int* o0, int* no);
+/* The partition itself, host only: slabs [z0s[r], z0s[r] + nzs[r]) tiling nz in rank order
+ * -> reached rows [t0[r], t1[r]) and owned rows [o0[r], o1[r]) (a partition of [0, nv)). */
+int ctk_band_partition(const ctk_geom_desc* desc, int nranks, const int* z0s, const int* nzs, int* t0, int* t1,
+                       int* o0, int* o1);
 
 /* ---- instrumentation ----------------------------------------------------------------- */
 /* Number of this library's kernel launches since load (for bench gpu_launches). */

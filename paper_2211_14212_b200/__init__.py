@@ -28,6 +28,7 @@ from .api import (  # noqa: F401
     UnsupportedError,
     VolumeShape,
     ab_gmres,
+    band_partition,
     ba_gmres,
     back_project,
     canonical_angle,

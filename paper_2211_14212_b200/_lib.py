@@ -77,6 +77,13 @@ ALLREDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.
 ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_double, C.POINTER(C.c_double), C.c_void_p)
 
 
+class P2POp(C.Structure):
+    _fields_ = [("peer", C.c_int), ("is_send", C.c_int), ("d_buf", C.c_void_p), ("count", C.c_size_t)]
+
+
+EXCHANGE = C.CFUNCTYPE(C.c_int, C.POINTER(P2POp), C.c_int, C.c_int, C.c_void_p, C.c_void_p)
+
+
 class CommCallbacks(C.Structure):
     _fields_ = [
         ("rank", C.c_int),
@@ -84,6 +91,7 @@ class CommCallbacks(C.Structure):
         ("allreduce_sum", ALLREDUCE),
         ("allgather_f64", ALLGATHER),
         ("user", C.c_void_p),
+        ("exchange", EXCHANGE),
     ]
 
 
@@ -111,6 +119,10 @@ def load():
         "ctk_geom_set_projector": (i, [vp, i]),
         "ctk_geom_set_bp_partitions": (i, [vp, i]),
         "ctk_geom_set_slab": (i, [vp, i, i]),
+        "ctk_geom_shard_range": (i, [vp]),
+        "ctk_geom_range_rows": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(i)]),
+        "ctk_band_partition": (i, [C.POINTER(GeomDesc), i, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(i),
+                                   C.POINTER(i), C.POINTER(i)]),
         "ctk_geom_set_stream": (i, [vp, vp]),
         "ctk_geom_attach_comm": (i, [vp, vp]),
         "ctk_geom_last_kernel_ms": (d, [vp]),

@@ -215,6 +215,17 @@ class ConeGeometry:
                             list(np.asarray(self.angles, dtype=np.float64)[first:first + count]))
 
 
+def band_partition(geom: ConeGeometry, z0s, nzs):
+    """The band-sharded range's row partition (ctk_band_partition): per slab, the detector
+    rows its rays reach [t0, t1) and the rows its rank owns [o0, o1)."""
+    lib = L.load()
+    R = len(z0s)
+    arr = lambda v: (C.c_int * R)(*v)
+    t0, t1, o0, o1 = arr([0] * R), arr([0] * R), arr([0] * R), arr([0] * R)
+    _check(lib.ctk_band_partition(C.byref(geom.desc()), R, arr(z0s), arr(nzs), t0, t1, o0, o1))
+    return [list(x) for x in (t0, t1, o0, o1)]
+
+
 def equidistant_angles(n: int, start_rad: float = 0.0, range_rad: float = TWO_PI):
     """geometry.hpp:57-64."""
     if n <= 0:
@@ -291,6 +302,31 @@ class Projector:
     def attach_comm(self, comm):
         _check(self.lib.ctk_geom_attach_comm(self.handle, comm.handle))
         self._comm = comm
+
+    def shard_range(self):
+        """Band-sharded range (z-slab + communicator, collective): range vectors hold this
+        rank's detector-row window (range_rows) with the rows it does not own at zero."""
+        _check(self.lib.ctk_geom_shard_range(self.handle))
+        ds, rs = C.c_size_t(), C.c_size_t()
+        _check(self.lib.ctk_geom_sizes(self.handle, C.byref(ds), C.byref(rs)))
+        self.domain_size, self.range_size = ds.value, rs.value
+
+    def range_rows(self):
+        """(w0, nw, o0, no): rows held [w0, w0 + nw) and owned [o0, o0 + no)."""
+        v = [C.c_int() for _ in range(4)]
+        _check(self.lib.ctk_geom_range_rows(self.handle, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def local_range(self, y_full):
+        """The held rows of a whole-range vector [n_angles][nv][nu], non-owned rows zeroed
+        (the layout of this rank's range vectors under the band-sharded range)."""
+        w0, nw, o0, no = self.range_rows()
+        g = self.geom
+        yv = y_full.reshape(len(g.angles), g.nv, g.nu)
+        out = yv[:, w0:w0 + nw, :].copy() if isinstance(yv, np.ndarray) else yv[:, w0:w0 + nw, :].clone()
+        out[:, :o0 - w0, :] = 0
+        out[:, o0 - w0 + no:, :] = 0
+        return out.reshape(-1)
 
     def last_kernel_ms(self) -> float:
         return float(self.lib.ctk_geom_last_kernel_ms(self.handle))
@@ -413,10 +449,13 @@ class OperatorPair:
 
 def projector_pair(geom: ConeGeometry, variant: BackprojectVariant = BackprojectVariant.matched,
                    dtype=np.float32, projector: ProjectorKind = ProjectorKind.joseph,
-                   bp_partitions: int = 1, slab: Optional[Tuple[int, int]] = None) -> OperatorPair:
+                   bp_partitions: int = 1, slab: Optional[Tuple[int, int]] = None, comm=None,
+                   shard_range: bool = False) -> OperatorPair:
     """operators.hpp:91-115 -- the projector pair of a geometry, backed by the sm_100a kernels.
     slab = (z0, nz_local): the pair acts on slices [z0, z0 + nz_local) of the volume
-    (z-slab sharding; f32 Joseph operators)."""
+    (z-slab sharding; f32 Joseph operators).  comm: attach a communicator; shard_range (with
+    a slab): the band-sharded range -- range vectors hold this rank's detector-row window
+    (Projector.range_rows / local_range)."""
     geom.validate()
     canon = ConeGeometry(geom.mode, geom.source_to_origin, geom.origin_to_detector, geom.detector_pixel_size,
                          geom.nu, geom.nv, geom.vol, [canonical_angle(a) for a in geom.angles])
@@ -425,6 +464,10 @@ def projector_pair(geom: ConeGeometry, variant: BackprojectVariant = Backproject
     if slab is not None:
         proj.set_slab(*slab)
         shape = VolumeShape(canon.vol.nx, canon.vol.ny, int(slab[1]), canon.vol.spacing)
+    if comm is not None:
+        proj.attach_comm(comm)
+        if shard_range:
+            proj.shard_range()
     v = BackprojectVariant(variant)
     return OperatorPair(proj.domain_size, proj.range_size, v == BackprojectVariant.matched, shape,
                         lambda x, y: proj.forward(x, y), lambda y, x: proj.back(y, x, v), np.dtype(dtype), proj, v)

@@ -68,7 +68,8 @@ class TorchComm:
         self.rank, self.nranks, self.group, self.device = rank, nranks, group, device
         self._ar = L.ALLREDUCE(self._allreduce)
         self._ag = L.ALLGATHER(self._allgather)
-        self.callbacks = L.CommCallbacks(rank, nranks, self._ar, self._ag, None)
+        self._ex = L.EXCHANGE(self._exchange)
+        self.callbacks = L.CommCallbacks(rank, nranks, self._ar, self._ag, None, self._ex)
         self._handle = None
 
     @property
@@ -122,6 +123,42 @@ class TorchComm:
                 ext.synchronize()
                 dist.all_reduce(t, group=self.group)
                 torch.cuda.synchronize()
+            return 0
+        except Exception:  # surfaced by the library as CTK_E_CUDA
+            return 1
+
+    def _exchange(self, ops, n_ops, dtype, stream, user):
+        """Point-to-point transfers of the band-sharded range (bands.cpp): NCCL batches them
+        on the library's stream; host-staged backends (gloo) copy through host memory."""
+        import torch
+        import torch.distributed as dist
+
+        try:
+            lst = [ops[i] for i in range(n_ops)]
+            if self.device == "cpu":
+                ts = [self._wrap(o.d_buf, o.count, dtype) for o in lst]
+                reqs = [(dist.isend if o.is_send else dist.irecv)(t, o.peer, group=self.group) for o, t in zip(lst, ts)]
+                for r in reqs:
+                    r.wait()
+                return 0
+            ext = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream()
+            if dist.get_backend(self.group) == "nccl":
+                with torch.cuda.stream(ext):
+                    p2p = [dist.P2POp(dist.isend if o.is_send else dist.irecv, self._wrap(o.d_buf, o.count, dtype),
+                                      o.peer, group=self.group) for o in lst]
+                    for r in dist.batch_isend_irecv(p2p):
+                        r.wait()
+                return 0
+            ext.synchronize()
+            host = [self._wrap(o.d_buf, o.count, dtype).cpu() if o.is_send else
+                    torch.empty(o.count, dtype=torch.float32 if dtype == 0 else torch.float64) for o in lst]
+            reqs = [(dist.isend if o.is_send else dist.irecv)(t, o.peer, group=self.group) for o, t in zip(lst, host)]
+            for r in reqs:
+                r.wait()
+            for o, t in zip(lst, host):
+                if not o.is_send:
+                    self._wrap(o.d_buf, o.count, dtype).copy_(t)
+            torch.cuda.synchronize()
             return 0
         except Exception:  # surfaced by the library as CTK_E_CUDA
             return 1

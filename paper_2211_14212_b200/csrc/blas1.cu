@@ -479,6 +479,35 @@ void block_axpy(size_t n, int m, double alpha, const double* d_coef, const T* ba
     }
 }
 
+// band-sharded range (bands.cpp): y's owned rows <- rank-ordered sum of the partials of
+// every source that covers the row; y's other held rows <- 0.  In place: a thread reads the
+// local partial of its element before writing it.
+template <class T>
+__global__ void k_band_sum(BandSum<T> bs, int na, int nu, int w0, int nw, T* __restrict__ y) {
+    const size_t n = size_t(na) * nw * nu;
+    for (size_t id = size_t(blockIdx.x) * blockDim.x + threadIdx.x; id < n; id += size_t(gridDim.x) * blockDim.x) {
+        const int iu = int(id % nu);
+        const size_t ar = id / nu;
+        const int row = w0 + int(ar % nw), a = int(ar / nw);
+        T acc = T(0);
+        if (row >= bs.o0 && row < bs.o1) {
+            for (int i = 0; i < bs.n; ++i) {
+                const auto& sr = bs.src[i];
+                if (row >= sr.r0 && row < sr.r1) acc += sr.p[(size_t(a) * sr.rp + size_t(row - sr.roff)) * nu + iu];
+            }
+        }
+        y[id] = acc;
+    }
+}
+
+template <class T>
+void band_sum(const Geometry& g, const BandSum<T>& bs, T* y, cudaStream_t s) {
+    const size_t n = g.range();
+    const unsigned blocks = unsigned(std::min<size_t>((n + 255) / 256, 148 * 16));
+    k_band_sum<T><<<blocks, 256, 0, s>>>(bs, g.na, g.nu, g.w0, g.nw, y);
+    after_launch("k_band_sum");
+}
+
 #define CTK_INST(T)                                                                                        \
     template void reduce_dot<T>(size_t, const T*, const T*, double*, RedWork, cudaStream_t);              \
     template void reduce_diff_nrm2sq<T>(size_t, const T*, const T*, double*, RedWork, cudaStream_t);      \
@@ -496,7 +525,8 @@ void block_axpy(size_t n, int m, double alpha, const double* d_coef, const T* ba
     template void lsmr_update<T>(size_t, double, double, double, T*, T*, T*, const T*, cudaStream_t);     \
     template void fill<T>(size_t, T, T*, cudaStream_t);                                                   \
     template void block_dot<T>(size_t, int, const T*, size_t, const T*, double*, double*, cudaStream_t);  \
-    template void block_axpy<T>(size_t, int, double, const double*, const T*, size_t, T*, cudaStream_t);
+    template void block_axpy<T>(size_t, int, double, const double*, const T*, size_t, T*, cudaStream_t); \
+    template void band_sum<T>(const Geometry&, const BandSum<T>&, T*, cudaStream_t);
 CTK_INST(float)
 CTK_INST(double)
 #undef CTK_INST

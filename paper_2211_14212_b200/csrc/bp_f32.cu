@@ -16,16 +16,16 @@ __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __
     __shared__ float tile[32][33];
     const int a = blockIdx.z;
     const int u0 = blockIdx.x * 32, v0 = blockIdx.y * 32;
-    const float* fr = y + size_t(a) * g.nu * g.nv;
+    const float* fr = y + size_t(a) * g.nu * g.nw;  // rows held: [w0, w0 + nw), local index iv
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int iu = u0 + threadIdx.x, iv = v0 + r;
-        tile[r][threadIdx.x] = (iu < g.nu && iv < g.nv) ? __ldg(fr + size_t(iv) * g.nu + iu) : 0.f;
+        tile[r][threadIdx.x] = (iu < g.nu && iv < g.nw) ? __ldg(fr + size_t(iv) * g.nu + iu) : 0.f;
     }
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int iu = u0 + r, iv = v0 + threadIdx.x;
-        if (iu < g.nu && iv < g.nv) {
-            pt[(size_t(a) * g.nu + iu) * g.nv + iv] = tile[threadIdx.x][r];
+        if (iu < g.nu && iv < g.nw) {
+            pt[(size_t(a) * g.nu + iu) * g.nw + iv] = tile[threadIdx.x][r];
         }
     }
 }
@@ -39,23 +39,23 @@ __global__ void k_proj_transpose(KGeom g, const float* __restrict__ y, float* __
 // (the padding groups are zero)
 __host__ __device__ __forceinline__ int pg_groups(int nv) { return (((nv + 3) >> 2) + 1) & ~1; }
 __device__ __forceinline__ size_t pg_index(const KGeom& g, int a, int iu, int iv) {
-    return ((size_t(a) * pg_groups(g.nv) + (iv >> 2)) * g.nu + iu) * 4 + (iv & 3);
+    return ((size_t(a) * pg_groups(g.nw) + (iv >> 2)) * g.nu + iu) * 4 + (iv & 3);  // iv local (held rows)
 }
 
 __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __restrict__ pg) {
     // block: 32 columns x 8 row groups; thread (u, q) writes one float4
     const int a = blockIdx.z;
     const int iu = blockIdx.x * 32 + threadIdx.x, q = blockIdx.y * 8 + threadIdx.y;
-    const int nq = pg_groups(g.nv);
+    const int nq = pg_groups(g.nw);  // groups of the held rows [w0, w0 + nw)
     if (iu >= g.nu || q >= nq) return;
     const int c = a * g.nu + iu;
     const double2 cs = g.colstep[c];
-    const float* fr = y + size_t(a) * g.nu * g.nv;
+    const float* fr = y + size_t(a) * g.nu * g.nw;
     float r[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        const int iv = 4 * q + j;
-        r[j] = iv < g.nv ? __ldg(fr + size_t(iv) * g.nu + iu) * ray_step(g, cs, row_coord(g, iv)) : 0.f;
+        const int iv = 4 * q + j;  // local row
+        r[j] = iv < g.nw ? __ldg(fr + size_t(iv) * g.nu + iu) * ray_step(g, cs, row_coord(g, g.w0 + iv)) : 0.f;
     }
     reinterpret_cast<float4*>(pg)[(size_t(a) * nq + q) * g.nu + iu] = make_float4(r[0], r[1], r[2], r[3]);
 }
@@ -125,7 +125,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     int* cnt = lists + NL * BP_SL;                              // [NL]
     float* eth = reinterpret_cast<float*>(cnt + NL);            // [BP_PB]
     static_assert((NL * BP_SL) % 4 == 0 && NL % 4 == 0, "keeps vrtab 16-byte aligned");
-    const int nv4 = 4 * pg_groups(g.nv);
+    const int nv4 = 4 * pg_groups(g.nw);  // held rows, local index (band-sharded range)
     float* vrtab = eth + BP_PB;                                 // [nv4] iv - (nv-1)/2, 16-byte aligned
     float* ivrtab = vrtab + (SID ? nv4 : 0);                    // Siddon: [nv4] 1/|iv - (nv-1)/2|
     int2* urange = reinterpret_cast<int2*>(vrtab + (SID ? 2 : 1) * nv4);  // [na]
@@ -141,8 +141,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
     for (int q = t; q < nv4; q += BP_PB) {
-        vrtab[q] = row_vr(g, q);
-        if (SID) ivrtab[q] = __frcp_rn(fabsf(row_vr(g, q)));
+        vrtab[q] = row_vr(g, g.w0 + q);
+        if (SID) ivrtab[q] = __frcp_rn(fabsf(row_vr(g, g.w0 + q)));
     }
     const int sc = slice_centre(s);  // anchored positions (f32_common.cuh): block centre of plane s
     const float kf = float(s - sc);
@@ -152,7 +152,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const float invdu = float(1.0 / g.du);
     const float fs = float(s);
     const double h = g.h;
-    const int nq = pg_groups(g.nv);  // row groups of the grouped projection layout
+    const int nq = pg_groups(g.nw);  // row groups of the grouped projection layout
     // world coordinates of the plane and of the tile's row segment ends
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - (SID ? 2.5 : 1.5) - 0.5 * (nh - 1)) * h,
@@ -275,6 +275,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             v0 = lo;
                             v1 = hi;
                         }
+                        v0 = max(v0, g.w0) - g.w0;  // held rows, local index
+                        v1 = min(v1, g.w0 + g.nw - 1) - g.w0;
                         const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
                         const size_t qs = size_t(g.nu);
                         float* zc = Z + z_col(t);
@@ -412,6 +414,9 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             v0 = lo;
                             v1 = hi;
                         }
+                        // the held rows, local index from here on
+                        v0 = max(v0, g.w0) - g.w0;
+                        v1 = min(v1, g.w0 + g.nw - 1) - g.w0;
                         // column iu of view a, row group q: pc4[q * nu] (grouped layout)
                         const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
                         const size_t qs = size_t(g.nu);
@@ -646,6 +651,8 @@ __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, f
             iv0 = max(iv0, int(floor(fmax(vmin, -1e9))) - 1);
             iv1 = min(iv1, int(ceil(fmin(vmax, 1e9))) + 1);
         }
+        iv0 = max(iv0, g.w0);  // the held rows (band-sharded range)
+        iv1 = min(iv1, g.w0 + g.nw - 1);
         for (int iv = iv0; iv <= iv1; ++iv) {
             const double v = row_coord(g, iv);
             for (int iu = iu0; iu <= iu1; ++iu) {
@@ -662,7 +669,7 @@ __global__ void k_atb_matched_zrays_f32(KGeom g, const float* __restrict__ pg, f
                 float wb, wc;
                 if (i == ib) wb = 1.f - tb; else if (i == ib + 1) wb = tb; else continue;
                 if (j == ic) wc = 1.f - tc; else if (j == ic + 1) wc = tc; else continue;
-                acc = fmaf(wb * wc, __ldg(pg + chk_idx(g, pg_index(g, a, iu, iv), size_t(g.na) * pg_groups(g.nv) * g.nu * 4, 6)), acc);
+                acc = fmaf(wb * wc, __ldg(pg + chk_idx(g, pg_index(g, a, iu, iv - g.w0), size_t(g.na) * pg_groups(g.nw) * g.nu * 4, 6)), acc);
             }
         }
     }
@@ -749,8 +756,8 @@ k_atb_voxel_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
             const float vsp = __shfl_sync(0xffffffffu, spar, L);
             const bool u0ok = iu >= 0, u1ok = iu + 1 < g.nu;
             CTK_CHK(g, a < g.na && iu >= -1 && iu < g.nu, 5);
-            const float* c0 = pt + size_t(a * g.nu + iu) * g.nv;
-            const float* c1 = c0 + g.nv;
+            const float* c0 = pt + (ptrdiff_t(a * g.nu + iu) * g.nw - g.w0);  // by global row; rows held [w0, w0+nw)
+            const float* c1 = c0 + g.nw;
 #pragma unroll
             for (int m = 0; m < KZ; ++m) {
                 const int k = kb + lane + 32 * m;
@@ -759,7 +766,7 @@ k_atb_voxel_f32(KGeom g, const float* __restrict__ pt, float* __restrict__ x, in
                 float tv = 0.f;
                 if (!flat)  // clamped far outside the detector so the split stays exact (taps then read nothing)
                     dsplit(fmin(fmax(__fma_rn(cone ? t : 1.0, zq[m], cv), -4.0), g.nv + 4.0), iv, tv);
-                const bool v0ok = iv >= 0 && iv < g.nv, v1ok = iv + 1 >= 0 && iv + 1 < g.nv;
+                const bool v0ok = iv >= g.w0 && iv < g.w0 + g.nw, v1ok = iv + 1 >= g.w0 && iv + 1 < g.w0 + g.nw;
                 const float p00 = (u0ok && v0ok) ? __ldg(c0 + iv) : 0.f;
                 const float p10 = (u1ok && v0ok) ? __ldg(c1 + iv) : 0.f;
                 const float p01 = (u0ok && v1ok) ? __ldg(c0 + iv + 1) : 0.f;
@@ -795,13 +802,13 @@ int pick_kz(int nz) {
 
 void transpose_proj(Geometry& g, const float* y, cudaStream_t s) {
     g.proj_t.ensure(g.range() * sizeof(float));
-    dim3 blk(32, 8), grd((g.nu + 31) / 32, (g.nv + 31) / 32, g.na);
+    dim3 blk(32, 8), grd((g.nu + 31) / 32, (g.rows_local() + 31) / 32, g.na);
     k_proj_transpose<<<grd, blk, 0, s>>>(g.kgeom(), y, g.proj_t.as<float>());
     after_launch("k_proj_transpose");
 }
 
 void group_proj(Geometry& g, const float* y, cudaStream_t s) {
-    const int nq = pg_groups(g.nv);
+    const int nq = pg_groups(g.rows_local());
     g.proj_t.ensure(size_t(g.na) * g.nu * nq * 4 * sizeof(float));
     dim3 blk(32, 8), grd((g.nu + 31) / 32, (nq + 7) / 8, g.na);
     k_proj_group4<<<grd, blk, 0, s>>>(g.kgeom(), y, g.proj_t.as<float>());
@@ -818,7 +825,7 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     constexpr int NL = PB;
     const size_t smem = sizeof(float) * (size_t(z_stride<PB>()) * (BP_KB + 2 * BP_ZG) * (SID ? 2 : 1) +
                                          size_t(NL) * BP_SL + NL + BP_PB +
-                                         4 * size_t(pg_groups(g.nv)) * (SID ? 2 : 1)) +
+                                         4 * size_t(pg_groups(g.rows_local())) * (SID ? 2 : 1)) +
                         sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     // opt in once to the largest size this launcher accepts (occupancy follows the size of

@@ -69,13 +69,17 @@ template <class T>
 void ax_dev(ctkb::Geometry& g, const T* x, T* y, cudaStream_t s) {
     g.require_angles();
     ctkb::op_ax<T>(g, x, y, s);
-    if (g.comm && g.slab) ctkb::comm_allreduce(g.comm, y, g.range(), sizeof(T) == 8 ? 1 : 0, s);
+    if (g.comm && g.slab) {
+        if (g.band) ctkb::band_reduce<T>(g, y, s);  // partials to the rows' owners
+        else ctkb::comm_allreduce(g.comm, y, g.range(), sizeof(T) == 8 ? 1 : 0, s);
+    }
 }
 
 template <class T>
 void atb_dev(ctkb::Geometry& g, int variant, const T* y, T* x, cudaStream_t s) {
     g.require_angles();
     check_variant(variant);
+    if (g.band) y = ctkb::band_halo<T>(g, y, s);  // the reached rows other ranks own
     ctkb::op_atb<T>(g, variant, y, x, s);
     if (g.comm && !g.slab) ctkb::comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
 }
@@ -191,6 +195,7 @@ int ctk_geom_set_slab(ctk_geom* g, int z0, int nz_local) {
             gg.z0 = z0;
             gg.nzl = nz_local;
         }
+        gg.band = false;  // the row window depends on the slab: ctk_geom_shard_range again
         gg.vx.release();  // padded relayouts depend on the slab height
         gg.vy.release();
     });
@@ -243,7 +248,7 @@ int ctk_ax_residual_f32(ctk_geom* g, const float* x, const float* b, double* out
         CTK_CUDA(cudaMemcpyAsync(gg.pinned, w.results, sizeof(double), cudaMemcpyDeviceToHost, st));
         CTK_CUDA(cudaStreamSynchronize(st));
         double v = gg.pinned[0];
-        if (gg.comm && !gg.slab) v = ctkb::comm_sum_scalar(gg.comm, v);  // angle shards: range partials
+        if (gg.comm && (!gg.slab || gg.band)) v = ctkb::comm_sum_scalar(gg.comm, v);  // sharded range: partials
         *out = v;
     });
 }
@@ -446,7 +451,57 @@ int ctk_comm_create_nccl(const void* id, int nranks, int rank, ctk_comm** out) {
 }
 void ctk_comm_destroy(ctk_comm* c) { ctkb::comm_destroy(reinterpret_cast<ctkb::Comm*>(c)); }
 int ctk_geom_attach_comm(ctk_geom* g, ctk_comm* c) {
-    return guard([&] { G(g).comm = reinterpret_cast<ctkb::Comm*>(c); });
+    return guard([&] {
+        G(g).comm = reinterpret_cast<ctkb::Comm*>(c);
+        G(g).band = false;
+    });
+}
+
+int ctk_geom_shard_range(ctk_geom* g) {
+    return guard([&] {
+        auto& gg = G(g);
+        if (!gg.slab || !gg.comm) ctkb::fail(CTK_E_PARAMETER, "band-sharded range needs a slab and a communicator");
+        const int R = gg.comm->cb.nranks, me = gg.comm->cb.rank;
+        const std::vector<double> z0s = ctkb::comm_allgather_scalar(gg.comm, double(gg.z0));
+        const std::vector<double> nzs = ctkb::comm_allgather_scalar(gg.comm, double(gg.nzl));
+        std::vector<int> z0i(static_cast<size_t>(R)), nzi(static_cast<size_t>(R));
+        for (int r = 0; r < R; ++r) {
+            z0i[size_t(r)] = int(z0s[size_t(r)]);
+            nzi[size_t(r)] = int(nzs[size_t(r)]);
+        }
+        gg.bt0.assign(size_t(R), 0);
+        gg.bt1.assign(size_t(R), 0);
+        gg.bo0.assign(size_t(R), 0);
+        gg.bo1.assign(size_t(R), 0);
+        ctkb::band_partition(gg.mode, gg.nx, gg.ny, gg.nz, gg.nv, gg.h, gg.du, gg.dso, gg.dod, R, z0i.data(),
+                             nzi.data(), gg.bt0.data(), gg.bt1.data(), gg.bo0.data(), gg.bo1.data());
+        const size_t m = size_t(me);
+        const int t0 = gg.bt0[m], t1 = std::max(gg.bt1[m], gg.bt0[m]), o0 = gg.bo0[m], o1 = gg.bo1[m];
+        gg.w0 = t1 > t0 ? std::min(t0, o0) : o0;
+        gg.nw = std::max(std::max(t1, o1), gg.w0 + 1) - gg.w0;
+        gg.band = true;
+    });
+}
+
+int ctk_geom_range_rows(const ctk_geom* g, int* w0, int* nw, int* o0, int* no) {
+    return guard([&] {
+        auto& gg = G(g);
+        const int me = gg.band ? gg.comm->cb.rank : 0;
+        if (w0) *w0 = gg.band ? gg.w0 : 0;
+        if (nw) *nw = gg.band ? gg.nw : gg.nv;
+        if (o0) *o0 = gg.band ? gg.bo0[size_t(me)] : 0;
+        if (no) *no = gg.band ? gg.bo1[size_t(me)] - gg.bo0[size_t(me)] : gg.nv;
+    });
+}
+
+int ctk_band_partition(const ctk_geom_desc* d, int nranks, const int* z0s, const int* nzs, int* t0, int* t1, int* o0,
+                       int* o1) {
+    return guard([&] {
+        ctkb::geometry_validate(d);
+        if (!z0s || !nzs || !t0 || !t1 || !o0 || !o1) ctkb::fail(CTK_E_PARAMETER, "null partition array");
+        ctkb::band_partition(d->mode, d->nx, d->ny, d->nz, d->nv, d->spacing, d->detector_pixel_size,
+                             d->source_to_origin, d->origin_to_detector, nranks, z0s, nzs, t0, t1, o0, o1);
+    });
 }
 
 uint64_t ctk_launch_count(void) { return ctkb::launch_count(); }

@@ -25,6 +25,10 @@ struct NcclApi {
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -44,6 +48,10 @@ NcclApi& nccl() {
         api.AllGather = reinterpret_cast<decltype(api.AllGather)>(dlsym(h, "ncclAllGather"));
         api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
         api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+        api.Send = reinterpret_cast<decltype(api.Send)>(dlsym(h, "ncclSend"));
+        api.Recv = reinterpret_cast<decltype(api.Recv)>(dlsym(h, "ncclRecv"));
+        api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(dlsym(h, "ncclGroupStart"));
+        api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
         api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.AllGather && api.CommDestroy;
         if (!api.ok) api.err = "libnccl.so.2 lacks required symbols";
     });
@@ -99,6 +107,33 @@ std::vector<double> comm_gather_scalar(Comm* c, double v) {
     return all;
 }
 }  // namespace
+
+// Point-to-point exchange of the band-sharded range (bands.cpp): NCCL grouped Send/Recv on
+// the library's stream, or the caller's exchange callback.
+void comm_exchange(Comm* c, const std::vector<ctk_p2p_op>& ops, int dtype, cudaStream_t s) {
+    if (!c || c->cb.nranks <= 1 || ops.empty()) return;
+    if (c->nccl_comm) {
+        auto& api = nccl();
+        if (!api.Send || !api.Recv || !api.GroupStart || !api.GroupEnd)
+            fail(CTK_E_UNSUPPORTED, "libnccl.so.2 lacks ncclSend/ncclRecv");
+        auto* st = static_cast<NcclState*>(c->nccl_comm);
+        const ncclDataType_t dt = dtype == 1 ? ncclFloat64 : ncclFloat32;
+        nccl_check(api.GroupStart(), "ncclGroupStart");
+        for (const ctk_p2p_op& o : ops) {
+            if (o.is_send) nccl_check(api.Send(o.d_buf, o.count, dt, o.peer, st->comm, s), "ncclSend");
+            else nccl_check(api.Recv(o.d_buf, o.count, dt, o.peer, st->comm, s), "ncclRecv");
+        }
+        nccl_check(api.GroupEnd(), "ncclGroupEnd");
+        return;
+    }
+    if (!c->cb.exchange) fail(CTK_E_PARAMETER, "communicator lacks the exchange callback (band-sharded range)");
+    if (c->cb.exchange(ops.data(), int(ops.size()), dtype, s, c->cb.user) != 0) fail(CTK_E_CUDA, "exchange callback failed");
+}
+
+std::vector<double> comm_allgather_scalar(Comm* c, double v) {
+    if (!c || c->cb.nranks <= 1) return {v};
+    return comm_gather_scalar(c, v);
+}
 
 double comm_sum_scalar(Comm* c, double v) {
     if (!c || c->cb.nranks <= 1) return v;

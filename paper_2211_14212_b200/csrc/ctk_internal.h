@@ -51,6 +51,7 @@ struct DevBuf {
 struct KGeom {
     int mode, nu, nv, nx, ny, nz, na;
     int nzg, z0;                  // z-slab: the handle holds slices [z0, z0 + nz) of nzg
+    int w0, nw;                   // range rows held: [w0, w0 + nw) of nv (band-sharded range; else 0, nv)
     int has_zrays;
     double dso, dod, du, h;
     const double2* ctst;          // per view (cos, sin), host libm values
@@ -78,6 +79,14 @@ struct Geometry {
     // z-slab sharding: domain vectors hold slices [z0, z0 + nzl) of nz
     bool slab = false;
     int z0 = 0, nzl = 0;
+    // band-sharded range (ctk_geom_shard_range, z-slab + communicator): range vectors hold
+    // detector rows [w0, w0 + nw) of every view -- the rows this slab's rays reach (t0..t1)
+    // and the rows this rank owns (o0..o1); per rank r of the communicator bt0/bt1 (reached)
+    // and bo0/bo1 (owned, a partition of [0, nv)) -- SURVEY.md 8(e)
+    bool band = false;
+    int w0 = 0, nw = 0;
+    std::vector<int> bt0, bt1, bo0, bo1;
+    DevBuf band_send, band_recv, band_scratch;
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -114,7 +123,8 @@ struct Geometry {
 
     size_t domain() const { return size_t(nx) * ny * (slab ? nzl : nz); }
     int nz_local() const { return slab ? nzl : nz; }
-    size_t range() const { return size_t(na) * nu * nv; }
+    size_t range() const { return size_t(na) * nu * (band ? nw : nv); }
+    int rows_local() const { return band ? nw : nv; }
     KGeom kgeom() const;
     void require_angles() const;
     ~Geometry();
@@ -225,10 +235,37 @@ struct Comm {
 void comm_allreduce(Comm* c, void* d_buf, size_t count, int dtype, cudaStream_t s);
 double comm_sum_scalar(Comm* c, double v);  // rank-ordered sum of per-rank partials
 double comm_max_scalar(Comm* c, double v);
+std::vector<double> comm_allgather_scalar(Comm* c, double v);  // every rank's value, rank order
 // d_v[0..m) <- rank-ordered sum over ranks of every rank's d_v, on stream s: one collective
 // for the whole vector (CGS2 coefficients), no host round trip
 void comm_sum_vector(Comm* c, double* d_v, int m, cudaStream_t s);
 void rank_sum(const double* gathered, int nranks, int m, double* d_out, cudaStream_t s);
+
+// ---- band-sharded range of z-slab sharding (bands.cpp) ----------------------------------
+void slab_rows(int mode, int nx, int ny, int nz, int nv, double h, double du, double dso, double dod, int z0, int n,
+               int& r0, int& r1);
+void slab_rows(const Geometry& g, int z0, int n, int& r0, int& r1);  // rows a z-slab's rays reach
+void band_partition(int mode, int nx, int ny, int nz, int nv, double h, double du, double dso, double dod, int nranks,
+                    const int* z0s, const int* ns, int* t0, int* t1, int* o0, int* o1);
+template <class T>
+struct BandSum {
+    struct Src {
+        const T* p;
+        int r0, r1;  // global rows covered
+        int rp, roff;  // rows per view in the buffer, global row of its first row
+    } src[32];
+    int n;
+    int o0, o1;  // this rank's owned rows
+};
+template <class T>
+void band_sum(const Geometry& g, const BandSum<T>& bs, T* y, cudaStream_t s);
+// A x partials -> owners (rank-ordered sums, other held rows zeroed), in place
+template <class T>
+void band_reduce(Geometry& g, T* y, cudaStream_t s);
+// y with the held rows other ranks own filled in (for A^T b); returns the handle's scratch
+template <class T>
+const T* band_halo(Geometry& g, const T* y, cudaStream_t s);
+void comm_exchange(Comm* c, const std::vector<ctk_p2p_op>& ops, int dtype, cudaStream_t s);
 
 uint64_t launch_count();
 

@@ -186,7 +186,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
     const int a = vorder[blockIdx.y];
     const int iu = blockIdx.x * ZW_BC + threadIdx.y;
     float out = 0.f;
-    const bool live = iu < g.nu && iv < g.nv;
+    const bool live = iu < g.nu && iv < g.nv && iv >= g.w0 && iv < g.w0 + g.nw;  // rows held (band-sharded range)
     if (live) {
         const int c = a * g.nu + iu;
         const double2 cs = g.colstep[c];
@@ -363,15 +363,15 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
         const int t = threadIdx.x + ZW_BR * threadIdx.y;
         const int r = t / ZW_BC, cc = t % ZW_BC;
         const int ivw = band * ZW_BR + r, iuw = blockIdx.x * ZW_BC + cc;
-        if (ivw < g.nv && iuw < g.nu) {
-            float* yo = y + size_t(a) * g.nu * g.nv + size_t(ivw) * g.nu + iuw;
+        if (ivw >= g.w0 && ivw < g.w0 + g.nw && iuw < g.nu) {
+            float* yo = y + (size_t(a) * g.nw + size_t(ivw - g.w0)) * g.nu + iuw;
             *yo = chunk == 0 ? outs[r][cc] : *yo + outs[r][cc];
         }
     }
     if (MODE != 0) {
         double rr = 0.0;
         if (live) {
-            const double d = double(out) - double(__ldg(b + size_t(a) * g.nu * g.nv + size_t(iv) * g.nu + iu));
+            const double d = double(out) - double(__ldg(b + (size_t(a) * g.nw + size_t(iv - g.w0)) * g.nu + iu));
             rr = d * d;
         }
         rr = block_sum(rr);
@@ -453,19 +453,12 @@ void slab_bands(const Geometry& g, int& b0, int& b1) {
     b0 = 0;
     b1 = nb;
     if (!g.slab || g.nv == 1) return;
-    const double h = g.h, cz = 0.5 * (g.nz - 1);
-    const double zlo = (g.z0 - 2.0 - cz) * h, zhi = (g.z0 + g.nz_local() + 1.0 - cz) * h;  // taps + margin
-    double vlo = zlo, vhi = zhi;
-    if (g.mode == CTK_CONE3D) {
-        const double R = 0.5 * h * std::sqrt(double(g.nx) * g.nx + double(g.ny) * g.ny) + 2.0 * h;
-        if (!(g.dso - R > 0.0)) return;
-        const double D = g.dso + g.dod, dn = g.dso - R, df = g.dso + R;
-        vlo = std::min(zlo * D / dn, zlo * D / df);
-        vhi = std::max(zhi * D / dn, zhi * D / df);
+    int r0, r1;
+    slab_rows(g, g.z0, g.nz_local(), r0, r1);
+    if (g.band) {  // only the rows this rank holds
+        r0 = std::max(r0, g.w0);
+        r1 = std::min(r1, g.w0 + g.nw);
     }
-    const double cv = 0.5 * (g.nv - 1);
-    const int r0 = std::max(0, int(std::floor(vlo / g.du + cv)) - 2);
-    const int r1 = std::min(g.nv, int(std::ceil(vhi / g.du + cv)) + 3);
     if (r1 <= r0) {
         b1 = b0;
         return;
@@ -489,7 +482,7 @@ void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
     int b0, b1;
     slab_bands(g, b0, b1);
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    if (b0 > 0 || b1 < int((g.nv + ZW_BR - 1) / ZW_BR))
+    if (b0 > 0 || b1 < int((g.nv + ZW_BR - 1) / ZW_BR) || g.band)
         CTK_CUDA(cudaMemsetAsync(y, 0, g.range() * sizeof(float), s));  // rows no launched band writes
     for (int c = 0; c < nch; ++c) launch_ax<0>(g, x, y, nullptr, nullptr, s, nch, c, b0, b1);
     CTK_CUDA(cudaEventRecord(g.ev1, s));

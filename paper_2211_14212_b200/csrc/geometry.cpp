@@ -44,6 +44,8 @@ KGeom Geometry::kgeom() const {
     k.nz = nz_local();
     k.nzg = nz;
     k.z0 = slab ? z0 : 0;
+    k.w0 = band ? w0 : 0;
+    k.nw = band ? nw : nv;
     k.na = na;
     k.has_zrays = has_zrays ? 1 : 0;
     k.dso = dso;

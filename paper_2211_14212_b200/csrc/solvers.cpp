@@ -15,7 +15,10 @@
 //   z-slab          domain vectors are this rank's slab of z-slices; domain reductions are
 //                   summed in rank order and every A x partial projection set is
 //                   sum-reduced (by linearity A x = sum_r A x_r), so all ranks hold
-//                   identical range vectors; the TV stencils exchange one-slice halos.
+//                   identical range vectors; the TV stencils exchange one-slice halos;
+//   z-slab + band   (ctk_geom_shard_range) range vectors hold the rank's detector-row window
+//                   too: A x partials go to the rows' owners, A^T b fetches its halo rows
+//                   (bands.cpp) and range reductions are summed over ranks as well.
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -66,14 +69,19 @@ struct Dev {
     Dev(Geometry& g_, int v) : g(g_), variant(v), s(g_.stream), w(red_work(&g_)) {}
 
     bool slab_mode() const { return g.comm && g.slab; }
-    // are vectors of this space split across ranks (their reductions summed)?
-    bool sharded(bool range) const { return g.comm && (g.slab ? !range : range); }
+    // are vectors of this space split across ranks (their reductions summed)?  With the
+    // band-sharded range (bands.cpp) both spaces are: range vectors hold this rank's row
+    // window with the rows it does not own at zero
+    bool sharded(bool range) const { return g.comm && (g.slab ? (!range || g.band) : range); }
     void ax(const T* x, T* y) {
         op_ax<T>(g, x, y, s);
-        if (slab_mode()) comm_allreduce(g.comm, y, g.range(), sizeof(T) == 8 ? 1 : 0, s);
+        if (slab_mode()) {
+            if (g.band) band_reduce<T>(g, y, s);  // partials to the rows' owners, rank order
+            else comm_allreduce(g.comm, y, g.range(), sizeof(T) == 8 ? 1 : 0, s);
+        }
     }
     void atb(const T* y, T* x) {
-        op_atb<T>(g, variant, y, x, s);
+        op_atb<T>(g, variant, g.band ? band_halo<T>(g, y, s) : y, x, s);
         if (g.comm && !g.slab) comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
     }
     double fetch(int slot) {
@@ -99,9 +107,24 @@ struct Dev {
         comm_allreduce(g.comm, halo->p, S * R, sizeof(T) == 8 ? 1 : 0, s);
         return halo->as<T>();
     }
+    // point-to-point halo when the transport has it (NCCL, or an exchange callback): send
+    // `mine` to rank `to`, receive rank `from`'s slice into the halo buffer (-1: none)
+    bool p2p() const { return g.comm->nccl_comm || g.comm->cb.exchange; }
+    const T* swap_slice(const T* mine, int to, int from) {
+        const size_t S = size_t(g.nx) * g.ny;
+        if (!halo) halo = &pooled();
+        halo->ensure(sizeof(T) * S);
+        std::vector<ctk_p2p_op> ops;
+        if (to >= 0) ops.push_back({to, 1, const_cast<T*>(mine), S});
+        if (from >= 0) ops.push_back({from, 0, halo->p, S});
+        comm_exchange(g.comm, ops, sizeof(T) == 8 ? 1 : 0, s);
+        return from >= 0 ? halo->as<T>() : nullptr;
+    }
     // the next rank's first slice of x (null when unsharded or on the last slab)
     const T* slice_above(const T* x) {
         if (!slab_mode()) return nullptr;
+        const int r = g.comm->cb.rank;
+        if (p2p()) return swap_slice(x, r > 0 ? r - 1 : -1, last_slab() ? -1 : r + 1);
         const T* all = gather_slices(x);
         return last_slab() ? nullptr : all + size_t(g.comm->cb.rank + 1) * size_t(g.nx) * g.ny;
     }
@@ -117,6 +140,8 @@ struct Dev {
         } else {
             CTK_CUDA(cudaMemcpyAsync(wtop.p, gz + top, sizeof(T) * S, cudaMemcpyDeviceToDevice, s));
         }
+        const int r = g.comm->cb.rank;
+        if (p2p()) return swap_slice(wtop.p, last_slab() ? -1 : r + 1, r > 0 ? r - 1 : -1);
         const T* all = gather_slices(wtop.p);
         return g.comm->cb.rank == 0 ? nullptr : all + size_t(g.comm->cb.rank - 1) * S;
     }
