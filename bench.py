@@ -302,23 +302,23 @@ def main():
         return getattr(ctk, args.solver)(pair, bb, opts)
     # synthetic inputs, resident in HBM: phantom rasterised on the device, b = A x
     x_true = ctk.shepp_logan_3d(n)
+    comm = NcclComm(rank, world) if world > 1 else None
     if args.shard == "slab":
-        # z-slab: this rank's slices of x; b (replicated) from the whole-volume operator (setup)
+        # z-slab with the band-sharded range: this rank's slices of x and its
+        # detector-row window of b; b from the whole-volume operator (setup, not timed)
         z0, nzl = shard_slabs(n, world, rank)
         b = torch.empty(ctk.projector_pair(full).range_size, dtype=torch.float32, device="cuda")
         ctk.projector_pair(full).forward(x_true, b)
         x_true = x_true[z0 * n * n:(z0 + nzl) * n * n].contiguous()
-        pair = ctk.projector_pair(full, slab=(z0, nzl), projector=proj_kind)
+        pair = ctk.projector_pair(full, slab=(z0, nzl), projector=proj_kind, comm=comm, shard_range=comm is not None)
+        if comm is not None:
+            b = pair.projector.local_range(b).contiguous()
     else:
         first, count = shard_angles(na, world, rank)
-        pair = ctk.projector_pair(full.subset(first, count), projector=proj_kind)
+        pair = ctk.projector_pair(full.subset(first, count), projector=proj_kind, comm=comm)
         b = torch.empty(pair.range_size, dtype=torch.float32, device="cuda")
         pair.forward(x_true, b)
     proj = pair.projector
-    comm = None
-    if world > 1:
-        comm = NcclComm(rank, world)
-        proj.attach_comm(comm)
     torch.cuda.synchronize()
     opts = ctk.SolverOptions(max_iters=args.iters, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
 

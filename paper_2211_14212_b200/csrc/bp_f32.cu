@@ -112,9 +112,12 @@ __device__ __forceinline__ int z_col(int e) { return e; }
 // SID = 1: the transpose of the f32 Siddon forward (f32_common.cuh model) in the same
 // structure: phase 1 fills two Z columns per slot (the column's two in-plane cells at the
 // plane), each registered in its row with weight 1 (L is in pg).
-template <int CLASS, int PB, int SID = 0>
+template <int CLASS, int PB, int SID = 0, int WIN = 0>
 __global__ void __launch_bounds__(PB, PlaneCfg<PB>::MINB)
 k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles) {
+    // WIN: the band-sharded range's row window (W0, NW); else the whole detector, with
+    // the window folded to constants so the common case keeps its register allocation
+    const int W0 = WIN ? g.w0 : 0, NW = WIN ? g.nw : g.nv;
     constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
     constexpr int NL = PB;  // registration lists, one per row
     extern __shared__ __align__(16) float sm[];
@@ -125,7 +128,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     int* cnt = lists + NL * BP_SL;                              // [NL]
     float* eth = reinterpret_cast<float*>(cnt + NL);            // [BP_PB]
     static_assert((NL * BP_SL) % 4 == 0 && NL % 4 == 0, "keeps vrtab 16-byte aligned");
-    const int nv4 = 4 * pg_groups(g.nw);  // held rows, local index (band-sharded range)
+    const int nv4 = 4 * pg_groups(NW);  // held rows, local index (band-sharded range)
     float* vrtab = eth + BP_PB;                                 // [nv4] iv - (nv-1)/2, 16-byte aligned
     float* ivrtab = vrtab + (SID ? nv4 : 0);                    // Siddon: [nv4] 1/|iv - (nv-1)/2|
     int2* urange = reinterpret_cast<int2*>(vrtab + (SID ? 2 : 1) * nv4);  // [na]
@@ -141,8 +144,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
     for (int q = t; q < nv4; q += BP_PB) {
-        vrtab[q] = row_vr(g, g.w0 + q);
-        if (SID) ivrtab[q] = __frcp_rn(fabsf(row_vr(g, g.w0 + q)));
+        vrtab[q] = row_vr(g, W0 + q);
+        if (SID) ivrtab[q] = __frcp_rn(fabsf(row_vr(g, W0 + q)));
     }
     const int sc = slice_centre(s);  // anchored positions (f32_common.cuh): block centre of plane s
     const float kf = float(s - sc);
@@ -152,7 +155,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     const float invdu = float(1.0 / g.du);
     const float fs = float(s);
     const double h = g.h;
-    const int nq = pg_groups(g.nw);  // row groups of the grouped projection layout
+    const int nq = pg_groups(NW);  // row groups of the grouped projection layout
     // world coordinates of the plane and of the tile's row segment ends
     const double plane_c = (s - 0.5 * ((CLASS ? g.ny : g.nx) - 1)) * h;
     const double r_lo = (p0 - (SID ? 2.5 : 1.5) - 0.5 * (nh - 1)) * h,
@@ -275,8 +278,10 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             v0 = lo;
                             v1 = hi;
                         }
-                        v0 = max(v0, g.w0) - g.w0;  // held rows, local index
-                        v1 = min(v1, g.w0 + g.nw - 1) - g.w0;
+                        if constexpr (WIN) {  // held rows, local index
+                            v0 = max(v0, W0) - W0;
+                            v1 = min(v1, W0 + NW - 1) - W0;
+                        }
                         const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
                         const size_t qs = size_t(g.nu);
                         float* zc = Z + z_col(t);
@@ -414,9 +419,10 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             v0 = lo;
                             v1 = hi;
                         }
-                        // the held rows, local index from here on
-                        v0 = max(v0, g.w0) - g.w0;
-                        v1 = min(v1, g.w0 + g.nw - 1) - g.w0;
+                        if constexpr (WIN) {  // the held rows, local index from here on
+                            v0 = max(v0, W0) - W0;
+                            v1 = min(v1, W0 + NW - 1) - W0;
+                        }
                         // column iu of view a, row group q: pc4[q * nu] (grouped layout)
                         const float4* pc4 = reinterpret_cast<const float4*>(pg) + size_t(a) * nq * g.nu + iu;
                         const size_t qs = size_t(g.nu);
@@ -815,7 +821,7 @@ void group_proj(Geometry& g, const float* y, cudaStream_t s) {
     after_launch("k_proj_group4");
 }
 
-template <int CLASS, int PB, int SID>
+template <int CLASS, int PB, int SID, int WIN>
 void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
     const int nh = CLASS ? g.nx : g.ny;
@@ -834,11 +840,11 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
     int dev = 0;
     CTK_CUDA(cudaGetDevice(&dev));
     std::call_once(opted[dev & 63], [] {
-        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB, SID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB, SID, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
     });
     dim3 grd(unsigned(planes), unsigned(ptiles * kbands));
-    k_atb_plane_f32<CLASS, PB, SID><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
+    k_atb_plane_f32<CLASS, PB, SID, WIN><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
     after_launch(SID ? "k_atb_plane_f32_siddon" : "k_atb_plane_f32");
 }
 
@@ -850,13 +856,15 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
         return e ? std::atoi(e) : 0;
     }();
     const int pb = forced == 128 || forced == 256 ? forced : (nh <= 768 ? 128 : 256);
-    const bool sid = g.projector == CTK_PROJ_SIDDON;
+    const bool sid = g.projector == CTK_PROJ_SIDDON;  // (Siddon has no band-sharded range)
     if (pb == 128) {
-        if (sid) launch_plane_pb<CLASS, 128, 1>(g, x, s);
-        else launch_plane_pb<CLASS, 128, 0>(g, x, s);
+        if (sid) launch_plane_pb<CLASS, 128, 1, 0>(g, x, s);
+        else if (g.band) launch_plane_pb<CLASS, 128, 0, 1>(g, x, s);
+        else launch_plane_pb<CLASS, 128, 0, 0>(g, x, s);
     } else {
-        if (sid) launch_plane_pb<CLASS, 256, 1>(g, x, s);
-        else launch_plane_pb<CLASS, 256, 0>(g, x, s);
+        if (sid) launch_plane_pb<CLASS, 256, 1, 0>(g, x, s);
+        else if (g.band) launch_plane_pb<CLASS, 256, 0, 1>(g, x, s);
+        else launch_plane_pb<CLASS, 256, 0, 0>(g, x, s);
     }
 }
 

@@ -36,7 +36,10 @@ namespace {
 #ifndef CTK_FWD_CHUNKS
 #define CTK_FWD_CHUNKS 2  // minimum slice chunks per ray (fwd_chunks); 64.8 -> 50.4 ms at 512^3 vs unchunked
 #endif
-constexpr int ZW_BR = 32, ZW_BC = CTK_FWD_BC;  // block: 32 detector rows (lanes) x ZW_BC columns
+#ifndef CTK_FWD_UNROLL
+#define CTK_FWD_UNROLL 1
+#endif
+constexpr int ZW_BR = 32, ZW_BC = CTK_FWD_BC, kFwdUnroll = CTK_FWD_UNROLL;  // block: 32 detector rows (lanes) x ZW_BC columns
 // zero guard planes on each side of the z-fast layouts (h and z): a tap index may step one
 // beyond the contributing range where anchored positions round across a voxel boundary
 constexpr int kPad = 2;
@@ -307,7 +310,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
                 const float2 thA2 = make_float2(thA, thA), Wr2 = make_float2(Wr, Wr), S2 = make_float2(S, S);
                 float2 k2 = make_float2(float(s - sc), float(s - sc + 1));
                 const int cnt = se - s + 1;
-#pragma unroll 1
+#pragma unroll kFwdUnroll
                 for (int np = cnt >> 1; np > 0; --np) {
                     const float2 fh = __ffma2_rn(k2, fhd2, thA2);
                     const float2 wlo = __ffma2_rn(k2, Wd2, Wr2);

@@ -58,7 +58,9 @@ KGeom Geometry::kgeom() const {
     k.colaxis = d_colaxis.as<unsigned char>();
     k.vclass = d_vclass.as<int4>();
     k.colstep = d_colstep.as<double2>();
+#ifdef CTK_CHECKED
     k.chk = d_chk.as<unsigned>();
+#endif
     return k;
 }
 
