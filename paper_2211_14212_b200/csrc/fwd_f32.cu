@@ -178,18 +178,20 @@ __device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int n
 // (deterministic: the launches are ordered on the stream).
 // SID = 1: the f32 Siddon model (f32_common.cuh) on the same layouts: per slab the four
 // cells (ja|ja+sy, ka|ka+sz) of the chord instead of the four bilinear taps.
-template <int MODE, class Off, int SID = 0>
+template <int MODE, class Off, int SID = 0, int WIN = 0>
 __global__ void __launch_bounds__(ZW_BR * ZW_BC)
 k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
                const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
                double* __restrict__ partials, int nch, int chunk, int band0) {
+    // WIN: the band-sharded range's row window; else the whole detector (constants)
+    const int W0 = WIN ? g.w0 : 0, NW = WIN ? g.nw : g.nv;
     __shared__ float outs[ZW_BR][ZW_BC + 1];
     const int band = blockIdx.z + band0;
     const int iv = band * ZW_BR + threadIdx.x;
     const int a = vorder[blockIdx.y];
     const int iu = blockIdx.x * ZW_BC + threadIdx.y;
     float out = 0.f;
-    const bool live = iu < g.nu && iv < g.nv && iv >= g.w0 && iv < g.w0 + g.nw;  // rows held (band-sharded range)
+    const bool live = iu < g.nu && iv < g.nv && iv >= W0 && iv < W0 + NW;  // rows held (band-sharded range)
     if (live) {
         const int c = a * g.nu + iu;
         const double2 cs = g.colstep[c];
@@ -366,15 +368,15 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
         const int t = threadIdx.x + ZW_BR * threadIdx.y;
         const int r = t / ZW_BC, cc = t % ZW_BC;
         const int ivw = band * ZW_BR + r, iuw = blockIdx.x * ZW_BC + cc;
-        if (ivw >= g.w0 && ivw < g.w0 + g.nw && iuw < g.nu) {
-            float* yo = y + (size_t(a) * g.nw + size_t(ivw - g.w0)) * g.nu + iuw;
+        if (ivw >= W0 && ivw < W0 + NW && iuw < g.nu) {
+            float* yo = y + (size_t(a) * NW + size_t(ivw - W0)) * g.nu + iuw;
             *yo = chunk == 0 ? outs[r][cc] : *yo + outs[r][cc];
         }
     }
     if (MODE != 0) {
         double rr = 0.0;
         if (live) {
-            const double d = double(out) - double(__ldg(b + (size_t(a) * g.nw + size_t(iv - g.w0)) * g.nu + iu));
+            const double d = double(out) - double(__ldg(b + (size_t(a) * NW + size_t(iv - W0)) * g.nu + iu));
             rr = d * d;
         }
         rr = block_sum(rr);
@@ -416,12 +418,14 @@ void launch_ax(Geometry& g, const float* x, float* y, const float* b, double* pa
     dim3 grd = fwd_grid(g);
     if (band1 >= 0) grd.z = unsigned(band1 - band0);
     if (grd.z == 0) return;
-    const bool sid = g.projector == CTK_PROJ_SIDDON;
+    const bool sid = g.projector == CTK_PROJ_SIDDON;  // (no band-sharded range with Siddon)
     if (wide_offsets(g)) {
         if (sid) k_ax_zfast_f32<MODE, long long, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
+        else if (g.band) k_ax_zfast_f32<MODE, long long, 0, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
         else k_ax_zfast_f32<MODE, long long><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
     } else {
         if (sid) k_ax_zfast_f32<MODE, int, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
+        else if (g.band) k_ax_zfast_f32<MODE, int, 0, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
         else k_ax_zfast_f32<MODE, int><<<grd, blk, 0, s>>>(k, vo, a0, a1, x, y, b, partials, nch, chunk, band0);
     }
     after_launch(MODE == 0 ? "k_ax_zfast_f32" : "k_ax_zfast_f32_residual");
