@@ -137,3 +137,19 @@ def test_c4_hybrid_gcv_subset(ctk, reference):
     lam = np.array(res.log.lambda_)
     assert lam.size == want["lambda"].size
     assert np.all(np.abs(lam - want["lambda"]) <= 1e-3 * np.abs(want["lambda"]))
+
+
+@pytest.mark.timeout(2400)
+def test_c5_cgls_tv_subset(ctk, reference):
+    """C5: IRN-TV-CGLS 1 outer x 3 inner, 1024^3 / 1024^2 on 4 of the 1600 views (f32 device
+    path vs the reference T=double; lambda 0.1 as the bench preset)."""
+    g = _geom(1024, 1600, 4)
+    reference.set_threads(_threads())
+    try:
+        _, b = _phantom_b(ctk, reference, g, 1024)
+        want = reference.solve(g, b, "cgls_tv", 3, lam=0.1, outer=1, inner=3, tol=0.0, stop_inc=False)
+    finally:
+        reference.set_threads(1)
+    res = ctk.cgls_tv(ctk.projector_pair(to_ctk(g)), b.astype(np.float32), 0.1, 1, 3, _opts(ctk, 3))
+    _check(res, want, 3)
+    assert list(res.outer_starts) == list(want["outer_starts"])
