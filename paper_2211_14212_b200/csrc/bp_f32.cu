@@ -91,10 +91,6 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 template <int PB>
 struct PlaneCfg;
 template <>
-struct PlaneCfg<64> {  // small planes (<= 64 rows, e.g. C1): a 128-row tile would idle half its threads
-    static constexpr int SL = CTK_BP_SL128, MINB = 12;
-};
-template <>
 struct PlaneCfg<128> {
     static constexpr int SL = CTK_BP_SL128, MINB = 6;
 };
@@ -856,16 +852,12 @@ template <int CLASS>
 void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int nh = CLASS ? g.nx : g.ny;
     static const int forced = [] {
-        const char* e = std::getenv("CTK_BP_TILE");  // A/B timing: 64, 128 or 256
+        const char* e = std::getenv("CTK_BP_TILE");  // A/B timing: 128 or 256
         return e ? std::atoi(e) : 0;
     }();
-    const int pb = forced == 64 || forced == 128 || forced == 256 ? forced : (nh <= 64 ? 64 : nh <= 768 ? 128 : 256);
+    const int pb = forced == 128 || forced == 256 ? forced : (nh <= 768 ? 128 : 256);
     const bool sid = g.projector == CTK_PROJ_SIDDON;  // (Siddon has no band-sharded range)
-    if (pb == 64) {
-        if (sid) launch_plane_pb<CLASS, 64, 1, 0>(g, x, s);
-        else if (g.band) launch_plane_pb<CLASS, 64, 0, 1>(g, x, s);
-        else launch_plane_pb<CLASS, 64, 0, 0>(g, x, s);
-    } else if (pb == 128) {
+    if (pb == 128) {
         if (sid) launch_plane_pb<CLASS, 128, 1, 0>(g, x, s);
         else if (g.band) launch_plane_pb<CLASS, 128, 0, 1>(g, x, s);
         else launch_plane_pb<CLASS, 128, 0, 0>(g, x, s);
