@@ -1,0 +1,6 @@
+for rep in 1 2; do
+for v in default c_bce3caa; do
+  if [ $v = default ]; then L=""; else L="build_variants/$v/libctk_b200.so"; fi
+  CTK_B200_LIB=$L timeout 300 python tools/time_bp.py --n 512 --angles 360 --reps 7
+done
+done
