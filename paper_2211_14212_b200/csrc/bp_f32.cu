@@ -266,8 +266,11 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                         int v0 = 0, v1 = g.nv - 1;
                         if (gs > 0.f) {
                             const float rg = invdu / gs;
-                            v0 = max(v0, int(floorf(fmaf(float(kg0) - 1.5f - czf, rg, cvf))) - 2);
-                            v1 = min(v1, int(ceilf(fmaf(float(kg0 + BP_KB) + 0.5f - czf, rg, cvf))) + 2);
+                            // a row reaches the band iff its centre-plane fz lies in
+                            // [kg0 - 2, kg0 + KB) (cells kl, kl+1 at the slab boundaries, which are
+                            // within half a slice of the centre plane); one row of margin
+                            v0 = max(v0, int(floorf(fmaf(float(kg0) - 2.f - czf, rg, cvf))) - 1);
+                            v1 = min(v1, int(ceilf(fmaf(float(kg0 + BP_KB) - czf, rg, cvf))) + 1);
                         }
                         if (g.has_zrays) {  // z-dominant rows: the exact gather (siddon.cu, zonly)
                             const double dA = g.colstep[c].y;
