@@ -70,33 +70,26 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 //           in shared memory; it registers itself in the (at most two) rows its in-plane
 //           stencil touches;
 //  phase 2  thread p owns row p (BP_KB accumulators in registers) and adds wh * Z[:][e] of
-//           the columns registered in its row, sorted by column -> deterministic order.
+//           the slots registered in its row: a per-row bit mask over the batch's slots,
+//           walked with __ffs in slot order -> deterministic, the (view, column) order.
+//           (Round 1 kept sorted per-row lists of up to 11 entries with an overflow scan;
+//           the masks take 1 KB less shared memory, one 16-byte load per row, no sort.)
 // Z[k][e] has row stride BP_PB: phase-1 lanes (consecutive e) hit distinct banks whatever
 // their k, phase-2 lanes (consecutive rows -> consecutive e) likewise.
-// Tile size PB (rows = threads per CTA) is a template parameter with its own row-list
-// capacity SL and occupancy (measured, matched A^T b f32):
-//   PB = 128, 6 CTAs/SM: 256^3/180 4.61 ms, 512^3/360 66.9 ms (SL = 9/10/11/12: 71.2/67.7/66.9/69.0)
-//   PB = 256, 3 CTAs/SM: 256^3/180 5.32 ms, 512^3/360 72.8 ms, 512^3/720 147 ms,
-//                        1024^3/1600 2518 ms at SL = 11 (SL = 10/12/14: 2563/2565/3275;
-//                        PB = 128: 3034 ms -- per-CTA setup over 1600 views, twice the tiles)
-// so the launcher takes PB = 128 up to 768 rows per plane and PB = 256 beyond.  Smaller
-// lists (SL = 8 at PB = 128) overflow into the slow scan: 74.5 ms.  Without view batching
-// 4 CTAs/SM (64 regs) was best.
-#ifndef CTK_BP_SL128
-#define CTK_BP_SL128 11
-#endif
-#ifndef CTK_BP_SL256
-#define CTK_BP_SL256 11
-#endif
+// Tile size PB (rows = threads per CTA) is a template parameter with its own occupancy
+// (round 1, matched A^T b f32): PB = 128, 6 CTAs/SM: 512^3/360 66.9 ms; PB = 256, 3 CTAs/SM:
+// 512^3/360 72.8 ms, 1024^3/1600 2518 ms (PB = 128: 3034 ms -- per-CTA setup over 1600
+// views, twice the tiles), so the launcher takes PB = 128 up to 768 rows per plane and
+// PB = 256 beyond.
 template <int PB>
 struct PlaneCfg;
 template <>
 struct PlaneCfg<128> {
-    static constexpr int SL = CTK_BP_SL128, MINB = 6;
+    static constexpr int MINB = 6;
 };
 template <>
 struct PlaneCfg<256> {
-    static constexpr int SL = CTK_BP_SL256, MINB = 3;
+    static constexpr int MINB = 3;
 };
 #ifndef CTK_BP_KB
 #define CTK_BP_KB 32
@@ -118,22 +111,23 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     // WIN: the band-sharded range's row window (W0, NW); else the whole detector, with
     // the window folded to constants so the common case keeps its register allocation
     const int W0 = WIN ? g.w0 : 0, NW = WIN ? g.nw : g.nv;
-    constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
-    constexpr int NL = PB;  // registration lists, one per row
+    constexpr int BP_PB = PB;
+    constexpr int MW = PB / 32;  // registration mask words per row
     extern __shared__ __align__(16) float sm[];
     constexpr int ZS = z_stride<PB>();                          // row stride of Z
     float* Z = sm + BP_ZG * ZS;                                 // [-BP_ZG, BP_KB+BP_ZG) x [ZS]
     float* Z2 = Z + (BP_KB + 2 * BP_ZG) * ZS;                   // Siddon: the second in-plane cell
-    int* lists = reinterpret_cast<int*>(Z + (BP_KB + BP_ZG + (SID ? BP_KB + 2 * BP_ZG : 0)) * ZS);  // [NL][BP_SL]
-    int* cnt = lists + NL * BP_SL;                              // [NL]
-    float* eth = reinterpret_cast<float*>(cnt + NL);            // [BP_PB]
-    static_assert((NL * BP_SL) % 4 == 0 && NL % 4 == 0, "keeps vrtab 16-byte aligned");
+    // registration: bit e of row p's mask <=> slot e touches row p (its in-plane stencil rows
+    // are eih[e] and eih[e] + 1, with weights 1 - eth[e] and eth[e]; Siddon: its cells)
+    unsigned* rmask = reinterpret_cast<unsigned*>(Z + (BP_KB + BP_ZG + (SID ? BP_KB + 2 * BP_ZG : 0)) * ZS);  // [PB][MW]
+    int* eih = reinterpret_cast<int*>(rmask + BP_PB * MW);     // [BP_PB]
+    float* eth = reinterpret_cast<float*>(eih + BP_PB);         // [BP_PB]
+    static_assert(MW % 4 == 0 && BP_PB % 4 == 0, "keeps the masks and vrtab 16-byte aligned");
     const int nv4 = 4 * pg_groups(NW);  // held rows, local index (band-sharded range)
     float* vrtab = eth + BP_PB;                                 // [nv4] iv - (nv-1)/2, 16-byte aligned
     float* ivrtab = vrtab + (SID ? nv4 : 0);                    // Siddon: [nv4] 1/|iv - (nv-1)/2|
     int2* urange = reinterpret_cast<int2*>(vrtab + (SID ? 2 : 1) * nv4);  // [na]
     int* pref = reinterpret_cast<int*>(urange + g.na);          // [na + 1] candidate prefix sums
-    int* slotcol = pref + g.na + 1;                             // [BP_PB] (view, column) of a slot
 
     const int t = threadIdx.x;
     // plane index fastest: a wave of resident CTAs shares one (row tile, z band), so per
@@ -231,7 +225,8 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     for (int b0 = 0; b0 < total; b0 += BP_PB) {
         {
             // ---- phase 1 ----
-            if (t < NL) cnt[t] = 0;
+#pragma unroll
+            for (int w = 0; w < MW; w += 4) *reinterpret_cast<uint4*>(rmask + t * MW + w) = make_uint4(0u, 0u, 0u, 0u);
             int a = -1, iu = 0;
             const int gidx = b0 + t;
             if (gidx < total) {  // the view of this slot: pref[a] <= gidx < pref[a + 1]
@@ -239,7 +234,6 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                 a = a_run;
                 iu = urange[a].x + (gidx - pref[a]);
             }
-            slotcol[t] = a >= 0 ? a * g.nu + iu : -1;
             __syncthreads();
             if (a >= 0) {
                 const int c = a * g.nu + iu;
@@ -384,15 +378,12 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                                 }
                             }
                         }
-                        // register: row ja reads Z (entry 2t), row jb != ja reads Z2 (entry 2t+1)
-                        if (ja >= p0 && ja <= p0 + BP_PB - 1 && ja >= 0 && ja < nh) {
-                            const int sl = atomicAdd(&cnt[ja - p0], 1);
-                            if (sl < BP_SL) lists[(ja - p0) * BP_SL + sl] = (t << 1);
-                        }
-                        if (jb != ja && jb >= p0 && jb <= p0 + BP_PB - 1 && jb >= 0 && jb < nh) {
-                            const int sl = atomicAdd(&cnt[jb - p0], 1);
-                            if (sl < BP_SL) lists[(jb - p0) * BP_SL + sl] = (t << 1) | 1;
-                        }
+                        // register: row ja reads Z, row jb != ja reads Z2
+                        eih[t] = ja;
+                        if (ja >= p0 && ja <= p0 + BP_PB - 1 && ja >= 0 && ja < nh)
+                            atomicOr(&rmask[(ja - p0) * MW + (t >> 5)], 1u << (t & 31));
+                        if (jb != ja && jb >= p0 && jb <= p0 + BP_PB - 1 && jb >= 0 && jb < nh)
+                            atomicOr(&rmask[(jb - p0) * MW + (t >> 5)], 1u << (t & 31));
                     }
                 } else {
                     const float4 cd = g.col[c];
@@ -534,79 +525,35 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
                             }
                         }
                         eth[t] = th;
-                        if (ih >= p0) {
-                            const int sl = atomicAdd(&cnt[ih - p0], 1);
-                            if (sl < BP_SL) lists[(ih - p0) * BP_SL + sl] = (t << 1);
-                        }
-                        if (ih + 1 <= p0 + BP_PB - 1 && th != 0.f) {
-                            const int sl = atomicAdd(&cnt[ih + 1 - p0], 1);
-                            if (sl < BP_SL) lists[(ih + 1 - p0) * BP_SL + sl] = (t << 1) | 1;
-                        }
+                        eih[t] = ih;
+                        if (ih >= p0) atomicOr(&rmask[(ih - p0) * MW + (t >> 5)], 1u << (t & 31));
+                        if (ih + 1 <= p0 + BP_PB - 1 && th != 0.f)
+                            atomicOr(&rmask[(ih + 1 - p0) * MW + (t >> 5)], 1u << (t & 31));
                     }
                 }
                 }
             }
             __syncthreads();
-            // ---- phase 2: row p gathers its registered columns in column order ----
-            const int n = cnt[t];
-            if (n > 0 && p < nh) {
-                if (n <= BP_SL) {
-                    int lst[BP_SL];
+            // ---- phase 2: row p gathers its registered slots in slot order, i.e. in (view,
+            // column) order: deterministic, and the order of the reference's scatter ----
+            if (p < nh) {
 #pragma unroll
-                    for (int q = 0; q < BP_SL; ++q) lst[q] = q < n ? lists[t * BP_SL + q] : 0x7fffffff;
-                    // insertion sort of the n registered entries (n is small: 2-6 typically)
+                for (int w4 = 0; w4 < MW; w4 += 4) {
+                    const uint4 m4 = *reinterpret_cast<const uint4*>(rmask + t * MW + w4);
+                    const unsigned mw[4] = {m4.x, m4.y, m4.z, m4.w};
 #pragma unroll
-                    for (int i = 1; i < BP_SL; ++i) {
-                        if (i >= n) break;
-#pragma unroll
-                        for (int j = i; j > 0; --j)
-                            if (lst[j - 1] > lst[j]) { const int tmp = lst[j]; lst[j] = lst[j - 1]; lst[j - 1] = tmp; }
-                    }
-#pragma unroll
-                    for (int q = 0; q < BP_SL; ++q) {
-                        if (q >= n) break;
-                        const int e = lst[q] >> 1;
-                        CTK_CHK(g, e < BP_PB, 3);
-                        if constexpr (SID) {
-                            add_sid((lst[q] & 1) ? Z2 : Z, e);
-                        } else {
-                            const float th = eth[e];
-                            const float wh = (lst[q] & 1) ? th : 1.f - th;
-                            add_entry(wh, e);
-                        }
-                    }
-                } else {
-                    // overflow (very fine detector sampling): scan every slot of the batch in order
-                    for (int e = 0; e < BP_PB; ++e) {
-                        const int c = slotcol[e];
-                        if (c < 0 || g.colaxis[c] != CLASS) continue;
-                        if constexpr (SID) {
-                            int jA, ja;
-                            float tA, fy;
-                            double G;
-                            const float fhd = g.col[c].y;
-                            sid_anchor(g.col64[c], sc, jA, tA, G);
-                            split(fmaf(kf - 0.5f, fhd, tA), ja, fy);
-                            ja += jA;
-                            const float cy = sid_cross(fy, sid_coef(fhd >= 0.f, __frcp_rn(fabsf(fhd))));
-                            const int jb = cy < 1.f ? (fhd >= 0.f ? ja + 1 : ja - 1) : ja;
-                            if (jlo_ok(ja, jb)) {
-                                if (ja == p) add_sid(Z, e);
-                                if (jb != ja && jb == p) add_sid(Z2, e);
+                    for (int j = 0; j < 4; ++j) {
+                        unsigned bits = mw[j];
+                        while (bits) {
+                            const int e = (w4 + j) * 32 + __ffs(bits) - 1;
+                            bits &= bits - 1;
+                            if constexpr (SID) {
+                                add_sid(eih[e] == p ? Z : Z2, e);
+                            } else {
+                                const float th = eth[e];
+                                add_entry(eih[e] == p ? 1.f - th : th, e);
                             }
-                            continue;
                         }
-                        int ih, ihA;
-                        float th, thA;
-                        double G;
-                        slice_anchor(g.col64[c], sc, ihA, thA, G);
-                        split(fmaf(kf, g.col[c].y, thA), ih, th);
-                        ih += ihA;
-                        float wh;
-                        if (ih == p) wh = 1.f - th;
-                        else if (ih + 1 == p && th != 0.f) wh = th;
-                        else continue;
-                        add_entry(wh, e);
                     }
                 }
             }
@@ -826,16 +773,15 @@ void group_proj(Geometry& g, const float* y, cudaStream_t s) {
 
 template <int CLASS, int PB, int SID, int WIN>
 void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
-    constexpr int BP_PB = PB, BP_SL = PlaneCfg<PB>::SL;
+    constexpr int BP_PB = PB;
     const int nh = CLASS ? g.nx : g.ny;
     const int planes = CLASS ? g.ny : g.nx;
     const int ptiles = (nh + BP_PB - 1) / BP_PB;
     const int kbands = (g.nz_local() + BP_KB - 1) / BP_KB;
-    constexpr int NL = PB;
     const size_t smem = sizeof(float) * (size_t(z_stride<PB>()) * (BP_KB + 2 * BP_ZG) * (SID ? 2 : 1) +
-                                         size_t(NL) * BP_SL + NL + BP_PB +
+                                         size_t(BP_PB) * (BP_PB / 32) + 2 * BP_PB +
                                          4 * size_t(pg_groups(g.rows_local())) * (SID ? 2 : 1)) +
-                        sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1 + BP_PB);
+                        sizeof(int2) * g.na + sizeof(int) * (size_t(g.na) + 1);
     if (smem > 200 * 1024) fail(CTK_E_UNSUPPORTED, "too many views / detector rows for the plane backprojector");
     // opt in once to the largest size this launcher accepts (occupancy follows the size of
     // each launch, not the opt-in); call_once keeps concurrent handles on other threads safe
