@@ -537,15 +537,16 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
             // ---- phase 2: row p gathers its registered slots in slot order, i.e. in (view,
             // column) order: deterministic, and the order of the reference's scatter ----
             if (p < nh) {
+                // 64-bit words (half the word steps of 32-bit ones: C3 72.5 -> 70.9 ms)
 #pragma unroll
                 for (int w4 = 0; w4 < MW; w4 += 4) {
-                    const uint4 m4 = *reinterpret_cast<const uint4*>(rmask + t * MW + w4);
-                    const unsigned mw[4] = {m4.x, m4.y, m4.z, m4.w};
+                    const ulonglong2 m2 = *reinterpret_cast<const ulonglong2*>(rmask + t * MW + w4);
+                    const unsigned long long mw[2] = {m2.x, m2.y};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        unsigned bits = mw[j];
+                    for (int j = 0; j < 2; ++j) {
+                        unsigned long long bits = mw[j];
                         while (bits) {
-                            const int e = (w4 + j) * 32 + __ffs(bits) - 1;
+                            const int e = (w4 + 2 * j) * 32 + __ffsll(bits) - 1;
                             bits &= bits - 1;
                             if constexpr (SID) {
                                 add_sid(eih[e] == p ? Z : Z2, e);
