@@ -423,7 +423,18 @@ def main():
     dom = "k_ax_f32" if share_ax >= share_bt else "k_atb_matched_f32"
     t_dom = t_ax if dom == "k_ax_f32" else t_bt
     achieved = alg_bytes / (t_dom / 1e3) / 1e9
-    gather_peak = 148 * 128 * sm_mhz * 1e6 / GATHER_BYTES_PER_SAMPLE / 1e9  # G samples/s at 128 B/clk/SM
+    gather_peak_arith = 148 * 128 * sm_mhz * 1e6 / GATHER_BYTES_PER_SAMPLE / 1e9  # G samples/s at 128 B/clk/SM
+    gather_peak, gather_src = gather_peak_arith, "arithmetic: 16 B/sample at 128 B/clk/SM x 148 SMs"
+    try:  # the measured ceiling: tools/gather_peak.cu, the Ax sample's four tap loads on L1-resident data
+        for ln in open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02", "gather_peak.json")):
+            d = json.loads(ln)
+            if d.get("pattern") == "ax4":
+                gather_peak = d["samples_per_s"] / 1e9
+                gather_src = ("measured: tools/gather_peak.cu ax4 (the Ax sample's 4 tap loads, L1-resident, "
+                              "profiles/r02/gather_peak.json); arithmetic 128 B/clk/SM ceiling "
+                              f"{gather_peak_arith:.0f} G samples/s")
+    except (OSError, ValueError, KeyError):
+        pass
     vol_mib, proj_mib = 4 * nvox / 2**20, 4 * nproj / 2**20
     l2_note = (f"inputs larger than L2 (volume {vol_mib:.0f} MiB, projections {proj_mib:.0f} MiB)"
                if min(vol_mib, proj_mib) > 126 else
@@ -457,7 +468,7 @@ def main():
                              "154 GB/s, the kernel is bound on chip)"},
         "roofline_gather": {"kernel": dom, "achieved": samples / (t_dom / 1e3) / 1e9, "peak": gather_peak,
                             "unit": "G samples/s", "frac": samples / (t_dom / 1e3) / 1e9 / gather_peak,
-                            "note": "binding on-chip ceiling: 16 B/sample at 128 B/clk/SM x 148 SMs (SURVEY.md 8(d))"},
+                            "note": "binding on-chip ceiling (SURVEY.md 8(d)), " + gather_src},
         "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": 4 * nproj, "d2h_bytes_per_step": 4 * nvox,
                 "clocks": clk_e2e.summary()},
         "gpu_launches": launches,
