@@ -107,7 +107,7 @@ __device__ __forceinline__ int z_col(int e) { return e; }
 // plane), each registered in its row with weight 1 (L is in pg).
 template <int CLASS, int PB, int SID = 0, int WIN = 0>
 __global__ void __launch_bounds__(PB, PlaneCfg<PB>::MINB)
-k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles) {
+k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, int ptiles, int nvc) {
     // WIN: the band-sharded range's row window (W0, NW); else the whole detector, with
     // the window folded to constants so the common case keeps its register allocation
     const int W0 = WIN ? g.w0 : 0, NW = WIN ? g.nw : g.nv;
@@ -133,7 +133,12 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
     // plane index fastest: a wave of resident CTAs shares one (row tile, z band), so per
     // view it reads only that band's detector rows -> the projections stay L2-resident
     const int s = blockIdx.x;
-    const int ptile = blockIdx.y % ptiles, kband = blockIdx.y / ptiles;
+    // view chunks (small problems): CTA chunk vc sums the views [a_lo, a_hi) into its own
+    // partial volume x + vc * N (k_sum_parts adds the chunks in order afterwards)
+    const int vch = blockIdx.y % nvc, ptk = blockIdx.y / nvc;
+    const int a_lo = int((long(vch) * g.na) / nvc), a_hi = int((long(vch + 1) * g.na) / nvc);
+    x += size_t(vch) * size_t(g.nx) * g.ny * g.nz;
+    const int ptile = ptk % ptiles, kband = ptk / ptiles;
     const int p0 = ptile * BP_PB, k0 = kband * BP_KB;
     const int nh = CLASS ? g.nx : g.ny;
     const int p = p0 + t;
@@ -195,6 +200,7 @@ k_atb_plane_f32(KGeom g, const float* __restrict__ pg, float* __restrict__ x, in
         const int4 vc = g.vclass[a];
         i0 = max(i0, CLASS ? vc.z : vc.x);
         i1 = min(i1, CLASS ? vc.w : vc.y);
+        if (a < a_lo || a >= a_hi) i1 = i0 - 1;  // another view chunk's
         urange[a] = make_int2(i0, i1);
     }
     __syncthreads();
@@ -773,7 +779,7 @@ void group_proj(Geometry& g, const float* y, cudaStream_t s) {
 }
 
 template <int CLASS, int PB, int SID, int WIN>
-void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
+void launch_plane_pb(Geometry& g, float* x, cudaStream_t s, int nvc) {
     constexpr int BP_PB = PB;
     const int nh = CLASS ? g.nx : g.ny;
     const int planes = CLASS ? g.ny : g.nx;
@@ -793,13 +799,13 @@ void launch_plane_pb(Geometry& g, float* x, cudaStream_t s) {
         CTK_CUDA(cudaFuncSetAttribute(k_atb_plane_f32<CLASS, PB, SID, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       200 * 1024));
     });
-    dim3 grd(unsigned(planes), unsigned(ptiles * kbands));
-    k_atb_plane_f32<CLASS, PB, SID, WIN><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles);
+    dim3 grd(unsigned(planes), unsigned(ptiles * kbands * nvc));
+    k_atb_plane_f32<CLASS, PB, SID, WIN><<<grd, BP_PB, smem, s>>>(g.kgeom(), g.proj_t.as<float>(), x, ptiles, nvc);
     after_launch(SID ? "k_atb_plane_f32_siddon" : "k_atb_plane_f32");
 }
 
 template <int CLASS>
-void launch_plane(Geometry& g, float* x, cudaStream_t s) {
+void launch_plane(Geometry& g, float* x, cudaStream_t s, int nvc) {
     const int nh = CLASS ? g.nx : g.ny;
     static const int forced = [] {
         const char* e = std::getenv("CTK_BP_TILE");  // A/B timing: 128 or 256
@@ -808,13 +814,13 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s) {
     const int pb = forced == 128 || forced == 256 ? forced : (nh <= 768 ? 128 : 256);
     const bool sid = g.projector == CTK_PROJ_SIDDON;  // (Siddon has no band-sharded range)
     if (pb == 128) {
-        if (sid) launch_plane_pb<CLASS, 128, 1, 0>(g, x, s);
-        else if (g.band) launch_plane_pb<CLASS, 128, 0, 1>(g, x, s);
-        else launch_plane_pb<CLASS, 128, 0, 0>(g, x, s);
+        if (sid) launch_plane_pb<CLASS, 128, 1, 0>(g, x, s, nvc);
+        else if (g.band) launch_plane_pb<CLASS, 128, 0, 1>(g, x, s, nvc);
+        else launch_plane_pb<CLASS, 128, 0, 0>(g, x, s, nvc);
     } else {
-        if (sid) launch_plane_pb<CLASS, 256, 1, 0>(g, x, s);
-        else if (g.band) launch_plane_pb<CLASS, 256, 0, 1>(g, x, s);
-        else launch_plane_pb<CLASS, 256, 0, 0>(g, x, s);
+        if (sid) launch_plane_pb<CLASS, 256, 1, 0>(g, x, s, nvc);
+        else if (g.band) launch_plane_pb<CLASS, 256, 0, 1>(g, x, s, nvc);
+        else launch_plane_pb<CLASS, 256, 0, 0>(g, x, s, nvc);
     }
 }
 
@@ -830,11 +836,48 @@ void launch_voxel(Geometry& g, float* x, cudaStream_t s) {
 
 }  // namespace
 
+// View chunks of the plane A^T b: a small problem launches fewer (plane, tile, band) CTAs
+// than one wave of the GPU (C1: 128 against 148 SMs x 6) and each loops over every view;
+// splitting the views into nvc chunks multiplies the CTAs, each chunk summing into its own
+// partial volume, added in chunk order afterwards (deterministic)
+int view_chunks(const Geometry& g) {
+    static const int forced = [] {
+        const char* e = std::getenv("CTK_BP_VCHUNKS");  // A/B timing
+        return e ? std::max(1, std::atoi(e)) : 0;
+    }();
+    if (forced) return std::min(forced, std::max(1, g.na));
+    const int nh = std::max(g.nx, g.ny), pb = nh <= 768 ? 128 : 256;
+    const long ctas = long(std::max(g.nx, g.ny)) * ((nh + pb - 1) / pb) * ((g.nz_local() + BP_KB - 1) / BP_KB);
+    const long wave = 148L * (pb == 128 ? 6 : 3);
+    // measured at C1 (64^3/100, 128 CTAs per pass): 1 / 4 / 8 chunks 0.279 / 0.129 / 0.138 ms; at
+    // 128^3 (512 CTAs) 2 chunks lose 2 %: chunk only while a pass fills less than half a wave
+    return int(std::max(1L, std::min(std::min(4L, long(g.na)), wave / ctas)));
+}
+
+__global__ void k_sum_parts(size_t n, int nparts, const float* __restrict__ parts, float* __restrict__ x) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        float acc = parts[i];
+        for (int q = 1; q < nparts; ++q) acc += parts[size_t(q) * n + i];
+        x[i] = acc;
+    }
+}
+
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s) {
     group_proj(g, y, s);
+    const int nvc = view_chunks(g);
+    float* xt = x;
+    if (nvc > 1) {
+        g.bp_parts_buf.ensure(size_t(nvc) * g.domain() * sizeof(float));
+        xt = g.bp_parts_buf.as<float>();
+    }
     CTK_CUDA(cudaEventRecord(g.ev0, s));
-    launch_plane<0>(g, x, s);
-    launch_plane<1>(g, x, s);
+    launch_plane<0>(g, xt, s, nvc);
+    launch_plane<1>(g, xt, s, nvc);
+    if (nvc > 1) {
+        const size_t n = g.domain();
+        k_sum_parts<<<unsigned(std::min<size_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(n, nvc, xt, x);
+        after_launch("k_sum_parts");
+    }
     CTK_CUDA(cudaEventRecord(g.ev1, s));
     if (g.has_zrays && g.projector == CTK_PROJ_SIDDON) {
         siddon_atb_zrays_f32(g, y, x, s);  // exact gather of the z-dominant rays, accumulated

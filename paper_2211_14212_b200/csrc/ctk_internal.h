@@ -102,6 +102,7 @@ struct Geometry {
     DevBuf d_vclass;  // per view: hull of the columns of each ray class (matched A^T b batching)
     DevBuf d_chk;     // checked builds: one word of bounds-violation bits (kernels atomicOr into it)
     DevBuf d_rayinv;  // per ray: 1/d of make_ray, for the exact gathers (built on first use)
+    DevBuf bp_parts_buf;  // view-chunk partial volumes of the plane A^T b (small problems)
     bool rayinv_ready = false;
     DevBuf d_walk;    // per ray: the plan_walk parameters of the exact f64 path (built on first use)
     DevBuf d_vscale;  // per view: parallel-beam scale of the voxel-driven f64 path (built on first use)
