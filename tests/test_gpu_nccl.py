@@ -55,6 +55,13 @@ SCRIPT = textwrap.dedent("""
     e = rel(t1.x, t0.x)
     assert e < 1e-6, ("cgls_tv", e)
     print("cgls_tv slab rel", e)
+    # band-sharded range over the NCCL communicator (one rank owns every row)
+    p = ctk.projector_pair(g, slab=(0, n), comm=comm, shard_range=True)
+    assert p.projector.range_rows() == (0, g.nv, 0, g.nv)
+    t2 = ctk.cgls_tv(p, b, 0.05, 2, 3, opts)
+    e = rel(t2.x, t0.x)
+    assert e < 1e-6, ("cgls_tv band", e)
+    print("cgls_tv band rel", e)
     del comm
     dist.destroy_process_group()
     print("NCCL_OK")
