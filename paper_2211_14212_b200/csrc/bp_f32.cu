@@ -79,8 +79,8 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 // Tile size PB (rows = threads per CTA) is a template parameter with its own occupancy
 // (round 1, matched A^T b f32): PB = 128, 6 CTAs/SM: 512^3/360 66.9 ms; PB = 256, 3 CTAs/SM:
 // 512^3/360 72.8 ms, 1024^3/1600 2518 ms (PB = 128: 3034 ms -- per-CTA setup over 1600
-// views, twice the tiles), so the launcher takes PB = 128 up to 768 rows per plane and
-// PB = 256 beyond.
+// views, twice the tiles); with the registration masks PB = 256 pays only beyond 768 rows
+// per plane AND about 1000 views (launch_plane).
 template <int PB>
 struct PlaneCfg;
 template <>
@@ -811,7 +811,10 @@ void launch_plane(Geometry& g, float* x, cudaStream_t s, int nvc) {
         const char* e = std::getenv("CTK_BP_TILE");  // A/B timing: 128 or 256
         return e ? std::atoi(e) : 0;
     }();
-    const int pb = forced == 128 || forced == 256 ? forced : (nh <= 768 ? 128 : 256);
+    // 256-row tiles halve the CTAs, i.e. the per-CTA setup over all views: measured with the
+    // registration masks at 1024^3, 400 views 680 vs 628 ms (128 wins), 1600 views 2778 vs
+    // 2859 ms (256 wins); 512^3/720: 128 wins (142 vs 154 ms)
+    const int pb = forced == 128 || forced == 256 ? forced : (nh > 768 && g.na >= 1000 ? 256 : 128);
     const bool sid = g.projector == CTK_PROJ_SIDDON;  // (Siddon has no band-sharded range)
     if (pb == 128) {
         if (sid) launch_plane_pb<CLASS, 128, 1, 0>(g, x, s, nvc);
