@@ -30,14 +30,21 @@ namespace {
 //   wx[i][j+2][k+2]  (x-dominant rays: slice i, h = j)     wy[j][i+2][k+2]  (h = i)
 // each of the 4 tap loads of a warp covers one contiguous z run (1-2 cache lines) instead
 // of two partial rows of a y/x-fastest plane.
+// Block = 32 detector rows x CTK_FWD_BC columns.  4 columns (128 threads) capped at 56
+// registers (9 blocks = 36 warps per SM; a few bytes of spill outside the slice loop):
+// 48.4 vs 49.9 ms at C3 with 8 columns / 64 registers / 32 warps, 3.35 vs 3.45 ms at
+// 256^3/180, 273 vs 278 ms at 1024^3/200 -- the loop is latency-bound, occupancy pays
 #ifndef CTK_FWD_BC
-#define CTK_FWD_BC 8
+#define CTK_FWD_BC 4
 #endif
 #ifndef CTK_FWD_CHUNKS
 #define CTK_FWD_CHUNKS 2  // minimum slice chunks per ray (fwd_chunks); 64.8 -> 50.4 ms at 512^3 vs unchunked
 #endif
 #ifndef CTK_FWD_UNROLL
 #define CTK_FWD_UNROLL 1
+#endif
+#ifndef CTK_FWD_MINB
+#define CTK_FWD_MINB 9  // minimum resident blocks per SM for the register allocator (56 registers)
 #endif
 constexpr int ZW_BR = 32, ZW_BC = CTK_FWD_BC, kFwdUnroll = CTK_FWD_UNROLL;  // block: 32 detector rows (lanes) x ZW_BC columns
 // zero guard planes on each side of the z-fast layouts (h and z): a tap index may step one
@@ -199,7 +206,7 @@ __device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int n
 // SID = 1: the f32 Siddon model (f32_common.cuh) on the same layouts: per slab the four
 // cells (ja|ja+sy, ka|ka+sz) of the chord instead of the four bilinear taps.
 template <int MODE, class Off, int SID = 0, int WIN = 0>
-__global__ void __launch_bounds__(ZW_BR * ZW_BC)
+__global__ void __launch_bounds__(ZW_BR * ZW_BC, CTK_FWD_MINB)
 k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict__ wx, const float* __restrict__ wy,
                const float* __restrict__ xs, float* __restrict__ y, const float* __restrict__ b,
                double* __restrict__ partials, int nch, int chunk, int band0) {
