@@ -81,11 +81,16 @@ __global__ void k_proj_group4(KGeom g, const float* __restrict__ y, float* __res
 // 512^3/360 72.8 ms, 1024^3/1600 2518 ms (PB = 128: 3034 ms -- per-CTA setup over 1600
 // views, twice the tiles); with the registration masks PB = 256 pays only beyond 768 rows
 // per plane AND about 1000 views (launch_plane).
+// 128-row tiles: 6 blocks/SM at 80 registers (7 / 8 blocks: 72 / 64 registers with spills,
+// 73.0 / 81.2 ms vs 71.1 at C3)
+#ifndef CTK_BP_MINB128
+#define CTK_BP_MINB128 6
+#endif
 template <int PB>
 struct PlaneCfg;
 template <>
 struct PlaneCfg<128> {
-    static constexpr int MINB = 6;
+    static constexpr int MINB = CTK_BP_MINB128;
 };
 template <>
 struct PlaneCfg<256> {

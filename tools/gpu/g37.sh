@@ -1,0 +1,9 @@
+for v in default p7 p8 default p7 p8; do
+  if [ $v = default ]; then L=""; else L="build_variants/$v/libctk_b200.so"; fi
+  CTK_B200_LIB=$L timeout 300 python tools/time_bp.py --n 512 --angles 360 --reps 5
+done
+for v in default p7 p8; do
+  if [ $v = default ]; then L=""; else L="build_variants/$v/libctk_b200.so"; fi
+  CTK_B200_LIB=$L timeout 300 python tools/time_bp.py --n 256 --angles 180 --reps 7 --projector siddon
+  CTK_B200_LIB=$L timeout 300 python tools/time_bp.py --n 256 --angles 180 --reps 7
+done
