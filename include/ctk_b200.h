@@ -28,7 +28,9 @@
 extern "C" {
 #endif
 
-#define CTK_ABI_VERSION 1
+/* 2: ctk_comm_callbacks gained the `exchange` member (band-sharded range, p2p halos) -- callers
+ * must zero-initialise it when they do not provide one. */
+#define CTK_ABI_VERSION 2
 
 /* Error taxonomy of types.hpp:14-31 (DimensionError, GeometryError, ParameterError,
  * DegenerateInputError, NumericalError) plus device failures. */

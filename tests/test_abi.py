@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.ctk_abi_version() == 1
+    assert lib.ctk_abi_version() == 2
 
 
 def _desc(**kw):
