@@ -32,11 +32,15 @@ def _free_port():
     return port
 
 
-def _geom():
+def _geom(name="cone"):
+    if name == "parallel3d":
+        from geoms import parallel3d
+
+        return to_ctk(parallel3d(nx=20, ny=18, nz=30, na=12))
     return to_ctk(cone_bench(36, 20))
 
 
-def _ops_worker(rank, world, port, outdir):
+def _ops_worker(rank, world, port, outdir, name="cone"):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import torch
@@ -46,7 +50,7 @@ def _ops_worker(rank, world, port, outdir):
     from paper_2211_14212_b200.comm import TorchComm, shard_slabs
 
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    g = _geom()
+    g = _geom(name)
     n = g.vol.nx * g.vol.ny
     z0, cnt = shard_slabs(g.vol.nz, world, rank)
     rng = np.random.default_rng(7)
@@ -65,13 +69,14 @@ def _ops_worker(rank, world, port, outdir):
 
 
 @pytest.mark.timeout(300)
-def test_band_operators_three_ranks(tmp_path):
+@pytest.mark.parametrize("name", ["cone", "parallel3d"])
+def test_band_operators_three_ranks(tmp_path, name):
     import torch.multiprocessing as mp
 
     import paper_2211_14212_b200 as ctk
 
-    mp.spawn(_ops_worker, args=(WORLD, _free_port(), str(tmp_path)), nprocs=WORLD, join=True)
-    g = _geom()
+    mp.spawn(_ops_worker, args=(WORLD, _free_port(), str(tmp_path), name), nprocs=WORLD, join=True)
+    g = _geom(name)
     n, na = g.vol.nx * g.vol.ny, len(g.angles)
     rng = np.random.default_rng(7)
     x = rng.standard_normal(n * g.vol.nz).astype(np.float32)
@@ -83,7 +88,7 @@ def test_band_operators_three_ranks(tmp_path):
     owned = []
     for r in ranks:
         w0, nw, o0, no = (int(r[k]) for k in ("w0", "nw", "o0", "no"))
-        assert int(r["rs"]) == na * nw * g.nu and nw < g.nv  # a window, not the whole range
+        assert int(r["rs"]) == na * nw * g.nu and (nw < g.nv or name != "cone")  # a window, not the whole range
         ax = r["ax"].reshape(na, nw, g.nu)
         own = ax[:, o0 - w0:o0 - w0 + no, :]
         assert rel_l2(own, ax_full[:, o0:o0 + no, :]) < 2e-6
@@ -163,3 +168,12 @@ def test_band_sharded_solvers_three_ranks(tmp_path):
             assert np.allclose(r[which + "_expl"], ref.log.explicit_residual, rtol=1e-4), which
             assert np.allclose(r[which + "_impl"], ref.log.implicit_residual, rtol=1e-4), which
         assert np.array_equal(ranks[0][which + "_expl"], ranks[2][which + "_expl"]), which
+
+
+def test_band_needs_slab_and_comm():
+    import paper_2211_14212_b200 as ctk
+
+    g = _geom()
+    p = ctk.projector_pair(g, slab=(0, 12))
+    with pytest.raises(ctk.ParameterError, match="needs a slab and a communicator"):
+        p.projector.shard_range()
