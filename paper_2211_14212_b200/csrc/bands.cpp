@@ -92,6 +92,7 @@ void copy_rows(const Geometry& g, T* packed, T* local, int r0, int r1, bool pack
 template <class T>
 void band_reduce(Geometry& g, T* y, cudaStream_t s) {
     const int R = g.comm->cb.nranks, me = g.comm->cb.rank;
+    if (R > 32) fail(CTK_E_UNSUPPORTED, "band-sharded range: at most 32 ranks");
     std::vector<Seg> sends, recvs;
     size_t ns = 0, nr = 0;
     for (int q = 0; q < R; ++q) {
@@ -115,7 +116,6 @@ void band_reduce(Geometry& g, T* y, cudaStream_t s) {
     bs.n = 0;
     bs.o0 = g.bo0[me];
     bs.o1 = g.bo1[me];
-    if (R > 32) fail(CTK_E_UNSUPPORTED, "band-sharded range: at most 32 ranks");
     for (int r = 0; r < R; ++r) {
         if (r == me) {
             bs.src[bs.n++] = {y, std::max(g.bt0[me], g.w0), std::min(g.bt1[me], g.w0 + g.nw), g.nw, g.w0};
