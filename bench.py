@@ -82,14 +82,15 @@ def peaks():
 def traffic_bytes(kernel, n, na):
     """DRAM bytes per operation of the dominant kernel from the committed ncu capture (same
     workload only), else None."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r01", "traffic_ax_512_360.json")
-    try:
-        with open(path) as f:
-            t = json.load(f)
-    except (OSError, ValueError):
-        return None
-    if t.get("kernel") == kernel and t.get("n") == n and t.get("angles") == na:
-        return t["dram_bytes_per_op"]  # bytes per operation (compare "algorithmic_bytes")
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02")
+    for name in ("traffic_ax_512_360.json", "traffic_atb_512_360.json"):
+        try:
+            with open(os.path.join(here, name)) as f:
+                t = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if t.get("kernel") == kernel and t.get("n") == n and t.get("angles") == na:
+            return t["dram_bytes_per_op"]  # bytes per operation (compare "algorithmic_bytes")
     return None
 
 
@@ -463,9 +464,9 @@ def main():
                      "frac": achieved / hbm_peak, "traffic": traffic_bytes(dom, n, my_angles) if my_slices == n else None, "algorithmic_bytes": alg_bytes,
                      "note": f"algorithmic bytes 4*(N_vox+N_proj) per launch; peak {peak_src}; traffic = measured "
                              "DRAM bytes of the same operation (both slice-chunk launches) from the committed ncu "
-                             "capture, profiles/r01/traffic_ax_512_360.json, when the workload matches; the volume "
+                             "capture, profiles/r02/traffic_{ax,atb}_512_360.json, when the workload matches; the volume "
                              "slab of each detector-row band is re-read from DRAM by design (L2 residency per band; "
-                             "154 GB/s, the kernel is bound on chip)"},
+                             "8.4 GB per Ax at C3 = 176 GB/s, 2.7 % of HBM: the kernel is bound on chip)"},
         "roofline_gather": {"kernel": dom, "achieved": samples / (t_dom / 1e3) / 1e9, "peak": gather_peak,
                             "unit": "G samples/s", "frac": samples / (t_dom / 1e3) / 1e9 / gather_peak,
                             "note": "binding on-chip ceiling (SURVEY.md 8(d)), " + gather_src},
