@@ -110,6 +110,7 @@ struct Geometry {
     bool walk_ready = false;
     // workspaces (grown lazily)
     DevBuf vx, vy;      // padded f32 relayouts for x- / y-dominant rays
+    DevBuf vx2, vy2;    // the same layouts with two volumes interleaved (float2), for ax2_f32
     DevBuf dx64, dy64;  // z-fast f64 copies for the exact forward: X[i][j][k], Y[j][i][k]
     DevBuf proj_t;      // transposed (and step-scaled) projections for the gathers
     DevBuf host_x, host_y;  // device staging for host-pointer entry points
@@ -144,6 +145,10 @@ void launch_atb_voxel_f64(Geometry& g, const double* y, double* x, cudaStream_t 
 // f32 performance path (kernels_f32.cu)
 void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s);
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s);
+// y1 = A x1 and y2 = A x2 in one pass (f32 Joseph, whole-volume handles): the positions and
+// weights are computed once for both volumes; each output is bit-identical to ax_f32's
+bool ax2_f32_supported(const Geometry& g);
+void ax2_f32(Geometry& g, const float* x1, float* y1, const float* x2, float* y2, cudaStream_t s);
 void atb_matched_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
 void atb_voxel_f32(Geometry& g, const float* y, float* x, cudaStream_t s);
 

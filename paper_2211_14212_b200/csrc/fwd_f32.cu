@@ -46,6 +46,9 @@ namespace {
 #ifndef CTK_FWD_MINB
 #define CTK_FWD_MINB 9  // minimum resident blocks per SM for the register allocator (56 registers)
 #endif
+#ifndef CTK_FWD2_MINB
+#define CTK_FWD2_MINB 8  // the two-volume march (k_ax2_zfast_f32)
+#endif
 constexpr int ZW_BR = 32, ZW_BC = CTK_FWD_BC, kFwdUnroll = CTK_FWD_UNROLL;  // block: 32 detector rows (lanes) x ZW_BC columns
 // zero guard planes on each side of the z-fast layouts (h and z): a tap index may step one
 // beyond the contributing range where anchored positions round across a voxel boundary
@@ -412,6 +415,200 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
     }
 }
 
+// Two volumes through one ray march (y1 = A x1, y2 = A x2; f32 Joseph, whole volume).  The
+// solvers need A v for the next Krylov step and A x for the explicit residual of the
+// iteration just finished (solve_log.hpp:102-115); both exist at the same time, and their
+// samples share every position, floor and weight.  The layouts hold the two volumes
+// interleaved (float2: .x from x1, .y from x2), so one 8-byte tap load serves both, and
+// per volume the operation sequence is exactly k_ax_zfast_f32's (slice pairs: even slices
+// in one accumulator, odd in the other, the odd tail scalar), so each output is
+// bit-identical to a single-volume launch with the same chunking.
+template <class Off>
+__global__ void __launch_bounds__(ZW_BR * ZW_BC, CTK_FWD2_MINB)
+k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restrict__ wx, const float2* __restrict__ wy,
+                const float* __restrict__ xs1, const float* __restrict__ xs2, float* __restrict__ y1,
+                float* __restrict__ y2, int nch, int chunk) {
+    __shared__ float outs[2][ZW_BR][ZW_BC + 1];
+    const int band = blockIdx.z;
+    const int iv = band * ZW_BR + threadIdx.x;
+    const int a = vorder[blockIdx.y];
+    const int iu = blockIdx.x * ZW_BC + threadIdx.y;
+    float out1 = 0.f, out2 = 0.f;
+    if (iu < g.nu && iv < g.nv) {
+        const int c = a * g.nu + iu;
+        const double2 cs = g.colstep[c];
+        const double v = row_coord(g, iv);
+        if (g.has_zrays && is_zray(g, cs, v)) {
+            if (chunk == 0) {
+                const double2 tr = g.ctst[a];
+                WalkF w;
+                walk_generic(g, tr.x, tr.y, iu, iv, w);
+                out1 = march_generic(g, w, xs1);
+                out2 = march_generic(g, w, xs2);
+            }
+        } else {
+            const float4 cd = g.col[c];
+            const double4 c64 = g.col64[c];
+            const int A = g.colaxis[c];
+            const int nh = A ? g.nx : g.ny;
+            const int ns = A ? g.ny : g.nx;
+            const Off pz = g.nz + 2 * kPad;
+            const Off plane = pz * Off(nh + 2 * kPad);
+            const float2* base = (A ? wy : wx) + kPad * pz + kPad;
+            const float vd = float(v);
+            const float czf = 0.5f * float(g.nzg - 1);
+            const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            const float Wd = z_cross(g, c64), vr = row_vr(g, iv), fc = cz_frac(g);
+            const int izc = cz_int(g);
+            // the slice interval of k_ax_zfast_f32 (same arithmetic)
+            auto pos = [&](int s, int& ih, int& iz) {
+                const int sc = slice_centre(s);
+                int ihA, pa, pb;
+                float thA, Whi, Wr, t0, t1;
+                double G;
+                slice_anchor(c64, sc, ihA, thA, G);
+                z_split(g, G, Whi, Wr);
+                const float kf = float(s - sc);
+                split(fmaf(kf, cd.y, thA), pa, t0);
+                split(fmaf(vr, fmaf(kf, Wd, Wr), fmaf(vr, Whi, fc)), pb, t1);
+                ih = ihA + pa;
+                iz = izc + pb;
+            };
+            auto inside = [&](int s) {
+                int ih, iz;
+                pos(s, ih, iz);
+                return unsigned(ih + 1) <= unh && unsigned(iz + 1) <= unz;
+            };
+            int s0 = 0, s1 = ns - 1;
+            clip_affine(cd.x, cd.y, -1.0, nh, s0, s1);
+            clip_affine(double(vd) * cd.z + czf, double(vd) * cd.w, -1.0, g.nz, s0, s1);
+            while (s0 <= s1 && !inside(s0)) ++s0;
+            while (s1 >= s0 && !inside(s1)) --s1;
+            if (s0 <= s1) {
+                while (s0 > 0 && inside(s0 - 1)) --s0;
+                while (s1 < ns - 1 && inside(s1 + 1)) ++s1;
+            }
+            if (nch > 1) {
+                const int len = (ns + nch - 1) / nch;
+                s0 = max(s0, chunk * len);
+                s1 = min(s1, chunk * len + len - 1);
+            }
+            float acc1 = 0.f, acc2 = 0.f;
+            using U = typename std::conditional<sizeof(Off) == 4, unsigned, unsigned long long>::type;
+            const U upz = U(pz), uplane = U(plane), uplane2 = uplane + uplane;
+            const U cbias = U(kSplitBias) * (upz + 1u) - U(unsigned(izc));
+            const float2* base1 = base + pz;
+            const float2 fhd2 = make_float2(cd.y, cd.y), Wd2 = make_float2(Wd, Wd), vr2 = make_float2(vr, vr);
+            const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
+            const float2 m1 = make_float2(-1.f, -1.f), two = make_float2(2.f, 2.f);
+            // (volume 1, volume 2) of the even and of the odd slices
+            float2 accE = make_float2(0.f, 0.f), accO = make_float2(0.f, 0.f);
+            for (int s = s0; s <= s1;) {
+                const int sc = slice_centre(s);
+                const int se = min(s1, sc + kSB / 2 - 1);
+                int ihA;
+                float thA, Whi, Wr;
+                double G;
+                slice_anchor(c64, sc, ihA, thA, G);
+                z_split(g, G, Whi, Wr);
+                const float S = fmaf(vr, Whi, fc);
+                U sb = U(s) * uplane + U(Off(ihA)) * upz - cbias;
+                const float2 thA2 = make_float2(thA, thA), Wr2 = make_float2(Wr, Wr), S2 = make_float2(S, S);
+                float2 k2 = make_float2(float(s - sc), float(s - sc + 1));
+                const int cnt = se - s + 1;
+                for (int np = cnt >> 1; np > 0; --np) {
+                    const float2 fh = __ffma2_rn(k2, fhd2, thA2);
+                    const float2 wlo = __ffma2_rn(k2, Wd2, Wr2);
+                    const float2 tht = __fadd2_rd(fh, M2);
+                    const float2 tzt = __fadd2_rd(__ffma2_rn(vr2, wlo, S2), M2);
+                    const float2 th = __ffma2_rn(__fadd2_rn(tht, nM2), m1, fh);
+                    const float2 tz = __ffma2_rn(vr2, wlo, __ffma2_rn(__fadd2_rn(tzt, nM2), m1, S2));
+                    const Off o0 = Off(U(unsigned(__float_as_int(tht.x))) * upz + (sb + U(unsigned(__float_as_int(tzt.x)))));
+                    const Off o1 =
+                        Off(U(unsigned(__float_as_int(tht.y))) * upz + (sb + uplane + U(unsigned(__float_as_int(tzt.y)))));
+                    k2 = __fadd2_rn(k2, two);
+                    sb += uplane2;
+                    const float2 A00 = __ldg(base + o0), A01 = __ldg(base + o0 + 1);
+                    const float2 A10 = __ldg(base1 + o0), A11 = __ldg(base1 + o0 + 1);
+                    const float2 B00 = __ldg(base + o1), B01 = __ldg(base + o1 + 1);
+                    const float2 B10 = __ldg(base1 + o1), B11 = __ldg(base1 + o1 + 1);
+                    {  // even slice: weights th.x, tz.x on both volumes
+                        const float2 t = make_float2(th.x, th.x), u = make_float2(tz.x, tz.x);
+                        const float2 a0 = __ffma2_rn(t, __ffma2_rn(A00, m1, A10), A00);
+                        const float2 a1 = __ffma2_rn(t, __ffma2_rn(A01, m1, A11), A01);
+                        accE = __fadd2_rn(accE, __ffma2_rn(u, __ffma2_rn(a0, m1, a1), a0));
+                    }
+                    {  // odd slice
+                        const float2 t = make_float2(th.y, th.y), u = make_float2(tz.y, tz.y);
+                        const float2 a0 = __ffma2_rn(t, __ffma2_rn(B00, m1, B10), B00);
+                        const float2 a1 = __ffma2_rn(t, __ffma2_rn(B01, m1, B11), B01);
+                        accO = __fadd2_rn(accO, __ffma2_rn(u, __ffma2_rn(a0, m1, a1), a0));
+                    }
+                }
+                if (cnt & 1) {
+                    const float kf = k2.x;
+                    const float fh = fmaf(kf, cd.y, thA);
+                    const float wlo = fmaf(kf, Wd, Wr);
+                    const float tht = split_t(fh), tzt = split_t(fmaf(vr, wlo, S));
+                    const float th = split_frac(fh, tht);
+                    const float tz = fmaf(vr, wlo, fmaf(__fsub_rn(tzt, kSplitM), -1.f, S));
+                    const Off off = Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt)))));
+                    const float2 v00 = __ldg(base + off), v01 = __ldg(base + off + 1);
+                    const float2 v10 = __ldg(base1 + off), v11 = __ldg(base1 + off + 1);
+                    {
+                        const float a0 = fmaf(th, v10.x - v00.x, v00.x), a1 = fmaf(th, v11.x - v01.x, v01.x);
+                        acc1 += fmaf(tz, a1 - a0, a0);
+                    }
+                    {
+                        const float a0 = fmaf(th, v10.y - v00.y, v00.y), a1 = fmaf(th, v11.y - v01.y, v01.y);
+                        acc2 += fmaf(tz, a1 - a0, a0);
+                    }
+                }
+                s = se + 1;
+            }
+            acc1 += accE.x + accO.x;
+            acc2 += accE.y + accO.y;
+            const float stp = ray_step(g, cs, v);
+            out1 = stp * acc1;
+            out2 = stp * acc2;
+        }
+    }
+    outs[0][threadIdx.x][threadIdx.y] = out1;
+    outs[1][threadIdx.x][threadIdx.y] = out2;
+    __syncthreads();
+    const int t = threadIdx.x + ZW_BR * threadIdx.y;
+    const int r = t / ZW_BC, cc = t % ZW_BC;
+    const int ivw = band * ZW_BR + r, iuw = blockIdx.x * ZW_BC + cc;
+    if (ivw < g.nv && iuw < g.nu) {
+        const size_t o = (size_t(a) * g.nv + size_t(ivw)) * g.nu + iuw;
+        y1[o] = chunk == 0 ? outs[0][r][cc] : y1[o] + outs[0][r][cc];
+        y2[o] = chunk == 0 ? outs[1][r][cc] : y2[o] + outs[1][r][cc];
+    }
+}
+
+// x1, x2 -> interleaved wx[i][j+kPad][k+kPad], wy[j][i+kPad][k+kPad] (float2 {x1, x2})
+__global__ void k_relayout2_zfast(int nx, int ny, int nz, const float* __restrict__ x1, const float* __restrict__ x2,
+                                  float2* __restrict__ wx, float2* __restrict__ wy) {
+    __shared__ float2 tile[32][33];
+    const int i0 = blockIdx.x * 32, k0 = blockIdx.y * 32, j = blockIdx.z;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + threadIdx.x, k = k0 + r;
+        const bool in = i < nx && k < nz;
+        const size_t src = size_t(i) + size_t(nx) * (j + size_t(ny) * k);
+        tile[r][threadIdx.x] = make_float2(in ? __ldg(x1 + src) : 0.f, in ? __ldg(x2 + src) : 0.f);
+    }
+    __syncthreads();
+    const size_t pz = size_t(nz) + 2 * kPad;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int i = i0 + r, k = k0 + threadIdx.x;
+        if (i < nx && k < nz) {
+            const float2 v = tile[threadIdx.x][r];
+            wx[(size_t(i) * (ny + 2 * kPad) + (j + kPad)) * pz + k + kPad] = v;
+            wy[(size_t(j) * (nx + 2 * kPad) + (i + kPad)) * pz + k + kPad] = v;
+        }
+    }
+}
+
 void relayout_zfast(Geometry& g, const float* x, DevBuf& wx, DevBuf& wy, cudaStream_t s) {
     const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2 * kPad) * (size_t(g.nz_local()) + 2 * kPad);
     const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2 * kPad) * (size_t(g.nz_local()) + 2 * kPad);
@@ -522,6 +719,35 @@ void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
     CTK_CUDA(cudaEventRecord(g.ev1, s));
     // Siddon: the z-dominant rays take the exact DDA (siddon.cu), writing only their entries
     if (g.projector == CTK_PROJ_SIDDON && g.has_zrays) siddon_ax_zrays_f32(g, x, y, s);
+}
+
+bool ax2_f32_supported(const Geometry& g) {
+    const char* e = std::getenv("CTK_FWD_NO_PAIR");  // read per call: tests switch it in-process
+    return !(e && e[0] == '1') && g.projector == CTK_PROJ_JOSEPH && !g.slab && !g.band;
+}
+
+void ax2_f32(Geometry& g, const float* x1, float* y1, const float* x2, float* y2, cudaStream_t s) {
+    if (!ax2_f32_supported(g)) throw Error(CTK_E_UNSUPPORTED, "ax2_f32: f32 Joseph on a whole-volume handle only");
+    const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2 * kPad) * (size_t(g.nz) + 2 * kPad);
+    const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2 * kPad) * (size_t(g.nz) + 2 * kPad);
+    if (g.vx2.ensure(nwx * sizeof(float2))) CTK_CUDA(cudaMemsetAsync(g.vx2.p, 0, nwx * sizeof(float2), s));
+    if (g.vy2.ensure(nwy * sizeof(float2))) CTK_CUDA(cudaMemsetAsync(g.vy2.p, 0, nwy * sizeof(float2), s));
+    {
+        dim3 blk(32, 8), grd((g.nx + 31) / 32, (g.nz + 31) / 32, g.ny);
+        k_relayout2_zfast<<<grd, blk, 0, s>>>(g.nx, g.ny, g.nz, x1, x2, g.vx2.as<float2>(), g.vy2.as<float2>());
+        after_launch("k_relayout2_zfast");
+    }
+    const int nch = fwd_chunks(g);  // as ax_f32: the chunk sums must match for bit-identical outputs
+    const KGeom k = g.kgeom();
+    const int* vo = g.d_vorder.as<int>();
+    const float2 *a0 = g.vx2.as<float2>(), *a1 = g.vy2.as<float2>();
+    const dim3 blk(ZW_BR, ZW_BC), grd = fwd_grid(g);
+    // 64-bit offsets once the float2 layout's element count passes 2^31 (offsets index float2)
+    for (int c = 0; c < nch; ++c) {
+        if (wide_offsets(g)) k_ax2_zfast_f32<long long><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
+        else k_ax2_zfast_f32<int><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
+        after_launch("k_ax2_zfast_f32");
+    }
 }
 
 void ax_residual_f32(Geometry& g, const float* x, const float* b, double* d_out, cudaStream_t s) {

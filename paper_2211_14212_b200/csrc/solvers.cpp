@@ -73,7 +73,24 @@ struct Dev {
     // band-sharded range (bands.cpp) both spaces are: range vectors hold this rank's row
     // window with the rows it does not own at zero
     bool sharded(bool range) const { return g.comm && (g.slab ? (!range || g.band) : range); }
+    // The solver's next forward application, announced before the monitor records an
+    // iterate: the explicit residual's A x and that A v then run as one two-volume march
+    // (ax2_f32), and the next ax(v, y) finds y already written.  Only the solvers that leave
+    // v and y untouched between record() and that call announce it (lsqr, lsmr, hybrid_lsqr).
+    const T* next_in = nullptr;
+    T* next_out = nullptr;
+    bool next_ready = false;
+    void announce_ax(const T* x, T* y) {
+        next_in = x;
+        next_out = y;
+        next_ready = false;
+    }
     void ax(const T* x, T* y) {
+        const bool ready = next_ready && x == next_in && y == next_out;
+        next_in = nullptr;
+        next_out = nullptr;
+        next_ready = false;
+        if (ready) return;
         op_ax<T>(g, x, y, s);
         if (slab_mode()) {
             if (g.band) band_reduce<T>(g, y, s);  // partials to the rows' owners, rank order
@@ -81,6 +98,7 @@ struct Dev {
         }
     }
     void atb(const T* y, T* x) {
+        next_ready = false;
         op_atb<T>(g, variant, g.band ? band_halo<T>(g, y, s) : y, x, s);
         if (g.comm && !g.slab) comm_allreduce(g.comm, x, g.domain(), sizeof(T) == 8 ? 1 : 0, s);
     }
@@ -165,6 +183,13 @@ struct Dev {
     // ||A x - b||^2 over all ranks (solve_log.hpp:111-115), never storing A x in T=float
     double resid2(const T* x, const T* b) {
         if constexpr (sizeof(T) == 4) {
+            if (next_in && !next_ready && ax2_f32_supported(g)) {
+                if (!tmp_range.p) tmp_range.alloc(g.range());
+                ax2_f32(g, reinterpret_cast<const float*>(next_in), reinterpret_cast<float*>(next_out), x,
+                        reinterpret_cast<float*>(tmp_range.p), s);
+                next_ready = true;
+                return diff_nrm2sq(tmp_range.p, b, g.range(), true);
+            }
             if (g.projector == CTK_PROJ_JOSEPH && !slab_mode()) {
                 ax_residual_f32(g, x, b, w.results, s);
                 return part_sum(fetch(0), true);
@@ -337,6 +362,7 @@ void lsqr(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
         const double phi = c * phibar;
         phibar = sn * phibar;
         lsqr_update<T>(nd, phi / rho, theta / rho, x, w.p, v.p, d.s);
+        if (k < o.max_iters && !down) d.announce_ax(v.p, un.p);
         if (mon.record(k, x, phibar / beta1)) break;
         if (down) {
             mon.reason = CTK_STOP_BREAKDOWN;
@@ -418,6 +444,7 @@ void lsmr(Dev<T>& d, const T* b, double lambda, const ctk_solver_opts& o, T* x, 
         const double taud = (zeta - thetatilde * tautildeold) / rhodold;
         dsq += betacheck * betacheck;
         const double normr = std::sqrt(dsq + (betad - taud) * (betad - taud) + betadd * betadd);
+        if (k < o.max_iters && !down) d.announce_ax(v.p, un.p);
         if (mon.record(k, x, normr / beta1, true, lambda)) break;
         if (down) {
             mon.reason = CTK_STOP_BREAKDOWN;
@@ -520,6 +547,7 @@ void hybrid_lsqr(Dev<T>& d, const T* b, const ctk_hybrid_strategy& strat, const 
         fill<T>(nd, T(0), x, d.s);
         block_axpy<T>(nd, int(y.size()), 1.0, dy.as<double>(), V, nd, x, d.s);
         CTK_CUDA(cudaStreamSynchronize(d.s));  // y (host) must outlive the async copy
+        if (k < o.max_iters && !breakdown) d.announce_ax(Vi(nv_ - 1), Ui(nu_));
         if (mon.record(k, x, fit / beta1, true, lambda_k)) break;
         if (breakdown) {
             mon.reason = CTK_STOP_BREAKDOWN;
@@ -900,6 +928,7 @@ void flsqr_tv(Dev<T>& d, const T* b, const ctk_hybrid_strategy& strat, const ctk
         fill<T>(nd, T(0), x, d.s);
         block_axpy<T>(nd, int(y.size()), 1.0, coefb.as<double>(), Zb.as<T>(), nd, x, d.s);
         CTK_CUDA(cudaStreamSynchronize(d.s));  // y (host) must outlive the async copy
+        if (k < o.max_iters && !breakdown) d.announce_ax(Vi(nv_ - 1), Ui(nu_));
         if (mon.record(k, x, fit / beta1, true, lambda_k)) break;
         if (breakdown) {
             mon.reason = CTK_STOP_BREAKDOWN;

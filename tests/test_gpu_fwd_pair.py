@@ -1,0 +1,100 @@
+"""The two-volume forward march (ax2_f32, fwd_f32.cu) inside the solvers.
+
+lsqr, lsmr and hybrid_lsqr announce their next A v before the monitor records an iterate;
+the explicit residual's A x (solve_log.hpp:102-115) and that A v then run as one march over
+interleaved layouts.  Each output is bit-identical to a single-volume launch, so every
+solve must be bitwise the same with the pairing switched off (CTK_FWD_NO_PAIR=1): x, both
+residual histories, lambda and relative-error logs.  The geometries cover x- and
+y-dominant rays, z-dominant rays (cone_steep), odd slice counts and ragged extents.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from geoms import ALL, cone_bench, to_ctk
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctk():
+    import paper_2211_14212_b200 as m
+
+    m.load()
+    return m
+
+
+def _solve(ctk, pair, b, solver, k, paired):
+    if paired:
+        os.environ.pop("CTK_FWD_NO_PAIR", None)
+    else:
+        os.environ["CTK_FWD_NO_PAIR"] = "1"
+    try:
+        opts = ctk.SolverOptions(max_iters=k, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
+        if solver == "lsmr":
+            return ctk.lsmr(pair, b, 3.0, opts)
+        if solver == "hybrid_lsqr":
+            return ctk.hybrid_lsqr(pair, b, ctk.HybridStrategy.gcv(), opts)
+        return ctk.lsqr(pair, b, opts)
+    finally:
+        os.environ.pop("CTK_FWD_NO_PAIR", None)
+
+
+def _same(r1, r2):
+    assert r1.iterations_run == r2.iterations_run
+    assert np.array_equal(r1.x, r2.x)
+    assert r1.log.implicit_residual == r2.log.implicit_residual
+    assert r1.log.explicit_residual == r2.log.explicit_residual
+    assert r1.log.lambda_ == r2.log.lambda_
+
+
+@pytest.mark.parametrize("solver", ["lsqr", "lsmr", "hybrid_lsqr"])
+@pytest.mark.parametrize("name", ["cone_default", "cone_steep", "cone_ragged", "parallel3d", "cone_multitile"])
+def test_paired_residual_bitwise(ctk, name, solver):
+    g = ALL[name]()
+    rng = np.random.default_rng(7)
+    b = rng.standard_normal(g.na * g.nv * g.nu).astype(np.float32)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float32)
+    _same(_solve(ctk, pair, b, solver, 6, True), _solve(ctk, pair, b, solver, 6, False))
+
+
+def test_paired_residual_bench_geometry(ctk):
+    # 128^3 with several slice chunks per ray (fwd_chunks) and 90 views
+    g = cone_bench(128, 90)
+    rng = np.random.default_rng(11)
+    b = np.abs(rng.standard_normal(g.na * g.nv * g.nu)).astype(np.float32)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float32)
+    _same(_solve(ctk, pair, b, "lsmr", 4, True), _solve(ctk, pair, b, "lsmr", 4, False))
+
+
+def test_paired_residual_wide_offsets(tmp_path):
+    # the 64-bit-offset instantiation (CTK_FWD_WIDE=1 is read once per process)
+    import subprocess
+    import sys
+
+    code = r'''
+import os, sys
+import numpy as np
+sys.path.insert(0, "tests")
+import paper_2211_14212_b200 as ctk
+from geoms import cone_ragged, to_ctk
+ctk.load()
+g = cone_ragged()
+b = np.random.default_rng(3).standard_normal(g.na * g.nv * g.nu).astype(np.float32)
+pair = ctk.projector_pair(to_ctk(g), dtype=np.float32)
+def run():
+    opts = ctk.SolverOptions(max_iters=5, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
+    return ctk.lsqr(pair, b, opts)
+r1 = run()
+os.environ["CTK_FWD_NO_PAIR"] = "1"
+r2 = run()
+assert np.array_equal(r1.x, r2.x)
+assert r1.log.explicit_residual == r2.log.explicit_residual
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {**os.environ, "CTK_FWD_WIDE": "1"}
+    env.pop("CTK_FWD_NO_PAIR", None)
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
