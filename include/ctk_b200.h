@@ -105,6 +105,11 @@ int ctk_atb_f32(ctk_geom* g, int variant, const float* d_y, float* d_x, void* st
 int ctk_atb_f64(ctk_geom* g, int variant, const double* d_y, double* d_x, void* stream);
 /* Fused explicit residual: out = ||A x - b||^2 (fp64), y never stored (solve_log.hpp:111-115). */
 int ctk_ax_residual_f32(ctk_geom* g, const float* d_x, const float* d_b, double* h_out, void* stream);
+/* Two forward projections in one ray march: d_y1 = A d_x1, d_y2 = A d_x2 (f32, Joseph or Siddon, on a
+ * whole-volume handle; CTK_E_UNSUPPORTED otherwise).  No reference counterpart: the solvers
+ * use it for the explicit residual's A x (solve_log.hpp:111-115) together with the next
+ * Krylov A v.  Each output is bit-identical to ctk_ax_f32's. */
+int ctk_ax_pair_f32(ctk_geom* g, const float* d_x1, float* d_y1, const float* d_x2, float* d_y2, void* stream);
 
 /* ---- operators on HOST pointers: OperatorPair::forward / back semantics
  *      (operators.hpp:18-45, 102-113).  Synchronous. ---------------------------------- */

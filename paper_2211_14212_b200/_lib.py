@@ -131,6 +131,7 @@ def load():
         "ctk_atb_f32": (i, [vp, i, vp, vp, vp]),
         "ctk_atb_f64": (i, [vp, i, vp, vp, vp]),
         "ctk_ax_residual_f32": (i, [vp, vp, vp, pd, vp]),
+        "ctk_ax_pair_f32": (i, [vp, vp, vp, vp, vp, vp]),
         "ctk_ax_host_f32": (i, [vp, vp, vp]),
         "ctk_ax_host_f64": (i, [vp, vp, vp]),
         "ctk_atb_host_f32": (i, [vp, i, vp, vp]),

@@ -378,6 +378,21 @@ class Projector:
             _check(getattr(self.lib, f"ctk_atb_host_{t}")(self.handle, int(variant), y.ctypes.data_as(C.c_void_p),
                                                            x.ctypes.data_as(C.c_void_p)))
 
+    def forward_pair(self, x1, y1, x2, y2, stream=None):
+        """y1 <- A x1 and y2 <- A x2 in one ray march (float32 CUDA tensors, Joseph or Siddon,
+        whole-volume handle); each output bit-identical to forward()."""
+        for x, y in ((x1, y1), (x2, y2)):
+            if _numel(x) != self.domain_size or _numel(y) != self.range_size:
+                raise DimensionError("operator domain size mismatch")
+            if not _is_torch_cuda(x):
+                raise ParameterError("forward_pair takes CUDA tensors")
+            self._check_buffers(x, y)
+            if str(x.dtype) != "torch.float32":
+                raise ParameterError("forward_pair is float32")
+        _check(self.lib.ctk_ax_pair_f32(self.handle, C.c_void_p(x1.data_ptr()), C.c_void_p(y1.data_ptr()),
+                                        C.c_void_p(x2.data_ptr()), C.c_void_p(y2.data_ptr()),
+                                        stream if stream is not None else _torch_stream()))
+
     def residual2(self, x, b) -> float:
         """||A x - b||^2 without storing A x (float32 CUDA tensors)."""
         out = C.c_double()

@@ -231,6 +231,14 @@ int ctk_atb_f32(ctk_geom* g, int v, const float* y, float* x, void* s) {
 int ctk_atb_f64(ctk_geom* g, int v, const double* y, double* x, void* s) {
     return guard([&] { atb_dev<double>(G(g), v, y, x, S(G(g), s)); });
 }
+int ctk_ax_pair_f32(ctk_geom* g, const float* x1, float* y1, const float* x2, float* y2, void* s) {
+    return guard([&] {
+        auto& gg = G(g);
+        gg.require_angles();
+        if (gg.comm) ctkb::fail(CTK_E_UNSUPPORTED, "ax_pair: not on a sharded handle");
+        ctkb::ax2_f32(gg, x1, y1, x2, y2, S(gg, s));
+    });
+}
 int ctk_ax_residual_f32(ctk_geom* g, const float* x, const float* b, double* out, void* s) {
     return guard([&] {
         auto& gg = G(g);

@@ -47,14 +47,23 @@ namespace {
 #define CTK_FWD_MINB 9  // minimum resident blocks per SM for the register allocator (56 registers)
 #endif
 #ifndef CTK_FWD2_MINB
-#define CTK_FWD2_MINB 8  // the two-volume march (k_ax2_zfast_f32)
+#define CTK_FWD2_MINB 6  // the two-volume march: 80 registers, 6 CTAs/SM (69.2 ms per pair at C3; 81.2 at 8 CTAs / 64 registers, 74.1 at 9 with spills)
 #endif
+#ifndef CTK_FWD2_UNROLL
+#define CTK_FWD2_UNROLL 1
+#endif
+constexpr int kFwd2Unroll = CTK_FWD2_UNROLL;
 constexpr int ZW_BR = 32, ZW_BC = CTK_FWD_BC, kFwdUnroll = CTK_FWD_UNROLL;  // block: 32 detector rows (lanes) x ZW_BC columns
 // zero guard planes on each side of the z-fast layouts (h and z): a tap index may step one
 // beyond the contributing range where anchored positions round across a voxel boundary
 constexpr int kPad = 2;
 
 __device__ __forceinline__ const float* opaque_ptr(const float* p) {
+    asm("" : "+l"(p));
+    return p;
+}
+
+__device__ __forceinline__ const float2* opaque_ptr2(const float2* p) {
     asm("" : "+l"(p));
     return p;
 }
@@ -84,9 +93,16 @@ __global__ void k_relayout_zfast(int nx, int ny, int nz, const float* __restrict
 // Siddon sum of one ray over its slabs (f32_common.cuh), before the factor L = ray_step:
 // sum over slabs of min(cy,cz) v(ja,ka) + (cy-min) v(ja,ka+sz) + (cz-min) v(ja+sy,ka)
 // + (1-max) v(ja+sy,ka+sz), with (ja, ka) the cells at the slab's s - 1/2 boundary.
-template <class Off>
-__device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int nh, int ns, const float* base, Off pz,
-                            Off plane, float vd, float czf, float vr, int nch, int chunk) {
+__device__ __forceinline__ float fma_v(float w, float v, float acc) { return fmaf(w, v, acc); }
+__device__ __forceinline__ float2 fma_v(float w, float2 v, float2 acc) {  // per volume, the scalar op
+    return make_float2(fmaf(w, v.x, acc.x), fmaf(w, v.y, acc.y));
+}
+
+// V = float: one volume; V = float2: two interleaved volumes (k_ax2_zfast_f32), each with
+// exactly the one-volume operation sequence
+template <class Off, class V>
+__device__ V siddon_ray(const KGeom& g, const double4& c64, float fhd, int nh, int ns, const V* base, Off pz,
+                        Off plane, float vd, float czf, float vr, int nch, int chunk) {
     const float Wd = z_cross(g, c64), fcs = sid_fc(g);
     const int izs = sid_izc(g);
     const float dz = vr * Wd;
@@ -135,7 +151,9 @@ __device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int n
 #ifdef CTK_CHECKED
     const long long lay_n = (long long)ns * (long long)plane, base_abs = (long long)(kPad * pz + kPad);
 #endif
-    float acc = 0.f;
+    V acc;
+    if constexpr (sizeof(V) == 4) acc = 0.f;
+    else acc = make_float2(0.f, 0.f);
     for (int s = s0; s <= s1;) {  // slice blocks: fp64 anchors once per block
         const int sc = slice_centre(s);
         const int se = min(s1, sc + kSB / 2 - 1);
@@ -165,11 +183,11 @@ __device__ float siddon_ray(const KGeom& g, const double4& c64, float fhd, int n
             // the second-cell loads)
             const bool xy = cy < 1.f, xz = cz < 1.f;
             const Off o01 = o + (xz ? dz1 : Off(0)), o10 = o + (xy ? dy : Off(0)), o11 = o10 + (xz ? dz1 : Off(0));
-            const float v00 = __ldg(base + o), v01 = __ldg(base + o01), v10 = __ldg(base + o10), v11 = __ldg(base + o11);
-            acc = fmaf(m, v00, acc);        // (ja, ka)
-            acc = fmaf(cy - m, v01, acc);   // (ja, kb)
-            acc = fmaf(cz - m, v10, acc);   // (jb, ka)
-            acc = fmaf(1.f - M, v11, acc);  // (jb, kb)
+            const V v00 = __ldg(base + o), v01 = __ldg(base + o01), v10 = __ldg(base + o10), v11 = __ldg(base + o11);
+            acc = fma_v(m, v00, acc);        // (ja, ka)
+            acc = fma_v(cy - m, v01, acc);   // (ja, kb)
+            acc = fma_v(cz - m, v10, acc);   // (jb, ka)
+            acc = fma_v(1.f - M, v11, acc);  // (jb, kb)
         };
         // two slabs at a time: boundary positions in packed f32x2 arithmetic (per lane the
         // scalar sequence of the transpose: fmaf, split_t, exact fraction)
@@ -423,7 +441,7 @@ k_ax_zfast_f32(KGeom g, const int* __restrict__ vorder, const float* __restrict_
 // per volume the operation sequence is exactly k_ax_zfast_f32's (slice pairs: even slices
 // in one accumulator, odd in the other, the odd tail scalar), so each output is
 // bit-identical to a single-volume launch with the same chunking.
-template <class Off>
+template <class Off, int SID>
 __global__ void __launch_bounds__(ZW_BR * ZW_BC, CTK_FWD2_MINB)
 k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restrict__ wx, const float2* __restrict__ wy,
                 const float* __restrict__ xs1, const float* __restrict__ xs2, float* __restrict__ y1,
@@ -439,7 +457,9 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
         const double2 cs = g.colstep[c];
         const double v = row_coord(g, iv);
         if (g.has_zrays && is_zray(g, cs, v)) {
-            if (chunk == 0) {
+            if (SID) {
+                // Siddon z-rays: the exact DDA fills them after the launches (as ax_f32)
+            } else if (chunk == 0) {
                 const double2 tr = g.ctst[a];
                 WalkF w;
                 walk_generic(g, tr.x, tr.y, iu, iv, w);
@@ -458,6 +478,12 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
             const float vd = float(v);
             const float czf = 0.5f * float(g.nzg - 1);
             const unsigned unh = unsigned(nh), unz = unsigned(g.nz);
+            if constexpr (SID) {
+                const float2 r = siddon_ray(g, c64, cd.y, nh, ns, base, pz, plane, vd, czf, row_vr(g, iv), nch, chunk);
+                const float stp = ray_step(g, cs, v);
+                out1 = r.x * stp;
+                out2 = r.y * stp;
+            } else {
             const float Wd = z_cross(g, c64), vr = row_vr(g, iv), fc = cz_frac(g);
             const int izc = cz_int(g);
             // the slice interval of k_ax_zfast_f32 (same arithmetic)
@@ -497,7 +523,7 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
             using U = typename std::conditional<sizeof(Off) == 4, unsigned, unsigned long long>::type;
             const U upz = U(pz), uplane = U(plane), uplane2 = uplane + uplane;
             const U cbias = U(kSplitBias) * (upz + 1u) - U(unsigned(izc));
-            const float2* base1 = base + pz;
+            const float2* base1 = opaque_ptr2(base + pz);  // one IMAD.WIDE per tap row
             const float2 fhd2 = make_float2(cd.y, cd.y), Wd2 = make_float2(Wd, Wd), vr2 = make_float2(vr, vr);
             const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
             const float2 m1 = make_float2(-1.f, -1.f), two = make_float2(2.f, 2.f);
@@ -516,6 +542,7 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
                 const float2 thA2 = make_float2(thA, thA), Wr2 = make_float2(Wr, Wr), S2 = make_float2(S, S);
                 float2 k2 = make_float2(float(s - sc), float(s - sc + 1));
                 const int cnt = se - s + 1;
+#pragma unroll kFwd2Unroll
                 for (int np = cnt >> 1; np > 0; --np) {
                     const float2 fh = __ffma2_rn(k2, fhd2, thA2);
                     const float2 wlo = __ffma2_rn(k2, Wd2, Wr2);
@@ -571,6 +598,7 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
             const float stp = ray_step(g, cs, v);
             out1 = stp * acc1;
             out2 = stp * acc2;
+            }
         }
     }
     outs[0][threadIdx.x][threadIdx.y] = out1;
@@ -723,11 +751,11 @@ void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
 
 bool ax2_f32_supported(const Geometry& g) {
     const char* e = std::getenv("CTK_FWD_NO_PAIR");  // read per call: tests switch it in-process
-    return !(e && e[0] == '1') && g.projector == CTK_PROJ_JOSEPH && !g.slab && !g.band;
+    return !(e && e[0] == '1') && !g.slab && !g.band;
 }
 
 void ax2_f32(Geometry& g, const float* x1, float* y1, const float* x2, float* y2, cudaStream_t s) {
-    if (!ax2_f32_supported(g)) throw Error(CTK_E_UNSUPPORTED, "ax2_f32: f32 Joseph on a whole-volume handle only");
+    if (!ax2_f32_supported(g)) throw Error(CTK_E_UNSUPPORTED, "ax2_f32: whole-volume handles only");
     const size_t nwx = size_t(g.nx) * (size_t(g.ny) + 2 * kPad) * (size_t(g.nz) + 2 * kPad);
     const size_t nwy = size_t(g.ny) * (size_t(g.nx) + 2 * kPad) * (size_t(g.nz) + 2 * kPad);
     if (g.vx2.ensure(nwx * sizeof(float2))) CTK_CUDA(cudaMemsetAsync(g.vx2.p, 0, nwx * sizeof(float2), s));
@@ -744,9 +772,20 @@ void ax2_f32(Geometry& g, const float* x1, float* y1, const float* x2, float* y2
     const dim3 blk(ZW_BR, ZW_BC), grd = fwd_grid(g);
     // 64-bit offsets once the float2 layout's element count passes 2^31 (offsets index float2)
     for (int c = 0; c < nch; ++c) {
-        if (wide_offsets(g)) k_ax2_zfast_f32<long long><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
-        else k_ax2_zfast_f32<int><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
+        const bool sid = g.projector == CTK_PROJ_SIDDON;
+        if (wide_offsets(g)) {
+            if (sid) k_ax2_zfast_f32<long long, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
+            else k_ax2_zfast_f32<long long, 0><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
+        } else {
+            if (sid) k_ax2_zfast_f32<int, 1><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
+            else k_ax2_zfast_f32<int, 0><<<grd, blk, 0, s>>>(k, vo, a0, a1, x1, x2, y1, y2, nch, c);
+        }
         after_launch("k_ax2_zfast_f32");
+    }
+    // Siddon: the z-dominant rays by the exact DDA, writing only their entries (as ax_f32)
+    if (g.projector == CTK_PROJ_SIDDON && g.has_zrays) {
+        siddon_ax_zrays_f32(g, x1, y1, s);
+        siddon_ax_zrays_f32(g, x2, y2, s);
     }
 }
 

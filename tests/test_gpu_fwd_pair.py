@@ -59,6 +59,15 @@ def test_paired_residual_bitwise(ctk, name, solver):
     _same(_solve(ctk, pair, b, solver, 6, True), _solve(ctk, pair, b, solver, 6, False))
 
 
+@pytest.mark.parametrize("name", ["cone_default", "cone_steep", "cone_ragged", "parallel3d"])
+def test_paired_residual_bitwise_siddon(ctk, name):
+    # the f32 Siddon slab model (k_ax2_zfast_f32<SID=1>) and its z-ray DDA
+    g = ALL[name]()
+    b = np.random.default_rng(9).standard_normal(g.na * g.nv * g.nu).astype(np.float32)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float32, projector=ctk.ProjectorKind.siddon)
+    _same(_solve(ctk, pair, b, "lsqr", 6, True), _solve(ctk, pair, b, "lsqr", 6, False))
+
+
 def test_paired_residual_bench_geometry(ctk):
     # 128^3 with several slice chunks per ray (fwd_chunks) and 90 views
     g = cone_bench(128, 90)
@@ -98,3 +107,33 @@ print("ok")
     env.pop("CTK_FWD_NO_PAIR", None)
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("projector", ["joseph", "siddon"])
+@pytest.mark.parametrize("name", ["cone_default", "cone_steep", "parallel3d", "cone_multitile"])
+def test_forward_pair_bitwise(ctk, name, projector):
+    import torch
+
+    g = ALL[name]()
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float32, projector=ctk.ProjectorKind[projector])
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    x1 = torch.randn(g.nx * g.ny * g.nz, device="cuda", generator=gen)
+    x2 = torch.randn(g.nx * g.ny * g.nz, device="cuda", generator=gen)
+    y1, y2 = (torch.full((pair.range_size,), float("nan"), device="cuda") for _ in range(2))
+    z1, z2 = (torch.empty(pair.range_size, device="cuda") for _ in range(2))
+    pair.projector.forward_pair(x1, y1, x2, y2)
+    pair.forward(x1, z1)
+    pair.forward(x2, z2)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, z1) and torch.equal(y2, z2)
+
+
+def test_forward_pair_unsupported(ctk):
+    import torch
+
+    g = ALL["cone_default"]()
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float32, slab=(4, 8))  # a z-slab handle
+    x = torch.zeros(pair.domain_size, device="cuda")
+    y = torch.zeros(pair.range_size, device="cuda")
+    with pytest.raises(ctk.UnsupportedError):
+        pair.projector.forward_pair(x, y, x, y)
