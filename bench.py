@@ -83,7 +83,7 @@ def traffic_bytes(kernel, n, na):
     """DRAM bytes per operation of the dominant kernel from the committed ncu capture (same
     workload only), else None."""
     here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02")
-    for name in ("traffic_ax_512_360.json", "traffic_atb_512_360.json"):
+    for name in ("traffic_ax_512_360.json", "traffic_atb_512_360.json", "traffic_ax2_512_360.json"):
         try:
             with open(os.path.join(here, name)) as f:
                 t = json.load(f)
@@ -353,6 +353,18 @@ def main():
         bt_ms.append(proj.last_kernel_ms())
     t_ax = statistics.median(ax_ms[1:])
     t_bt = statistics.median(bt_ms[1:])
+    # the two-volume march the solvers run once per iteration (the explicit residual's A x
+    # with the next A v; lsqr / lsmr / hybrid_lsqr on whole-volume handles)
+    t_pair = None
+    if args.solver in ("lsqr", "lsmr", "hybrid_lsqr") and args.shard != "slab" and os.environ.get("CTK_FWD_NO_PAIR") != "1":
+        y2 = torch.empty_like(b)
+        pair_ms = []
+        for _ in range(4):
+            proj.forward_pair(x_true, y, xb, y2)
+            torch.cuda.synchronize()
+            pair_ms.append(proj.last_kernel_ms())
+        t_pair = statistics.median(pair_ms[1:])
+        del y2
 
     # ---- the solve: W warmup steps, K timed steps (device-resident b and x).  The clock
     # sampler starts before the warmup so its start-up never overlaps the timed region.
@@ -419,10 +431,17 @@ def main():
     samples = my_angles * n * n * my_slices  # Gray-voxel normaliser (rays x slices)
     ax_gvox = 1e-9 * samples / (t_ax / 1e3)
     bt_gvox = 1e-9 * samples / (t_bt / 1e3)
-    alg_bytes = 4.0 * (nvox + nproj)
-    share_ax, share_bt = 2 * t_ax, t_bt
-    dom = "k_ax_f32" if share_ax >= share_bt else "k_atb_matched_f32"
-    t_dom = t_ax if dom == "k_ax_f32" else t_bt
+    # per iteration: A^T b once, and either two forward marches or one two-volume march
+    if t_pair is None:
+        share_ax, share_bt = 2 * t_ax, t_bt
+        dom = "k_ax_f32" if share_ax >= share_bt else "k_atb_matched_f32"
+        t_dom = t_ax if dom == "k_ax_f32" else t_bt
+        vols = 1
+    else:
+        dom = "k_ax2_f32" if t_pair >= t_bt else "k_atb_matched_f32"
+        t_dom = t_pair if dom == "k_ax2_f32" else t_bt
+        vols = 2 if dom == "k_ax2_f32" else 1
+    alg_bytes = 4.0 * (nvox + nproj) * vols
     achieved = alg_bytes / (t_dom / 1e3) / 1e9
     gather_peak_arith = 148 * 128 * sm_mhz * 1e6 / GATHER_BYTES_PER_SAMPLE / 1e9  # G samples/s at 128 B/clk/SM
     gather_peak, gather_src = gather_peak_arith, "arithmetic: 16 B/sample at 128 B/clk/SM x 148 SMs"
@@ -459,7 +478,8 @@ def main():
                    "l2": l2_note},
         "ax_gvox_s": ax_gvox,
         "atb_gvox_s": bt_gvox,
-        "kernels_ms": {"k_ax_f32": t_ax, "k_atb_matched_f32": t_bt, "ax_call": statistics.median(ax_call_ms[1:])},
+        "kernels_ms": {"k_ax_f32": t_ax, "k_atb_matched_f32": t_bt, "k_ax2_f32": t_pair,
+                       "ax_call": statistics.median(ax_call_ms[1:])},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_bytes(dom, n, my_angles) if my_slices == n else None, "algorithmic_bytes": alg_bytes,
                      "note": f"algorithmic bytes 4*(N_vox+N_proj) per launch; peak {peak_src}; traffic = measured "
@@ -467,9 +487,11 @@ def main():
                              "capture, profiles/r02/traffic_{ax,atb}_512_360.json, when the workload matches; the volume "
                              "slab of each detector-row band is re-read from DRAM by design (L2 residency per band; "
                              "8.4 GB per Ax at C3 = 176 GB/s, 2.7 % of HBM: the kernel is bound on chip)"},
-        "roofline_gather": {"kernel": dom, "achieved": samples / (t_dom / 1e3) / 1e9, "peak": gather_peak,
-                            "unit": "G samples/s", "frac": samples / (t_dom / 1e3) / 1e9 / gather_peak,
-                            "note": "binding on-chip ceiling (SURVEY.md 8(d)), " + gather_src},
+        "roofline_gather": {"kernel": dom, "achieved": vols * samples / (t_dom / 1e3) / 1e9, "peak": gather_peak,
+                            "unit": "G samples/s", "frac": vols * samples / (t_dom / 1e3) / 1e9 / gather_peak,
+                            "note": "binding on-chip ceiling (SURVEY.md 8(d)), " + gather_src +
+                                    ("; k_ax2_f32 = the two-volume march (two samples per ray-slice, one per volume)"
+                                     if vols == 2 else "")},
         "e2e": {"value": e2e_value, "unit": "iters/s", "h2d_bytes_per_step": 4 * nproj, "d2h_bytes_per_step": 4 * nvox,
                 "clocks": clk_e2e.summary()},
         "gpu_launches": launches,

@@ -770,6 +770,7 @@ void ax2_f32(Geometry& g, const float* x1, float* y1, const float* x2, float* y2
     const int* vo = g.d_vorder.as<int>();
     const float2 *a0 = g.vx2.as<float2>(), *a1 = g.vy2.as<float2>();
     const dim3 blk(ZW_BR, ZW_BC), grd = fwd_grid(g);
+    CTK_CUDA(cudaEventRecord(g.ev0, s));
     // 64-bit offsets once the float2 layout's element count passes 2^31 (offsets index float2)
     for (int c = 0; c < nch; ++c) {
         const bool sid = g.projector == CTK_PROJ_SIDDON;
@@ -782,6 +783,7 @@ void ax2_f32(Geometry& g, const float* x1, float* y1, const float* x2, float* y2
         }
         after_launch("k_ax2_zfast_f32");
     }
+    CTK_CUDA(cudaEventRecord(g.ev1, s));
     // Siddon: the z-dominant rays by the exact DDA, writing only their entries (as ax_f32)
     if (g.projector == CTK_PROJ_SIDDON && g.has_zrays) {
         siddon_ax_zrays_f32(g, x1, y1, s);

@@ -80,6 +80,8 @@ struct Dev {
     const T* next_in = nullptr;
     T* next_out = nullptr;
     bool next_ready = false;
+    // can the monitor's A x run paired with a following forward application?
+    bool can_pair() const { return sizeof(T) == 4 && ax2_f32_supported(g); }
     void announce_ax(const T* x, T* y) {
         next_in = x;
         next_out = y;
@@ -309,12 +311,22 @@ void cgls(Dev<T>& d, const T* b, const ctk_solver_opts& o, T* x, ctk_solve_log* 
         const double alpha = gamma / delta;
         axpy<T>(nd, alpha, p.p, x, d.s);
         const double rr = d.axpy_n2(-alpha, q.p, r.p, nr, true);
+        auto advance = [&] {  // s = A^T r, p = s + beta p
+            d.atb(r.p, s.p);
+            const double gnew = d.nrm2sq(s.p, nd, false);
+            const double beta = gnew / gamma;
+            gamma = gnew;
+            xpby<T>(nd, s.p, beta, p.p, d.s);
+        };
+        // With the two-volume march the recurrence advances before the monitor records x_k,
+        // so its A x pairs with the next A p (the same values; on a stop the advance is unused)
+        const bool ahead = k < o.max_iters && d.can_pair();
+        if (ahead) {
+            advance();
+            d.announce_ax(p.p, q.p);
+        }
         if (mon.record(k, x, std::sqrt(rr) / bnorm)) break;
-        d.atb(r.p, s.p);
-        const double gnew = d.nrm2sq(s.p, nd, false);
-        const double beta = gnew / gamma;
-        gamma = gnew;
-        xpby<T>(nd, s.p, beta, p.p, d.s);
+        if (!ahead) advance();
     }
     mon.finish(k);
 }
@@ -626,15 +638,23 @@ void cgls_tv(Dev<T>& d, const T* b, double lambda, int outer_iters, int inner_it
             axpy<T>(nd, alpha, p.p, x, d.s);
             const double rr = K.axpy_n2(-alpha, q.p, r.p);
             ++k;
+            auto advance = [&] {
+                K.back(r.p, s.p);
+                const double gnew = d.nrm2sq(s.p, nd, false);
+                const double beta = gnew / gamma;
+                gamma = gnew;
+                xpby<T>(nd, s.p, beta, p.p, d.s);
+            };
+            const bool ahead = inner + 1 < inner_iters && d.can_pair();  // as cgls: pair A x with the next A p
+            if (ahead) {
+                advance();
+                d.announce_ax(p.p, q.p);
+            }
             if (mon.record(k, x, std::sqrt(rr) / rhs_norm, true, lambda)) {
                 stopped = true;
                 break;
             }
-            K.back(r.p, s.p);
-            const double gnew = d.nrm2sq(s.p, nd, false);
-            const double beta = gnew / gamma;
-            gamma = gnew;
-            xpby<T>(nd, s.p, beta, p.p, d.s);
+            if (!ahead) advance();
         }
     }
     mon.finish(k);

@@ -1,7 +1,8 @@
 """The two-volume forward march (ax2_f32, fwd_f32.cu) inside the solvers.
 
-lsqr, lsmr and hybrid_lsqr announce their next A v before the monitor records an iterate;
-the explicit residual's A x (solve_log.hpp:102-115) and that A v then run as one march over
+lsqr, lsmr and hybrid_lsqr announce their next A v before the monitor records an iterate
+(cgls and cgls_tv advance their recurrence first to have the next A p); the explicit
+residual's A x (solve_log.hpp:102-115) and that product then run as one march over
 interleaved layouts.  Each output is bit-identical to a single-volume launch, so every
 solve must be bitwise the same with the pairing switched off (CTK_FWD_NO_PAIR=1): x, both
 residual histories, lambda and relative-error logs.  The geometries cover x- and
@@ -25,17 +26,21 @@ def ctk():
     return m
 
 
-def _solve(ctk, pair, b, solver, k, paired):
+def _solve(ctk, pair, b, solver, k, paired, tol=0.0):
     if paired:
         os.environ.pop("CTK_FWD_NO_PAIR", None)
     else:
         os.environ["CTK_FWD_NO_PAIR"] = "1"
     try:
-        opts = ctk.SolverOptions(max_iters=k, stop_on_explicit_residual_increase=False, residual_tolerance=0.0)
+        opts = ctk.SolverOptions(max_iters=k, stop_on_explicit_residual_increase=False, residual_tolerance=tol)
         if solver == "lsmr":
             return ctk.lsmr(pair, b, 3.0, opts)
         if solver == "hybrid_lsqr":
             return ctk.hybrid_lsqr(pair, b, ctk.HybridStrategy.gcv(), opts)
+        if solver == "cgls":
+            return ctk.cgls(pair, b, opts)
+        if solver == "cgls_tv":
+            return ctk.cgls_tv(pair, b, 0.05, 2, 4, opts, warm_start=True)
         return ctk.lsqr(pair, b, opts)
     finally:
         os.environ.pop("CTK_FWD_NO_PAIR", None)
@@ -43,20 +48,22 @@ def _solve(ctk, pair, b, solver, k, paired):
 
 def _same(r1, r2):
     assert r1.iterations_run == r2.iterations_run
+    assert r1.stop_reason == r2.stop_reason
     assert np.array_equal(r1.x, r2.x)
     assert r1.log.implicit_residual == r2.log.implicit_residual
     assert r1.log.explicit_residual == r2.log.explicit_residual
     assert r1.log.lambda_ == r2.log.lambda_
 
 
-@pytest.mark.parametrize("solver", ["lsqr", "lsmr", "hybrid_lsqr"])
+@pytest.mark.parametrize("solver", ["lsqr", "lsmr", "hybrid_lsqr", "cgls", "cgls_tv"])
 @pytest.mark.parametrize("name", ["cone_default", "cone_steep", "cone_ragged", "parallel3d", "cone_multitile"])
 def test_paired_residual_bitwise(ctk, name, solver):
     g = ALL[name]()
     rng = np.random.default_rng(7)
     b = rng.standard_normal(g.na * g.nv * g.nu).astype(np.float32)
     pair = ctk.projector_pair(to_ctk(g), dtype=np.float32)
-    _same(_solve(ctk, pair, b, solver, 6, True), _solve(ctk, pair, b, solver, 6, False))
+    k = 8 if solver == "cgls_tv" else 6
+    _same(_solve(ctk, pair, b, solver, k, True), _solve(ctk, pair, b, solver, k, False))
 
 
 @pytest.mark.parametrize("name", ["cone_default", "cone_steep", "cone_ragged", "parallel3d"])
@@ -66,6 +73,20 @@ def test_paired_residual_bitwise_siddon(ctk, name):
     b = np.random.default_rng(9).standard_normal(g.na * g.nv * g.nu).astype(np.float32)
     pair = ctk.projector_pair(to_ctk(g), dtype=np.float32, projector=ctk.ProjectorKind.siddon)
     _same(_solve(ctk, pair, b, "lsqr", 6, True), _solve(ctk, pair, b, "lsqr", 6, False))
+
+
+@pytest.mark.parametrize("solver", ["cgls", "lsqr", "cgls_tv"])
+def test_paired_tolerance_stop(ctk, solver):
+    # a tolerance stop mid-run: the advanced recurrence (cgls) and the announced product go
+    # unused, the solve ends at the same iteration with the same x
+    g = ALL["cone_default"]()
+    b = np.abs(np.random.default_rng(4).standard_normal(g.na * g.nv * g.nu)).astype(np.float32)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float32)
+    full = _solve(ctk, pair, b, solver, 8, False)
+    tol = full.log.explicit_residual[2] * (1 + 1e-9)
+    r1, r2 = _solve(ctk, pair, b, solver, 8, True, tol), _solve(ctk, pair, b, solver, 8, False, tol)
+    assert r1.iterations_run <= 3 < 8
+    _same(r1, r2)
 
 
 def test_paired_residual_bench_geometry(ctk):
