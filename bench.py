@@ -354,9 +354,10 @@ def main():
     t_ax = statistics.median(ax_ms[1:])
     t_bt = statistics.median(bt_ms[1:])
     # the two-volume march the solvers run once per iteration (the explicit residual's A x
-    # with the next A v; lsqr / lsmr / hybrid_lsqr on whole-volume handles)
+    # with the next A v or A p; every bench solver on a whole-volume handle)
     t_pair = None
-    if args.solver in ("lsqr", "lsmr", "hybrid_lsqr") and args.shard != "slab" and os.environ.get("CTK_FWD_NO_PAIR") != "1":
+    if args.solver in ("lsqr", "lsmr", "hybrid_lsqr", "cgls", "cgls_tv") and args.shard != "slab" \
+            and os.environ.get("CTK_FWD_NO_PAIR") != "1":
         y2 = torch.empty_like(b)
         pair_ms = []
         for _ in range(4):
