@@ -356,7 +356,7 @@ def main():
     # the two-volume march the solvers run once per iteration (the explicit residual's A x
     # with the next A v or A p; every bench solver on a whole-volume handle)
     t_pair = None
-    if args.solver in ("lsqr", "lsmr", "hybrid_lsqr", "cgls", "cgls_tv") and args.shard != "slab" \
+    if args.solver in ("lsqr", "lsmr", "hybrid_lsqr", "cgls", "cgls_tv") and not (args.shard == "slab" and world > 1) \
             and os.environ.get("CTK_FWD_NO_PAIR") != "1":
         y2 = torch.empty_like(b)
         pair_ms = []

@@ -751,7 +751,9 @@ void ax_f32(Geometry& g, const float* x, float* y, cudaStream_t s) {
 
 bool ax2_f32_supported(const Geometry& g) {
     const char* e = std::getenv("CTK_FWD_NO_PAIR");  // read per call: tests switch it in-process
-    return !(e && e[0] == '1') && !g.slab && !g.band;
+    // whole volume: no slab, or a slab handle that holds every slice (a one-rank z-slab run)
+    const bool whole = !g.slab || (g.z0 == 0 && g.nz_local() == g.nz);
+    return !(e && e[0] == '1') && whole && !g.band;
 }
 
 void ax2_f32(Geometry& g, const float* x1, float* y1, const float* x2, float* y2, cudaStream_t s) {

@@ -89,6 +89,16 @@ def test_paired_tolerance_stop(ctk, solver):
     _same(r1, r2)
 
 
+@pytest.mark.parametrize("solver", ["cgls_tv", "lsqr"])
+def test_paired_residual_whole_slab(ctk, solver):
+    # a z-slab handle holding every slice (bench --shard slab at one rank) pairs too
+    g = ALL["cone_ragged"]()
+    b = np.random.default_rng(6).standard_normal(g.na * g.nv * g.nu).astype(np.float32)
+    pair = ctk.projector_pair(to_ctk(g), dtype=np.float32, slab=(0, g.nz))
+    k = 8 if solver == "cgls_tv" else 6
+    _same(_solve(ctk, pair, b, solver, k, True), _solve(ctk, pair, b, solver, k, False))
+
+
 def test_paired_residual_bench_geometry(ctk):
     # 128^3 with several slice chunks per ray (fwd_chunks) and 90 views
     g = cone_bench(128, 90)
