@@ -524,6 +524,20 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
             const U upz = U(pz), uplane = U(plane), uplane2 = uplane + uplane;
             const U cbias = U(kSplitBias) * (upz + 1u) - U(unsigned(izc));
             const float2* base1 = opaque_ptr2(base + pz);  // one IMAD.WIDE per tap row
+#ifdef CTK_CHECKED
+            // checked build: the four taps o, o+1, o+pz, o+pz+1 must lie inside the layout
+            const long long lay_n = (long long)ns * (long long)plane, base_abs = (long long)(kPad * pz + kPad);
+            auto chk_tap = [&](Off o) -> Off {
+                const long long lo = base_abs + (long long)o;
+                if (lo < 0 || lo + (long long)pz + 1 >= lay_n) {
+                    atomicOr(g.chk, 1u << 0);
+                    return Off(-base_abs);
+                }
+                return o;
+            };
+#else
+            auto chk_tap = [](Off o) { return o; };
+#endif
             const float2 fhd2 = make_float2(cd.y, cd.y), Wd2 = make_float2(Wd, Wd), vr2 = make_float2(vr, vr);
             const float2 M2 = make_float2(kSplitM, kSplitM), nM2 = make_float2(-kSplitM, -kSplitM);
             const float2 m1 = make_float2(-1.f, -1.f), two = make_float2(2.f, 2.f);
@@ -550,9 +564,10 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
                     const float2 tzt = __fadd2_rd(__ffma2_rn(vr2, wlo, S2), M2);
                     const float2 th = __ffma2_rn(__fadd2_rn(tht, nM2), m1, fh);
                     const float2 tz = __ffma2_rn(vr2, wlo, __ffma2_rn(__fadd2_rn(tzt, nM2), m1, S2));
-                    const Off o0 = Off(U(unsigned(__float_as_int(tht.x))) * upz + (sb + U(unsigned(__float_as_int(tzt.x)))));
-                    const Off o1 =
-                        Off(U(unsigned(__float_as_int(tht.y))) * upz + (sb + uplane + U(unsigned(__float_as_int(tzt.y)))));
+                    const Off o0 =
+                        chk_tap(Off(U(unsigned(__float_as_int(tht.x))) * upz + (sb + U(unsigned(__float_as_int(tzt.x))))));
+                    const Off o1 = chk_tap(
+                        Off(U(unsigned(__float_as_int(tht.y))) * upz + (sb + uplane + U(unsigned(__float_as_int(tzt.y))))));
                     k2 = __fadd2_rn(k2, two);
                     sb += uplane2;
                     const float2 A00 = __ldg(base + o0), A01 = __ldg(base + o0 + 1);
@@ -579,7 +594,8 @@ k_ax2_zfast_f32(KGeom g, const int* __restrict__ vorder, const float2* __restric
                     const float tht = split_t(fh), tzt = split_t(fmaf(vr, wlo, S));
                     const float th = split_frac(fh, tht);
                     const float tz = fmaf(vr, wlo, fmaf(__fsub_rn(tzt, kSplitM), -1.f, S));
-                    const Off off = Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt)))));
+                    const Off off =
+                        chk_tap(Off(U(unsigned(__float_as_int(tht))) * upz + (sb + U(unsigned(__float_as_int(tzt))))));
                     const float2 v00 = __ldg(base + off), v01 = __ldg(base + off + 1);
                     const float2 v10 = __ldg(base1 + off), v11 = __ldg(base1 + off + 1);
                     {

@@ -5,7 +5,7 @@ backprojector (grouped-projection loads, registration-list entries, volume store
 gather and the voxel-driven gather use, substitutes a safe index and fails the operator call
 (CTK_E_CUDA "checked build: ...") on any violation.  Run here over every parity geometry in both
 plane-tile sizes, the slab pair and small solves (tools/sanitize_cases.py), and over the full
-parity suite."""
+parity suite and the two-volume march's bitwise solver tests."""
 import os
 import subprocess
 import sys
@@ -35,4 +35,11 @@ def test_checked_cases(case, tile):
 def test_checked_parity_suite(tile):
     r = _run(["-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu", "tests/test_gpu_parity.py",
               "tests/test_gpu_operators.py"], tile, timeout=2400)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+
+
+def test_checked_pair_suite():
+    # the two-volume forward march (k_ax2_zfast_f32) inside every solver that pairs
+    r = _run(["-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu", "tests/test_gpu_fwd_pair.py"],
+             timeout=1800)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
